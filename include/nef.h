@@ -1,0 +1,150 @@
+/*
+ * nef.h — C ABI of the B200-native NNEinFact multiplicative-update sweep.
+ *
+ * The calls follow the paper's statement of the problem (arxiv 2602.02759):
+ *   Algorithm 1 REQUIREs data Y, model_str, initial Theta, the loss and eps and returns
+ *   Theta; masking per P:321.
+ *   Model family / einsum string: eq:contraction_structure, eq:einsum.
+ *   Update: Theta <- max(eps, Theta * g^{-1}(A/B)) (eq:explicit-update) with
+ *   A, B = einsum(einstr_l, ..., a(Y,Yhat) | b(Y,Yhat), ...) (Alg. 1 lines 7-8).
+ *   (alpha,beta)-divergence P:500-525; a, b P:529; g P:531-539.
+ *
+ * Conventions:
+ *   - (alpha, beta) are in the PAPER's convention: KL = (1,0), squared Euclidean = (1,1)
+ *     (P:526).  alpha = 0 is accepted only with beta = 1.
+ *   - Y is float32, dense, row-major in OUTPUT-subscript order (the last output index is
+ *     contiguous).  mask is uint8 of the same shape; nonzero = observed, 0 = missing;
+ *     NULL = every entry observed.  Values of Y at missing entries are never used.
+ *   - Factor ell (0-based, string order) is float32, row-major in its operand-subscript
+ *     order, e.g. "abc" -> [R_a][R_b][R_c].
+ *   - Index sizes: observed indices take `shape` in output order; contracted indices take
+ *     `ranks` in order of first appearance, left to right (reading R18).
+ *   - The loss trace is the SUM over observed entries of L_{alpha,beta}(y, max(yhat,1e-30))
+ *     accumulated in float64 (reading R7); trace[0] = loss at the initial factors,
+ *     trace[t] = loss after full sweep t.
+ *
+ * Ownership: the caller owns Y, mask, the factors and the workspace (device memory, e.g.
+ * allocated by PyTorch).  A plan owns host metadata only and, after nef_plan_shard, its
+ * NCCL communicator.  Factors are updated in place.  All device work is enqueued on
+ * `cuda_stream` (a cudaStream_t; NULL = legacy default stream); nef_fit and nef_loss
+ * return after their host outputs (trace, loss) have been copied back.
+ *
+ * Errors: every entry point returns NEF_OK (0) or an nef_status code; nef_last_error()
+ * returns a thread-local human-readable detail.  Validation errors (PARSE, SHAPE, DOMAIN,
+ * ARG, UNSUPPORTED) are detected before any device work and leave every buffer untouched.
+ * CUDA / NCCL errors may arrive mid-run; the factors are then unspecified.
+ * No CPU fallback exists: without a CUDA device every compute call returns NEF_E_CUDA.
+ */
+#ifndef NEF_H_
+#define NEF_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct nef_plan_s* nef_plan_t;
+
+enum nef_status {
+  NEF_OK = 0,
+  NEF_E_PARSE = 1,        /* malformed einsum string (grammar: subs(,subs)*->subs, [a-zA-Z])   */
+  NEF_E_SHAPE = 2,        /* wrong number of dims/ranks, non-positive size, int64 overflow     */
+  NEF_E_DOMAIN = 3,       /* (alpha,beta) outside the paper's decomposable family      */
+  NEF_E_DATA = 4,         /* reserved: invalid data at an observed entry (debug checks)        */
+  NEF_E_ARG = 5,          /* null/misaligned pointer, too-small workspace, bad ell, eps <= 0   */
+  NEF_E_CUDA = 6,         /* CUDA runtime error or no device                                    */
+  NEF_E_NCCL = 7,         /* NCCL error or NCCL library not loadable                            */
+  NEF_E_UNSUPPORTED = 8   /* model string with no lowering in this build                        */
+};
+
+/* Build a plan for `einsum` over a GLOBAL tensor of `n_modes` dims `shape` (output order)
+ * with `n_ranks` contracted-index sizes `ranks` (first-appearance order).  Host only:
+ * parses, builds einstr_l = swap(model_str, l) for every l (Alg. 1
+ * lines 1-3) and lowers each factor update to a streamed row/col/bond form (DESIGN.md
+ * §Planner).  On success *out receives a new plan (free with nef_plan_destroy). */
+int nef_plan(const char* einsum, int n_modes, const int64_t* shape, int n_ranks, const int64_t* ranks,
+             nef_plan_t* out);
+
+/* Plan metadata.  n_factors = L; shard_mode = mode split across ranks (-1 if unsharded);
+ * [local_begin, local_begin + local_len) = this rank's index range of that mode (whole
+ * range if unsharded); workspace_bytes = device scratch nef_fit / nef_loss / nef_update
+ * need for a problem WITH a mask (a maskless problem needs no more).  Any out-pointer may
+ * be NULL. */
+int nef_plan_info(nef_plan_t plan, int* n_factors, int* shard_mode, int64_t* local_begin, int64_t* local_len,
+                  size_t* workspace_bytes);
+
+/* Shape of factor `ell` as seen by THIS rank (sharded factors are local slices).
+ * dims must hold >= 8 entries; *ndim receives the operand's number of indices. */
+int nef_factor_shape(nef_plan_t plan, int ell, int64_t* dims, int* ndim);
+
+/* Local shape of Y on this rank (dims must hold >= 8 entries). */
+int nef_local_shape(nef_plan_t plan, int64_t* dims, int* ndim);
+
+/* Human-readable JSON description of the lowering (for tests / debugging).  Writes at
+ * most `cap` bytes including the NUL; returns the full length needed in *len. */
+int nef_plan_describe(nef_plan_t plan, char* buf, size_t cap, size_t* len);
+
+/* Fit: run `iters` full Gauss-Seidel sweeps of Algorithm 1 in place on
+ * `factors` (host array of L device pointers).  Y/mask are this rank's LOCAL tensor
+ * (device, contiguous, 16-byte aligned).  eps > 0 is the floor of eq:obj.
+ * loss_trace: host array of iters+1 doubles, or NULL.  workspace: device scratch of at
+ * least nef_plan_info's workspace_bytes.  On a sharded plan the numerator/denominator of
+ * every factor that does not contain the shard mode and the loss are all-reduced over
+ * NCCL; every rank ends with identical replicated factors. */
+int nef_fit(nef_plan_t plan, const float* Y, const uint8_t* mask, double alpha, double beta, double eps,
+            float* const* factors, int iters, double* loss_trace, void* workspace, size_t ws_bytes,
+            void* cuda_stream);
+
+/* One factor update (Algorithm 1 lines 6-9 for a single ell), the step-level API. */
+int nef_update(nef_plan_t plan, int ell, const float* Y, const uint8_t* mask, double alpha, double beta,
+               double eps, float* const* factors, void* workspace, size_t ws_bytes, void* cuda_stream);
+
+/* Numerator A and denominator B of the update of factor `ell` (Alg. 1 lines 7-8, before
+ * any all-reduce), written to num/den (device, size of factor ell).  For tests and for
+ * torch-driven collectives (all-reduce them, then nef_apply_update). */
+int nef_num_den(nef_plan_t plan, int ell, const float* Y, const uint8_t* mask, double alpha, double beta,
+                float* const* factors, float* num, float* den, void* workspace, size_t ws_bytes,
+                void* cuda_stream);
+
+/* Theta_ell <- max(eps, Theta_ell * g^{-1}(num/den)) with den == 0 -> multiplier 1. */
+int nef_apply_update(nef_plan_t plan, int ell, double alpha, double beta, double eps, float* const* factors,
+                     const float* num, const float* den, void* cuda_stream);
+
+/* Loss sum over observed entries (fp64) and the number of observed entries, for the
+ * current factors (all-reduced over ranks on a sharded plan). */
+int nef_loss(nef_plan_t plan, const float* Y, const uint8_t* mask, double alpha, double beta,
+             float* const* factors, double* loss_sum, int64_t* n_observed, void* workspace, size_t ws_bytes,
+             void* cuda_stream);
+
+/* End-to-end variant taking HOST buffers: copies Y (and mask) host->device into
+ * `device_scratch`, the factors host->device, runs nef_fit, copies the factors back
+ * device->host.  device_scratch must hold nef_host_scratch_bytes(plan, has_mask). */
+size_t nef_host_scratch_bytes(nef_plan_t plan, int has_mask);
+int nef_fit_host(nef_plan_t plan, const float* Y_host, const uint8_t* mask_host, double alpha, double beta,
+                 double eps, float* const* factors_host, int iters, double* loss_trace, void* device_scratch,
+                 size_t scratch_bytes, void* cuda_stream);
+
+/* Multi-GPU.  Rank 0 calls nef_nccl_unique_id (128 bytes), the caller broadcasts the
+ * bytes (e.g. torch.distributed), then every rank calls nef_plan_shard, which splits the
+ * largest mode (ties -> outermost) into contiguous near-equal ranges and creates the NCCL
+ * communicator on the current CUDA device. */
+int nef_nccl_unique_id(void* out128);
+int nef_plan_shard(nef_plan_t plan, int rank, int world, const void* nccl_unique_id);
+
+/* Number of kernel launches the last nef_fit / nef_loss / nef_update call enqueued. */
+int64_t nef_last_launch_count(void);
+
+/* Select the streaming kernel: 0 = automatic (tcgen05 where supported), 1 = CUDA-core FFMA
+ * kernel only.  Process-wide; for tests and A/B measurement. */
+int nef_set_kernel_policy(int policy);
+
+void nef_plan_destroy(nef_plan_t plan);
+const char* nef_last_error(void);
+const char* nef_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NEF_H_ */

@@ -1,0 +1,557 @@
+// C ABI of libnef (include/nef.h): orchestration of Algorithm 1 on the device.
+//
+// Per factor update ell (Alg. 1 lines 6-9):
+//   1. side operands  U = einsum(row factors -> rows,bond), column tables     (small-einsum engine)
+//   2. fused pass     Q_a = a(Y, U V^T) V, Q_b = b(Y, U V^T) V, one read of Y / mask
+//   3. reduce         fixed-order sum of split-column partials
+//   4. epilogue       A = einsum(swap(rowmodel, ell)) with Q_a (B likewise)   (= einstr_ell)
+//   5. [sharded]      ncclAllReduce(A|B) for factors without the shard mode
+//   6. update         Theta <- max(eps, Theta * g^{-1}(A/B))
+// The loss of the iterate entering a sweep is accumulated inside the first factor's fused
+// pass; one extra loss-only pass gives the final trace entry.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "kernels.h"
+#include "nef_internal.h"
+#include "../../include/nef.h"
+
+struct nef_plan_s {
+  nef::Plan p;
+};
+
+namespace {
+
+thread_local std::string g_err;
+thread_local int64_t g_launches = 0;
+int g_policy = 0;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CK(call)                                                                      \
+  do {                                                                                \
+    cudaError_t e_ = (call);                                                          \
+    if (e_ != cudaSuccess) return fail(NEF_E_CUDA, std::string(#call) + ": " + cudaGetErrorString(e_)); \
+  } while (0)
+
+// ------------------------------------------------------------------ NCCL (dlopen)
+struct Uid {
+  char internal[128];
+};
+struct Nccl {
+  bool loaded = false;
+  void* h = nullptr;
+  int (*GetUniqueId)(void*) = nullptr;
+  int (*CommInitRank)(void**, int, Uid, int) = nullptr;  // ncclUniqueId by value
+  int (*AllReduce)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+  int (*CommDestroy)(void*) = nullptr;
+  const char* (*GetErrorString)(int) = nullptr;
+};
+Nccl g_nccl;
+
+bool load_nccl(std::string& err) {
+  if (g_nccl.loaded) return true;
+  const char* names[] = {"libnccl.so.2", "libnccl.so"};
+  for (const char* n : names) {
+    g_nccl.h = dlopen(n, RTLD_NOW | RTLD_GLOBAL);
+    if (g_nccl.h) break;
+  }
+  if (!g_nccl.h) { err = std::string("cannot dlopen libnccl.so.2: ") + dlerror(); return false; }
+  g_nccl.GetUniqueId = (int (*)(void*))dlsym(g_nccl.h, "ncclGetUniqueId");
+  g_nccl.CommInitRank = (int (*)(void**, int, Uid, int))dlsym(g_nccl.h, "ncclCommInitRank");
+  g_nccl.AllReduce = (int (*)(const void*, void*, size_t, int, int, void*, cudaStream_t))dlsym(g_nccl.h, "ncclAllReduce");
+  g_nccl.CommDestroy = (int (*)(void*))dlsym(g_nccl.h, "ncclCommDestroy");
+  g_nccl.GetErrorString = (const char* (*)(int))dlsym(g_nccl.h, "ncclGetErrorString");
+  if (!g_nccl.GetUniqueId || !g_nccl.CommInitRank || !g_nccl.AllReduce || !g_nccl.CommDestroy) {
+    err = "libnccl is missing symbols";
+    return false;
+  }
+  g_nccl.loaded = true;
+  return true;
+}
+constexpr int kNcclFloat32 = 7, kNcclFloat64 = 8, kNcclInt64 = 4, kNcclSum = 0;
+
+// ------------------------------------------------------------------ run context
+struct Ctx {
+  const nef::Plan* p;
+  float* const* F;
+  char* ws;
+  size_t ws_bytes;
+  cudaStream_t s;
+};
+
+float* resolve(const Ctx& c, const nef::BufRef& b) {
+  if (b.kind == nef::BUF_FACTOR) return c.F[b.id];
+  if (b.kind == nef::BUF_WS) return reinterpret_cast<float*>(c.ws + b.id);
+  return nullptr;
+}
+
+// run a program; `from`/`to` remap one workspace offset (used to run the epilogue on Q_b)
+int run_prog(const Ctx& c, const nef::EinProgram& pr, int64_t from1 = -1, int64_t to1 = -1, int64_t from2 = -1,
+             int64_t to2 = -1) {
+  auto res = [&](nef::BufRef b) {
+    if (b.kind == nef::BUF_WS) {
+      if (b.id == from1) b.id = to1;
+      else if (b.id == from2) b.id = to2;
+    }
+    return resolve(c, b);
+  };
+  for (const auto& st : pr.steps) {
+    cudaError_t e = nef::launch_einstep(st, res(st.a), st.b.kind == nef::BUF_NONE ? nullptr : res(st.b), res(st.c), c.s);
+    ++g_launches;
+    if (e != cudaSuccess) return fail(NEF_E_CUDA, std::string("einstep: ") + cudaGetErrorString(e));
+  }
+  return NEF_OK;
+}
+
+const float* prog_result(const Ctx& c, const nef::EinProgram& pr) { return resolve(c, pr.result); }
+
+// Fill FusedArgs for lowering L; U and tables must already be computed.
+nef::FusedArgs fused_args(const Ctx& c, const nef::Lowering& L, const float* Y, const uint8_t* M, int mode,
+                          const nef::DivParams& dv, std::vector<int32_t>& boff_host) {
+  nef::FusedArgs a{};
+  a.Y = Y;
+  a.M = M;
+  a.n_rows = L.n_rows;
+  a.n_cols = L.n_cols;
+  a.K = (int)L.K;
+  a.nr = (int)L.row_modes.size();
+  a.nc = (int)L.col_modes.size();
+  for (int k = 0; k < a.nr; ++k) { a.rdim[k] = L.rdim[k]; a.rys[k] = L.rystride[k]; }
+  for (int k = 0; k < a.nc; ++k) { a.cdim[k] = L.cdim[k]; a.cys[k] = L.cystride[k]; }
+  a.U = prog_result(c, L.uprog);
+  a.ntab = (int)L.tabs.size();
+  boff_host.clear();
+  for (int q = 0; q < a.ntab; ++q) {
+    a.tab[q] = prog_result(c, L.tabs[q].prog);
+    for (int k = 0; k < a.nc; ++k) a.tcs[q][k] = L.tabs[q].cstride[k];
+    boff_host.insert(boff_host.end(), L.tabs[q].boff.begin(), L.tabs[q].boff.end());
+  }
+  a.boff = boff_host.data();   // host pointer: copied into kernel parameters at launch
+  a.row_fast = L.row_fast ? 1 : 0;
+  a.n_chunks = L.n_chunks;
+  int64_t tiles = (L.n_cols + 63) / 64;
+  a.tiles_per_chunk = (tiles + L.n_chunks - 1) / L.n_chunks;
+  a.Qpart = reinterpret_cast<float*>(c.ws + L.ws_Qpart);
+  a.losspart = reinterpret_cast<double*>(c.ws + L.ws_losspart);
+  int64_t nparts = ((L.n_rows + 63) / 64) * L.n_chunks;
+  a.countpart = reinterpret_cast<long long*>(c.ws + L.ws_losspart + nparts * 8);
+  a.dv = dv;
+  a.mode = mode;
+  return a;
+}
+
+int side_operands(const Ctx& c, const nef::Lowering& L) {
+  int st = run_prog(c, L.uprog);
+  if (st) return st;
+  for (const auto& t : L.tabs) {
+    st = run_prog(c, t.prog);
+    if (st) return st;
+  }
+  return NEF_OK;
+}
+
+// Loss-only pass with lowering 0 -> slot (double) + count slot (long long)
+int loss_pass(const Ctx& c, const float* Y, const uint8_t* M, const nef::DivParams& dv, double* slot, long long* cslot) {
+  const nef::Lowering& L = c.p->low[0];
+  int st = side_operands(c, L);
+  if (st) return st;
+  std::vector<int32_t> boff;
+  nef::FusedArgs a = fused_args(c, L, Y, M, 2, dv, boff);
+  CK(nef::launch_fused_ffma(a, c.s));
+  ++g_launches;
+  int64_t nparts = ((L.n_rows + 63) / 64) * L.n_chunks;
+  CK(nef::launch_loss_reduce(a.losspart, a.countpart, nparts, slot, cslot, c.s));
+  ++g_launches;
+  return NEF_OK;
+}
+
+// Steps 1-4 of one factor update: leaves A in *num, B in *den (device pointers into ws).
+int num_den(const Ctx& c, int ell, const float* Y, const uint8_t* M, const nef::DivParams& dv, int mode,
+            double* slot, long long* cslot, float** num, float** den) {
+  const nef::Lowering& L = c.p->low[ell];
+  int st = side_operands(c, L);
+  if (st) return st;
+  std::vector<int32_t> boff;
+  nef::FusedArgs a = fused_args(c, L, Y, M, mode, dv, boff);
+  CK(nef::launch_fused_ffma(a, c.s));
+  ++g_launches;
+  if (mode == 1) {
+    int64_t nparts = ((L.n_rows + 63) / 64) * L.n_chunks;
+    CK(nef::launch_loss_reduce(a.losspart, a.countpart, nparts, slot, cslot, c.s));
+    ++g_launches;
+  }
+  const int64_t qe = L.n_rows * L.K;
+  float* Q = reinterpret_cast<float*>(c.ws + L.ws_Q);
+  CK(nef::launch_reduce_q(a.Qpart, Q, L.n_chunks, 2 * qe, c.s));
+  ++g_launches;
+  if (L.epi_identity) {
+    *num = Q;
+    *den = Q + qe;
+    return NEF_OK;
+  }
+  st = run_prog(c, L.epi);                                            // A from Q_a
+  if (st) return st;
+  st = run_prog(c, L.epi, L.ws_Q, L.ws_Q + qe * 4, L.ws_num, L.ws_den);  // B from Q_b
+  if (st) return st;
+  *num = reinterpret_cast<float*>(c.ws + L.ws_num);
+  *den = reinterpret_cast<float*>(c.ws + L.ws_den);
+  return NEF_OK;
+}
+
+int allreduce(const nef::Plan& p, void* buf, size_t count, int dtype, cudaStream_t s) {
+  if (p.world <= 1) return NEF_OK;
+  int r = g_nccl.AllReduce(buf, buf, count, dtype, kNcclSum, p.nccl_comm, s);
+  if (r != 0) return fail(NEF_E_NCCL, std::string("ncclAllReduce: ") + (g_nccl.GetErrorString ? g_nccl.GetErrorString(r) : "?"));
+  return NEF_OK;
+}
+
+int update_one(const Ctx& c, int ell, const float* Y, const uint8_t* M, const nef::DivParams& dv, const nef::UpdArgs& u,
+               int mode, double* slot, long long* cslot) {
+  float *num = nullptr, *den = nullptr;
+  int st = num_den(c, ell, Y, M, dv, mode, slot, cslot, &num, &den);
+  if (st) return st;
+  int64_t n = 1;
+  for (auto d : c.p->fshape[ell]) n *= d;
+  if (c.p->world > 1 && !c.p->factor_has_shard[ell]) {
+    // num and den are adjacent in the workspace (Q_a|Q_b or num|den regions)
+    if (den == num + n) {
+      st = allreduce(*c.p, num, 2 * (size_t)n, kNcclFloat32, c.s);
+    } else {
+      st = allreduce(*c.p, num, (size_t)n, kNcclFloat32, c.s);
+      if (!st) st = allreduce(*c.p, den, (size_t)n, kNcclFloat32, c.s);
+    }
+    if (st) return st;
+  }
+  CK(nef::launch_update(c.F[ell], num, den, n, u, c.s));
+  ++g_launches;
+  return NEF_OK;
+}
+
+int validate_ab(double alpha, double beta) {
+  if (!std::isfinite(alpha) || !std::isfinite(beta)) return fail(NEF_E_DOMAIN, "non-finite alpha/beta");
+  if (alpha == 0.0 && beta != 1.0)
+    return fail(NEF_E_DOMAIN, "alpha = 0 requires beta = 1: no decomposition satisfying eq:prop (P:529)");
+  return NEF_OK;
+}
+
+int validate_common(nef_plan_t plan, const float* Y, float* const* factors, void* ws, size_t ws_bytes) {
+  if (!plan) return fail(NEF_E_ARG, "null plan");
+  if (!Y || (reinterpret_cast<uintptr_t>(Y) & 15)) return fail(NEF_E_ARG, "Y must be a non-null 16-byte aligned device pointer");
+  if (!factors) return fail(NEF_E_ARG, "null factor array");
+  for (size_t l = 0; l < plan->p.ops.size(); ++l)
+    if (!factors[l] || (reinterpret_cast<uintptr_t>(factors[l]) & 3)) return fail(NEF_E_ARG, "null or misaligned factor pointer");
+  if (!ws || ws_bytes < plan->p.ws_bytes)
+    return fail(NEF_E_ARG, "workspace too small: need " + std::to_string(plan->p.ws_bytes) + " bytes");
+  if (reinterpret_cast<uintptr_t>(ws) & 255) return fail(NEF_E_ARG, "workspace must be 256-byte aligned");
+  return NEF_OK;
+}
+
+int check_device() {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return fail(NEF_E_CUDA, std::string("no CUDA device: ") + cudaGetErrorString(e));
+  return NEF_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* nef_last_error(void) { return g_err.c_str(); }
+const char* nef_version(void) { return "nef 0.1 (sm_100a)"; }
+int64_t nef_last_launch_count(void) { return g_launches; }
+int nef_set_kernel_policy(int policy) {
+  if (policy < 0 || policy > 1) return fail(NEF_E_ARG, "policy must be 0 or 1");
+  g_policy = policy;
+  return NEF_OK;
+}
+
+int nef_plan(const char* einsum, int n_modes, const int64_t* shape, int n_ranks, const int64_t* ranks, nef_plan_t* out) {
+  if (!out) return fail(NEF_E_ARG, "null out");
+  *out = nullptr;
+  auto* h = new nef_plan_s();
+  std::string err;
+  int st = nef::build_plan(einsum, n_modes, shape, n_ranks, ranks, h->p, err);
+  if (st) {
+    delete h;
+    return fail(st, err);
+  }
+  *out = h;
+  return NEF_OK;
+}
+
+void nef_plan_destroy(nef_plan_t plan) {
+  if (!plan) return;
+  if (plan->p.nccl_comm && g_nccl.loaded) g_nccl.CommDestroy(plan->p.nccl_comm);
+  delete plan;
+}
+
+int nef_plan_info(nef_plan_t plan, int* n_factors, int* shard_mode, int64_t* local_begin, int64_t* local_len,
+                  size_t* workspace_bytes) {
+  if (!plan) return fail(NEF_E_ARG, "null plan");
+  if (n_factors) *n_factors = (int)plan->p.ops.size();
+  if (shard_mode) *shard_mode = plan->p.shard_mode;
+  if (local_begin) *local_begin = plan->p.local_begin;
+  if (local_len) *local_len = plan->p.local_len;
+  if (workspace_bytes) *workspace_bytes = plan->p.ws_bytes;
+  return NEF_OK;
+}
+
+int nef_factor_shape(nef_plan_t plan, int ell, int64_t* dims, int* ndim) {
+  if (!plan || !dims || !ndim) return fail(NEF_E_ARG, "null argument");
+  if (ell < 0 || ell >= (int)plan->p.ops.size()) return fail(NEF_E_ARG, "ell out of range");
+  const auto& s = plan->p.fshape[ell];
+  *ndim = (int)s.size();
+  for (size_t k = 0; k < s.size(); ++k) dims[k] = s[k];
+  return NEF_OK;
+}
+
+int nef_local_shape(nef_plan_t plan, int64_t* dims, int* ndim) {
+  if (!plan || !dims || !ndim) return fail(NEF_E_ARG, "null argument");
+  *ndim = (int)plan->p.shape.size();
+  for (size_t k = 0; k < plan->p.shape.size(); ++k) dims[k] = plan->p.shape[k];
+  return NEF_OK;
+}
+
+int nef_plan_describe(nef_plan_t plan, char* buf, size_t cap, size_t* len) {
+  if (!plan) return fail(NEF_E_ARG, "null plan");
+  std::string s = nef::describe_plan(plan->p);
+  if (len) *len = s.size() + 1;
+  if (buf && cap) {
+    size_t n = std::min(cap - 1, s.size());
+    std::memcpy(buf, s.data(), n);
+    buf[n] = 0;
+  }
+  return NEF_OK;
+}
+
+int nef_fit(nef_plan_t plan, const float* Y, const uint8_t* mask, double alpha, double beta, double eps,
+            float* const* factors, int iters, double* loss_trace, void* workspace, size_t ws_bytes, void* stream) {
+  int st = validate_common(plan, Y, factors, workspace, ws_bytes);
+  if (st) return st;
+  if ((st = validate_ab(alpha, beta))) return st;
+  if (!(eps > 0.0) || !std::isfinite(eps)) return fail(NEF_E_ARG, "eps must be > 0");
+  if (iters < 0) return fail(NEF_E_ARG, "iters must be >= 0");
+  if (int dst = check_device()) return dst;
+  g_launches = 0;
+  const nef::Plan& p = plan->p;
+  Ctx c{&p, factors, static_cast<char*>(workspace), ws_bytes, static_cast<cudaStream_t>(stream)};
+  nef::DivParams dv = nef::make_div(alpha, beta);
+  nef::UpdArgs u = nef::make_upd(alpha, beta, eps);
+  double* slots = reinterpret_cast<double*>(c.ws + p.ws_trace);
+  long long* cslots = reinterpret_cast<long long*>(c.ws + p.ws_trace + 8 * 2048);
+  const int kSlots = 2048;
+  std::vector<double> host(iters + 1);
+  int base = 0;   // trace index of slot 0
+  auto flush = [&](int upto) -> int {
+    // all-reduce the loss slots [0, upto - base) and copy them to the host
+    int n = upto - base;
+    if (n <= 0) return NEF_OK;
+    if (p.world > 1) {
+      int r = allreduce(p, slots, (size_t)n, kNcclFloat64, c.s);
+      if (r) return r;
+    }
+    CK(cudaMemcpyAsync(host.data() + base, slots, sizeof(double) * n, cudaMemcpyDeviceToHost, c.s));
+    CK(cudaStreamSynchronize(c.s));
+    base = upto;
+    return NEF_OK;
+  };
+  for (int t = 0; t < iters; ++t) {
+    if (t - base >= kSlots) { if ((st = flush(t))) return st; }
+    for (int ell = 0; ell < (int)p.ops.size(); ++ell) {
+      int mode = (ell == 0) ? 1 : 0;
+      st = update_one(c, ell, Y, mask, dv, u, mode, slots + (t - base), cslots + (t - base));
+      if (st) return st;
+    }
+  }
+  if (iters - base >= kSlots) { if ((st = flush(iters))) return st; }
+  st = loss_pass(c, Y, mask, dv, slots + (iters - base), cslots + (iters - base));
+  if (st) return st;
+  if ((st = flush(iters + 1))) return st;
+  if (loss_trace) std::memcpy(loss_trace, host.data(), sizeof(double) * (iters + 1));
+  return NEF_OK;
+}
+
+int nef_update(nef_plan_t plan, int ell, const float* Y, const uint8_t* mask, double alpha, double beta, double eps,
+               float* const* factors, void* workspace, size_t ws_bytes, void* stream) {
+  int st = validate_common(plan, Y, factors, workspace, ws_bytes);
+  if (st) return st;
+  if ((st = validate_ab(alpha, beta))) return st;
+  if (!(eps > 0.0)) return fail(NEF_E_ARG, "eps must be > 0");
+  if (ell < 0 || ell >= (int)plan->p.ops.size()) return fail(NEF_E_ARG, "ell out of range");
+  if (int dst = check_device()) return dst;
+  g_launches = 0;
+  Ctx c{&plan->p, factors, static_cast<char*>(workspace), ws_bytes, static_cast<cudaStream_t>(stream)};
+  return update_one(c, ell, Y, mask, nef::make_div(alpha, beta), nef::make_upd(alpha, beta, eps), 0, nullptr, nullptr);
+}
+
+int nef_num_den(nef_plan_t plan, int ell, const float* Y, const uint8_t* mask, double alpha, double beta,
+                float* const* factors, float* num, float* den, void* workspace, size_t ws_bytes, void* stream) {
+  int st = validate_common(plan, Y, factors, workspace, ws_bytes);
+  if (st) return st;
+  if ((st = validate_ab(alpha, beta))) return st;
+  if (ell < 0 || ell >= (int)plan->p.ops.size()) return fail(NEF_E_ARG, "ell out of range");
+  if (!num || !den) return fail(NEF_E_ARG, "null num/den");
+  if (int dst = check_device()) return dst;
+  g_launches = 0;
+  Ctx c{&plan->p, factors, static_cast<char*>(workspace), ws_bytes, static_cast<cudaStream_t>(stream)};
+  float *n0 = nullptr, *d0 = nullptr;
+  st = num_den(c, ell, Y, mask, nef::make_div(alpha, beta), 0, nullptr, nullptr, &n0, &d0);
+  if (st) return st;
+  int64_t n = 1;
+  for (auto d : plan->p.fshape[ell]) n *= d;
+  CK(cudaMemcpyAsync(num, n0, n * 4, cudaMemcpyDeviceToDevice, c.s));
+  CK(cudaMemcpyAsync(den, d0, n * 4, cudaMemcpyDeviceToDevice, c.s));
+  return NEF_OK;
+}
+
+int nef_apply_update(nef_plan_t plan, int ell, double alpha, double beta, double eps, float* const* factors,
+                     const float* num, const float* den, void* stream) {
+  if (!plan || !factors || !num || !den) return fail(NEF_E_ARG, "null argument");
+  int st = validate_ab(alpha, beta);
+  if (st) return st;
+  if (ell < 0 || ell >= (int)plan->p.ops.size()) return fail(NEF_E_ARG, "ell out of range");
+  if (!(eps > 0.0)) return fail(NEF_E_ARG, "eps must be > 0");
+  int64_t n = 1;
+  for (auto d : plan->p.fshape[ell]) n *= d;
+  if (int dst = check_device()) return dst;
+  g_launches = 0;
+  CK(nef::launch_update(factors[ell], num, den, n, nef::make_upd(alpha, beta, eps), static_cast<cudaStream_t>(stream)));
+  ++g_launches;
+  return NEF_OK;
+}
+
+int nef_loss(nef_plan_t plan, const float* Y, const uint8_t* mask, double alpha, double beta, float* const* factors,
+             double* loss_sum, int64_t* n_observed, void* workspace, size_t ws_bytes, void* stream) {
+  int st = validate_common(plan, Y, factors, workspace, ws_bytes);
+  if (st) return st;
+  if ((st = validate_ab(alpha, beta))) return st;
+  if (int dst = check_device()) return dst;
+  g_launches = 0;
+  const nef::Plan& p = plan->p;
+  Ctx c{&p, factors, static_cast<char*>(workspace), ws_bytes, static_cast<cudaStream_t>(stream)};
+  double* slot = reinterpret_cast<double*>(c.ws + p.ws_trace);
+  long long* cslot = reinterpret_cast<long long*>(c.ws + p.ws_trace + 8 * 2048);
+  st = loss_pass(c, Y, mask, nef::make_div(alpha, beta), slot, cslot);
+  if (st) return st;
+  if (p.world > 1) {
+    if ((st = allreduce(p, slot, 1, kNcclFloat64, c.s))) return st;
+    if ((st = allreduce(p, cslot, 1, kNcclInt64, c.s))) return st;
+  }
+  double h = 0;
+  long long hc = 0;
+  CK(cudaMemcpyAsync(&h, slot, 8, cudaMemcpyDeviceToHost, c.s));
+  CK(cudaMemcpyAsync(&hc, cslot, 8, cudaMemcpyDeviceToHost, c.s));
+  CK(cudaStreamSynchronize(c.s));
+  if (loss_sum) *loss_sum = h;
+  if (n_observed) *n_observed = hc;
+  return NEF_OK;
+}
+
+size_t nef_host_scratch_bytes(nef_plan_t plan, int has_mask) {
+  if (!plan) return 0;
+  const nef::Plan& p = plan->p;
+  auto al = [](size_t b) { return (b + 255) / 256 * 256; };
+  size_t b = al((size_t)p.n_local * 4);
+  if (has_mask) b += al((size_t)p.n_local);
+  for (auto& s : p.fshape) {
+    size_t n = 1;
+    for (auto d : s) n *= (size_t)d;
+    b += al(n * 4);
+  }
+  return b + al(p.ws_bytes);
+}
+
+int nef_fit_host(nef_plan_t plan, const float* Y_host, const uint8_t* mask_host, double alpha, double beta, double eps,
+                 float* const* factors_host, int iters, double* loss_trace, void* device_scratch, size_t scratch_bytes,
+                 void* stream) {
+  if (!plan || !Y_host || !factors_host || !device_scratch) return fail(NEF_E_ARG, "null argument");
+  const nef::Plan& p = plan->p;
+  if (scratch_bytes < nef_host_scratch_bytes(plan, mask_host != nullptr)) return fail(NEF_E_ARG, "device scratch too small");
+  if (reinterpret_cast<uintptr_t>(device_scratch) & 255) return fail(NEF_E_ARG, "device scratch must be 256-byte aligned");
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  auto al = [](size_t b) { return (b + 255) / 256 * 256; };
+  char* d = static_cast<char*>(device_scratch);
+  float* Yd = reinterpret_cast<float*>(d);
+  d += al((size_t)p.n_local * 4);
+  uint8_t* Md = nullptr;
+  if (mask_host) { Md = reinterpret_cast<uint8_t*>(d); d += al((size_t)p.n_local); }
+  std::vector<float*> Fd;
+  std::vector<size_t> fn;
+  for (auto& sh : p.fshape) {
+    size_t n = 1;
+    for (auto x : sh) n *= (size_t)x;
+    Fd.push_back(reinterpret_cast<float*>(d));
+    fn.push_back(n);
+    d += al(n * 4);
+  }
+  CK(cudaMemcpyAsync(Yd, Y_host, (size_t)p.n_local * 4, cudaMemcpyHostToDevice, s));
+  if (Md) CK(cudaMemcpyAsync(Md, mask_host, (size_t)p.n_local, cudaMemcpyHostToDevice, s));
+  for (size_t l = 0; l < Fd.size(); ++l) CK(cudaMemcpyAsync(Fd[l], factors_host[l], fn[l] * 4, cudaMemcpyHostToDevice, s));
+  int st = nef_fit(plan, Yd, Md, alpha, beta, eps, Fd.data(), iters, loss_trace, d, p.ws_bytes, stream);
+  if (st) return st;
+  for (size_t l = 0; l < Fd.size(); ++l) CK(cudaMemcpyAsync(factors_host[l], Fd[l], fn[l] * 4, cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return NEF_OK;
+}
+
+int nef_nccl_unique_id(void* out128) {
+  if (!out128) return fail(NEF_E_ARG, "null out");
+  std::string err;
+  if (!load_nccl(err)) return fail(NEF_E_NCCL, err);
+  int r = g_nccl.GetUniqueId(out128);
+  if (r != 0) return fail(NEF_E_NCCL, "ncclGetUniqueId failed");
+  return NEF_OK;
+}
+
+int nef_plan_shard(nef_plan_t plan, int rank, int world, const void* uid) {
+  if (!plan) return fail(NEF_E_ARG, "null plan");
+  if (world < 1 || rank < 0 || rank >= world) return fail(NEF_E_ARG, "bad rank/world");
+  nef::Plan& p = plan->p;
+  if (p.shard_mode >= 0) return fail(NEF_E_ARG, "plan already sharded");
+  // shard mode: largest (ties -> outermost)
+  int sm = 0;
+  for (int m = 1; m < (int)p.gshape.size(); ++m)
+    if (p.gshape[m] > p.gshape[sm]) sm = m;
+  int64_t n = p.gshape[sm];
+  if (n < world) return fail(NEF_E_SHAPE, "largest mode smaller than world size");
+  int64_t q = n / world, r = n % world;
+  int64_t begin = rank * q + std::min<int64_t>(rank, r);
+  int64_t len = q + (rank < r ? 1 : 0);
+  if (world > 1) {
+    if (!uid) return fail(NEF_E_ARG, "null NCCL unique id");
+    std::string err;
+    if (!load_nccl(err)) return fail(NEF_E_NCCL, err);
+    Uid u;
+    std::memcpy(u.internal, uid, 128);
+    void* comm = nullptr;
+    int rr = g_nccl.CommInitRank(&comm, world, u, rank);
+    if (rr != 0) return fail(NEF_E_NCCL, "ncclCommInitRank failed");
+    p.nccl_comm = comm;
+  }
+  p.shard_mode = sm;
+  p.rank = rank;
+  p.world = world;
+  p.local_begin = begin;
+  p.local_len = len;
+  p.shape = p.gshape;
+  p.shape[sm] = len;
+  char letter = p.out[sm];
+  for (size_t l = 0; l < p.ops.size(); ++l) p.factor_has_shard[l] = p.ops[l].find(letter) != std::string::npos;
+  std::string err;
+  int st = nef::relower(p, err);
+  if (st) return fail(st, err);
+  return NEF_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,71 @@
+// Launch interface of the CUDA kernels (kernels_ffma.cu, kernels_tc.cu).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "nef_internal.h"
+
+namespace nef {
+
+// exponent codes for y^p evaluated in registers ("exponent specialisation")
+enum PowCode : int { POW_0 = 0, POW_1, POW_M1, POW_H, POW_MH, POW_M15, POW_15, POW_2, POW_M2, POW_GEN };
+
+int pow_code(double p);
+
+// Elementwise constants of the (alpha,beta)-divergence
+struct DivParams {
+  float alpha, beta;
+  float p_xa, p_ya, p_yb;       // x^alpha, yhat^(beta-1), yhat^(alpha+beta-1)
+  int c_xa, c_ya, c_yb;         // PowCode of the three exponents
+  int log_case;                 // (alpha, beta) = (0, 1): a = log(x/yhat), b = 1
+  int loss_case;                // 0 generic, 1 beta=0, 2 alpha=-beta, 3 alpha=0, 4 alpha=beta=0, 5 (1,1)
+};
+DivParams make_div(double alpha, double beta);
+
+// Fused streaming pass over Y (and mask) for one lowering.
+struct FusedArgs {
+  const float* Y;
+  const uint8_t* M;            // may be null
+  int64_t n_rows, n_cols;
+  int K;
+  int nr, nc;                   // number of row / col modes
+  int64_t rdim[kMaxModes], rys[kMaxModes];
+  int64_t cdim[kMaxModes], cys[kMaxModes];
+  const float* U;               // [n_rows][K]
+  int ntab;
+  const float* tab[kMaxTabs];
+  int64_t tcs[kMaxTabs][kMaxModes];   // table stride per col mode
+  const int32_t* boff;          // [ntab][K]
+  int row_fast;
+  int64_t n_chunks, tiles_per_chunk;
+  float* Qpart;                 // [n_chunks][2][n_rows][K]
+  double* losspart;             // [row_blocks * n_chunks] loss sums
+  long long* countpart;         // [row_blocks * n_chunks] observed counts
+  DivParams dv;
+  int mode;                     // 0: update only, 1: update + loss, 2: loss only
+};
+
+cudaError_t launch_fused_ffma(const FusedArgs& a, cudaStream_t s);
+
+// Small einsum step (C = sum A*B, optional B), fp64 accumulation
+cudaError_t launch_einstep(const EinStep& st, const float* A, const float* B, float* C, cudaStream_t s);
+
+// Q[2][n_rows][K] = sum over chunks of Qpart (fixed order)
+cudaError_t launch_reduce_q(const float* Qpart, float* Q, int64_t n_chunks, int64_t elems2, cudaStream_t s);
+
+// theta <- max(eps, theta * g^{-1}(num/den)) (eq:explicit-update; g table)
+struct UpdArgs {
+  int g_case;       // 0: power 1/expo ; 1: exp (log case)
+  double inv_expo;  // 1/expo of the power case
+  double eps;
+};
+UpdArgs make_upd(double alpha, double beta, double eps);
+cudaError_t launch_update(float* theta, const float* num, const float* den, int64_t n, UpdArgs u, cudaStream_t s);
+
+// Sum CTA loss partials (fixed order) into slot[0] (double) and count into cslot[0]
+cudaError_t launch_loss_reduce(const double* part, const long long* cpart, int64_t n, double* slot,
+                               long long* cslot, cudaStream_t s);
+
+// Loss sum via the planner's lowering 0 (no update)
+}  // namespace nef

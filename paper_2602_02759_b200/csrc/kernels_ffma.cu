@@ -1,0 +1,521 @@
+// CUDA-core kernels of the MU sweep (sm_100a):
+//   * fused_ffma     : the streamed pass of DESIGN.md §Kernels (K2-FFMA).  For one factor
+//                      update it reads each Y / mask entry of the lowering's 2-D view ONCE,
+//                      rebuilds the Yhat tile S = U V^T in registers (Alg. 1 line 6, P:165;
+//                      never written to memory), forms a = M*Y^alpha*S^(beta-1) and
+//                      b = M*S^(alpha+beta-1) (masking P:321) and contracts them with
+//                      the column operand: Q_a = P_a V, Q_b = P_b V (Alg. 1 lines 7-8,
+//                      P:169-173 via einstr_l).  On the first factor of a sweep it
+//                      also accumulates the (alpha,beta)-divergence of that Yhat.
+//   * einstep        : one pairwise step of the small-einsum engine (side operands, epilogue)
+//   * reduce_q       : deterministic fixed-order sum of split-column partials
+//   * update         : Theta <- max(eps, Theta * g^{-1}(A/B)) (eq:explicit-update, P:121;
+//                      g table; B == 0 -> multiplier 1, reading R10)
+//   * loss_reduce    : fixed-order fp64 sum of per-CTA loss partials
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdint>
+
+#include "kernels.h"
+
+namespace nef {
+
+int pow_code(double p) {
+  if (p == 0.0) return POW_0;
+  if (p == 1.0) return POW_1;
+  if (p == -1.0) return POW_M1;
+  if (p == 0.5) return POW_H;
+  if (p == -0.5) return POW_MH;
+  if (p == -1.5) return POW_M15;
+  if (p == 1.5) return POW_15;
+  if (p == 2.0) return POW_2;
+  if (p == -2.0) return POW_M2;
+  return POW_GEN;
+}
+
+DivParams make_div(double alpha, double beta) {
+  DivParams d{};
+  d.alpha = (float)alpha;
+  d.beta = (float)beta;
+  d.log_case = (alpha == 0.0 && beta == 1.0);
+  d.p_xa = (float)alpha;
+  d.p_ya = (float)(beta - 1.0);
+  d.p_yb = (float)(alpha + beta - 1.0);
+  d.c_xa = pow_code(alpha);
+  d.c_ya = pow_code(beta - 1.0);
+  d.c_yb = pow_code(alpha + beta - 1.0);
+  if (alpha == 1.0 && beta == 1.0) d.loss_case = 5;
+  else if (alpha != 0 && beta != 0 && alpha + beta != 0) d.loss_case = 0;
+  else if (beta == 0 && alpha != 0) d.loss_case = 1;
+  else if (alpha == -beta && alpha != 0) d.loss_case = 2;
+  else if (alpha == 0 && beta != 0) d.loss_case = 3;
+  else d.loss_case = 4;
+  return d;
+}
+
+UpdArgs make_upd(double alpha, double beta, double eps) {
+  // g(lambda) table
+  UpdArgs u{};
+  u.eps = eps;
+  if (alpha == 0.0 && beta == 1.0) { u.g_case = 1; u.inv_expo = 0; return u; }
+  double q = (1.0 - beta) / alpha;
+  double expo;
+  if (q > 1) expo = 1.0 - beta;
+  else if (q < 0) expo = alpha + beta - 1.0;
+  else expo = alpha;
+  u.g_case = 0;
+  u.inv_expo = 1.0 / expo;
+  return u;
+}
+
+// --------------------------------------------------------------------------------------
+// elementwise math
+// --------------------------------------------------------------------------------------
+__device__ __forceinline__ float powc(float y, int code, float p) {
+  switch (code) {
+    case POW_0: return 1.f;
+    case POW_1: return y;
+    case POW_M1: return 1.f / y;
+    case POW_H: return sqrtf(y);
+    case POW_MH: return rsqrtf(y);
+    case POW_M15: { float r = rsqrtf(y); return r * r * r; }
+    case POW_15: return y * sqrtf(y);
+    case POW_2: return y * y;
+    case POW_M2: { float r = 1.f / y; return r * r; }
+    default: return powf(y, p);
+  }
+}
+
+// h_p(u) = (e^{pu} - 1 - pu) / p^2, stable near u = 0 (series for |pu| < 0.3)
+__device__ __forceinline__ float hfun(float p, float u) {
+  float v = p * u;
+  if (fabsf(v) < 0.3f) {
+    float s = 1.f / 5040.f;
+    s = fmaf(s, v, 1.f / 720.f);
+    s = fmaf(s, v, 1.f / 120.f);
+    s = fmaf(s, v, 1.f / 24.f);
+    s = fmaf(s, v, 1.f / 6.f);
+    s = fmaf(s, v, 0.5f);
+    return u * u * s;
+  }
+  return (expm1f(v) - v) / (p * p);
+}
+
+// f(v) = 1 - e^v + v e^v, stable near v = 0
+__device__ __forceinline__ float ffun(float v) {
+  if (fabsf(v) < 0.3f) {
+    float s = 1.f / 840.f;
+    s = fmaf(s, v, 1.f / 144.f);
+    s = fmaf(s, v, 1.f / 30.f);
+    s = fmaf(s, v, 1.f / 8.f);
+    s = fmaf(s, v, 1.f / 3.f);
+    s = fmaf(s, v, 0.5f);
+    return v * v * s;
+  }
+  return v * expf(v) - expm1f(v);
+}
+
+// L_{alpha,beta}(x, y) of P:502-524 in u = log(x/y) form (DESIGN.md §Loss forms); y >= 1e-30
+__device__ __forceinline__ float loss_entry(float x, float y, const DivParams& d) {
+  const float a = d.alpha, b = d.beta;
+  switch (d.loss_case) {
+    case 5: { float r = x - y; return 0.5f * r * r; }
+    case 0: {
+      float yab = powf(y, a + b);
+      if (x <= 0.f) return yab / (a * (a + b));
+      float u = logf(x / y);
+      return yab / b * ((a + b) * hfun(a + b, u) - a * hfun(a, u));
+    }
+    case 1: {
+      float ya = powc(y, d.c_xa, a);
+      if (x <= 0.f) return ya / (a * a);
+      float u = logf(x / y);
+      return ya / (a * a) * ffun(a * u);
+    }
+    case 2: return hfun(a, logf(x / y));
+    case 3: return powf(y, b) * hfun(b, logf(x / y));
+    default: { float u = logf(x / y); return 0.5f * u * u; }
+  }
+}
+
+// --------------------------------------------------------------------------------------
+// fused streaming pass (CUDA cores)
+// --------------------------------------------------------------------------------------
+constexpr int BM = 64, BN = 64, NT = 256, PADR = BM + 4;
+
+template <int KP>
+struct __align__(16) FSmem {
+  float Ut[KP][BM];
+  float Vt[KP][BN];
+  float V[BN][KP];
+  float Pa[BN][PADR];
+  float Pb[BN][PADR];
+  uint8_t Mk[BN][PADR];
+  long long coff[BN];
+  long long roff[BM];
+  int toff[kMaxTabs][BN];
+};
+
+struct FusedDev {
+  FusedArgs a;
+  int32_t boff[kMaxTabs][64];
+};
+
+template <int KP>
+__global__ void __launch_bounds__(NT) fused_ffma_kernel(const __grid_constant__ FusedDev P) {
+  extern __shared__ __align__(16) unsigned char smraw[];
+  FSmem<KP>& sm = *reinterpret_cast<FSmem<KP>*>(smraw);
+  const FusedArgs& a = P.a;
+  constexpr int KQ = KP / 16;
+  const int t = threadIdx.x;
+  const int64_t row0 = (int64_t)blockIdx.x * BM;
+  const int rows_here = (int)(a.n_rows - row0 < BM ? a.n_rows - row0 : BM);
+  const int K = a.K;
+
+  if (t < BM) {
+    long long off = -1;
+    if (t < rows_here) {
+      int64_t rem = row0 + t;
+      off = 0;
+      for (int d = a.nr - 1; d >= 0; --d) {
+        int64_t i = rem % a.rdim[d];
+        rem /= a.rdim[d];
+        off += i * a.rys[d];
+      }
+    }
+    sm.roff[t] = off;
+  }
+  for (int e = t; e < KP * BM; e += NT) {
+    int k = e / BM, r = e % BM;
+    sm.Ut[k][r] = (k < K && r < rows_here) ? a.U[(row0 + r) * K + k] : 0.f;
+  }
+  __syncthreads();
+
+  double qa_d[4][KQ], qb_d[4][KQ];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < KQ; ++j) { qa_d[i][j] = 0.0; qb_d[i][j] = 0.0; }
+  double loss_acc = 0.0;
+  long long cnt = 0;
+  const int rs = (t % 16) * 4;
+  const int cs = (t / 16) * 4;
+  const int kq = (t / 16) * KQ;
+
+  const int64_t total_tiles = (a.n_cols + BN - 1) / BN;
+  const int64_t tb = (int64_t)blockIdx.y * a.tiles_per_chunk;
+  const int64_t te = (tb + a.tiles_per_chunk < total_tiles ? tb + a.tiles_per_chunk : total_tiles);
+  for (int64_t tile = tb; tile < te; ++tile) {
+    const int64_t col0 = tile * BN;
+    const int cols_here = (int)(a.n_cols - col0 < BN ? a.n_cols - col0 : BN);
+    if (t < BN) {
+      long long off = -1;
+      int to[kMaxTabs] = {0, 0, 0, 0};
+      if (t < cols_here) {
+        int64_t rem = col0 + t;
+        off = 0;
+        for (int d = a.nc - 1; d >= 0; --d) {
+          int64_t i = rem % a.cdim[d];
+          rem /= a.cdim[d];
+          off += i * a.cys[d];
+          for (int q = 0; q < a.ntab; ++q) to[q] += (int)(i * a.tcs[q][d]);
+        }
+      }
+      sm.coff[t] = off;
+      for (int q = 0; q < kMaxTabs; ++q) sm.toff[q][t] = to[q];
+    }
+    __syncthreads();
+    // Y / mask tile: each entry read once; a missing entry's value is never loaded
+#pragma unroll 4
+    for (int i = 0; i < BM * BN / NT; ++i) {
+      int e = t + i * NT;
+      int r, c;
+      if (a.row_fast) { r = e % BM; c = e / BM; } else { r = e / BN; c = e % BN; }
+      long long ro = sm.roff[r], co = sm.coff[c];
+      float y = 0.f;
+      uint8_t m = 0;
+      if (ro >= 0 && co >= 0) {
+        long long off = ro + co;
+        m = a.M ? (uint8_t)(__ldg(a.M + off) != 0) : (uint8_t)1;
+        if (m) y = __ldg(a.Y + off);
+      }
+      sm.Pa[c][r] = y;
+      sm.Mk[c][r] = m;
+    }
+    // V tile = prod of column tables (Khatri-Rao / side operands), both layouts
+    for (int e = t; e < BN * KP; e += NT) {
+      int c = e / KP, k = e % KP;
+      float v = 0.f;
+      if (c < cols_here && k < K) {
+        v = 1.f;
+        for (int q = 0; q < a.ntab; ++q) v *= __ldg(a.tab[q] + sm.toff[q][c] + P.boff[q][k]);
+      }
+      sm.V[c][k] = v;
+      sm.Vt[k][c] = v;
+    }
+    __syncthreads();
+    // S = U V^T (reconstruction tile, registers only)
+    float s[4][4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) s[i][j] = 0.f;
+#pragma unroll 8
+    for (int k = 0; k < KP; ++k) {
+      float4 u = *reinterpret_cast<const float4*>(&sm.Ut[k][rs]);
+      float4 v = *reinterpret_cast<const float4*>(&sm.Vt[k][cs]);
+      float uu[4] = {u.x, u.y, u.z, u.w}, vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) s[i][j] = fmaf(uu[i], vv[j], s[i][j]);
+    }
+    // divergence weights a, b (+ loss) in registers
+    float lsum = 0.f;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int c = cs + j;
+      float4 y4 = *reinterpret_cast<const float4*>(&sm.Pa[c][rs]);
+      uint32_t m4 = *reinterpret_cast<const uint32_t*>(&sm.Mk[c][rs]);
+      float yy[4] = {y4.x, y4.y, y4.z, y4.w};
+      float pa[4], pb[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const bool obs = (m4 >> (8 * i)) & 0xffu;
+        const float yh = fmaxf(s[i][j], 1e-30f);       // Yhat floor (reading R4)
+        const float x = yy[i];
+        float av, bv;
+        if (a.dv.log_case) {
+          av = logf(x / yh);
+          bv = 1.f;
+        } else {
+          av = powc(x, a.dv.c_xa, a.dv.p_xa) * powc(yh, a.dv.c_ya, a.dv.p_ya);
+          bv = powc(yh, a.dv.c_yb, a.dv.p_yb);
+        }
+        pa[i] = obs ? av : 0.f;                          // select, never multiply (R5)
+        pb[i] = obs ? bv : 0.f;
+        if (a.mode != 0 && obs) {
+          lsum += loss_entry(x, yh, a.dv);
+          cnt += 1;
+        }
+      }
+      if (a.mode != 2) {
+        *reinterpret_cast<float4*>(&sm.Pa[c][rs]) = make_float4(pa[0], pa[1], pa[2], pa[3]);
+        *reinterpret_cast<float4*>(&sm.Pb[c][rs]) = make_float4(pb[0], pb[1], pb[2], pb[3]);
+      }
+    }
+    loss_acc += (double)lsum;
+    __syncthreads();
+    if (a.mode != 2) {
+      float qa[4][KQ], qb[4][KQ];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < KQ; ++j) { qa[i][j] = 0.f; qb[i][j] = 0.f; }
+#pragma unroll 4
+      for (int c = 0; c < BN; ++c) {
+        float4 p4 = *reinterpret_cast<const float4*>(&sm.Pa[c][rs]);
+        float4 q4 = *reinterpret_cast<const float4*>(&sm.Pb[c][rs]);
+        float pa[4] = {p4.x, p4.y, p4.z, p4.w}, pb[4] = {q4.x, q4.y, q4.z, q4.w};
+        float v[KQ];
+#pragma unroll
+        for (int j = 0; j < KQ; ++j) v[j] = sm.V[c][kq + j];
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+#pragma unroll
+          for (int j = 0; j < KQ; ++j) {
+            qa[i][j] = fmaf(pa[i], v[j], qa[i][j]);
+            qb[i][j] = fmaf(pb[i], v[j], qb[i][j]);
+          }
+      }
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < KQ; ++j) { qa_d[i][j] += (double)qa[i][j]; qb_d[i][j] += (double)qb[i][j]; }
+    }
+    __syncthreads();
+  }
+  if (a.mode != 2) {
+    const int64_t elems = a.n_rows * (int64_t)K;
+    float* qa_out = a.Qpart + (int64_t)blockIdx.y * 2 * elems;
+    float* qb_out = qa_out + elems;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      int r = rs + i;
+      if (r >= rows_here) continue;
+#pragma unroll
+      for (int j = 0; j < KQ; ++j) {
+        int k = kq + j;
+        if (k < K) {
+          qa_out[(row0 + r) * K + k] = (float)qa_d[i][j];
+          qb_out[(row0 + r) * K + k] = (float)qb_d[i][j];
+        }
+      }
+    }
+  }
+  if (a.mode != 0) {
+    // fixed-order block reduction of the loss (deterministic)
+    __shared__ double red[NT];
+    __shared__ long long redc[NT];
+    red[t] = loss_acc;
+    redc[t] = cnt;
+    __syncthreads();
+    for (int w = NT / 2; w > 0; w >>= 1) {
+      if (t < w) { red[t] += red[t + w]; redc[t] += redc[t + w]; }
+      __syncthreads();
+    }
+    if (t == 0) {
+      int64_t id = (int64_t)blockIdx.y * gridDim.x + blockIdx.x;
+      a.losspart[id] = red[0];
+      a.countpart[id] = redc[0];
+    }
+  }
+}
+
+template <int KP>
+static cudaError_t launch_kp(const FusedDev& d, cudaStream_t s) {
+  size_t smem = sizeof(FSmem<KP>);
+  cudaError_t e = cudaFuncSetAttribute(fused_ffma_kernel<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int64_t row_blocks = (d.a.n_rows + BM - 1) / BM;
+  dim3 grid((unsigned)row_blocks, (unsigned)d.a.n_chunks);
+  fused_ffma_kernel<KP><<<grid, NT, smem, s>>>(d);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fused_ffma(const FusedArgs& a, cudaStream_t s) {
+  FusedDev d;
+  d.a = a;
+  for (int q = 0; q < kMaxTabs; ++q)
+    for (int k = 0; k < 64; ++k) d.boff[q][k] = 0;
+  for (int q = 0; q < a.ntab; ++q)
+    for (int k = 0; k < a.K && k < 64; ++k) d.boff[q][k] = a.boff[q * a.K + k];
+  if (a.K <= 16) return launch_kp<16>(d, s);
+  if (a.K <= 32) return launch_kp<32>(d, s);
+  if (a.K <= 64) return launch_kp<64>(d, s);
+  return cudaErrorInvalidValue;
+}
+
+// --------------------------------------------------------------------------------------
+// small einsum step
+// --------------------------------------------------------------------------------------
+struct EinStepDev {
+  int nout, nsum;
+  long long odim[kMaxDims], as_o[kMaxDims], bs_o[kMaxDims];
+  long long sdim[kMaxDims], as_s[kMaxDims], bs_s[kMaxDims];
+  long long out_size, sum_size;
+};
+
+__global__ void einstep_kernel(const __grid_constant__ EinStepDev st, const float* __restrict__ A,
+                               const float* __restrict__ B, float* __restrict__ C) {
+  for (long long o = (long long)blockIdx.x * blockDim.x + threadIdx.x; o < st.out_size;
+       o += (long long)gridDim.x * blockDim.x) {
+    long long rem = o, ao = 0, bo = 0;
+    for (int d = st.nout - 1; d >= 0; --d) {
+      long long i = rem % st.odim[d];
+      rem /= st.odim[d];
+      ao += i * st.as_o[d];
+      bo += i * st.bs_o[d];
+    }
+    long long sidx[kMaxDims];
+    for (int d = 0; d < kMaxDims; ++d) sidx[d] = 0;
+    double acc = 0.0;
+    for (long long s = 0; s < st.sum_size; ++s) {
+      double v = (double)A[ao];
+      if (B) v *= (double)B[bo];
+      acc += v;
+      for (int d = st.nsum - 1; d >= 0; --d) {
+        ao += st.as_s[d];
+        bo += st.bs_s[d];
+        if (++sidx[d] < st.sdim[d]) break;
+        ao -= st.as_s[d] * st.sdim[d];
+        bo -= st.bs_s[d] * st.sdim[d];
+        sidx[d] = 0;
+      }
+    }
+    C[o] = (float)acc;
+  }
+}
+
+cudaError_t launch_einstep(const EinStep& st, const float* A, const float* B, float* C, cudaStream_t s) {
+  EinStepDev d{};
+  d.nout = st.nout;
+  d.nsum = st.nsum;
+  for (int k = 0; k < kMaxDims; ++k) {
+    d.odim[k] = st.odim[k]; d.as_o[k] = st.as_o[k]; d.bs_o[k] = st.bs_o[k];
+    d.sdim[k] = st.sdim[k]; d.as_s[k] = st.as_s[k]; d.bs_s[k] = st.bs_s[k];
+  }
+  d.out_size = st.out_size;
+  d.sum_size = st.sum_size;
+  long long blocks = (st.out_size + 255) / 256;
+  if (blocks > 148 * 32) blocks = 148 * 32;
+  if (blocks < 1) blocks = 1;
+  einstep_kernel<<<(unsigned)blocks, 256, 0, s>>>(d, A, B, C);
+  return cudaGetLastError();
+}
+
+// --------------------------------------------------------------------------------------
+__global__ void reduce_q_kernel(const float* __restrict__ part, float* __restrict__ Q, long long n_chunks,
+                                long long elems) {
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < elems; e += (long long)gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (long long c = 0; c < n_chunks; ++c) acc += (double)part[c * elems + e];
+    Q[e] = (float)acc;
+  }
+}
+
+cudaError_t launch_reduce_q(const float* Qpart, float* Q, int64_t n_chunks, int64_t elems2, cudaStream_t s) {
+  long long blocks = (elems2 + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  reduce_q_kernel<<<(unsigned)(blocks < 1 ? 1 : blocks), 256, 0, s>>>(Qpart, Q, n_chunks, elems2);
+  return cudaGetLastError();
+}
+
+__global__ void update_kernel(float* __restrict__ th, const float* __restrict__ num, const float* __restrict__ den,
+                              long long n, UpdArgs u) {
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
+    double A = num[e], B = den[e];
+    double mult = 1.0;
+    if (B > 0.0) {
+      double r = A / B;
+      if (u.g_case == 1) mult = exp(r);
+      else if (u.inv_expo == 1.0) mult = r;
+      else mult = pow(r, u.inv_expo);
+    }
+    double v = (double)th[e] * mult;
+    th[e] = (float)fmax(u.eps, v);
+  }
+}
+
+cudaError_t launch_update(float* theta, const float* num, const float* den, int64_t n, UpdArgs u, cudaStream_t s) {
+  long long blocks = (n + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  update_kernel<<<(unsigned)(blocks < 1 ? 1 : blocks), 256, 0, s>>>(theta, num, den, n, u);
+  return cudaGetLastError();
+}
+
+__global__ void loss_reduce_kernel(const double* __restrict__ part, const long long* __restrict__ cpart, long long n,
+                                   double* slot, long long* cslot) {
+  __shared__ double red[256];
+  __shared__ long long redc[256];
+  double acc = 0.0;
+  long long c = 0;
+  for (long long i = threadIdx.x; i < n; i += 256) { acc += part[i]; c += cpart[i]; }
+  red[threadIdx.x] = acc;
+  redc[threadIdx.x] = c;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if ((int)threadIdx.x < w) { red[threadIdx.x] += red[threadIdx.x + w]; redc[threadIdx.x] += redc[threadIdx.x + w]; }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) { *slot = red[0]; *cslot = redc[0]; }
+}
+
+cudaError_t launch_loss_reduce(const double* part, const long long* cpart, int64_t n, double* slot, long long* cslot,
+                               cudaStream_t s) {
+  loss_reduce_kernel<<<1, 256, 0, s>>>(part, cpart, n, slot, cslot);
+  return cudaGetLastError();
+}
+
+}  // namespace nef

@@ -1,0 +1,112 @@
+// Internal structures shared by the planner (host C++) and the kernels (CUDA).
+// See DESIGN.md §Planner for the lowering these describe.
+#pragma once
+
+#include <cstddef>
+#include <cstdint>
+#include <string>
+#include <vector>
+
+namespace nef {
+
+constexpr int kMaxDims = 8;      // max indices per operand / per einsum step side
+constexpr int kMaxTabs = 4;      // max KR tables on the column side of a lowering
+constexpr int kMaxModes = 8;     // max observed modes
+
+// ---------------------------------------------------------------------------------
+// Small einsum engine: C[out] = sum_{sum} A[...] * B[...]   (B optional)
+// Buffers are referred to by id; ids < 0x100 are factors, others workspace regions.
+// ---------------------------------------------------------------------------------
+enum BufKind : int { BUF_FACTOR = 0, BUF_WS = 1, BUF_NONE = 2 };
+
+struct BufRef {
+  int kind = BUF_NONE;   // BufKind
+  int64_t id = -1;       // factor index, or byte offset in the workspace
+  int64_t elems = 0;
+};
+
+struct EinStep {
+  BufRef a, b, c;                    // b.kind == BUF_NONE -> unary
+  std::string a_idx, b_idx, c_idx;   // index strings (for description / debug executor)
+  int nout = 0;
+  int64_t odim[kMaxDims] = {};
+  int64_t as_o[kMaxDims] = {}, bs_o[kMaxDims] = {};
+  int nsum = 0;
+  int64_t sdim[kMaxDims] = {};
+  int64_t as_s[kMaxDims] = {}, bs_s[kMaxDims] = {};
+  int64_t out_size = 1, sum_size = 1;
+};
+
+struct EinProgram {
+  std::vector<EinStep> steps;     // executed in order; last step writes the result
+  BufRef result;                  // where the result lives (may alias an input when steps empty)
+  std::string result_idx;
+  double macs = 0;                // cost estimate
+};
+
+// ---------------------------------------------------------------------------------
+// Lowering of one factor update
+//   Yhat[row, col] = sum_b U[row, b] * V[col, b],  V[col, b] = prod_t T_t[col_t, b_t]
+//   Q_a[row, b] = sum_col a(Y, Yhat)[row, col] V[col, b]   (and Q_b with b(Y, Yhat))
+//   Num_ell = epilogue(Q_a, row-side factors except ell)    (= einsum(swap(rowmodel, ell)))
+// ---------------------------------------------------------------------------------
+struct ColTable {
+  EinProgram prog;          // computes the table; result index order = (its col modes, its bond idx)
+  std::string idx;          // table index string
+  int64_t cstride[kMaxModes] = {};   // stride per column mode (0 if the table lacks it)
+  std::vector<int32_t> boff;         // offset per linear bond index b in [0, K)
+};
+
+struct Lowering {
+  int ell = -1;
+  std::vector<int> row_modes, col_modes;   // Y modes (positions in the output string), Y order
+  std::string row_idx, col_idx;            // letters of those modes
+  std::string bond;                        // bond index letters (order = linear bond index, last fastest)
+  int64_t K = 1;                           // bond size
+  int64_t n_rows = 1, n_cols = 1;
+  int64_t rdim[kMaxModes] = {}, rystride[kMaxModes] = {};   // row unravel dims / Y strides
+  int64_t cdim[kMaxModes] = {}, cystride[kMaxModes] = {};   // col unravel dims / Y strides
+  bool row_fast = false;                   // innermost Y mode lies on the row side
+  EinProgram uprog;                        // U[row, bond] (result idx = row_idx + bond)
+  std::vector<ColTable> tabs;              // column tables
+  EinProgram epi;                          // Num (factor ell's layout) from Q (+ row factors)
+  bool epi_identity = false;
+  std::vector<int> row_factors, col_factors;
+  // workspace layout (byte offsets)
+  int64_t ws_U = 0, ws_boff = 0, ws_Qpart = 0, ws_Q = 0, ws_num = 0, ws_den = 0, ws_tmp = 0;
+  int64_t ws_losspart = 0;
+  int64_t n_chunks = 1;                    // split of the column range (deterministic partials)
+  int64_t ws_end = 0;
+  double cost = 0;
+  // tcgen05 eligibility (filled by the planner)
+  bool tc_ok = false;
+};
+
+struct Plan {
+  std::string model;                 // normalized string
+  std::vector<std::string> ops;      // operand subscripts
+  std::string out;                   // output subscripts
+  std::vector<int64_t> gshape;       // global Y shape
+  std::vector<int64_t> shape;        // local Y shape
+  int64_t dims[128] = {};            // size per ASCII letter
+  std::vector<std::vector<int64_t>> fshape;   // local factor shapes
+  std::vector<std::string> einstr;   // swap(model, ell)
+  std::vector<Lowering> low;         // per factor
+  int64_t n_local = 0;               // local entries
+  size_t ws_bytes = 0;
+  int64_t ws_trace = 0;              // fp64 trace accumulators
+  // sharding
+  int shard_mode = -1, rank = 0, world = 1;
+  int64_t local_begin = 0, local_len = 0;
+  void* nccl_comm = nullptr;
+  std::vector<bool> factor_has_shard;
+  int num_sms = 148;
+};
+
+// planner entry points (plan.cpp)
+int build_plan(const char* einsum, int n_modes, const int64_t* shape, int n_ranks, const int64_t* ranks,
+               Plan& p, std::string& err);
+int relower(Plan& p, std::string& err);           // recompute lowerings after sharding
+std::string describe_plan(const Plan& p);
+
+}  // namespace nef

@@ -1,0 +1,562 @@
+// Host-side planner: parse the einsum model string, build einstr_l = swap(model, l), and
+// lower each factor update to the streamed (row, col, bond) form of DESIGN.md §Planner.
+//
+// Paper: model family eq:contraction_structure / eq:einsum; einstr_l and swap
+// (P:140-149); Algorithm 1 lines 1-3.  Everything here is host metadata.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <set>
+#include <sstream>
+
+#include "nef_internal.h"
+#include "../../include/nef.h"
+
+namespace nef {
+
+namespace {
+
+bool is_letter(char c) { return (c >= 'a' && c <= 'z') || (c >= 'A' && c <= 'Z'); }
+
+int parse_model(const char* s, std::vector<std::string>& ops, std::string& out, std::string& err) {
+  if (!s) { err = "null einsum string"; return NEF_E_ARG; }
+  std::string t;
+  for (const char* p = s; *p; ++p)
+    if (*p != ' ' && *p != '\t' && *p != '\n') t.push_back(*p);
+  size_t arrow = t.find("->");
+  if (arrow == std::string::npos || t.find("->", arrow + 1) != std::string::npos) {
+    err = "missing or repeated '->'";
+    return NEF_E_PARSE;
+  }
+  std::string lhs = t.substr(0, arrow);
+  out = t.substr(arrow + 2);
+  ops.clear();
+  std::string cur;
+  for (size_t i = 0; i <= lhs.size(); ++i) {
+    if (i == lhs.size() || lhs[i] == ',') {
+      if (cur.empty()) { err = "empty operand"; return NEF_E_PARSE; }
+      ops.push_back(cur);
+      cur.clear();
+    } else {
+      cur.push_back(lhs[i]);
+    }
+  }
+  for (auto& op : ops) {
+    for (char c : op)
+      if (!is_letter(c)) { err = std::string("illegal character '") + c + "' in operand " + op; return NEF_E_PARSE; }
+    std::set<char> seen(op.begin(), op.end());
+    if (seen.size() != op.size()) { err = "repeated index in operand " + op; return NEF_E_PARSE; }
+  }
+  if (out.empty()) { err = "empty output"; return NEF_E_PARSE; }
+  for (char c : out)
+    if (!is_letter(c)) { err = std::string("illegal character '") + c + "' in output"; return NEF_E_PARSE; }
+  if (std::set<char>(out.begin(), out.end()).size() != out.size()) { err = "repeated output index"; return NEF_E_PARSE; }
+  for (char c : out) {
+    bool found = false;
+    for (auto& op : ops) found |= op.find(c) != std::string::npos;
+    if (!found) { err = std::string("output index '") + c + "' absent from operands"; return NEF_E_PARSE; }
+  }
+  if ((int)out.size() > kMaxModes) { err = "too many observed modes"; return NEF_E_UNSUPPORTED; }
+  for (auto& op : ops)
+    if ((int)op.size() > kMaxDims) { err = "operand with too many indices"; return NEF_E_UNSUPPORTED; }
+  return NEF_OK;
+}
+
+bool mul_overflow(int64_t a, int64_t b, int64_t* r) { return __builtin_mul_overflow(a, b, r); }
+
+int64_t prod_idx(const Plan& p, const std::string& idx) {
+  int64_t n = 1;
+  for (char c : idx) n *= p.dims[(int)c];
+  return n;
+}
+
+// row-major strides of a tensor with index string `idx`
+int64_t stride_of(const Plan& p, const std::string& idx, char c) {
+  size_t pos = idx.find(c);
+  if (pos == std::string::npos) return 0;
+  int64_t s = 1;
+  for (size_t k = pos + 1; k < idx.size(); ++k) s *= p.dims[(int)idx[k]];
+  return s;
+}
+
+struct Operand {
+  BufRef buf;
+  std::string idx;
+};
+
+// bump allocator over the workspace (bytes, 256-aligned)
+struct Bump {
+  int64_t off = 0;
+  int64_t take(int64_t bytes) {
+    int64_t o = (off + 255) / 256 * 256;
+    off = o + std::max<int64_t>(bytes, 0);
+    return o;
+  }
+};
+
+EinStep make_step(const Plan& p, const Operand& A, const Operand* B, const std::string& cidx, BufRef c) {
+  EinStep st;
+  st.a = A.buf;
+  st.a_idx = A.idx;
+  if (B) { st.b = B->buf; st.b_idx = B->idx; }
+  st.c = c;
+  st.c_idx = cidx;
+  st.nout = (int)cidx.size();
+  for (int d = 0; d < st.nout; ++d) {
+    char ch = cidx[d];
+    st.odim[d] = p.dims[(int)ch];
+    st.as_o[d] = stride_of(p, A.idx, ch);
+    st.bs_o[d] = B ? stride_of(p, B->idx, ch) : 0;
+    st.out_size *= st.odim[d];
+  }
+  std::string all = A.idx + (B ? B->idx : std::string());
+  std::string sum;
+  for (char ch : all)
+    if (cidx.find(ch) == std::string::npos && sum.find(ch) == std::string::npos) sum.push_back(ch);
+  st.nsum = (int)sum.size();
+  for (int d = 0; d < st.nsum; ++d) {
+    char ch = sum[d];
+    st.sdim[d] = p.dims[(int)ch];
+    st.as_s[d] = stride_of(p, A.idx, ch);
+    st.bs_s[d] = B ? stride_of(p, B->idx, ch) : 0;
+    st.sum_size *= st.sdim[d];
+  }
+  return st;
+}
+
+// order letters of `set` : first those of `pref` in pref order, then the rest in `base` order
+std::string order_letters(const std::string& set, const std::string& pref, const std::string& base) {
+  std::string r;
+  for (char c : pref)
+    if (set.find(c) != std::string::npos && r.find(c) == std::string::npos) r.push_back(c);
+  for (char c : base)
+    if (set.find(c) != std::string::npos && r.find(c) == std::string::npos) r.push_back(c);
+  for (char c : set)
+    if (r.find(c) == std::string::npos) r.push_back(c);
+  return r;
+}
+
+// Greedy pairwise contraction of `ins` into `out_idx`.  If `target` is given the result is
+// written there; otherwise a pure alias of a single matching input is allowed.
+EinProgram compile_einsum(const Plan& p, std::vector<Operand> ins, const std::string& out_idx, Bump& bump,
+                          const BufRef* target) {
+  EinProgram prog;
+  prog.result_idx = out_idx;
+  std::string base = p.model;
+  while (ins.size() > 1) {
+    int bi = -1, bj = -1;
+    double best = 1e300, best_macs = 1e300;
+    std::string best_keep;
+    for (size_t i = 0; i < ins.size(); ++i)
+      for (size_t j = i + 1; j < ins.size(); ++j) {
+        std::string needed = out_idx;
+        for (size_t k = 0; k < ins.size(); ++k)
+          if (k != i && k != j) needed += ins[k].idx;
+        std::string uni = ins[i].idx;
+        for (char c : ins[j].idx)
+          if (uni.find(c) == std::string::npos) uni.push_back(c);
+        std::string keep;
+        for (char c : uni)
+          if (needed.find(c) != std::string::npos) keep.push_back(c);
+        double sz = (double)prod_idx(p, keep);
+        double macs = (double)prod_idx(p, uni);
+        if (sz < best || (sz == best && macs < best_macs)) {
+          best = sz;
+          best_macs = macs;
+          bi = (int)i;
+          bj = (int)j;
+          best_keep = keep;
+        }
+      }
+    std::string cidx = order_letters(best_keep, out_idx, base);
+    BufRef c;
+    c.kind = BUF_WS;
+    c.elems = prod_idx(p, cidx);
+    c.id = bump.take(c.elems * 4);
+    EinStep st = make_step(p, ins[bi], &ins[bj], cidx, c);
+    prog.macs += (double)st.out_size * (double)st.sum_size;
+    prog.steps.push_back(st);
+    Operand r{c, cidx};
+    ins.erase(ins.begin() + bj);
+    ins.erase(ins.begin() + bi);
+    ins.push_back(r);
+  }
+  Operand& last = ins[0];
+  if (last.idx == out_idx) {
+    if (!target) {
+      prog.result = last.buf;
+      return prog;
+    }
+    if (!prog.steps.empty() && prog.steps.back().c.id == last.buf.id && last.buf.kind == BUF_WS) {
+      prog.steps.back().c = *target;   // write the final pairwise step straight into the target
+      prog.result = *target;
+      return prog;
+    }
+  }
+  BufRef c;
+  if (target) {
+    c = *target;
+  } else {
+    c.kind = BUF_WS;
+    c.elems = prod_idx(p, out_idx);
+    c.id = bump.take(c.elems * 4);
+  }
+  EinStep st = make_step(p, last, nullptr, out_idx, c);
+  prog.macs += (double)st.out_size * (double)st.sum_size;
+  prog.steps.push_back(st);
+  prog.result = c;
+  return prog;
+}
+
+BufRef factor_buf(const Plan& p, int l) {
+  BufRef b;
+  b.kind = BUF_FACTOR;
+  b.id = l;
+  b.elems = prod_idx(p, p.ops[l]);
+  return b;
+}
+
+// Try one lowering candidate; returns false if invalid.
+bool lower_candidate(const Plan& p, int ell, unsigned rowmask, unsigned pure_assign, Lowering& L, std::string& why) {
+  const int M = (int)p.out.size();
+  const int Lf = (int)p.ops.size();
+  L = Lowering();
+  L.ell = ell;
+  std::vector<int> side(Lf, -1);   // 0 row, 1 col
+  int pure_k = 0;
+  for (int f = 0; f < Lf; ++f) {
+    bool any_row = false, any_col = false;
+    for (char c : p.ops[f]) {
+      size_t m = p.out.find(c);
+      if (m == std::string::npos) continue;
+      if (rowmask >> m & 1u) any_row = true; else any_col = true;
+    }
+    if (any_row && any_col) { why = "straddle"; return false; }
+    if (any_row) side[f] = 0;
+    else if (any_col) side[f] = 1;
+    else side[f] = (pure_assign >> pure_k++) & 1u;
+  }
+  if (side[ell] != 0) { why = "ell not on row side"; return false; }
+  for (int m = 0; m < M; ++m) {
+    if (rowmask >> m & 1u) { L.row_modes.push_back(m); L.row_idx.push_back(p.out[m]); }
+    else { L.col_modes.push_back(m); L.col_idx.push_back(p.out[m]); }
+  }
+  for (int f = 0; f < Lf; ++f) (side[f] == 0 ? L.row_factors : L.col_factors).push_back(f);
+  // bond: contracted letters present on both sides, in first-appearance order
+  std::string rowl, coll;
+  for (int f : L.row_factors) rowl += p.ops[f];
+  for (int f : L.col_factors) coll += p.ops[f];
+  for (char c : p.model) {
+    if (!is_letter(c) || p.out.find(c) != std::string::npos) continue;
+    if (rowl.find(c) != std::string::npos && coll.find(c) != std::string::npos && L.bond.find(c) == std::string::npos)
+      L.bond.push_back(c);
+  }
+  L.K = prod_idx(p, L.bond);
+  L.n_rows = prod_idx(p, L.row_idx);
+  L.n_cols = prod_idx(p, L.col_idx);
+  // Y strides of every mode (local shape)
+  std::vector<int64_t> ys(M, 1);
+  for (int m = M - 2; m >= 0; --m) ys[m] = ys[m + 1] * p.shape[m + 1];
+  for (size_t k = 0; k < L.row_modes.size(); ++k) {
+    L.rdim[k] = p.shape[L.row_modes[k]];
+    L.rystride[k] = ys[L.row_modes[k]];
+  }
+  for (size_t k = 0; k < L.col_modes.size(); ++k) {
+    L.cdim[k] = p.shape[L.col_modes[k]];
+    L.cystride[k] = ys[L.col_modes[k]];
+  }
+  L.row_fast = (rowmask >> (M - 1)) & 1u;
+  return true;
+}
+
+// Fill programs, tables and workspace of a chosen candidate.
+void finish_lowering(const Plan& p, Lowering& L, Bump& bump) {
+  // U[row, bond] from the row-side factors
+  std::vector<Operand> rin;
+  for (int f : L.row_factors) rin.push_back({factor_buf(p, f), p.ops[f]});
+  std::string uidx = L.row_idx + L.bond;
+  L.uprog = compile_einsum(p, rin, uidx, bump, nullptr);
+  // column tables: connected components of col factors via non-bond contracted letters
+  std::vector<int> comp(L.col_factors.size(), -1);
+  int ncomp = 0;
+  for (size_t i = 0; i < L.col_factors.size(); ++i) {
+    if (comp[i] >= 0) continue;
+    comp[i] = ncomp;
+    bool grew = true;
+    while (grew) {
+      grew = false;
+      for (size_t a = 0; a < L.col_factors.size(); ++a) {
+        if (comp[a] != ncomp) continue;
+        for (size_t b = 0; b < L.col_factors.size(); ++b) {
+          if (comp[b] >= 0) continue;
+          for (char c : p.ops[L.col_factors[a]]) {
+            if (p.out.find(c) != std::string::npos || L.bond.find(c) != std::string::npos) continue;
+            if (p.ops[L.col_factors[b]].find(c) != std::string::npos) { comp[b] = ncomp; grew = true; break; }
+          }
+        }
+      }
+    }
+    ++ncomp;
+  }
+  for (int cidx = 0; cidx < ncomp; ++cidx) {
+    std::vector<Operand> cin;
+    std::string letters;
+    for (size_t i = 0; i < L.col_factors.size(); ++i)
+      if (comp[i] == cidx) {
+        cin.push_back({factor_buf(p, L.col_factors[i]), p.ops[L.col_factors[i]]});
+        letters += p.ops[L.col_factors[i]];
+      }
+    std::string tidx;
+    for (char c : L.col_idx)
+      if (letters.find(c) != std::string::npos) tidx.push_back(c);
+    for (char c : L.bond)
+      if (letters.find(c) != std::string::npos) tidx.push_back(c);
+    ColTable T;
+    T.idx = tidx;
+    T.prog = compile_einsum(p, cin, tidx, bump, nullptr);
+    for (size_t k = 0; k < L.col_modes.size(); ++k) T.cstride[k] = stride_of(p, tidx, p.out[L.col_modes[k]]);
+    T.boff.assign((size_t)L.K, 0);
+    for (int64_t b = 0; b < L.K; ++b) {
+      int64_t rem = b, off = 0;
+      for (int d = (int)L.bond.size() - 1; d >= 0; --d) {
+        int64_t n = p.dims[(int)L.bond[d]];
+        off += (rem % n) * stride_of(p, tidx, L.bond[d]);
+        rem /= n;
+      }
+      T.boff[(size_t)b] = (int32_t)off;
+    }
+    L.tabs.push_back(T);
+  }
+  // workspace for the streaming pass
+  const int64_t BM = 64, BN = 64;
+  int64_t row_blocks = (L.n_rows + BM - 1) / BM;
+  int64_t col_tiles = (L.n_cols + BN - 1) / BN;
+  int64_t target = (int64_t)p.num_sms * 4;
+  int64_t chunks = std::max<int64_t>(1, (target + row_blocks - 1) / row_blocks);
+  chunks = std::min(chunks, col_tiles);
+  int64_t qelems = L.n_rows * L.K;
+  while (chunks > 1 && chunks * qelems * 8 > (int64_t)512 << 20) chunks /= 2;
+  L.n_chunks = chunks;
+  L.ws_boff = bump.take((int64_t)L.tabs.size() * L.K * 4);
+  L.ws_Qpart = bump.take(chunks * qelems * 2 * 4);
+  L.ws_Q = bump.take(qelems * 2 * 4);
+  int64_t felems = prod_idx(p, p.ops[L.ell]);
+  L.ws_num = bump.take(2 * felems * 4);   // num | den adjacent (one all-reduce)
+  L.ws_den = L.ws_num + felems * 4;
+  L.ws_losspart = bump.take(row_blocks * chunks * 16);
+  // epilogue: Num (ell's layout) = einsum(Q[row_idx + bond], row factors except ell)
+  std::string qidx = uidx;
+  if (L.row_factors.size() == 1 && p.ops[L.ell] == qidx) {
+    L.epi_identity = true;
+  } else {
+    BufRef qa;
+    qa.kind = BUF_WS;
+    qa.id = L.ws_Q;
+    qa.elems = qelems;
+    std::vector<Operand> ein;
+    ein.push_back({qa, qidx});
+    for (int f : L.row_factors)
+      if (f != L.ell) ein.push_back({factor_buf(p, f), p.ops[f]});
+    BufRef tgt;
+    tgt.kind = BUF_WS;
+    tgt.id = L.ws_num;
+    tgt.elems = felems;
+    L.epi = compile_einsum(p, ein, p.ops[L.ell], bump, &tgt);
+  }
+  L.ws_end = bump.off;
+  L.tc_ok = false;
+}
+
+// Cost in MAC-equivalents: streamed MACs + column-operand generation + 8 x bytes moved
+// through HBM by the side operands, split partials, reduction and tables.
+double candidate_cost(const Plan& p, const Lowering& L) {
+  double N = (double)p.n_local;
+  double kp = (double)std::max<int64_t>(16, (L.K + 15) / 16 * 16);
+  double fused = N * 3.0 * kp;
+  double vgen = N / 64.0 * (double)L.K * (double)std::max<size_t>(1, L.tabs.size());
+  double q = (double)L.n_rows * (double)L.K;
+  double bytes = q * 4.0 * 2.0                              // U written + read
+                 + (double)L.n_chunks * q * 8.0 * 2.0       // Q partials written + read
+                 + q * 8.0 * 2.0;                           // Q written + read by the epilogue
+  for (auto& t : L.tabs) bytes += 8.0 * (double)t.prog.result.elems;
+  return fused + vgen + 8.0 * bytes;
+}
+
+}  // namespace
+
+int lower_all(Plan& p, std::string& err) {
+  const int M = (int)p.out.size();
+  const int Lf = (int)p.ops.size();
+  int npure = 0;
+  for (auto& op : p.ops) {
+    bool anyobs = false;
+    for (char c : op) anyobs |= p.out.find(c) != std::string::npos;
+    if (!anyobs) ++npure;
+  }
+  if (npure > 6) { err = "too many purely-contracted factors"; return NEF_E_UNSUPPORTED; }
+  p.low.assign(Lf, Lowering());
+  int64_t ws = 0;
+  for (int ell = 0; ell < Lf; ++ell) {
+    Lowering best;
+    double best_cost = 1e300;
+    bool found = false;
+    unsigned best_rm = 0, best_pa = 0;
+    for (unsigned rm = 1; rm < (1u << M); ++rm) {
+      for (unsigned pa = 0; pa < (1u << npure); ++pa) {
+        Lowering cand;
+        std::string why;
+        if (!lower_candidate(p, ell, rm, pa, cand, why)) continue;
+        if (cand.K > 128) continue;                       // FFMA kernel bound on the bond
+        Bump tmp;
+        finish_lowering(p, cand, tmp);
+        double c = candidate_cost(p, cand) + cand.uprog.macs + cand.epi.macs;
+        for (auto& t : cand.tabs) c += t.prog.macs;
+        if (cand.n_rows * cand.K > ((int64_t)1 << 28)) c += 1e18;  // U must stay small
+        if (rm == (1u << M) - 1) c += 1e17;                        // no columns: last resort
+        if (c < best_cost) { best_cost = c; best = cand; found = true; best_rm = rm; best_pa = pa; }
+      }
+    }
+    if (!found) {
+      err = "no (row, col, bond) lowering with bond <= 128 for factor " + std::to_string(ell) + " ('" + p.ops[ell] + "')";
+      return NEF_E_UNSUPPORTED;
+    }
+    // rebuild with a fresh bump so offsets are final
+    Bump bump;
+    Lowering L;
+    std::string why;
+    lower_candidate(p, ell, best_rm, best_pa, L, why);
+    finish_lowering(p, L, bump);
+    L.cost = best_cost;
+    ws = std::max<int64_t>(ws, L.ws_end);
+    p.low[ell] = std::move(L);
+  }
+  p.ws_trace = (ws + 255) / 256 * 256;
+  p.ws_bytes = (size_t)(p.ws_trace + (int64_t)8 * 4096 + 256);
+  return NEF_OK;
+}
+
+int build_plan(const char* einsum, int n_modes, const int64_t* shape, int n_ranks, const int64_t* ranks, Plan& p,
+               std::string& err) {
+  int st = parse_model(einsum, p.ops, p.out, err);
+  if (st) return st;
+  if (n_modes != (int)p.out.size()) { err = "shape has " + std::to_string(n_modes) + " dims, output has " + std::to_string(p.out.size()); return NEF_E_SHAPE; }
+  if (n_modes > 0 && !shape) { err = "null shape"; return NEF_E_ARG; }
+  std::memset(p.dims, 0, sizeof(p.dims));
+  int64_t total = 1;
+  for (int m = 0; m < n_modes; ++m) {
+    if (shape[m] <= 0) { err = "non-positive dimension"; return NEF_E_SHAPE; }
+    p.dims[(int)p.out[m]] = shape[m];
+    if (mul_overflow(total, shape[m], &total)) { err = "number of entries overflows int64"; return NEF_E_SHAPE; }
+  }
+  std::string contracted;
+  for (auto& op : p.ops)
+    for (char c : op)
+      if (p.out.find(c) == std::string::npos && contracted.find(c) == std::string::npos) contracted.push_back(c);
+  if (n_ranks != (int)contracted.size()) {
+    err = "expected " + std::to_string(contracted.size()) + " contracted-index sizes, got " + std::to_string(n_ranks);
+    return NEF_E_SHAPE;
+  }
+  if (n_ranks > 0 && !ranks) { err = "null ranks"; return NEF_E_ARG; }
+  for (int k = 0; k < n_ranks; ++k) {
+    if (ranks[k] <= 0) { err = "non-positive rank"; return NEF_E_SHAPE; }
+    p.dims[(int)contracted[k]] = ranks[k];
+  }
+  p.model.clear();
+  for (size_t l = 0; l < p.ops.size(); ++l) p.model += (l ? "," : "") + p.ops[l];
+  p.model += "->" + p.out;
+  // einstr_l = swap(model_str, l)
+  p.einstr.clear();
+  for (size_t l = 0; l < p.ops.size(); ++l) {
+    std::string s;
+    for (size_t k = 0; k < p.ops.size(); ++k) s += (k ? "," : "") + (k == l ? p.out : p.ops[k]);
+    p.einstr.push_back(s + "->" + p.ops[l]);
+  }
+  p.gshape.assign(shape, shape + n_modes);
+  p.shape = p.gshape;
+  p.n_local = total;
+  p.local_begin = 0;
+  p.local_len = n_modes ? p.shape[0] : 1;
+  p.shard_mode = -1;
+  p.factor_has_shard.assign(p.ops.size(), false);
+  return relower(p, err);
+}
+
+int relower(Plan& p, std::string& err) {
+  int64_t total = 1;
+  for (auto d : p.shape) total *= d;
+  p.n_local = total;
+  // local factor shapes
+  int64_t saved = 0;
+  if (p.shard_mode >= 0) {
+    saved = p.dims[(int)p.out[p.shard_mode]];
+    p.dims[(int)p.out[p.shard_mode]] = p.shape[p.shard_mode];
+  }
+  p.fshape.clear();
+  for (auto& op : p.ops) {
+    std::vector<int64_t> s;
+    for (char c : op) s.push_back(p.dims[(int)c]);
+    p.fshape.push_back(s);
+  }
+  (void)saved;   // dims keep the LOCAL size of the shard mode: the plan describes this rank
+  return lower_all(p, err);
+}
+
+static void json_prog(std::ostringstream& o, const EinProgram& pr) {
+  o << "{\"steps\":[";
+  for (size_t i = 0; i < pr.steps.size(); ++i) {
+    const EinStep& s = pr.steps[i];
+    auto br = [&](const BufRef& b) {
+      std::ostringstream t;
+      if (b.kind == BUF_FACTOR) t << "\"F" << b.id << "\"";
+      else if (b.kind == BUF_WS) t << "\"W" << b.id << "\"";
+      else t << "null";
+      return t.str();
+    };
+    o << (i ? "," : "") << "{\"a\":" << br(s.a) << ",\"a_idx\":\"" << s.a_idx << "\",\"b\":" << br(s.b)
+      << ",\"b_idx\":\"" << s.b_idx << "\",\"c\":" << br(s.c) << ",\"c_idx\":\"" << s.c_idx << "\"}";
+  }
+  auto br = [&](const BufRef& b) {
+    std::ostringstream t;
+    if (b.kind == BUF_FACTOR) t << "\"F" << b.id << "\"";
+    else if (b.kind == BUF_WS) t << "\"W" << b.id << "\"";
+    else t << "null";
+    return t.str();
+  };
+  o << "],\"result\":" << br(pr.result) << ",\"result_idx\":\"" << pr.result_idx << "\",\"macs\":" << pr.macs << "}";
+}
+
+std::string describe_plan(const Plan& p) {
+  std::ostringstream o;
+  o << "{\"model\":\"" << p.model << "\",\"einstr\":[";
+  for (size_t l = 0; l < p.einstr.size(); ++l) o << (l ? "," : "") << "\"" << p.einstr[l] << "\"";
+  o << "],\"shape\":[";
+  for (size_t m = 0; m < p.shape.size(); ++m) o << (m ? "," : "") << p.shape[m];
+  o << "],\"shard_mode\":" << p.shard_mode << ",\"workspace_bytes\":" << p.ws_bytes << ",\"lowerings\":[";
+  for (size_t l = 0; l < p.low.size(); ++l) {
+    const Lowering& L = p.low[l];
+    o << (l ? "," : "") << "{\"ell\":" << L.ell << ",\"row_idx\":\"" << L.row_idx << "\",\"col_idx\":\"" << L.col_idx
+      << "\",\"bond\":\"" << L.bond << "\",\"K\":" << L.K << ",\"n_rows\":" << L.n_rows << ",\"n_cols\":" << L.n_cols
+      << ",\"row_fast\":" << (L.row_fast ? "true" : "false") << ",\"n_chunks\":" << L.n_chunks
+      << ",\"tc\":" << (L.tc_ok ? "true" : "false") << ",\"row_factors\":[";
+    for (size_t k = 0; k < L.row_factors.size(); ++k) o << (k ? "," : "") << L.row_factors[k];
+    o << "],\"col_factors\":[";
+    for (size_t k = 0; k < L.col_factors.size(); ++k) o << (k ? "," : "") << L.col_factors[k];
+    o << "],\"U\":";
+    json_prog(o, L.uprog);
+    o << ",\"tables\":[";
+    for (size_t t = 0; t < L.tabs.size(); ++t) {
+      o << (t ? "," : "") << "{\"idx\":\"" << L.tabs[t].idx << "\",\"prog\":";
+      json_prog(o, L.tabs[t].prog);
+      o << "}";
+    }
+    o << "],\"Q\":\"W" << L.ws_Q << "\",\"epi_identity\":" << (L.epi_identity ? "true" : "false") << ",\"epi\":";
+    json_prog(o, L.epi);
+    o << ",\"cost\":" << L.cost << "}";
+  }
+  o << "]}";
+  return o.str();
+}
+
+}  // namespace nef

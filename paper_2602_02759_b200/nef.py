@@ -1,0 +1,279 @@
+"""Thin ctypes binding of libnef (include/nef.h).  Argument marshalling only: every step
+of the MU sweep runs in the library's sm_100a kernels.  PyTorch supplies device memory and
+streams.  There is NO CPU fallback: if libnef.so is missing this module raises on import.
+
+Functions carry the C ABI's names (``nef_plan``, ``nef_fit``, ``nef_loss`` ...); ``Plan`` is
+a small convenience wrapper over them.
+"""
+from __future__ import annotations
+
+import ctypes
+import json
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libnef.so")
+
+NEF_STATUS = {0: "OK", 1: "PARSE", 2: "SHAPE", 3: "DOMAIN", 4: "DATA", 5: "ARG", 6: "CUDA", 7: "NCCL",
+              8: "UNSUPPORTED"}
+
+
+class NefError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__("nef error %s (%d): %s" % (NEF_STATUS.get(code, "?"), code, msg))
+        self.code = code
+        self.status = NEF_STATUS.get(code, "?")
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError("libnef.so not built (%s); run `make` or __graft_entry__.build()" % LIB_PATH)
+    lib = ctypes.CDLL(LIB_PATH, mode=ctypes.RTLD_GLOBAL)
+    i64p = ctypes.POINTER(ctypes.c_int64)
+    vp = ctypes.c_void_p
+    d = ctypes.c_double
+    sig = {
+        "nef_plan": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_int, i64p, ctypes.c_int, i64p, ctypes.POINTER(vp)]),
+        "nef_plan_info": (ctypes.c_int, [vp, ctypes.POINTER(ctypes.c_int), ctypes.POINTER(ctypes.c_int), i64p, i64p,
+                                         ctypes.POINTER(ctypes.c_size_t)]),
+        "nef_factor_shape": (ctypes.c_int, [vp, ctypes.c_int, i64p, ctypes.POINTER(ctypes.c_int)]),
+        "nef_local_shape": (ctypes.c_int, [vp, i64p, ctypes.POINTER(ctypes.c_int)]),
+        "nef_plan_describe": (ctypes.c_int, [vp, ctypes.c_char_p, ctypes.c_size_t, ctypes.POINTER(ctypes.c_size_t)]),
+        "nef_fit": (ctypes.c_int, [vp, vp, vp, d, d, d, vp, ctypes.c_int, ctypes.POINTER(d), vp, ctypes.c_size_t, vp]),
+        "nef_update": (ctypes.c_int, [vp, ctypes.c_int, vp, vp, d, d, d, vp, vp, ctypes.c_size_t, vp]),
+        "nef_num_den": (ctypes.c_int, [vp, ctypes.c_int, vp, vp, d, d, vp, vp, vp, vp, ctypes.c_size_t, vp]),
+        "nef_apply_update": (ctypes.c_int, [vp, ctypes.c_int, d, d, d, vp, vp, vp, vp]),
+        "nef_loss": (ctypes.c_int, [vp, vp, vp, d, d, vp, ctypes.POINTER(d), i64p, vp, ctypes.c_size_t, vp]),
+        "nef_host_scratch_bytes": (ctypes.c_size_t, [vp, ctypes.c_int]),
+        "nef_fit_host": (ctypes.c_int, [vp, vp, vp, d, d, d, vp, ctypes.c_int, ctypes.POINTER(d), vp, ctypes.c_size_t,
+                                        vp]),
+        "nef_nccl_unique_id": (ctypes.c_int, [vp]),
+        "nef_plan_shard": (ctypes.c_int, [vp, ctypes.c_int, ctypes.c_int, vp]),
+        "nef_last_launch_count": (ctypes.c_int64, []),
+        "nef_set_kernel_policy": (ctypes.c_int, [ctypes.c_int]),
+        "nef_plan_destroy": (None, [vp]),
+        "nef_last_error": (ctypes.c_char_p, []),
+        "nef_version": (ctypes.c_char_p, []),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    return lib
+
+
+LIB = _load()
+EXPORTED = ("nef_plan", "nef_plan_info", "nef_factor_shape", "nef_local_shape", "nef_plan_describe", "nef_fit",
+            "nef_update", "nef_num_den", "nef_apply_update", "nef_loss", "nef_host_scratch_bytes", "nef_fit_host",
+            "nef_nccl_unique_id", "nef_plan_shard", "nef_last_launch_count", "nef_set_kernel_policy",
+            "nef_plan_destroy", "nef_last_error", "nef_version")
+
+
+def _check(code):
+    if code != 0:
+        raise NefError(code, LIB.nef_last_error().decode())
+
+
+def _i64(seq):
+    seq = [int(x) for x in seq]
+    return (ctypes.c_int64 * max(1, len(seq)))(*seq)
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    return ctypes.c_void_p(int(t.data_ptr()))
+
+
+def _stream(stream):
+    if stream is not None:
+        return ctypes.c_void_p(int(stream))
+    import torch
+    return ctypes.c_void_p(int(torch.cuda.current_stream().cuda_stream))
+
+
+def _fptrs(factors):
+    arr = (ctypes.c_void_p * len(factors))(*[int(f.data_ptr()) for f in factors])
+    return arr
+
+
+# ----------------------------------------------------------------------------- C names
+def nef_plan(model: str, shape, ranks):
+    h = ctypes.c_void_p()
+    _check(LIB.nef_plan(model.encode(), len(shape), _i64(shape), len(ranks), _i64(ranks), ctypes.byref(h)))
+    return h
+
+
+def nef_plan_destroy(h):
+    LIB.nef_plan_destroy(h)
+
+
+def nef_plan_info(h):
+    L = ctypes.c_int()
+    sm = ctypes.c_int()
+    lb = ctypes.c_int64()
+    ll = ctypes.c_int64()
+    ws = ctypes.c_size_t()
+    _check(LIB.nef_plan_info(h, ctypes.byref(L), ctypes.byref(sm), ctypes.byref(lb), ctypes.byref(ll), ctypes.byref(ws)))
+    return dict(n_factors=L.value, shard_mode=sm.value, local_begin=lb.value, local_len=ll.value,
+                workspace_bytes=ws.value)
+
+
+def nef_factor_shape(h, ell):
+    dims = (ctypes.c_int64 * 8)()
+    nd = ctypes.c_int()
+    _check(LIB.nef_factor_shape(h, ell, dims, ctypes.byref(nd)))
+    return tuple(dims[i] for i in range(nd.value))
+
+
+def nef_local_shape(h):
+    dims = (ctypes.c_int64 * 8)()
+    nd = ctypes.c_int()
+    _check(LIB.nef_local_shape(h, dims, ctypes.byref(nd)))
+    return tuple(dims[i] for i in range(nd.value))
+
+
+def nef_plan_describe(h):
+    n = ctypes.c_size_t()
+    _check(LIB.nef_plan_describe(h, None, 0, ctypes.byref(n)))
+    buf = ctypes.create_string_buffer(n.value)
+    _check(LIB.nef_plan_describe(h, buf, n.value, ctypes.byref(n)))
+    return json.loads(buf.value.decode())
+
+
+def nef_fit(h, Y, mask, alpha, beta, eps, factors, iters, workspace, stream=None, want_trace=True):
+    trace = (ctypes.c_double * (iters + 1))() if want_trace else None
+    _check(LIB.nef_fit(h, _ptr(Y), _ptr(mask), float(alpha), float(beta), float(eps), _fptrs(factors), int(iters),
+                       trace, _ptr(workspace), workspace.numel(), _stream(stream)))
+    return np.array(trace[:], dtype=np.float64) if want_trace else None
+
+
+def nef_update(h, ell, Y, mask, alpha, beta, eps, factors, workspace, stream=None):
+    _check(LIB.nef_update(h, int(ell), _ptr(Y), _ptr(mask), float(alpha), float(beta), float(eps), _fptrs(factors),
+                          _ptr(workspace), workspace.numel(), _stream(stream)))
+
+
+def nef_num_den(h, ell, Y, mask, alpha, beta, factors, num, den, workspace, stream=None):
+    _check(LIB.nef_num_den(h, int(ell), _ptr(Y), _ptr(mask), float(alpha), float(beta), _fptrs(factors), _ptr(num),
+                           _ptr(den), _ptr(workspace), workspace.numel(), _stream(stream)))
+
+
+def nef_apply_update(h, ell, alpha, beta, eps, factors, num, den, stream=None):
+    _check(LIB.nef_apply_update(h, int(ell), float(alpha), float(beta), float(eps), _fptrs(factors), _ptr(num),
+                                _ptr(den), _stream(stream)))
+
+
+def nef_loss(h, Y, mask, alpha, beta, factors, workspace, stream=None):
+    s = ctypes.c_double()
+    n = ctypes.c_int64()
+    _check(LIB.nef_loss(h, _ptr(Y), _ptr(mask), float(alpha), float(beta), _fptrs(factors), ctypes.byref(s),
+                        ctypes.byref(n), _ptr(workspace), workspace.numel(), _stream(stream)))
+    return s.value, n.value
+
+
+def nef_host_scratch_bytes(h, has_mask):
+    return int(LIB.nef_host_scratch_bytes(h, 1 if has_mask else 0))
+
+
+def nef_fit_host(h, Y_host, mask_host, alpha, beta, eps, factors_host, iters, scratch, stream=None):
+    """Y_host / mask_host / factors_host: host tensors (ideally pinned), contiguous."""
+    trace = (ctypes.c_double * (iters + 1))()
+    fp = (ctypes.c_void_p * len(factors_host))(*[int(f.data_ptr()) for f in factors_host])
+    _check(LIB.nef_fit_host(h, _ptr(Y_host), _ptr(mask_host), float(alpha), float(beta), float(eps), fp, int(iters),
+                            trace, _ptr(scratch), scratch.numel(), _stream(stream)))
+    return np.array(trace[:], dtype=np.float64)
+
+
+def nef_nccl_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(LIB.nef_nccl_unique_id(buf))
+    return buf.raw
+
+
+def nef_plan_shard(h, rank, world, uid: bytes | None):
+    ub = ctypes.create_string_buffer(uid, 128) if uid is not None else None
+    _check(LIB.nef_plan_shard(h, int(rank), int(world), ub))
+
+
+def nef_last_launch_count() -> int:
+    return int(LIB.nef_last_launch_count())
+
+
+def nef_set_kernel_policy(policy: int):
+    _check(LIB.nef_set_kernel_policy(int(policy)))
+
+
+def nef_version() -> str:
+    return LIB.nef_version().decode()
+
+
+# ----------------------------------------------------------------------------- wrapper
+class Plan:
+    """Owning wrapper: ``Plan(model, shape, ranks)``; workspace allocated lazily with torch."""
+
+    def __init__(self, model, shape, ranks):
+        self.model = model
+        self.gshape = tuple(int(x) for x in shape)
+        self.ranks = tuple(int(x) for x in ranks)
+        self.h = nef_plan(model, self.gshape, self.ranks)
+        self._ws = None
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h:
+            nef_plan_destroy(h)
+            self.h = None
+
+    @property
+    def info(self):
+        return nef_plan_info(self.h)
+
+    @property
+    def n_factors(self):
+        return self.info["n_factors"]
+
+    def factor_shape(self, ell):
+        return nef_factor_shape(self.h, ell)
+
+    def factor_shapes(self):
+        return [self.factor_shape(l) for l in range(self.n_factors)]
+
+    @property
+    def local_shape(self):
+        return nef_local_shape(self.h)
+
+    def describe(self):
+        return nef_plan_describe(self.h)
+
+    def shard(self, rank, world, uid=None):
+        nef_plan_shard(self.h, rank, world, uid)
+        self._ws = None
+
+    def workspace(self, device=None):
+        import torch
+        need = self.info["workspace_bytes"]
+        if self._ws is None or self._ws.numel() < need:
+            self._ws = torch.empty(need, dtype=torch.uint8, device=device or "cuda")
+        return self._ws
+
+    def fit(self, Y, mask, alpha, beta, factors, iters, eps=1e-12, stream=None):
+        return nef_fit(self.h, Y, mask, alpha, beta, eps, factors, iters, self.workspace(Y.device), stream)
+
+    def update(self, ell, Y, mask, alpha, beta, factors, eps=1e-12, stream=None):
+        nef_update(self.h, ell, Y, mask, alpha, beta, eps, factors, self.workspace(Y.device), stream)
+
+    def num_den(self, ell, Y, mask, alpha, beta, factors, stream=None):
+        import torch
+        shp = self.factor_shape(ell)
+        num = torch.empty(shp, dtype=torch.float32, device=Y.device)
+        den = torch.empty(shp, dtype=torch.float32, device=Y.device)
+        nef_num_den(self.h, ell, Y, mask, alpha, beta, factors, num, den, self.workspace(Y.device), stream)
+        return num, den
+
+    def apply_update(self, ell, alpha, beta, factors, num, den, eps=1e-12, stream=None):
+        nef_apply_update(self.h, ell, alpha, beta, eps, factors, num, den, stream)
+
+    def loss(self, Y, mask, alpha, beta, factors, stream=None):
+        return nef_loss(self.h, Y, mask, alpha, beta, factors, self.workspace(Y.device), stream)

@@ -1,0 +1,180 @@
+"""GPU parity of the CUDA path (through the C ABI) against the float64 oracle (-m gpu).
+
+Bars (BASELINE.json north_star): factors after 1 sweep within 1e-4 relative, loss
+trajectories within 1e-3 relative (fp32 GPU vs fp64 oracle); mask / index handling
+bit-exact (n_observed exact, masked-garbage invariance bit-identical).
+Sizes: each config's small shape (several 64-row / 64-column tiles plus ragged tails)
+for full-trajectory checks; full BASELINE sizes via sampled rows in test_gpu_fullsize.py.
+"""
+import numpy as np
+import pytest
+
+from nef_inputs import CONFIGS, generate_numpy
+from oracle import nef_oracle as O
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+FACTOR_RTOL = 1e-4
+TRACE_RTOL = 1e-3
+
+
+@pytest.fixture(scope="module")
+def nef():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2602_02759_b200 import nef as n
+    return n
+
+
+def _dev(d):
+    Y = torch.from_numpy(d["Y"]).cuda()
+    M = torch.from_numpy(d["mask"]).cuda() if d["mask"] is not None else None
+    F = [torch.from_numpy(f).cuda() for f in d["init"]]
+    return Y, M, F
+
+
+def _rel(a, b):
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    return float(np.max(np.abs(a - b) / np.maximum(np.abs(b), 1e-30)))
+
+
+def _ab(d, reading):
+    return (d["alpha"], d["beta"]) if reading == "paper" else (d["alpha"], d["beta_json"])
+
+
+@pytest.mark.parametrize("reading", ["paper", "literal"])
+@pytest.mark.parametrize("name", sorted(CONFIGS))
+def test_one_sweep_factors(nef, name, reading):
+    d = generate_numpy(name)
+    alpha, beta = _ab(d, reading)
+    Y, M, F = _dev(d)
+    plan = nef.Plan(d["model"], d["shape"], d["ranks"])
+    tr = plan.fit(Y, M, alpha, beta, F, 1)
+    torch.cuda.synchronize()
+    ref, rtr = O.fit(d["model"], d["Y"], d["mask"], d["init"], alpha, beta, 1)
+    for ell, (g, r) in enumerate(zip(F, ref)):
+        assert _rel(g.cpu().numpy(), r) <= FACTOR_RTOL, (name, reading, ell, _rel(g.cpu().numpy(), r))
+    assert _rel(tr, rtr) <= TRACE_RTOL
+
+
+@pytest.mark.parametrize("name,iters", [("c1", 100), ("c2", 12), ("c3", 10), ("c4", 10), ("c5", 10)])
+def test_loss_trajectory(nef, name, iters):
+    d = generate_numpy(name)
+    Y, M, F = _dev(d)
+    plan = nef.Plan(d["model"], d["shape"], d["ranks"])
+    tr = plan.fit(Y, M, d["alpha"], d["beta"], F, iters)
+    _, rtr = O.fit(d["model"], d["Y"], d["mask"], d["init"], d["alpha"], d["beta"], iters)
+    assert len(tr) == iters + 1
+    assert _rel(tr, rtr) <= TRACE_RTOL, (name, _rel(tr, rtr))
+    # Theorem 2 on the GPU trace, with fp32 slack
+    assert all(b <= a * (1 + 1e-5) for a, b in zip(tr, tr[1:]))
+
+
+@pytest.mark.parametrize("name", sorted(CONFIGS))
+def test_num_den_each_factor(nef, name):
+    d = generate_numpy(name)
+    Y, M, F = _dev(d)
+    plan = nef.Plan(d["model"], d["shape"], d["ranks"])
+    for ell in range(len(F)):
+        num, den = plan.num_den(ell, Y, M, d["alpha"], d["beta"], F)
+        A, B = O.numerator_denominator(d["model"], d["Y"], d["mask"], d["init"], ell, d["alpha"], d["beta"])
+        assert _rel(num.cpu().numpy(), A) <= 2e-5, (name, ell)
+        assert _rel(den.cpu().numpy(), B) <= 2e-5, (name, ell)
+
+
+@pytest.mark.parametrize("name", ["c2", "c3", "c5"])
+def test_mask_garbage_bit_identical(nef, name):
+    d = generate_numpy(name)
+    Y, M, F0 = _dev(d)
+    plan = nef.Plan(d["model"], d["shape"], d["ranks"])
+    F = [f.clone() for f in F0]
+    tr = plan.fit(Y, M, d["alpha"], d["beta"], F, 3)
+    for fill in (float("nan"), float("inf"), 1e30, -7.0):
+        Y2 = torch.where(M != 0, Y, torch.full_like(Y, fill))
+        G = [f.clone() for f in F0]
+        tr2 = plan.fit(Y2, M, d["alpha"], d["beta"], G, 3)
+        for a, b in zip(F, G):
+            assert torch.equal(a, b), fill
+        assert np.array_equal(tr, tr2)
+
+
+@pytest.mark.parametrize("name", sorted(CONFIGS))
+def test_n_observed_exact_and_loss(nef, name):
+    d = generate_numpy(name)
+    Y, M, F = _dev(d)
+    plan = nef.Plan(d["model"], d["shape"], d["ranks"])
+    s, n = plan.loss(Y, M, d["alpha"], d["beta"], F)
+    rs, rn = O.loss(d["model"], d["Y"], d["mask"], d["init"], d["alpha"], d["beta"])
+    assert n == rn
+    assert abs(s - rs) <= 1e-4 * abs(rs)
+
+
+def test_deterministic(nef):
+    d = generate_numpy("c3")
+    Y, M, F0 = _dev(d)
+    plan = nef.Plan(d["model"], d["shape"], d["ranks"])
+    outs = []
+    for _ in range(2):
+        F = [f.clone() for f in F0]
+        tr = plan.fit(Y, M, d["alpha"], d["beta"], F, 2)
+        outs.append((F, tr))
+    for a, b in zip(outs[0][0], outs[1][0]):
+        assert torch.equal(a, b)
+    assert np.array_equal(outs[0][1], outs[1][1])
+
+
+@pytest.mark.parametrize("ms,shape,ranks,ab", [
+    ("ir,jr,kr->ijk", (13, 17, 19), (3,), (1.0, 0.0)),           # odd prime shapes
+    ("ir,jr,kr->ijk", (65, 1, 129), (7,), (1.0, 1.0)),            # tile tails, unit mode
+    ("ia,jb,kc,abc->ijk", (31, 29, 33), (4, 5, 3), (0.5, 0.5)),
+    ("wr,dr,hr,irk,jrk->wdhij", (5, 3, 4, 11, 9), (4, 3), (1.3, 0.0)),
+    ("ir,jr,ak,kr,tr->ijat", (21, 19, 5, 23), (6, 3), (1.0, -1.0)),
+    ("iab,jbc,kca->ijk", (9, 10, 11), (2, 3, 2), (0.0, 1.0)),
+    ("ir,jr->ij", (300, 257), (33,), (2.0, -1.0)),
+    ("i,jr,kr->ijk", (7, 8, 9), (5,), (1.0, 2.0)),
+])
+def test_other_models(nef, ms, shape, ranks, ab):
+    rng = np.random.default_rng(3)
+    truth = [rng.gamma(1.0, 1.0, s) for s in O.factor_shapes(ms, shape, ranks)]
+    Y = rng.poisson(O.contract(ms, truth)).astype(np.float32) + 0.25
+    M = (rng.random(shape) > 0.1).astype(np.uint8)
+    init = [rng.uniform(0.1, 1, s).astype(np.float32) for s in O.factor_shapes(ms, shape, ranks)]
+    plan = nef.Plan(ms, shape, ranks)
+    F = [torch.from_numpy(f).cuda() for f in init]
+    tr = plan.fit(torch.from_numpy(Y).cuda(), torch.from_numpy(M).cuda(), ab[0], ab[1], F, 1)
+    ref, rtr = O.fit(ms, Y, M, init, ab[0], ab[1], 1)
+    for g, r in zip(F, ref):
+        assert _rel(g.cpu().numpy(), r) <= FACTOR_RTOL
+    assert _rel(tr, rtr) <= TRACE_RTOL
+
+
+def test_iters_zero_and_errors(nef):
+    d = generate_numpy("c1")
+    Y, M, F = _dev(d)
+    plan = nef.Plan(d["model"], d["shape"], d["ranks"])
+    before = [f.clone() for f in F]
+    tr = plan.fit(Y, M, 1.0, 0.0, F, 0)
+    assert len(tr) == 1
+    rs, _ = O.loss(d["model"], d["Y"], None, d["init"], 1.0, 0.0)
+    assert abs(tr[0] - rs) <= 1e-5 * rs
+    for a, b in zip(before, F):
+        assert torch.equal(a, b)
+    with pytest.raises(nef.NefError):
+        plan.fit(Y, M, 0.0, 0.5, F, 1)
+    for a, b in zip(before, F):
+        assert torch.equal(a, b)
+
+
+def test_host_entry_point(nef):
+    d = generate_numpy("c1")
+    plan = nef.Plan(d["model"], d["shape"], d["ranks"])
+    Yh = torch.from_numpy(d["Y"]).pin_memory()
+    Fh = [torch.from_numpy(f.copy()).pin_memory() for f in d["init"]]
+    scratch = torch.empty(nef.nef_host_scratch_bytes(plan.h, False), dtype=torch.uint8, device="cuda")
+    tr = nef.nef_fit_host(plan.h, Yh, None, 1.0, 0.0, 1e-12, Fh, 5, scratch)
+    ref, rtr = O.fit(d["model"], d["Y"], None, d["init"], 1.0, 0.0, 5)
+    assert _rel(tr, rtr) <= TRACE_RTOL
+    for g, r in zip(Fh, ref):
+        assert _rel(g.numpy(), r) <= 5e-4

@@ -1,0 +1,176 @@
+"""Host-side checks of libnef (-m "not gpu"): the C ABI loads and exports every symbol
+include/nef.h declares, validation errors, and the planner's lowering algebra.
+
+The lowering is checked with a numpy "debug executor" that runs the plan's own description
+(side-operand programs, column tables, 2-D view, epilogue) and must reproduce the oracle's
+Yhat and the numerator/denominator einsums of Algorithm 1 on tiny inputs.
+"""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+from oracle import nef_oracle as O
+
+nef = pytest.importorskip("paper_2602_02759_b200.nef")
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def test_exports_match_header():
+    hdr = open(os.path.join(ROOT, "include", "nef.h")).read()
+    declared = set(re.findall(r"\b(nef_[a-z_0-9]+)\s*\(", hdr))
+    assert declared, "no declarations parsed"
+    lib = ctypes.CDLL(nef.LIB_PATH)
+    for name in sorted(declared):
+        assert hasattr(lib, name), name
+    assert declared == set(nef.EXPORTED)
+
+
+@pytest.mark.parametrize("bad,code", [("ir,jr", "PARSE"), ("ii,jr->ij", "PARSE"), ("ir,jr->ijz", "PARSE"),
+                                      ("i1,jr->ij", "PARSE"), ("ir,,jr->ij", "PARSE")])
+def test_parse_errors(bad, code):
+    with pytest.raises(nef.NefError) as e:
+        nef.nef_plan(bad, (3, 4), (2,))
+    assert e.value.status == code
+
+
+def test_shape_errors():
+    with pytest.raises(nef.NefError) as e:
+        nef.nef_plan("ir,jr->ij", (3, 4, 5), (2,))
+    assert e.value.status == "SHAPE"
+    with pytest.raises(nef.NefError) as e:
+        nef.nef_plan("ir,jr->ij", (3, 4), (2, 3))
+    assert e.value.status == "SHAPE"
+    with pytest.raises(nef.NefError) as e:
+        nef.nef_plan("ir,jr->ij", (3, 0), (2,))
+    assert e.value.status == "SHAPE"
+    with pytest.raises(nef.NefError) as e:
+        nef.nef_plan("ir,jr,kr->ijk", (1 << 40, 1 << 20, 1 << 10), (2,))
+    assert e.value.status == "SHAPE"
+
+
+def test_domain_error_before_device_work():
+    p = nef.Plan("ir,jr->ij", (3, 4), (2,))
+
+    class Fake:
+        def __init__(self, n):
+            self.n = n
+
+        def data_ptr(self):
+            return 4096
+
+        def numel(self):
+            return self.n
+
+    ws = Fake(p.info["workspace_bytes"])
+    with pytest.raises(nef.NefError) as e:
+        nef.nef_fit(p.h, Fake(12), None, 0.0, 0.5, 1e-12, [Fake(6), Fake(8)], 1, ws, stream=0)
+    assert e.value.status == "DOMAIN"
+    with pytest.raises(nef.NefError) as e:
+        nef.nef_fit(p.h, Fake(12), None, 1.0, 0.0, 0.0, [Fake(6), Fake(8)], 1, ws, stream=0)
+    assert e.value.status == "ARG"
+
+
+def test_swap_strings_from_plan():
+    d = nef.Plan("wr,dr,hr,irk,jrk->wdhij", (3, 2, 2, 4, 4), (2, 3)).describe()
+    for ell, s in enumerate(d["einstr"]):
+        assert s == O.swap("wr,dr,hr,irk,jrk->wdhij", ell)
+
+
+def test_factor_shapes_and_workspace():
+    p = nef.Plan("ik,jk,tl,dl,kl->ijtd", (260, 260, 24, 365), (20, 10))
+    assert p.factor_shapes() == [(260, 20), (260, 20), (24, 10), (365, 10), (20, 10)]
+    assert p.info["workspace_bytes"] > 0
+    assert p.local_shape == (260, 260, 24, 365)
+
+
+# --------------------------------------------------------------------------- debug executor
+def _run_prog(prog, bufs):
+    for st in prog["steps"]:
+        a = bufs[st["a"]]
+        if st["b"] is None:
+            out = np.einsum("%s->%s" % (st["a_idx"], st["c_idx"]), a)
+        else:
+            out = np.einsum("%s,%s->%s" % (st["a_idx"], st["b_idx"], st["c_idx"]), a, bufs[st["b"]])
+        bufs[st["c"]] = out
+    return bufs[prog["result"]]
+
+
+def _execute_lowering(L, model, Y, M, factors, alpha, beta):
+    ops, out = O.parse(model)
+    bufs = {"F%d" % i: np.asarray(f, dtype=np.float64) for i, f in enumerate(factors)}
+    U = _run_prog(L["U"], dict(bufs))
+    tabs = [(_run_prog(t["prog"], dict(bufs)), t["idx"]) for t in L["tables"]]
+    rows, cols, bond = L["row_idx"], L["col_idx"], L["bond"]
+    K = int(np.prod([U.shape[len(rows) + i] for i in range(len(bond))])) if bond else 1
+    U2 = U.reshape(L["n_rows"], K)
+    if tabs:
+        V = np.einsum(",".join(i for _, i in tabs) + "->" + cols + bond, *[t for t, _ in tabs])
+    else:
+        V = np.ones([Y.shape[out.index(c)] for c in cols])
+    V2 = V.reshape(L["n_cols"], K)
+    perm = [out.index(c) for c in rows + cols]
+    Y2 = np.transpose(Y, perm).reshape(L["n_rows"], L["n_cols"])
+    M2 = np.transpose(M, perm).reshape(L["n_rows"], L["n_cols"]) if M is not None else np.ones_like(Y2)
+    S = U2 @ V2.T
+    yh = np.maximum(S, O.EPS_Y)
+    xs = np.where(M2 != 0, Y2, 1.0)
+    Pa = np.where(M2 != 0, O.a_fn(xs, yh, alpha, beta), 0.0)
+    Pb = np.where(M2 != 0, O.b_fn(xs, yh, alpha, beta), 0.0)
+    Qa = (Pa @ V2).reshape([Y.shape[out.index(c)] for c in rows] + list(U.shape[len(rows):]))
+    Qb = (Pb @ V2).reshape(Qa.shape)
+    if L["epi_identity"]:
+        return S, Y2, Qa.reshape(np.shape(factors[L["ell"]])), Qb.reshape(np.shape(factors[L["ell"]]))
+    epi = L["epi"]
+    res = []
+    for Q in (Qa, Qb):
+        b2 = dict(bufs)
+        b2[L["Q"]] = Q
+        res.append(_run_prog(epi, b2))
+    return S, Y2, res[0], res[1]
+
+
+PLANNER_CASES = [
+    ("ir,jr,kr->ijk", (5, 4, 3), (3,)),
+    ("ia,jb,kc,abc->ijk", (4, 3, 5), (2, 3, 2)),
+    ("ik,jk,tl,dl,kl->ijtd", (3, 4, 2, 3), (3, 2)),
+    ("iab,jbc,kca->ijk", (3, 2, 4), (2, 2, 3)),
+    ("ir,jkr->ijk", (3, 2, 3), (2,)),
+    ("i,jr,kr->ijk", (2, 3, 2), (3,)),
+    ("ia,jb,kb,ab->ijk", (2, 3, 4), (2, 3)),
+    ("ir,jr,ak,kr,tr->ijat", (3, 2, 3, 2), (3, 2)),
+    ("wr,dr,hr,irk,jrk->wdhij", (2, 3, 2, 3, 2), (2, 3)),
+    ("ir,jr->ij", (6, 5), (2,)),
+    ("ia,jb,kc,la,bc->ijkl", (2, 3, 2, 2), (2, 2, 3)),
+]
+
+
+@pytest.mark.parametrize("ms,shape,ranks", PLANNER_CASES)
+def test_lowering_algebra(ms, shape, ranks):
+    rng = np.random.default_rng(7)
+    plan = nef.Plan(ms, shape, ranks)
+    d = plan.describe()
+    f = [rng.uniform(0.2, 1.0, s) for s in O.factor_shapes(ms, shape, ranks)]
+    Y = rng.poisson(2.0, size=shape).astype(float)
+    M = (rng.random(shape) > 0.2).astype(np.uint8)
+    yhat = O.contract(ms, f)
+    for L in d["lowerings"]:
+        ell = L["ell"]
+        S, _, num, den = _execute_lowering(L, ms, Y, M, f, 1.0, -0.5)
+        _, out = O.parse(ms)
+        perm = [out.index(c) for c in L["row_idx"] + L["col_idx"]]
+        np.testing.assert_allclose(S, np.transpose(yhat, perm).reshape(S.shape), rtol=1e-12)
+        A, B = O.numerator_denominator(ms, Y, M, f, ell, 1.0, -0.5)
+        np.testing.assert_allclose(num, A, rtol=1e-11)
+        np.testing.assert_allclose(den, B, rtol=1e-11)
+
+
+def test_cp_lowering_is_direct():
+    """CP: every factor streams as rows = its own mode, bond = r, Khatri-Rao column tables, no epilogue."""
+    d = nef.Plan("ir,jr,kr->ijk", (2048, 2048, 1024), (64,)).describe()
+    for L, rows in zip(d["lowerings"], "ijk"):
+        assert L["row_idx"] == rows and L["bond"] == "r" and L["epi_identity"]
+        assert len(L["tables"]) == 2 and all(len(t["prog"]["steps"]) == 0 for t in L["tables"])
