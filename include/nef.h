@@ -136,9 +136,22 @@ int nef_plan_shard(nef_plan_t plan, int rank, int world, const void* nccl_unique
 /* Number of kernel launches the last nef_fit / nef_loss / nef_update call enqueued. */
 int64_t nef_last_launch_count(void);
 
+/* Live per-launch timing of the streaming (fused) kernel with CUDA events recorded on the
+ * launch stream around every launch (used by bench.py for the roofline).  enable != 0
+ * resets the counters and turns recording on; nef_profile_read synchronizes on the last
+ * recorded event and returns the summed kernel time (ms), the number of launches and the
+ * algorithmic bytes those launches had to read (Y: 4 B + mask: 1 B per entry). */
+int nef_profile_enable(int enable);
+int nef_profile_read(double* kernel_ms, int64_t* launches, double* algorithmic_bytes);
+
 /* Select the streaming kernel: 0 = automatic (tcgen05 where supported), 1 = CUDA-core FFMA
  * kernel only.  Process-wide; for tests and A/B measurement. */
 int nef_set_kernel_policy(int policy);
+
+/* Test hook: when device_buffer != NULL the tcgen05 streaming kernel writes the P_a tile
+ * (a(Y,Yhat) after masking, TF32-rounded) of its first column tile in CTA (0,0) as 128 x 64
+ * floats (row-major) to it.  NULL disables. */
+int nef_debug_dump(float* device_buffer);
 
 void nef_plan_destroy(nef_plan_t plan);
 const char* nef_last_error(void);

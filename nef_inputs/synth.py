@@ -130,19 +130,26 @@ def _apply_noise(cfg, yhat, rng):
 # ------------------------------------------------------------------------------------
 # device-side generator for the full-size configs
 # ------------------------------------------------------------------------------------
-def generate_torch(name, device, shape=None, seed_offset=0, slab_entries=1 << 28):
+SLAB = 8   # mode-0 rows per independently seeded draw (shard-friendly, reading R21)
+
+
+def generate_torch(name, device, shape=None, seed_offset=0, mode0_range=None):
     """Draw config ``name`` (default: FULL shape) directly into device memory.
 
-    Returns dict(Y=float32 tensor, mask=uint8 tensor or None, init=list[float32 tensor],
-    ...).  Planted mean is formed slab-wise along mode 0 with torch.einsum."""
+    The planted mean is formed slab-wise along mode 0 with torch.einsum; noise and mask of
+    each SLAB-row slab come from their own seeded generator, so the tensor is identical no
+    matter how it is split.  ``mode0_range=(b, e)`` returns only rows [b, e) of mode 0 (a
+    rank's shard), with the mode-0 factors of ``init`` / ``truth`` sliced accordingly.
+
+    Returns dict(Y=float32 tensor, mask=uint8 tensor or None, init=list[float32 tensor], ...).
+    """
     import torch
 
     cfg = CONFIGS[name]
     shape = tuple(shape or cfg.shape)
+    b0, e0 = mode0_range or (0, shape[0])
     base = 7919 * CONFIG_INDEX[name] + 104729 * seed_offset
     g_true = torch.Generator(device=device).manual_seed(base + 1)
-    g_noise = torch.Generator(device=device).manual_seed(base + 2)
-    g_mask = torch.Generator(device=device).manual_seed(base + 3)
     g_init = torch.Generator(device=device).manual_seed(base + 4)
     fshapes = factor_shapes(cfg.model, shape, cfg.ranks)
     k, th = _true_law(cfg)
@@ -151,27 +158,31 @@ def generate_torch(name, device, shape=None, seed_offset=0, slab_entries=1 << 28
         conc = torch.full(fs, k, dtype=torch.float32, device=device)
         truth.append(torch._standard_gamma(conc, generator=g_true) * th)
     ops, out = _parse(cfg.model)
-    Y = torch.empty(shape, dtype=torch.float32, device=device)
-    mask = torch.empty(shape, dtype=torch.uint8, device=device) if cfg.p_missing > 0 else None
-    row = int(math.prod(shape[1:]))
-    step = max(1, slab_entries // row)
     lead = out[0]
-    for s0 in range(0, shape[0], step):
-        s1 = min(shape[0], s0 + step)
+    for op in ops:
+        if lead in op and op[0] != lead:
+            raise ValueError("lead index must be first in its operand for slab generation")
+    lshape = (e0 - b0,) + shape[1:]
+    Y = torch.empty(lshape, dtype=torch.float32, device=device)
+    mask = torch.empty(lshape, dtype=torch.uint8, device=device) if cfg.p_missing > 0 else None
+    for s0 in range((b0 // SLAB) * SLAB, e0, SLAB):
+        s1 = min(shape[0], s0 + SLAB)
+        lo, hi = max(s0, b0), min(s1, e0)
         sl = [t[s0:s1] if op[0] == lead else t for t, op in zip(truth, ops)]
-        # operands whose FIRST index is the lead observed index are sliced; the planted
-        # models here all put that index first when they contain it
-        for t, op in zip(truth, ops):
-            if lead in op and op[0] != lead:
-                raise ValueError("lead index must be first in its operand for slab generation")
         yhat = torch.einsum(cfg.model, *sl)
-        Y[s0:s1] = _apply_noise_torch(cfg, yhat, g_noise)
+        g = torch.Generator(device=device).manual_seed(base * 1000003 + 2 * s0 + 11)
+        ys = _apply_noise_torch(cfg, yhat, g)
+        Y[lo - b0:hi - b0] = ys[lo - s0:hi - s0]
         if mask is not None:
-            mask[s0:s1] = (torch.rand(yhat.shape, generator=g_mask, device=device) >= cfg.p_missing).to(torch.uint8)
-        del yhat
+            ms = torch.rand(yhat.shape, generator=g, device=device) >= cfg.p_missing
+            mask[lo - b0:hi - b0] = ms[lo - s0:hi - s0].to(torch.uint8)
+        del yhat, ys
     init = [torch.rand(fs, generator=g_init, device=device) * 0.9 + 0.1 for fs in fshapes]
-    return dict(Y=Y, mask=mask, init=init, alpha=cfg.alpha, beta=cfg.beta, beta_json=cfg.beta_json,
-                model=cfg.model, ranks=cfg.ranks, iters=cfg.iters, shape=shape)
+    if mode0_range is not None:
+        init = [f[b0:e0].contiguous() if op[0] == lead else f for f, op in zip(init, ops)]
+        truth = [t[b0:e0].contiguous() if op[0] == lead else t for t, op in zip(truth, ops)]
+    return dict(Y=Y, mask=mask, init=init, truth=truth, alpha=cfg.alpha, beta=cfg.beta, beta_json=cfg.beta_json,
+                model=cfg.model, ranks=cfg.ranks, iters=cfg.iters, shape=shape, local_shape=lshape)
 
 
 def _apply_noise_torch(cfg, yhat, g):

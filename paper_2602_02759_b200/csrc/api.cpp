@@ -19,6 +19,7 @@
 #include <vector>
 
 #include "kernels.h"
+#include "kernels_tc.h"
 #include "nef_internal.h"
 #include "../../include/nef.h"
 
@@ -31,6 +32,35 @@ namespace {
 thread_local std::string g_err;
 thread_local int64_t g_launches = 0;
 int g_policy = 0;
+float* g_debug = nullptr;   // optional device dump of the tcgen05 kernel's first tile (tests)
+
+// live CUDA-event timing of the streaming kernel (nef_profile_*)
+struct Prof {
+  bool on = false;
+  std::vector<cudaEvent_t> ev;   // pairs (start, end)
+  size_t used = 0;               // number of pairs recorded since enable
+  double bytes = 0;
+};
+Prof g_prof;
+
+void prof_begin(cudaStream_t s) {
+  if (!g_prof.on) return;
+  if (2 * g_prof.used + 2 > g_prof.ev.size()) {
+    for (int k = 0; k < 64; ++k) {
+      cudaEvent_t e;
+      if (cudaEventCreate(&e) != cudaSuccess) { g_prof.on = false; return; }
+      g_prof.ev.push_back(e);
+    }
+  }
+  cudaEventRecord(g_prof.ev[2 * g_prof.used], s);
+}
+
+void prof_end(cudaStream_t s, double bytes) {
+  if (!g_prof.on) return;
+  cudaEventRecord(g_prof.ev[2 * g_prof.used + 1], s);
+  g_prof.used++;
+  g_prof.bytes += bytes;
+}
 
 int fail(int code, const std::string& msg) {
   g_err = msg;
@@ -160,17 +190,86 @@ int side_operands(const Ctx& c, const nef::Lowering& L) {
   return NEF_OK;
 }
 
+// Where one streaming launch left its partials.
+struct StreamOut {
+  float* Qpart = nullptr;
+  int64_t n_chunks = 1;
+  double* losspart = nullptr;
+  long long* countpart = nullptr;
+  int64_t nparts = 0;
+};
+
+bool use_tc(const nef::Lowering& L, const uint8_t* M) {
+  return g_policy == 0 && L.tc_ok && (!M || (L.tc_mask_ok && (reinterpret_cast<uintptr_t>(M) & 15) == 0));
+}
+
+// One streaming pass over Y (+mask) for lowering L: the tcgen05 kernel where the planner
+// found a TMA geometry, else the CUDA-core kernel.  U and the column tables must be ready.
+int stream_pass(const Ctx& c, const nef::Lowering& L, const float* Y, const uint8_t* M, int mode,
+                const nef::DivParams& dv, StreamOut& o) {
+  std::vector<int32_t> boff;
+  nef::FusedArgs a = fused_args(c, L, Y, M, mode, dv, boff);
+  const double bytes = (double)c.p->n_local * (M ? 5.0 : 4.0);
+  if (use_tc(L, M)) {
+    nef::tc::TcArgs t{};
+    t.layout = L.tc_layout;
+    t.R = L.tc_R;
+    t.CI = L.tc_CI;
+    t.CO = L.tc_CO;
+    t.tiles_inner = (L.tc_CI + 63) / 64;
+    t.tiles = L.tc_tiles;
+    int64_t tpc = (L.tc_tiles + L.tc_chunks - 1) / L.tc_chunks;
+    int64_t chunks = (L.tc_tiles + tpc - 1) / tpc;   // no empty chunk
+    t.tiles_per_chunk = tpc;
+    t.K = (int)L.K;
+    t.KB = L.tc_KB;
+    t.n_rows = L.n_rows;
+    t.U = a.U;
+    t.nc = a.nc;
+    for (int k = 0; k < a.nc; ++k) t.cdim[k] = a.cdim[k];
+    t.ntab = a.ntab;
+    for (int q = 0; q < a.ntab; ++q) {
+      t.tab[q] = a.tab[q];
+      for (int k = 0; k < a.nc; ++k) t.tcs[q][k] = a.tcs[q][k];
+      for (int k = 0; k < L.K; ++k) t.boff[q][k] = boff[(size_t)q * L.K + k];
+    }
+    t.Qpart = reinterpret_cast<float*>(c.ws + L.ws_tc_Qpart);
+    t.losspart = reinterpret_cast<double*>(c.ws + L.ws_tc_losspart);
+    o.nparts = L.tc_row_blocks * chunks;
+    t.countpart = reinterpret_cast<long long*>(c.ws + L.ws_tc_losspart + o.nparts * 8);
+    t.dv = dv;
+    t.mode = mode;
+    t.debug = g_debug;
+    prof_begin(c.s);
+    CK(nef::tc::launch(t, Y, M, L.tc_row_blocks, chunks, c.s));
+    prof_end(c.s, bytes);
+    ++g_launches;
+    o.Qpart = t.Qpart;
+    o.n_chunks = chunks;
+    o.losspart = t.losspart;
+    o.countpart = t.countpart;
+    return NEF_OK;
+  }
+  prof_begin(c.s);
+  CK(nef::launch_fused_ffma(a, c.s));
+  prof_end(c.s, bytes);
+  ++g_launches;
+  o.Qpart = a.Qpart;
+  o.n_chunks = L.n_chunks;
+  o.losspart = a.losspart;
+  o.countpart = a.countpart;
+  o.nparts = ((L.n_rows + 63) / 64) * L.n_chunks;
+  return NEF_OK;
+}
+
 // Loss-only pass with lowering 0 -> slot (double) + count slot (long long)
 int loss_pass(const Ctx& c, const float* Y, const uint8_t* M, const nef::DivParams& dv, double* slot, long long* cslot) {
   const nef::Lowering& L = c.p->low[0];
   int st = side_operands(c, L);
   if (st) return st;
-  std::vector<int32_t> boff;
-  nef::FusedArgs a = fused_args(c, L, Y, M, 2, dv, boff);
-  CK(nef::launch_fused_ffma(a, c.s));
-  ++g_launches;
-  int64_t nparts = ((L.n_rows + 63) / 64) * L.n_chunks;
-  CK(nef::launch_loss_reduce(a.losspart, a.countpart, nparts, slot, cslot, c.s));
+  StreamOut o;
+  if ((st = stream_pass(c, L, Y, M, 2, dv, o))) return st;
+  CK(nef::launch_loss_reduce(o.losspart, o.countpart, o.nparts, slot, cslot, c.s));
   ++g_launches;
   return NEF_OK;
 }
@@ -181,18 +280,15 @@ int num_den(const Ctx& c, int ell, const float* Y, const uint8_t* M, const nef::
   const nef::Lowering& L = c.p->low[ell];
   int st = side_operands(c, L);
   if (st) return st;
-  std::vector<int32_t> boff;
-  nef::FusedArgs a = fused_args(c, L, Y, M, mode, dv, boff);
-  CK(nef::launch_fused_ffma(a, c.s));
-  ++g_launches;
+  StreamOut o;
+  if ((st = stream_pass(c, L, Y, M, mode, dv, o))) return st;
   if (mode == 1) {
-    int64_t nparts = ((L.n_rows + 63) / 64) * L.n_chunks;
-    CK(nef::launch_loss_reduce(a.losspart, a.countpart, nparts, slot, cslot, c.s));
+    CK(nef::launch_loss_reduce(o.losspart, o.countpart, o.nparts, slot, cslot, c.s));
     ++g_launches;
   }
   const int64_t qe = L.n_rows * L.K;
   float* Q = reinterpret_cast<float*>(c.ws + L.ws_Q);
-  CK(nef::launch_reduce_q(a.Qpart, Q, L.n_chunks, 2 * qe, c.s));
+  CK(nef::launch_reduce_q(o.Qpart, Q, o.n_chunks, 2 * qe, c.s));
   ++g_launches;
   if (L.epi_identity) {
     *num = Q;
@@ -270,6 +366,36 @@ extern "C" {
 const char* nef_last_error(void) { return g_err.c_str(); }
 const char* nef_version(void) { return "nef 0.1 (sm_100a)"; }
 int64_t nef_last_launch_count(void) { return g_launches; }
+int nef_profile_enable(int enable) {
+  g_prof.on = enable != 0;
+  g_prof.used = 0;
+  g_prof.bytes = 0;
+  return NEF_OK;
+}
+
+int nef_profile_read(double* kernel_ms, int64_t* launches, double* algorithmic_bytes) {
+  double ms = 0;
+  if (g_prof.used) {
+    cudaError_t e = cudaEventSynchronize(g_prof.ev[2 * g_prof.used - 1]);
+    if (e != cudaSuccess) return fail(NEF_E_CUDA, std::string("cudaEventSynchronize: ") + cudaGetErrorString(e));
+    for (size_t i = 0; i < g_prof.used; ++i) {
+      float t = 0;
+      e = cudaEventElapsedTime(&t, g_prof.ev[2 * i], g_prof.ev[2 * i + 1]);
+      if (e != cudaSuccess) return fail(NEF_E_CUDA, std::string("cudaEventElapsedTime: ") + cudaGetErrorString(e));
+      ms += t;
+    }
+  }
+  if (kernel_ms) *kernel_ms = ms;
+  if (launches) *launches = (int64_t)g_prof.used;
+  if (algorithmic_bytes) *algorithmic_bytes = g_prof.bytes;
+  return NEF_OK;
+}
+
+int nef_debug_dump(float* device_buffer) {
+  g_debug = device_buffer;
+  return NEF_OK;
+}
+
 int nef_set_kernel_policy(int policy) {
   if (policy < 0 || policy > 1) return fail(NEF_E_ARG, "policy must be 0 or 1");
   g_policy = policy;

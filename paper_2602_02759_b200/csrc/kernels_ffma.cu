@@ -17,6 +17,7 @@
 #include <cmath>
 #include <cstdint>
 
+#include "divergence.cuh"
 #include "kernels.h"
 
 namespace nef {
@@ -67,76 +68,6 @@ UpdArgs make_upd(double alpha, double beta, double eps) {
   u.g_case = 0;
   u.inv_expo = 1.0 / expo;
   return u;
-}
-
-// --------------------------------------------------------------------------------------
-// elementwise math
-// --------------------------------------------------------------------------------------
-__device__ __forceinline__ float powc(float y, int code, float p) {
-  switch (code) {
-    case POW_0: return 1.f;
-    case POW_1: return y;
-    case POW_M1: return 1.f / y;
-    case POW_H: return sqrtf(y);
-    case POW_MH: return rsqrtf(y);
-    case POW_M15: { float r = rsqrtf(y); return r * r * r; }
-    case POW_15: return y * sqrtf(y);
-    case POW_2: return y * y;
-    case POW_M2: { float r = 1.f / y; return r * r; }
-    default: return powf(y, p);
-  }
-}
-
-// h_p(u) = (e^{pu} - 1 - pu) / p^2, stable near u = 0 (series for |pu| < 0.3)
-__device__ __forceinline__ float hfun(float p, float u) {
-  float v = p * u;
-  if (fabsf(v) < 0.3f) {
-    float s = 1.f / 5040.f;
-    s = fmaf(s, v, 1.f / 720.f);
-    s = fmaf(s, v, 1.f / 120.f);
-    s = fmaf(s, v, 1.f / 24.f);
-    s = fmaf(s, v, 1.f / 6.f);
-    s = fmaf(s, v, 0.5f);
-    return u * u * s;
-  }
-  return (expm1f(v) - v) / (p * p);
-}
-
-// f(v) = 1 - e^v + v e^v, stable near v = 0
-__device__ __forceinline__ float ffun(float v) {
-  if (fabsf(v) < 0.3f) {
-    float s = 1.f / 840.f;
-    s = fmaf(s, v, 1.f / 144.f);
-    s = fmaf(s, v, 1.f / 30.f);
-    s = fmaf(s, v, 1.f / 8.f);
-    s = fmaf(s, v, 1.f / 3.f);
-    s = fmaf(s, v, 0.5f);
-    return v * v * s;
-  }
-  return v * expf(v) - expm1f(v);
-}
-
-// L_{alpha,beta}(x, y) of P:502-524 in u = log(x/y) form (DESIGN.md §Loss forms); y >= 1e-30
-__device__ __forceinline__ float loss_entry(float x, float y, const DivParams& d) {
-  const float a = d.alpha, b = d.beta;
-  switch (d.loss_case) {
-    case 5: { float r = x - y; return 0.5f * r * r; }
-    case 0: {
-      float yab = powf(y, a + b);
-      if (x <= 0.f) return yab / (a * (a + b));
-      float u = logf(x / y);
-      return yab / b * ((a + b) * hfun(a + b, u) - a * hfun(a, u));
-    }
-    case 1: {
-      float ya = powc(y, d.c_xa, a);
-      if (x <= 0.f) return ya / (a * a);
-      float u = logf(x / y);
-      return ya / (a * a) * ffun(a * u);
-    }
-    case 2: return hfun(a, logf(x / y));
-    case 3: return powf(y, b) * hfun(b, logf(x / y));
-    default: { float u = logf(x / y); return 0.5f * u * u; }
-  }
 }
 
 // --------------------------------------------------------------------------------------
@@ -286,13 +217,7 @@ __global__ void __launch_bounds__(NT) fused_ffma_kernel(const __grid_constant__ 
         const float yh = fmaxf(s[i][j], 1e-30f);       // Yhat floor (reading R4)
         const float x = yy[i];
         float av, bv;
-        if (a.dv.log_case) {
-          av = logf(x / yh);
-          bv = 1.f;
-        } else {
-          av = powc(x, a.dv.c_xa, a.dv.p_xa) * powc(yh, a.dv.c_ya, a.dv.p_ya);
-          bv = powc(yh, a.dv.c_yb, a.dv.p_yb);
-        }
+        ab_entry(x, yh, a.dv, av, bv);
         pa[i] = obs ? av : 0.f;                          // select, never multiply (R5)
         pb[i] = obs ? bv : 0.f;
         if (a.mode != 0 && obs) {

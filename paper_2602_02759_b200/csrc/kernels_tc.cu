@@ -1,0 +1,598 @@
+// sm_100a fused streaming pass on the 5th-generation tensor cores (tcgen05 + TMEM + TMA).
+//
+// One launch = one factor update ell (Algorithm 1 lines 6-8) over the planner's
+// 2-D view Y[row, col] of the data:
+//   S   = U V^T               (reconstruction tile, TF32 MMA into TMEM; U split hi+lo)
+//   P_a = M ? Y^alpha S^(beta-1) : 0,  P_b = M ? S^(alpha+beta-1) : 0     (registers)
+//   N  += P_a V,  D += P_b V  (TF32 MMAs, A operand = P in TMEM, accumulators in TMEM)
+// Y and the mask are streamed HBM -> smem by TMA exactly once; Yhat, a and b never leave the SM.
+//
+// CTA = 128 rows (TMEM lanes) x a contiguous range of 64-column tiles.  384 threads:
+//   warp 0      TMA producer (Y / mask ring of NS stages)
+//   warp 1      TMEM allocator + single-thread MMA issuer
+//   warps 2-3   column-operand generator: V tile = prod of column tables (Khatri-Rao), TF32
+//               round-to-nearest, written in the UMMA SW128 K-major layout (NV stages)
+//   warps 4-11  elementwise: tcgen05.ld S -> a, b (+ loss) -> tcgen05.st P; epilogue N, D
+// TMEM (512 columns): S[2] (2x64) | P_a, P_b (2x64) | N, D (2xKB) | U_hi, U_lo (2xKB)
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstring>
+
+#include "divergence.cuh"
+#include "kernels.h"
+#include "kernels_tc.h"
+
+namespace nef {
+namespace tc {
+
+constexpr int BM = 128, BN = 64;
+constexpr int NS = 4;        // Y / mask pipeline stages
+constexpr int NV = 3;        // V tile stages
+constexpr int NTHREADS = 384;
+constexpr int Y_STAGE = BM * BN * 4;      // 32 KB
+constexpr int M_STAGE = BM * BN;          // 8 KB
+constexpr int V_STAGE_MAX = BN * 64 * 4;  // 16 KB (KB = 64)
+
+struct __align__(64) Params {
+  CUtensorMap tmY;
+  CUtensorMap tmM;
+  TcArgs a;
+};
+
+// ------------------------------------------------------------------ PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+}
+// Bounded wait: a pipeline bug traps (kernel error) instead of hanging the GPU.
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  uint32_t done = 0;
+  for (uint32_t it = 0;; ++it) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    if (done) return;
+    if (it > (1u << 26)) __trap();
+  }
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* tm, int c0, int c1, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* tm, int c0, int c1, int c2, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(tm)), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// D[tmem] (+)= A[tmem] * B[smem desc], kind::tf32, one CTA
+__device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}" ::"r"(d),
+      "r"(a), "l"(bdesc), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
+}
+
+#define NEF_R32(x)                                                                                                    \
+  "=r"(x[0]), "=r"(x[1]), "=r"(x[2]), "=r"(x[3]), "=r"(x[4]), "=r"(x[5]), "=r"(x[6]), "=r"(x[7]), "=r"(x[8]),      \
+      "=r"(x[9]), "=r"(x[10]), "=r"(x[11]), "=r"(x[12]), "=r"(x[13]), "=r"(x[14]), "=r"(x[15]), "=r"(x[16]),        \
+      "=r"(x[17]), "=r"(x[18]), "=r"(x[19]), "=r"(x[20]), "=r"(x[21]), "=r"(x[22]), "=r"(x[23]), "=r"(x[24]),       \
+      "=r"(x[25]), "=r"(x[26]), "=r"(x[27]), "=r"(x[28]), "=r"(x[29]), "=r"(x[30]), "=r"(x[31])
+#define NEF_W32(x)                                                                                                    \
+  "r"(x[0]), "r"(x[1]), "r"(x[2]), "r"(x[3]), "r"(x[4]), "r"(x[5]), "r"(x[6]), "r"(x[7]), "r"(x[8]), "r"(x[9]),     \
+      "r"(x[10]), "r"(x[11]), "r"(x[12]), "r"(x[13]), "r"(x[14]), "r"(x[15]), "r"(x[16]), "r"(x[17]), "r"(x[18]),   \
+      "r"(x[19]), "r"(x[20]), "r"(x[21]), "r"(x[22]), "r"(x[23]), "r"(x[24]), "r"(x[25]), "r"(x[26]), "r"(x[27]),   \
+      "r"(x[28]), "r"(x[29]), "r"(x[30]), "r"(x[31])
+
+// 32 consecutive TMEM columns of this thread's lane
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
+      "%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
+      : NEF_R32(r)
+      : "r"(taddr));
+}
+// wait for tcgen05.ld; the registers are tied in so no use can be scheduled above the wait
+__device__ __forceinline__ void tmem_ld_wait(uint32_t (&r)[32]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;"
+               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
+                 "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]), "+r"(r[15]),
+                 "+r"(r[16]), "+r"(r[17]), "+r"(r[18]), "+r"(r[19]), "+r"(r[20]), "+r"(r[21]), "+r"(r[22]),
+                 "+r"(r[23]), "+r"(r[24]), "+r"(r[25]), "+r"(r[26]), "+r"(r[27]), "+r"(r[28]), "+r"(r[29]),
+                 "+r"(r[30]), "+r"(r[31])
+               :
+               : "memory");
+}
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
+      "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};" ::"r"(taddr),
+      NEF_W32(r)
+      : "memory");
+}
+__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+__device__ __forceinline__ uint32_t tf32_rna(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return r;
+}
+
+// UMMA shared-memory descriptor, SWIZZLE_128B, sm_100 (version 1)
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+// instruction descriptor: kind::tf32, D f32, A/B tf32, A K-major, B K- or MN-major
+__host__ __device__ constexpr uint32_t idesc_tf32(int M, int N, int b_mn_major) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)b_mn_major << 16) | ((uint32_t)(N >> 3) << 17) |
+         ((uint32_t)(M >> 4) << 24);
+}
+
+// ------------------------------------------------------------------ the kernel
+template <int KB>
+__global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_constant__ Params P) {
+  extern __shared__ unsigned char smraw[];
+  const TcArgs& a = P.a;
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5;
+  const int lane = tid & 31;
+
+  // 1024-aligned carve-up
+  const uint32_t raw = smem_u32(smraw);
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  unsigned char* gbase = smraw + (base - raw);
+  const uint32_t sY = base;                                  // NS x 32 KB
+  const uint32_t sM = sY + NS * Y_STAGE;                     // NS x 8 KB
+  const uint32_t sV = sM + NS * M_STAGE;                     // NV x V_STAGE
+  const uint32_t sBar = sV + NV * V_STAGE_MAX;
+  const uint32_t y_full = sBar, y_empty = sBar + 8 * NS, v_full = sBar + 16 * NS, v_empty = v_full + 8 * NV;
+  const uint32_t s_full = v_empty + 8 * NV, s_empty = s_full + 16, p_full = s_empty + 16, p_empty = p_full + 8;
+  const uint32_t nd_full = p_empty + 8, u_ready = nd_full + 8;
+  const uint32_t sTmem = u_ready + 8;
+  unsigned char* gY = gbase;
+  unsigned char* gM = gbase + NS * Y_STAGE;
+  unsigned char* gV = gM + NS * M_STAGE;
+  uint32_t* gTmem = reinterpret_cast<uint32_t*>(gbase + (sTmem - base));
+  double* gRed = reinterpret_cast<double*>(gbase + (sTmem - base) + 64);
+  long long* gRedC = reinterpret_cast<long long*>(gbase + (sTmem - base) + 64 + 256 * 8);
+
+  const int64_t rb = blockIdx.x;
+  const int64_t ch = blockIdx.y;
+  const int64_t t_begin = ch * a.tiles_per_chunk;
+  const int64_t t_end = (t_begin + a.tiles_per_chunk < a.tiles) ? t_begin + a.tiles_per_chunk : a.tiles;
+  const int T = (int)(t_end > t_begin ? t_end - t_begin : 0);
+  const int64_t row0 = rb * BM;
+  const int rows_here = (int)((a.n_rows - row0) < BM ? (a.n_rows - row0) : BM);
+
+  if (tid == 0) {
+    for (int i = 0; i < NS; ++i) { mbar_init(y_full + 8 * i, 1); mbar_init(y_empty + 8 * i, 8); }
+    for (int i = 0; i < NV; ++i) { mbar_init(v_full + 8 * i, 2); mbar_init(v_empty + 8 * i, 1); }
+    for (int i = 0; i < 2; ++i) { mbar_init(s_full + 8 * i, 1); mbar_init(s_empty + 8 * i, 8); }
+    mbar_init(p_full, 8);
+    mbar_init(p_empty, 1);
+    mbar_init(nd_full, 1);
+    mbar_init(u_ready, 8);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&P.tmY)) : "memory");
+    if (a.has_mask) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&P.tmM)) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(sTmem) : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *gTmem;
+  const uint32_t tS = tmem, tPa = tmem + 128, tPb = tmem + 192, tNa = tmem + 256, tNb = tmem + 256 + KB;
+  const uint32_t tUh = tmem + 256 + 2 * KB, tUl = tmem + 256 + 3 * KB;
+
+  if (warp == 0) {
+    // ------------------------------------------------------------ TMA producer
+    if (lane == 0) {
+      const uint32_t bytes = (uint32_t)Y_STAGE + (a.has_mask ? (uint32_t)M_STAGE : 0u);
+      for (int t = 0; t < T; ++t) {
+        const int st = t % NS;
+        mbar_wait(y_empty + 8 * st, ((t / NS) & 1) ^ 1);
+        const int64_t tile = t_begin + t;
+        const uint32_t bar = y_full + 8 * st;
+        mbar_expect_tx(bar, bytes);
+        const uint32_t dY = sY + st * Y_STAGE, dM = sM + st * M_STAGE;
+        if (a.layout == 0) {
+          tma_load_2d(dY, &P.tmY, (int)row0, (int)(tile * BN), bar);
+          if (a.has_mask) tma_load_2d(dM, &P.tmM, (int)row0, (int)(tile * BN), bar);
+        } else {
+          const int64_t ti = tile % a.tiles_inner, to = tile / a.tiles_inner;
+          if (a.layout == 1) {
+            tma_load_2d(dY, &P.tmY, (int)(ti * BN), (int)row0, bar);
+            tma_load_2d(dY + Y_STAGE / 2, &P.tmY, (int)(ti * BN + 32), (int)row0, bar);
+            if (a.has_mask) tma_load_2d(dM, &P.tmM, (int)(ti * BN), (int)row0, bar);
+          } else {
+            tma_load_3d(dY, &P.tmY, (int)(ti * BN), (int)row0, (int)to, bar);
+            tma_load_3d(dY + Y_STAGE / 2, &P.tmY, (int)(ti * BN + 32), (int)row0, (int)to, bar);
+            if (a.has_mask) tma_load_3d(dM, &P.tmM, (int)(ti * BN), (int)row0, (int)to, bar);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ------------------------------------------------------------ MMA issuer (one thread)
+    if (lane == 0 && T > 0) {
+      constexpr uint32_t id1 = idesc_tf32(128, BN, 0);   // S = U V^T : N = 64 tile columns, B K-major
+      constexpr uint32_t id2 = idesc_tf32(128, KB, 1);   // N = P V   : N = bond, B MN-major
+      mbar_wait(u_ready, 0);
+      tc_fence_after();
+      for (int t = 0; t <= T; ++t) {
+        if (t < T) {
+          const int vs = t % NV, s = t & 1;
+          mbar_wait(v_full + 8 * vs, (t / NV) & 1);
+          mbar_wait(s_empty + 8 * s, ((t >> 1) & 1) ^ 1);
+          tc_fence_after();
+          const uint32_t vb = sV + vs * V_STAGE_MAX;
+          const uint32_t d = tS + 64 * s;
+#pragma unroll
+          for (int kk = 0; kk < KB / 8; ++kk) {
+            const uint64_t bd = sdesc(vb + (kk >> 2) * (BN * 128) + (kk & 3) * 32, 16, 1024);
+            mma_ts(d, tUh + kk * 8, bd, id1, kk > 0 ? 1u : 0u);
+          }
+#pragma unroll
+          for (int kk = 0; kk < KB / 8; ++kk) {
+            const uint64_t bd = sdesc(vb + (kk >> 2) * (BN * 128) + (kk & 3) * 32, 16, 1024);
+            mma_ts(d, tUl + kk * 8, bd, id1, 1u);
+          }
+          mma_commit(s_full + 8 * s);
+          if (a.mode == 2) mma_commit(v_empty + 8 * vs);
+        }
+        if (t >= 1 && a.mode != 2) {
+          const int u = t - 1, vs = u % NV;
+          mbar_wait(p_full, u & 1);
+          tc_fence_after();
+          const uint32_t vb = sV + vs * V_STAGE_MAX;
+#pragma unroll
+          for (int kk = 0; kk < BN / 8; ++kk) {
+            const uint64_t bd = sdesc(vb + kk * 1024, BN * 128, 1024);
+            mma_ts(tNa, tPa + kk * 8, bd, id2, (u > 0 || kk > 0) ? 1u : 0u);
+            mma_ts(tNb, tPb + kk * 8, bd, id2, (u > 0 || kk > 0) ? 1u : 0u);
+          }
+          mma_commit(p_empty);
+          mma_commit(v_empty + 8 * vs);
+        }
+      }
+      mma_commit(nd_full);
+    }
+  } else if (warp < 4) {
+    // ------------------------------------------------------------ column operand V (Khatri-Rao)
+    const int x = tid - 64;   // tile column slot
+    for (int t = 0; t < T; ++t) {
+      const int vs = t % NV;
+      mbar_wait(v_empty + 8 * vs, ((t / NV) & 1) ^ 1);
+      const int64_t tile = t_begin + t;
+      int64_t col;
+      bool valid;
+      if (a.layout == 0) {
+        col = tile * BN + x;
+        valid = col < a.CO;
+      } else {
+        const int64_t ti = tile % a.tiles_inner, to = tile / a.tiles_inner;
+        const int64_t ci = ti * BN + x;
+        valid = ci < a.CI;
+        col = to * a.CI + ci;
+      }
+      int toff[kMaxTabs] = {0, 0, 0, 0};
+      if (valid) {
+        int64_t rem = col;
+        for (int d = a.nc - 1; d >= 0; --d) {
+          const int64_t i = rem % a.cdim[d];
+          rem /= a.cdim[d];
+          for (int q = 0; q < a.ntab; ++q) toff[q] += (int)(i * a.tcs[q][d]);
+        }
+      }
+      unsigned char* vrow = gV + vs * V_STAGE_MAX;
+#pragma unroll
+      for (int q4 = 0; q4 < KB / 4; ++q4) {
+        float v[4] = {0.f, 0.f, 0.f, 0.f};
+        if (valid) {
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int k = q4 * 4 + e;
+            if (k < a.K) {
+              float p = 1.f;
+              for (int q = 0; q < a.ntab; ++q) p *= __ldg(a.tab[q] + toff[q] + a.boff[q][k]);
+              v[e] = p;
+            }
+          }
+        }
+        const int atom = q4 >> 3, chunk = q4 & 7;
+        uint4 w = make_uint4(tf32_rna(v[0]), tf32_rna(v[1]), tf32_rna(v[2]), tf32_rna(v[3]));
+        const int off = atom * (BN * 128) + (x >> 3) * 1024 + (x & 7) * 128 + ((chunk ^ (x & 7)) << 4);
+        *reinterpret_cast<uint4*>(vrow + off) = w;
+      }
+      fence_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(v_full + 8 * vs);
+    }
+  } else {
+    // ------------------------------------------------------------ elementwise + epilogue
+    const int ew = tid - 128;
+    const int g = ew >> 7;                 // column half of the tile
+    const int qd = warp & 3;               // TMEM lane quarter
+    const int m = qd * 32 + lane;          // row within the block (= TMEM lane)
+    const uint32_t lane_off = (uint32_t)(qd * 32) << 16;
+    const int64_t row = row0 + m;
+    const bool row_ok = m < rows_here;
+    // U -> TMEM, split hi (g = 0) / lo (g = 1)
+    {
+#pragma unroll
+      for (int h = 0; h < KB / 32; ++h) {
+        uint32_t r[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const int k = h * 32 + j;
+          float u = (row_ok && k < a.K) ? __ldg(a.U + row * a.K + k) : 0.f;
+          const uint32_t hi = tf32_rna(u);
+          r[j] = g == 0 ? hi : tf32_rna(u - __uint_as_float(hi));
+        }
+        tmem_st32((g == 0 ? tUh : tUl) + lane_off + h * 32, r);
+      }
+      tmem_st_wait();
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(u_ready);
+    }
+    double loss_acc = 0.0;
+    long long cnt = 0;
+    for (int t = 0; t < T; ++t) {
+      const int s = t & 1;
+      const int64_t tile = t_begin + t;
+      int cols_here;
+      if (a.layout == 0) {
+        const int64_t c = a.CO - tile * BN;
+        cols_here = (int)(c < BN ? c : BN);
+      } else {
+        const int64_t ti = tile % a.tiles_inner;
+        const int64_t c = a.CI - ti * BN;
+        cols_here = (int)(c < BN ? c : BN);
+      }
+      mbar_wait(s_full + 8 * s, (t >> 1) & 1);
+      tc_fence_after();
+      uint32_t sv[32];
+      tmem_ld32(tS + 64 * s + lane_off + 32 * g, sv);
+      tmem_ld_wait(sv);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(s_empty + 8 * s);
+      const int st = t % NS;
+      mbar_wait(y_full + 8 * st, (t / NS) & 1);
+      // gather my row's 32 Y values and mask bytes
+      float yv[32];
+      uint32_t mk[8];   // 32 mask bytes packed
+      const unsigned char* ys = gY + st * Y_STAGE;
+      const unsigned char* ms = gM + st * M_STAGE;
+      if (a.layout == 0) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) yv[j] = reinterpret_cast<const float*>(ys)[(32 * g + j) * BM + m];
+        if (a.has_mask) {
+#pragma unroll
+          for (int j4 = 0; j4 < 8; ++j4) {
+            uint32_t w = 0;
+#pragma unroll
+            for (int e = 0; e < 4; ++e) w |= (uint32_t)ms[(32 * g + 4 * j4 + e) * BM + m] << (8 * e);
+            mk[j4] = w;
+          }
+        }
+      } else {
+        const unsigned char* sub = ys + g * (Y_STAGE / 2) + m * 128;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const float4 f = *reinterpret_cast<const float4*>(sub + ((q ^ (m & 7)) << 4));
+          yv[4 * q] = f.x; yv[4 * q + 1] = f.y; yv[4 * q + 2] = f.z; yv[4 * q + 3] = f.w;
+        }
+        if (a.has_mask) {
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int q = 2 * g + h;
+            const uint4 w = *reinterpret_cast<const uint4*>(ms + m * 64 + ((q ^ ((m >> 1) & 3)) << 4));
+            mk[4 * h] = w.x; mk[4 * h + 1] = w.y; mk[4 * h + 2] = w.z; mk[4 * h + 3] = w.w;
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(y_empty + 8 * st);
+      // in place: sv[] becomes P_a, yb[] becomes P_b (register pressure)
+      uint32_t (&pa)[32] = sv;
+      uint32_t yb[32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j) yb[j] = __float_as_uint(yv[j]);
+      uint32_t (&pb)[32] = yb;
+      float lsum = 0.f;
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        const int c = 32 * g + j;
+        bool obs = row_ok && c < cols_here;
+        if (a.has_mask) obs = obs && (((mk[j >> 2] >> (8 * (j & 3))) & 0xffu) != 0u);
+        const float yh = fmaxf(__uint_as_float(sv[j]), 1e-30f);
+        const float x = __uint_as_float(yb[j]);
+        float av = 0.f, bv = 0.f;
+        if (obs) {
+          ab_entry(x, yh, a.dv, av, bv);
+          if (a.mode != 0) {
+            lsum += loss_entry(x, yh, a.dv);
+            cnt += 1;
+          }
+        }
+        pa[j] = tf32_rna(av);
+        pb[j] = tf32_rna(bv);
+      }
+      loss_acc += (double)lsum;
+      if (a.mode != 2) {
+        mbar_wait(p_empty, (t & 1) ^ 1);
+        tc_fence_after();
+        tmem_st32(tPa + lane_off + 32 * g, pa);
+        tmem_st32(tPb + lane_off + 32 * g, pb);
+        tmem_st_wait();
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(p_full);
+      }
+      if (a.debug && blockIdx.x == 0 && blockIdx.y == 0 && t == 0) {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) a.debug[m * 64 + 32 * g + j] = __uint_as_float(pa[j]);
+      }
+    }
+    // epilogue: N (g = 0) / D (g = 1) for this lane -> split partials
+    if (a.mode != 2) {
+      const int64_t elems = a.n_rows * (int64_t)a.K;
+      float* out = a.Qpart + ch * 2 * elems + (int64_t)g * elems;
+      if (T > 0) {
+        mbar_wait(nd_full, 0);
+        tc_fence_after();
+#pragma unroll
+        for (int h = 0; h < KB / 32; ++h) {
+          uint32_t r[32];
+          tmem_ld32((g == 0 ? tNa : tNb) + lane_off + h * 32, r);
+          tmem_ld_wait(r);
+          if (row_ok) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (h * 32 + j < a.K) out[row * a.K + h * 32 + j] = __uint_as_float(r[j]);
+          }
+        }
+      } else if (row_ok) {
+        for (int k = 0; k < a.K; ++k) out[row * a.K + k] = 0.f;
+      }
+    }
+    if (a.mode != 0) {
+      gRed[ew] = loss_acc;
+      gRedC[ew] = cnt;
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      for (int w = 128; w > 0; w >>= 1) {
+        if (ew < w) { gRed[ew] += gRed[ew + w]; gRedC[ew] += gRedC[ew + w]; }
+        asm volatile("bar.sync 1, 256;" ::: "memory");
+      }
+      if (ew == 0) {
+        const int64_t id = (int64_t)blockIdx.y * gridDim.x + blockIdx.x;
+        a.losspart[id] = gRed[0];
+        a.countpart[id] = gRedC[0];
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+  }
+}
+
+// ------------------------------------------------------------------ host side
+static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+
+static bool get_encode() {
+  if (g_encode) return true;
+  void* fn = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn) return false;
+  g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  return true;
+}
+
+static bool encode(CUtensorMap* tm, CUtensorMapDataType dt, int rank, const void* ptr, const uint64_t* dims,
+                   const uint64_t* strides_bytes, const uint32_t* box, CUtensorMapSwizzle sw) {
+  uint32_t es[3] = {1, 1, 1};
+  CUresult r = g_encode(tm, dt, (cuuint32_t)rank, const_cast<void*>(ptr), dims, strides_bytes, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+size_t smem_bytes() { return 1024 + NS * (Y_STAGE + M_STAGE) + NV * V_STAGE_MAX + 256 + 64 + 256 * 16; }
+
+cudaError_t launch(const TcArgs& args, const float* Y, const uint8_t* M, int64_t row_blocks, int64_t chunks,
+                   cudaStream_t s) {
+  if (!get_encode()) return cudaErrorNotSupported;
+  Params P;
+  std::memset(&P, 0, sizeof(P));
+  P.a = args;
+  const int L = args.layout;
+  bool ok;
+  if (L == 0) {
+    uint64_t d[2] = {(uint64_t)args.R, (uint64_t)args.CO};
+    uint64_t sy[1] = {(uint64_t)args.R * 4};
+    uint32_t by[2] = {128, 64};
+    ok = encode(&P.tmY, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, Y, d, sy, by, CU_TENSOR_MAP_SWIZZLE_NONE);
+    if (ok && M) {
+      uint64_t sm[1] = {(uint64_t)args.R};
+      ok = encode(&P.tmM, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, M, d, sm, by, CU_TENSOR_MAP_SWIZZLE_NONE);
+    }
+  } else if (L == 1) {
+    uint64_t d[2] = {(uint64_t)args.CI, (uint64_t)args.R};
+    uint64_t sy[1] = {(uint64_t)args.CI * 4};
+    uint32_t by[2] = {32, 128};
+    ok = encode(&P.tmY, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, Y, d, sy, by, CU_TENSOR_MAP_SWIZZLE_128B);
+    if (ok && M) {
+      uint64_t sm[1] = {(uint64_t)args.CI};
+      uint32_t bm[2] = {64, 128};
+      ok = encode(&P.tmM, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, M, d, sm, bm, CU_TENSOR_MAP_SWIZZLE_64B);
+    }
+  } else {
+    uint64_t d[3] = {(uint64_t)args.CI, (uint64_t)args.R, (uint64_t)args.CO};
+    uint64_t sy[2] = {(uint64_t)args.CI * 4, (uint64_t)args.CI * (uint64_t)args.R * 4};
+    uint32_t by[3] = {32, 128, 1};
+    ok = encode(&P.tmY, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, Y, d, sy, by, CU_TENSOR_MAP_SWIZZLE_128B);
+    if (ok && M) {
+      uint64_t sm[2] = {(uint64_t)args.CI, (uint64_t)args.CI * (uint64_t)args.R};
+      uint32_t bm[3] = {64, 128, 1};
+      ok = encode(&P.tmM, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, M, d, sm, bm, CU_TENSOR_MAP_SWIZZLE_64B);
+    }
+  }
+  if (!ok) return cudaErrorInvalidValue;
+  P.a.has_mask = M ? 1 : 0;
+  const size_t smem = smem_bytes();
+  dim3 grid((unsigned)row_blocks, (unsigned)chunks);
+  cudaError_t e;
+  if (args.KB == 32) {
+    e = cudaFuncSetAttribute(fused_tc_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    fused_tc_kernel<32><<<grid, NTHREADS, smem, s>>>(P);
+  } else {
+    e = cudaFuncSetAttribute(fused_tc_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    fused_tc_kernel<64><<<grid, NTHREADS, smem, s>>>(P);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace tc
+}  // namespace nef

@@ -1,0 +1,42 @@
+// Host interface of the tcgen05 streaming kernel (kernels_tc.cu).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "kernels.h"
+#include "nef_internal.h"
+
+namespace nef {
+namespace tc {
+
+struct TcArgs {
+  int layout;                 // 0: rows innermost {R, CO}; 1: {CI, R}; 2: {CI, R, CO}
+  int has_mask;
+  int64_t R, CI, CO;          // merged extents (elements)
+  int64_t tiles_inner;        // 64-wide tiles along CI (layouts 1, 2)
+  int64_t tiles;              // total column tiles
+  int64_t tiles_per_chunk;
+  int K, KB;                  // bond and padded bond (32 | 64)
+  int64_t n_rows;             // = R
+  const float* U;             // [n_rows][K]
+  int nc;                     // column modes (linear column index unravel)
+  int64_t cdim[kMaxModes];
+  int ntab;
+  const float* tab[kMaxTabs];
+  int64_t tcs[kMaxTabs][kMaxModes];
+  int32_t boff[kMaxTabs][64];
+  float* Qpart;               // [chunks][2][n_rows][K]
+  double* losspart;           // [row_blocks * chunks]
+  long long* countpart;
+  DivParams dv;
+  int mode;                   // 0 update, 1 update + loss, 2 loss only
+  float* debug;               // optional debug dump (first tile of CTA (0,0))
+};
+
+size_t smem_bytes();
+cudaError_t launch(const TcArgs& args, const float* Y, const uint8_t* M, int64_t row_blocks, int64_t chunks,
+                   cudaStream_t s);
+
+}  // namespace tc
+}  // namespace nef

@@ -78,8 +78,20 @@ struct Lowering {
   int64_t n_chunks = 1;                    // split of the column range (deterministic partials)
   int64_t ws_end = 0;
   double cost = 0;
-  // tcgen05 eligibility (filled by the planner)
+  // tcgen05 path geometry (filled by the planner)
   bool tc_ok = false;
+  bool tc_mask_ok = false;      // uint8 mask strides are TMA-legal too
+  int tc_layout = 0;           // 0: rows innermost (2-D {R, CO}); 1: cols inner 2-D {CI, R}; 2: 3-D {CI, R, CO}
+  int64_t tc_R = 0;             // merged row extent
+  int64_t tc_CI = 1, tc_CO = 1; // merged inner / outer column extents
+  int64_t tc_rstride = 0;       // Y element stride of the merged row dim
+  int64_t tc_costride = 0;      // Y element stride of the merged outer column dim
+  int tc_KB = 32;               // padded bond (32 or 64)
+  int64_t tc_tiles = 0;         // column tiles (64 wide)
+  int64_t tc_chunks = 1;        // split of the tile range per row block
+  int64_t tc_row_blocks = 0;    // 128-row blocks
+  int64_t ws_tc_Qpart = 0;      // partial buffer for the tcgen05 path
+  int64_t ws_tc_losspart = 0;   // per-CTA loss / count partials of the tcgen05 path
 };
 
 struct Plan {

@@ -365,8 +365,52 @@ void finish_lowering(const Plan& p, Lowering& L, Bump& bump) {
     tgt.elems = felems;
     L.epi = compile_einsum(p, ein, p.ops[L.ell], bump, &tgt);
   }
-  L.ws_end = bump.off;
+  // tcgen05 / TMA geometry: the row modes must be one adjacent block of Y modes; the column
+  // modes then split into an outer block (before) and an inner block (after).
   L.tc_ok = false;
+  bool adjacent = !L.row_modes.empty();
+  for (size_t k = 1; k < L.row_modes.size(); ++k) adjacent &= L.row_modes[k] == L.row_modes[k - 1] + 1;
+  if (adjacent && L.K <= 64 && !L.col_modes.empty()) {
+    const int M = (int)p.out.size();
+    int r0 = L.row_modes.front(), r1 = L.row_modes.back();
+    int64_t R = 1, CI = 1, CO = 1;
+    for (int m = r0; m <= r1; ++m) R *= p.shape[m];
+    for (int m = r1 + 1; m < M; ++m) CI *= p.shape[m];
+    for (int m = 0; m < r0; ++m) CO *= p.shape[m];
+    bool has_inner = r1 + 1 < M, has_outer = r0 > 0;
+    L.tc_R = R;
+    L.tc_CI = CI;
+    L.tc_CO = CO;
+    L.tc_rstride = CI;
+    L.tc_costride = R * CI;
+    L.tc_layout = !has_inner ? 0 : (has_outer ? 2 : 1);
+    L.tc_KB = L.K <= 32 ? 32 : 64;
+    // TMA: every non-innermost global stride must be a multiple of 16 bytes: 4 elements for
+    // Y (fp32), 16 for the uint8 mask (a masked problem needs both)
+    bool ok = true;
+    auto strides_ok = [&](int64_t q) {
+      if (L.tc_layout == 0) return R % q == 0;                      // stride of the column dim = R
+      if (L.tc_layout == 1) return CI % q == 0;
+      return CI % q == 0 && (R * CI) % q == 0;
+    };
+    ok = strides_ok(4);
+    L.tc_mask_ok = strides_ok(16);
+    // useful width: at least half of every 64-wide column box / 128-row box must be real data
+    if (L.tc_layout == 0) ok = ok && R >= 64 && CO >= 32;
+    else ok = ok && CI >= 32 && R >= 64;
+    if (ok) {
+      L.tc_ok = true;
+      L.tc_row_blocks = (R + 127) / 128;
+      L.tc_tiles = (L.tc_layout == 0) ? (CO + 63) / 64 : ((CI + 63) / 64) * (L.tc_layout == 2 ? CO : 1);
+      int64_t ch = std::max<int64_t>(1, (p.num_sms + L.tc_row_blocks / 2) / L.tc_row_blocks);
+      ch = std::min(ch, L.tc_tiles);
+      L.tc_chunks = ch;
+      L.ws_tc_Qpart = bump.take(ch * L.tc_row_blocks * 128 * L.K * 2 * 4);
+      int64_t nparts = L.tc_row_blocks * ch;
+      L.ws_tc_losspart = bump.take(nparts * 16);
+    }
+  }
+  L.ws_end = bump.off;
 }
 
 // Cost in MAC-equivalents: streamed MACs + column-operand generation + 8 x bytes moved
@@ -539,7 +583,9 @@ std::string describe_plan(const Plan& p) {
     o << (l ? "," : "") << "{\"ell\":" << L.ell << ",\"row_idx\":\"" << L.row_idx << "\",\"col_idx\":\"" << L.col_idx
       << "\",\"bond\":\"" << L.bond << "\",\"K\":" << L.K << ",\"n_rows\":" << L.n_rows << ",\"n_cols\":" << L.n_cols
       << ",\"row_fast\":" << (L.row_fast ? "true" : "false") << ",\"n_chunks\":" << L.n_chunks
-      << ",\"tc\":" << (L.tc_ok ? "true" : "false") << ",\"row_factors\":[";
+      << ",\"tc\":" << (L.tc_ok ? "true" : "false") << ",\"tc_layout\":" << L.tc_layout << ",\"tc_R\":" << L.tc_R
+      << ",\"tc_CI\":" << L.tc_CI << ",\"tc_CO\":" << L.tc_CO << ",\"tc_KB\":" << L.tc_KB
+      << ",\"tc_tiles\":" << L.tc_tiles << ",\"tc_chunks\":" << L.tc_chunks << ",\"row_factors\":[";
     for (size_t k = 0; k < L.row_factors.size(); ++k) o << (k ? "," : "") << L.row_factors[k];
     o << "],\"col_factors\":[";
     for (size_t k = 0; k < L.col_factors.size(); ++k) o << (k ? "," : "") << L.col_factors[k];

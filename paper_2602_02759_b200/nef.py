@@ -53,6 +53,9 @@ def _load():
         "nef_plan_shard": (ctypes.c_int, [vp, ctypes.c_int, ctypes.c_int, vp]),
         "nef_last_launch_count": (ctypes.c_int64, []),
         "nef_set_kernel_policy": (ctypes.c_int, [ctypes.c_int]),
+        "nef_profile_enable": (ctypes.c_int, [ctypes.c_int]),
+        "nef_debug_dump": (ctypes.c_int, [vp]),
+        "nef_profile_read": (ctypes.c_int, [ctypes.POINTER(d), i64p, ctypes.POINTER(d)]),
         "nef_plan_destroy": (None, [vp]),
         "nef_last_error": (ctypes.c_char_p, []),
         "nef_version": (ctypes.c_char_p, []),
@@ -68,6 +71,7 @@ LIB = _load()
 EXPORTED = ("nef_plan", "nef_plan_info", "nef_factor_shape", "nef_local_shape", "nef_plan_describe", "nef_fit",
             "nef_update", "nef_num_den", "nef_apply_update", "nef_loss", "nef_host_scratch_bytes", "nef_fit_host",
             "nef_nccl_unique_id", "nef_plan_shard", "nef_last_launch_count", "nef_set_kernel_policy",
+            "nef_profile_enable", "nef_profile_read", "nef_debug_dump",
             "nef_plan_destroy", "nef_last_error", "nef_version")
 
 
@@ -203,6 +207,22 @@ def nef_last_launch_count() -> int:
 
 def nef_set_kernel_policy(policy: int):
     _check(LIB.nef_set_kernel_policy(int(policy)))
+
+
+def nef_profile_enable(on: bool = True):
+    _check(LIB.nef_profile_enable(1 if on else 0))
+
+
+def nef_profile_read():
+    ms = ctypes.c_double()
+    n = ctypes.c_int64()
+    b = ctypes.c_double()
+    _check(LIB.nef_profile_read(ctypes.byref(ms), ctypes.byref(n), ctypes.byref(b)))
+    return ms.value, n.value, b.value
+
+
+def nef_debug_dump(buf):
+    _check(LIB.nef_debug_dump(_ptr(buf)))
 
 
 def nef_version() -> str:
