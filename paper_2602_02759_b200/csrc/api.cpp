@@ -14,6 +14,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -240,6 +241,12 @@ int stream_pass(const Ctx& c, const nef::Lowering& L, const float* Y, const uint
     t.dv = dv;
     t.mode = mode;
     t.debug = g_debug;
+    {
+      const char* e = std::getenv("NEF_TC_VT");
+      t.vt = e ? std::atoi(e) : 1;
+      e = std::getenv("NEF_TC_DBG");
+      t.dbg = e ? std::atoi(e) : 0;
+    }
     prof_begin(c.s);
     CK(nef::tc::launch(t, Y, M, L.tc_row_blocks, chunks, c.s));
     prof_end(c.s, bytes);

@@ -29,12 +29,13 @@ namespace nef {
 namespace tc {
 
 constexpr int BM = 128, BN = 64;
-constexpr int NS = 4;        // Y / mask pipeline stages
+constexpr int NS = 3;        // Y / mask pipeline stages
 constexpr int NV = 3;        // V tile stages
 constexpr int NTHREADS = 384;
 constexpr int Y_STAGE = BM * BN * 4;      // 32 KB
 constexpr int M_STAGE = BM * BN;          // 8 KB
-constexpr int V_STAGE_MAX = BN * 64 * 4;  // 16 KB (KB = 64)
+constexpr int VT_OFF = BN * 64 * 4;       // V^T copy after V inside a stage
+constexpr int V_STAGE_MAX = 2 * VT_OFF;   // V (16 KB) + V^T (16 KB) for KB = 64
 
 struct __align__(64) Params {
   CUtensorMap tmY;
@@ -280,11 +281,27 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
           mbar_wait(p_full, u & 1);
           tc_fence_after();
           const uint32_t vb = sV + vs * V_STAGE_MAX;
+          const bool acc_all = (a.dbg & 1) != 0;
+          if (a.vt) {
+            // B = V^T copy, K-major SW128: rows = bond (N), K = tile columns (2 atoms of 32)
+            constexpr uint32_t id2k = idesc_tf32(128, KB, 0);
+            const uint32_t vtb = vb + VT_OFF;
 #pragma unroll
-          for (int kk = 0; kk < BN / 8; ++kk) {
-            const uint64_t bd = sdesc(vb + kk * 1024, BN * 128, 1024);
-            mma_ts(tNa, tPa + kk * 8, bd, id2, (u > 0 || kk > 0) ? 1u : 0u);
-            mma_ts(tNb, tPb + kk * 8, bd, id2, (u > 0 || kk > 0) ? 1u : 0u);
+            for (int kk = 0; kk < BN / 8; ++kk) {
+              const uint64_t bd = sdesc(vtb + (kk >> 2) * (KB * 128) + (kk & 3) * 32, 16, 1024);
+              const uint32_t acc = (acc_all || u > 0 || kk > 0) ? 1u : 0u;
+              mma_ts(tNa, tPa + kk * 8, bd, id2k, acc);
+              mma_ts(tNb, tPb + kk * 8, bd, id2k, acc);
+            }
+          } else {
+            const uint32_t idv = (a.dbg & 2) ? idesc_tf32(128, KB, 0) : id2;
+#pragma unroll
+            for (int kk = 0; kk < BN / 8; ++kk) {
+              const uint64_t bd = (a.dbg & 4) ? sdesc(vb + kk * 1024, 1024, BN * 128) : sdesc(vb + kk * 1024, BN * 128, 1024);
+              const uint32_t acc = (acc_all || u > 0 || kk > 0) ? 1u : 0u;
+              mma_ts(tNa, tPa + kk * 8, bd, idv, acc);
+              mma_ts(tNb, tPb + kk * 8, bd, idv, acc);
+            }
           }
           mma_commit(p_empty);
           mma_commit(v_empty + 8 * vs);
@@ -338,6 +355,17 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
         uint4 w = make_uint4(tf32_rna(v[0]), tf32_rna(v[1]), tf32_rna(v[2]), tf32_rna(v[3]));
         const int off = atom * (BN * 128) + (x >> 3) * 1024 + (x & 7) * 128 + ((chunk ^ (x & 7)) << 4);
         *reinterpret_cast<uint4*>(vrow + off) = w;
+        if (a.vt) {
+          // V^T[b][x]: rows = bond, K = tile column; SW128 K-major, 2 atoms of 32 columns
+          const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const int b = q4 * 4 + e;
+            const int offt = VT_OFF + (x >> 5) * (KB * 128) + (b >> 3) * 1024 + (b & 7) * 128 +
+                             ((((x & 31) >> 2) ^ (b & 7)) << 4) + (x & 3) * 4;
+            *reinterpret_cast<uint32_t*>(vrow + offt) = wv[e];
+          }
+        }
       }
       fence_async_smem();
       __syncwarp();
@@ -365,6 +393,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
           r[j] = g == 0 ? hi : tf32_rna(u - __uint_as_float(hi));
         }
         tmem_st32((g == 0 ? tUh : tUl) + lane_off + h * 32, r);
+      }
+      if (a.dbg & 1) {   // diagnostic: prefill the N / D accumulators with 1.0
+        uint32_t one[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) one[j] = __float_as_uint(1.f);
+#pragma unroll
+        for (int h = 0; h < KB / 32; ++h) tmem_st32((g == 0 ? tNa : tNb) + lane_off + h * 32, one);
       }
       tmem_st_wait();
       tc_fence_before();
