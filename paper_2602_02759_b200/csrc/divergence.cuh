@@ -1,6 +1,11 @@
 // Device-side elementwise math of the (alpha,beta)-divergence shared by the streaming
 // kernels: a(x,y) = x^alpha y^(beta-1), b(x,y) = y^(alpha+beta-1) and the loss
 // L_{alpha,beta}(x,y) in the cancellation-free u = log(x/y) forms of DESIGN.md §6.
+//
+// The streaming kernels are templated on an EwKind so that the common (alpha,beta) pairs
+// compile to a handful of instructions per entry (exponents folded into rsqrt / rcp / mul);
+// the generic pair keeps runtime exponent codes and an out-of-line loss (code size: the
+// per-tile loop is unrolled 32x and must stay inside the instruction cache).
 #pragma once
 #include <cuda_runtime.h>
 
@@ -52,8 +57,8 @@ __device__ __forceinline__ float ffun(float v) {
   return v * expf(v) - expm1f(v);
 }
 
-// L_{alpha,beta}(x, y), x = data, y = max(yhat, 1e-30)
-__device__ __forceinline__ float loss_entry(float x, float y, const DivParams& d) {
+// L_{alpha,beta}(x, y), x = data, y = max(yhat, 1e-30); out of line (generic pairs only)
+static __device__ __noinline__ float loss_entry(float x, float y, const DivParams d) {
   const float a = d.alpha, b = d.beta;
   switch (d.loss_case) {
     case 5: { float r = x - y; return 0.5f * r * r; }
@@ -75,7 +80,7 @@ __device__ __forceinline__ float loss_entry(float x, float y, const DivParams& d
   }
 }
 
-// a and b at one entry (unmasked values; the caller selects 0 at missing entries)
+// a and b at one entry, runtime exponents (unmasked values; callers select 0 when missing)
 __device__ __forceinline__ void ab_entry(float x, float yh, const DivParams& d, float& av, float& bv) {
   if (d.log_case) {
     av = logf(x / yh);
@@ -83,6 +88,124 @@ __device__ __forceinline__ void ab_entry(float x, float yh, const DivParams& d, 
   } else {
     av = powc(x, d.c_xa, d.p_xa) * powc(yh, d.c_ya, d.p_ya);
     bv = powc(yh, d.c_yb, d.p_yb);
+  }
+}
+
+// out-of-line variant for the generic kind (keeps the unrolled tile loop small)
+static __device__ __noinline__ float2 ab_entry_ool(float x, float yh, const DivParams d) {
+  float av, bv;
+  ab_entry(x, yh, d, av, bv);
+  return make_float2(av, bv);
+}
+
+// KL-type loss y f(log(x/y)) for (1, 0): x log(x/y) - x + y, stable near x = y
+__device__ __forceinline__ float kl_loss(float x, float y) {
+  if (x <= 0.f) return y;
+  const float u = logf(x / y);
+  return y * ffun(u);
+}
+
+// Compile-time specialisations of (a, b, L) for the (alpha, beta) pairs of the configs
+// (paper convention; EW_* in kernels.h).  Ew<EW_GENERIC> defers to the runtime codes.
+template <int KIND>
+struct Ew {
+  static __device__ __forceinline__ void ab(float x, float yh, const DivParams& d, float& av, float& bv) {
+    const float2 r = ab_entry_ool(x, yh, d);
+    av = r.x;
+    bv = r.y;
+  }
+  static __device__ __forceinline__ float loss(float x, float yh, const DivParams& d) { return loss_entry(x, yh, d); }
+};
+
+template <>
+struct Ew<EW_KL> {   // (1, 0): a = x / y, b = 1
+  static __device__ __forceinline__ void ab(float x, float yh, const DivParams&, float& av, float& bv) {
+    av = __fdividef(x, yh);
+    bv = 1.f;
+  }
+  static __device__ __forceinline__ float loss(float x, float yh, const DivParams&) { return kl_loss(x, yh); }
+};
+
+template <>
+struct Ew<EW_EUC> {  // (1, 1): a = x, b = y
+  static __device__ __forceinline__ void ab(float x, float yh, const DivParams&, float& av, float& bv) {
+    av = x;
+    bv = yh;
+  }
+  static __device__ __forceinline__ float loss(float x, float yh, const DivParams&) {
+    const float r = x - yh;
+    return 0.5f * r * r;
+  }
+};
+
+template <>
+struct Ew<EW_B_M05> {  // (1, -0.5): a = x y^-3/2, b = y^-1/2; L = 2 (sqrt x - sqrt y)^2 / sqrt y
+  static __device__ __forceinline__ void ab(float x, float yh, const DivParams&, float& av, float& bv) {
+    const float r = rsqrtf(yh);
+    bv = r;
+    av = x * r * r * r;
+  }
+  static __device__ __forceinline__ float loss(float x, float yh, const DivParams&) {
+    const float r = rsqrtf(yh);
+    const float d = sqrtf(x) - yh * r;
+    return 2.f * d * d * r;
+  }
+};
+
+template <>
+struct Ew<EW_A05_B0> {  // (0.5, 0): a = sqrt(x) / y, b = y^-1/2; L = 4 y^1/2 f(log(x/y)/2)
+  static __device__ __forceinline__ void ab(float x, float yh, const DivParams&, float& av, float& bv) {
+    const float r = rsqrtf(yh);
+    bv = r;
+    av = sqrtf(x) * r * r;
+  }
+  static __device__ __forceinline__ float loss(float x, float yh, const DivParams&) {
+    const float sy = sqrtf(yh);
+    if (x <= 0.f) return 4.f * sy;
+    return 4.f * sy * ffun(0.5f * logf(x / yh));
+  }
+};
+
+template <>
+struct Ew<EW_B05> {  // (1, 0.5): a = x y^-1/2, b = y^1/2
+  static __device__ __forceinline__ void ab(float x, float yh, const DivParams&, float& av, float& bv) {
+    const float r = rsqrtf(yh);
+    av = x * r;
+    bv = yh * r;
+  }
+  static __device__ __forceinline__ float loss(float x, float yh, const DivParams& d) { return loss_entry(x, yh, d); }
+};
+
+template <>
+struct Ew<EW_B2> {  // (1, 2): a = x y, b = y^2
+  static __device__ __forceinline__ void ab(float x, float yh, const DivParams&, float& av, float& bv) {
+    av = x * yh;
+    bv = yh * yh;
+  }
+  static __device__ __forceinline__ float loss(float x, float yh, const DivParams& d) { return loss_entry(x, yh, d); }
+};
+
+template <>
+struct Ew<EW_A05_B1> {  // (0.5, 1): a = sqrt(x), b = sqrt(y)
+  static __device__ __forceinline__ void ab(float x, float yh, const DivParams&, float& av, float& bv) {
+    av = sqrtf(x);
+    bv = sqrtf(yh);
+  }
+  static __device__ __forceinline__ float loss(float x, float yh, const DivParams& d) { return loss_entry(x, yh, d); }
+};
+
+// dispatch helper: calls f.template operator()<KIND>() for the pair's kind
+template <typename F>
+inline cudaError_t dispatch_ew(int kind, F&& f) {
+  switch (kind) {
+    case EW_KL: return f.template operator()<EW_KL>();
+    case EW_EUC: return f.template operator()<EW_EUC>();
+    case EW_B_M05: return f.template operator()<EW_B_M05>();
+    case EW_A05_B0: return f.template operator()<EW_A05_B0>();
+    case EW_B05: return f.template operator()<EW_B05>();
+    case EW_B2: return f.template operator()<EW_B2>();
+    case EW_A05_B1: return f.template operator()<EW_A05_B1>();
+    default: return f.template operator()<EW_GENERIC>();
   }
 }
 

@@ -13,6 +13,10 @@ enum PowCode : int { POW_0 = 0, POW_1, POW_M1, POW_H, POW_MH, POW_M15, POW_15, P
 
 int pow_code(double p);
 
+// compile-time specialisations of the elementwise stage (divergence.cuh)
+enum EwKind : int { EW_GENERIC = 0, EW_KL, EW_EUC, EW_B_M05, EW_A05_B0, EW_B05, EW_B2, EW_A05_B1 };
+int ew_kind(double alpha, double beta);
+
 // Elementwise constants of the (alpha,beta)-divergence
 struct DivParams {
   float alpha, beta;
@@ -20,6 +24,7 @@ struct DivParams {
   int c_xa, c_ya, c_yb;         // PowCode of the three exponents
   int log_case;                 // (alpha, beta) = (0, 1): a = log(x/yhat), b = 1
   int loss_case;                // 0 generic, 1 beta=0, 2 alpha=-beta, 3 alpha=0, 4 alpha=beta=0, 5 (1,1)
+  int kind;                     // EwKind
 };
 DivParams make_div(double alpha, double beta);
 

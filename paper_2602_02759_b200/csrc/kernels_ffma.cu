@@ -35,8 +35,20 @@ int pow_code(double p) {
   return POW_GEN;
 }
 
+int ew_kind(double alpha, double beta) {
+  if (alpha == 1.0 && beta == 0.0) return EW_KL;
+  if (alpha == 1.0 && beta == 1.0) return EW_EUC;
+  if (alpha == 1.0 && beta == -0.5) return EW_B_M05;
+  if (alpha == 0.5 && beta == 0.0) return EW_A05_B0;
+  if (alpha == 1.0 && beta == 0.5) return EW_B05;
+  if (alpha == 1.0 && beta == 2.0) return EW_B2;
+  if (alpha == 0.5 && beta == 1.0) return EW_A05_B1;
+  return EW_GENERIC;
+}
+
 DivParams make_div(double alpha, double beta) {
   DivParams d{};
+  d.kind = ew_kind(alpha, beta);
   d.alpha = (float)alpha;
   d.beta = (float)beta;
   d.log_case = (alpha == 0.0 && beta == 1.0);
@@ -93,7 +105,7 @@ struct FusedDev {
   int32_t boff[kMaxTabs][64];
 };
 
-template <int KP>
+template <int KP, int KIND>
 __global__ void __launch_bounds__(NT) fused_ffma_kernel(const __grid_constant__ FusedDev P) {
   extern __shared__ __align__(16) unsigned char smraw[];
   FSmem<KP>& sm = *reinterpret_cast<FSmem<KP>*>(smraw);
@@ -217,11 +229,11 @@ __global__ void __launch_bounds__(NT) fused_ffma_kernel(const __grid_constant__ 
         const float yh = fmaxf(s[i][j], 1e-30f);       // Yhat floor (reading R4)
         const float x = yy[i];
         float av, bv;
-        ab_entry(x, yh, a.dv, av, bv);
+        Ew<KIND>::ab(x, yh, a.dv, av, bv);
         pa[i] = obs ? av : 0.f;                          // select, never multiply (R5)
         pb[i] = obs ? bv : 0.f;
         if (a.mode != 0 && obs) {
-          lsum += loss_entry(x, yh, a.dv);
+          lsum += Ew<KIND>::loss(x, yh, a.dv);
           cnt += 1;
         }
       }
@@ -298,16 +310,28 @@ __global__ void __launch_bounds__(NT) fused_ffma_kernel(const __grid_constant__ 
   }
 }
 
-template <int KP>
+template <int KP, int KIND>
 static cudaError_t launch_kp(const FusedDev& d, cudaStream_t s) {
   size_t smem = sizeof(FSmem<KP>);
-  cudaError_t e = cudaFuncSetAttribute(fused_ffma_kernel<KP>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = cudaFuncSetAttribute(fused_ffma_kernel<KP, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int64_t row_blocks = (d.a.n_rows + BM - 1) / BM;
   dim3 grid((unsigned)row_blocks, (unsigned)d.a.n_chunks);
-  fused_ffma_kernel<KP><<<grid, NT, smem, s>>>(d);
+  fused_ffma_kernel<KP, KIND><<<grid, NT, smem, s>>>(d);
   return cudaGetLastError();
 }
+
+struct FfmaLauncher {
+  const FusedDev& d;
+  cudaStream_t s;
+  template <int KIND>
+  cudaError_t operator()() const {
+    if (d.a.K <= 16) return launch_kp<16, KIND>(d, s);
+    if (d.a.K <= 32) return launch_kp<32, KIND>(d, s);
+    if (d.a.K <= 64) return launch_kp<64, KIND>(d, s);
+    return cudaErrorInvalidValue;
+  }
+};
 
 cudaError_t launch_fused_ffma(const FusedArgs& a, cudaStream_t s) {
   FusedDev d;
@@ -316,10 +340,7 @@ cudaError_t launch_fused_ffma(const FusedArgs& a, cudaStream_t s) {
     for (int k = 0; k < 64; ++k) d.boff[q][k] = 0;
   for (int q = 0; q < a.ntab; ++q)
     for (int k = 0; k < a.K && k < 64; ++k) d.boff[q][k] = a.boff[q * a.K + k];
-  if (a.K <= 16) return launch_kp<16>(d, s);
-  if (a.K <= 32) return launch_kp<32>(d, s);
-  if (a.K <= 64) return launch_kp<64>(d, s);
-  return cudaErrorInvalidValue;
+  return dispatch_ew(a.dv.kind, FfmaLauncher{d, s});
 }
 
 // --------------------------------------------------------------------------------------

@@ -162,7 +162,7 @@ __host__ __device__ constexpr uint32_t idesc_tf32(int M, int N, int b_mn_major) 
 }
 
 // ------------------------------------------------------------------ the kernel
-template <int KB>
+template <int KB, int KIND>
 __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_constant__ Params P) {
   extern __shared__ unsigned char smraw[];
   const TcArgs& a = P.a;
@@ -337,34 +337,37 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
         }
       }
       unsigned char* vrow = gV + vs * V_STAGE_MAX;
+      // V[x][k] = prod_q T_q[toff_q + boff_q[k]] (Khatri-Rao row), then TF32 round-to-nearest
+      float v[KB];
+#pragma unroll
+      for (int k = 0; k < KB; ++k) v[k] = (valid && k < a.K) ? 1.f : 0.f;
+      if (valid) {
+#pragma unroll 1
+        for (int q = 0; q < a.ntab; ++q) {
+          const float* tp = a.tab[q] + toff[q];
+#pragma unroll
+          for (int k = 0; k < KB; ++k)
+            if (k < a.K) v[k] *= __ldg(tp + a.boff[q][k]);
+        }
+      }
+      uint32_t w[KB];
+#pragma unroll
+      for (int k = 0; k < KB; ++k) w[k] = tf32_rna(v[k]);
+      // V: rows = tile column x, K = bond; SW128 K-major atoms of 32 bond elements
 #pragma unroll
       for (int q4 = 0; q4 < KB / 4; ++q4) {
-        float v[4] = {0.f, 0.f, 0.f, 0.f};
-        if (valid) {
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const int k = q4 * 4 + e;
-            if (k < a.K) {
-              float p = 1.f;
-              for (int q = 0; q < a.ntab; ++q) p *= __ldg(a.tab[q] + toff[q] + a.boff[q][k]);
-              v[e] = p;
-            }
-          }
-        }
         const int atom = q4 >> 3, chunk = q4 & 7;
-        uint4 w = make_uint4(tf32_rna(v[0]), tf32_rna(v[1]), tf32_rna(v[2]), tf32_rna(v[3]));
         const int off = atom * (BN * 128) + (x >> 3) * 1024 + (x & 7) * 128 + ((chunk ^ (x & 7)) << 4);
-        *reinterpret_cast<uint4*>(vrow + off) = w;
-        if (a.vt) {
-          // V^T[b][x]: rows = bond, K = tile column; SW128 K-major, 2 atoms of 32 columns
-          const uint32_t wv[4] = {w.x, w.y, w.z, w.w};
+        *reinterpret_cast<uint4*>(vrow + off) = make_uint4(w[4 * q4], w[4 * q4 + 1], w[4 * q4 + 2], w[4 * q4 + 3]);
+      }
+      if (a.vt) {
+        // V^T[b][x]: rows = bond, K = tile column; SW128 K-major, 2 atoms of 32 columns
+        const int base_t = VT_OFF + (x >> 5) * (KB * 128) + (x & 3) * 4;
+        const int cx = (x & 31) >> 2;
 #pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const int b = q4 * 4 + e;
-            const int offt = VT_OFF + (x >> 5) * (KB * 128) + (b >> 3) * 1024 + (b & 7) * 128 +
-                             ((((x & 31) >> 2) ^ (b & 7)) << 4) + (x & 3) * 4;
-            *reinterpret_cast<uint32_t*>(vrow + offt) = wv[e];
-          }
+        for (int b = 0; b < KB; ++b) {
+          const int offt = base_t + (b >> 3) * 1024 + (b & 7) * 128 + ((cx ^ (b & 7)) << 4);
+          *reinterpret_cast<uint32_t*>(vrow + offt) = w[b];
         }
       }
       fence_async_smem();
@@ -382,7 +385,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
     const bool row_ok = m < rows_here;
     // U -> TMEM, split hi (g = 0) / lo (g = 1)
     {
-#pragma unroll
+#pragma unroll 1
       for (int h = 0; h < KB / 32; ++h) {
         uint32_t r[32];
 #pragma unroll
@@ -481,9 +484,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
         const float x = __uint_as_float(yb[j]);
         float av = 0.f, bv = 0.f;
         if (obs) {
-          ab_entry(x, yh, a.dv, av, bv);
+          Ew<KIND>::ab(x, yh, a.dv, av, bv);
           if (a.mode != 0) {
-            lsum += loss_entry(x, yh, a.dv);
+            lsum += Ew<KIND>::loss(x, yh, a.dv);
             cnt += 1;
           }
         }
@@ -513,7 +516,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
       if (T > 0) {
         mbar_wait(nd_full, 0);
         tc_fence_after();
-#pragma unroll
+#pragma unroll 1
         for (int h = 0; h < KB / 32; ++h) {
           uint32_t r[32];
           tmem_ld32((g == 0 ? tNa : tNb) + lane_off + h * 32, r);
@@ -572,6 +575,28 @@ static bool encode(CUtensorMap* tm, CUtensorMapDataType dt, int rank, const void
   return r == CUDA_SUCCESS;
 }
 
+struct TcLauncher {
+  const Params& P;
+  dim3 grid;
+  size_t smem;
+  cudaStream_t s;
+  int KB;
+  template <int KIND>
+  cudaError_t operator()() const {
+    cudaError_t e;
+    if (KB == 32) {
+      e = cudaFuncSetAttribute(fused_tc_kernel<32, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      fused_tc_kernel<32, KIND><<<grid, NTHREADS, smem, s>>>(P);
+    } else {
+      e = cudaFuncSetAttribute(fused_tc_kernel<64, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      fused_tc_kernel<64, KIND><<<grid, NTHREADS, smem, s>>>(P);
+    }
+    return cudaGetLastError();
+  }
+};
+
 size_t smem_bytes() { return 1024 + NS * (Y_STAGE + M_STAGE) + NV * V_STAGE_MAX + 256 + 64 + 256 * 16; }
 
 cudaError_t launch(const TcArgs& args, const float* Y, const uint8_t* M, int64_t row_blocks, int64_t chunks,
@@ -616,17 +641,7 @@ cudaError_t launch(const TcArgs& args, const float* Y, const uint8_t* M, int64_t
   P.a.has_mask = M ? 1 : 0;
   const size_t smem = smem_bytes();
   dim3 grid((unsigned)row_blocks, (unsigned)chunks);
-  cudaError_t e;
-  if (args.KB == 32) {
-    e = cudaFuncSetAttribute(fused_tc_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    fused_tc_kernel<32><<<grid, NTHREADS, smem, s>>>(P);
-  } else {
-    e = cudaFuncSetAttribute(fused_tc_kernel<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    fused_tc_kernel<64><<<grid, NTHREADS, smem, s>>>(P);
-  }
-  return cudaGetLastError();
+  return dispatch_ew(args.dv.kind, TcLauncher{P, grid, smem, s, args.KB});
 }
 
 }  // namespace tc
