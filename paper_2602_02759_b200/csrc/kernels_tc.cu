@@ -468,32 +468,44 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(y_empty + 8 * st);
-      // in place: sv[] becomes P_a, yb[] becomes P_b (register pressure)
+      // observed-entry bits: row / column in range and mask byte nonzero (R5, R6)
+      const int cv = cols_here - 32 * g;
+      uint32_t obs = (!row_ok || cv <= 0) ? 0u : (cv >= 32 ? 0xffffffffu : ((1u << cv) - 1u));
+      if (a.has_mask) {
+        uint32_t mb = 0;
+#pragma unroll
+        for (int j4 = 0; j4 < 8; ++j4) {
+          const uint32_t nz = __vcmpne4(mk[j4], 0u);   // 0xff per nonzero byte
+          mb |= ((nz & 1u) | ((nz >> 7) & 2u) | ((nz >> 14) & 4u) | ((nz >> 21) & 8u)) << (4 * j4);
+        }
+        obs &= mb;
+      }
+      // masked values are replaced before any arithmetic (never used, NaN-safe)
+#pragma unroll
+      for (int j = 0; j < 32; ++j) yv[j] = ((obs >> j) & 1u) ? yv[j] : 1.f;
+      if (a.mode != 0) {   // loss of the iterate entering the sweep (uniform branch)
+        float lsum = 0.f;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const float l = Ew<KIND>::loss(yv[j], fmaxf(__uint_as_float(sv[j]), 1e-30f), a.dv);
+          lsum += ((obs >> j) & 1u) ? l : 0.f;
+        }
+        loss_acc += (double)lsum;
+        cnt += __popc(obs);
+      }
+      // in place: sv[] becomes P_a, yb[] becomes P_b (register pressure); branch-free selects
       uint32_t (&pa)[32] = sv;
       uint32_t yb[32];
-#pragma unroll
-      for (int j = 0; j < 32; ++j) yb[j] = __float_as_uint(yv[j]);
       uint32_t (&pb)[32] = yb;
-      float lsum = 0.f;
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
-        const int c = 32 * g + j;
-        bool obs = row_ok && c < cols_here;
-        if (a.has_mask) obs = obs && (((mk[j >> 2] >> (8 * (j & 3))) & 0xffu) != 0u);
         const float yh = fmaxf(__uint_as_float(sv[j]), 1e-30f);
-        const float x = __uint_as_float(yb[j]);
-        float av = 0.f, bv = 0.f;
-        if (obs) {
-          Ew<KIND>::ab(x, yh, a.dv, av, bv);
-          if (a.mode != 0) {
-            lsum += Ew<KIND>::loss(x, yh, a.dv);
-            cnt += 1;
-          }
-        }
-        pa[j] = tf32_rna(av);
-        pb[j] = tf32_rna(bv);
+        float av, bv;
+        Ew<KIND>::ab(yv[j], yh, a.dv, av, bv);
+        const bool o = (obs >> j) & 1u;
+        pa[j] = o ? tf32_rna(av) : 0u;
+        pb[j] = o ? tf32_rna(bv) : 0u;
       }
-      loss_acc += (double)lsum;
       if (a.mode != 2) {
         mbar_wait(p_empty, (t & 1) ^ 1);
         tc_fence_after();
