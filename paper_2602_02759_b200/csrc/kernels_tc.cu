@@ -311,7 +311,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
     }
   } else if (warp < 4) {
     // ------------------------------------------------------------ column operand V (Khatri-Rao)
-    const int x = tid - 64;   // tile column slot
+    // Each warp owns 32 tile columns; lane = column slot for the offset arithmetic, then
+    // lane = bond index for the coalesced table-row loads and the swizzled stores.
+    const int xw = (warp - 2) * 32;
+    const int x = xw + lane;   // tile column slot whose offsets this lane computes
     for (int t = 0; t < T; ++t) {
       const int vs = t % NV;
       mbar_wait(v_empty + 8 * vs, ((t / NV) & 1) ^ 1);
@@ -337,37 +340,42 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
         }
       }
       unsigned char* vrow = gV + vs * V_STAGE_MAX;
-      // V[x][k] = prod_q T_q[toff_q + boff_q[k]] (Khatri-Rao row), then TF32 round-to-nearest
-      float v[KB];
+      // V[x][k] = prod_q T_q[toff_q(x) + boff_q[k]] (Khatri-Rao row), TF32 round-to-nearest.
+      // lane = bond index k (+32 h): each warp load reads one contiguous table row.
+      int bo[kMaxTabs][KB / 32];
 #pragma unroll
-      for (int k = 0; k < KB; ++k) v[k] = (valid && k < a.K) ? 1.f : 0.f;
-      if (valid) {
-#pragma unroll 1
+      for (int q = 0; q < kMaxTabs; ++q)
+#pragma unroll
+        for (int h = 0; h < KB / 32; ++h) bo[q][h] = (q < a.ntab && h * 32 + lane < a.K) ? a.boff[q][h * 32 + lane] : 0;
+      const uint32_t vmask = __ballot_sync(0xffffffffu, valid);
+#pragma unroll 4
+      for (int i = 0; i < 32; ++i) {
+        const int xi = xw + i;
+        const bool vi = (vmask >> i) & 1u;
+        float p[KB / 32];
+#pragma unroll
+        for (int h = 0; h < KB / 32; ++h) p[h] = (vi && h * 32 + lane < a.K) ? 1.f : 0.f;
         for (int q = 0; q < a.ntab; ++q) {
-          const float* tp = a.tab[q] + toff[q];
+          const int to = __shfl_sync(0xffffffffu, toff[q], i);
+          const float* tp = a.tab[q] + to;
 #pragma unroll
-          for (int k = 0; k < KB; ++k)
-            if (k < a.K) v[k] *= __ldg(tp + a.boff[q][k]);
+          for (int h = 0; h < KB / 32; ++h)
+            if (p[h] != 0.f) p[h] *= __ldg(tp + bo[q][h]);
         }
-      }
-      uint32_t w[KB];
 #pragma unroll
-      for (int k = 0; k < KB; ++k) w[k] = tf32_rna(v[k]);
-      // V: rows = tile column x, K = bond; SW128 K-major atoms of 32 bond elements
-#pragma unroll
-      for (int q4 = 0; q4 < KB / 4; ++q4) {
-        const int atom = q4 >> 3, chunk = q4 & 7;
-        const int off = atom * (BN * 128) + (x >> 3) * 1024 + (x & 7) * 128 + ((chunk ^ (x & 7)) << 4);
-        *reinterpret_cast<uint4*>(vrow + off) = make_uint4(w[4 * q4], w[4 * q4 + 1], w[4 * q4 + 2], w[4 * q4 + 3]);
-      }
-      if (a.vt) {
-        // V^T[b][x]: rows = bond, K = tile column; SW128 K-major, 2 atoms of 32 columns
-        const int base_t = VT_OFF + (x >> 5) * (KB * 128) + (x & 3) * 4;
-        const int cx = (x & 31) >> 2;
-#pragma unroll
-        for (int b = 0; b < KB; ++b) {
-          const int offt = base_t + (b >> 3) * 1024 + (b & 7) * 128 + ((cx ^ (b & 7)) << 4);
-          *reinterpret_cast<uint32_t*>(vrow + offt) = w[b];
+        for (int h = 0; h < KB / 32; ++h) {
+          const uint32_t w = tf32_rna(p[h]);
+          const int k = h * 32 + lane;
+          // V: row xi, K = bond (SW128 K-major atoms of 32 bond elements)
+          const int off = h * (BN * 128) + (xi >> 3) * 1024 + (xi & 7) * 128 + ((((k & 31) >> 2) ^ (xi & 7)) << 4) +
+                          (k & 3) * 4;
+          *reinterpret_cast<uint32_t*>(vrow + off) = w;
+          if (a.vt) {
+            // V^T: row k (bond), K = tile column xi; SW128 K-major, 2 atoms of 32 columns
+            const int offt = VT_OFF + (xi >> 5) * (KB * 128) + (k >> 3) * 1024 + (k & 7) * 128 +
+                             ((((xi & 31) >> 2) ^ (k & 7)) << 4) + (xi & 3) * 4;
+            *reinterpret_cast<uint32_t*>(vrow + offt) = w;
+          }
         }
       }
       fence_async_smem();

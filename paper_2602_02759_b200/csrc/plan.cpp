@@ -402,7 +402,8 @@ void finish_lowering(const Plan& p, Lowering& L, Bump& bump) {
       L.tc_ok = true;
       L.tc_row_blocks = (R + 127) / 128;
       L.tc_tiles = (L.tc_layout == 0) ? (CO + 63) / 64 : ((CI + 63) / 64) * (L.tc_layout == 2 ? CO : 1);
-      int64_t ch = std::max<int64_t>(1, (p.num_sms + L.tc_row_blocks / 2) / L.tc_row_blocks);
+      // one CTA per SM (TMEM 512 columns, ~220 KB smem): never exceed one wave
+      int64_t ch = std::max<int64_t>(1, p.num_sms / L.tc_row_blocks);
       ch = std::min(ch, L.tc_tiles);
       L.tc_chunks = ch;
       L.ws_tc_Qpart = bump.take(ch * L.tc_row_blocks * 128 * L.K * 2 * 4);
