@@ -234,6 +234,15 @@ int stream_pass(const Ctx& c, const nef::Lowering& L, const float* Y, const uint
       for (int k = 0; k < a.nc; ++k) t.tcs[q][k] = a.tcs[q][k];
       for (int k = 0; k < L.K; ++k) t.boff[q][k] = boff[(size_t)q * L.K + k];
     }
+    {
+      bool v4 = (L.K % 4 == 0);
+      for (int q = 0; q < a.ntab && v4; ++q) {
+        v4 = (reinterpret_cast<uintptr_t>(a.tab[q]) & 15) == 0;
+        for (int k = 0; k < a.nc; ++k) v4 = v4 && (a.tcs[q][k] % 4 == 0);
+        for (int k = 0; k < L.K; ++k) v4 = v4 && (boff[(size_t)q * L.K + k] == k);
+      }
+      t.vec4 = v4 && a.ntab > 0 ? 1 : 0;
+    }
     t.Qpart = reinterpret_cast<float*>(c.ws + L.ws_tc_Qpart);
     t.losspart = reinterpret_cast<double*>(c.ws + L.ws_tc_losspart);
     o.nparts = L.tc_row_blocks * chunks;

@@ -340,14 +340,64 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
         }
       }
       unsigned char* vrow = gV + vs * V_STAGE_MAX;
-      // V[x][k] = prod_q T_q[toff_q(x) + boff_q[k]] (Khatri-Rao row), TF32 round-to-nearest.
-      // lane = bond index k (+32 h): each warp load reads one contiguous table row.
+      const uint32_t vmask = __ballot_sync(0xffffffffu, valid);
+      if (a.vec4) {
+        // Vector path (bond contiguous in every table, rows 16-byte aligned): lane = (row
+        // sub-index, 16-byte chunk); each warp load covers 32/C full table rows and all loads
+        // of a table are in flight together (L1 is small next to ~220 KB of smem).
+        constexpr int C = KB / 4;          // 16-byte chunks per padded row
+        constexpr int RL = 32 / C;         // rows per warp load
+        constexpr int NL = 32 / RL;        // loads per table per warp (= C)
+        const int rs = lane / C, c = lane % C;
+        const bool kok = c * 4 < a.K;
+        float4 acc[NL];
+#pragma unroll
+        for (int l = 0; l < NL; ++l) acc[l] = make_float4(1.f, 1.f, 1.f, 1.f);
+        for (int q = 0; q < a.ntab; ++q) {
+          float4 ld[NL];
+#pragma unroll
+          for (int l = 0; l < NL; ++l) {
+            const int xl = l * RL + rs;
+            const int to = __shfl_sync(0xffffffffu, toff[q], xl);
+            ld[l] = (((vmask >> xl) & 1u) && kok) ? __ldg(reinterpret_cast<const float4*>(a.tab[q] + to) + c)
+                                                  : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+#pragma unroll
+          for (int l = 0; l < NL; ++l) {
+            acc[l].x *= ld[l].x; acc[l].y *= ld[l].y; acc[l].z *= ld[l].z; acc[l].w *= ld[l].w;
+          }
+        }
+#pragma unroll
+        for (int l = 0; l < NL; ++l) {
+          const int xi = xw + l * RL + rs;
+          const bool ok = ((vmask >> (l * RL + rs)) & 1u) && kok && a.ntab > 0;
+          const uint32_t w0 = ok ? tf32_rna(acc[l].x) : 0u, w1 = ok ? tf32_rna(acc[l].y) : 0u;
+          const uint32_t w2 = ok ? tf32_rna(acc[l].z) : 0u, w3 = ok ? tf32_rna(acc[l].w) : 0u;
+          const int atom = c >> 3, chunk = c & 7;
+          const int off = atom * (BN * 128) + (xi >> 3) * 1024 + (xi & 7) * 128 + ((chunk ^ (xi & 7)) << 4);
+          *reinterpret_cast<uint4*>(vrow + off) = make_uint4(w0, w1, w2, w3);
+          if (a.vt) {
+            const uint32_t wv[4] = {w0, w1, w2, w3};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int k = 4 * c + e;
+              const int offt = VT_OFF + (xi >> 5) * (KB * 128) + (k >> 3) * 1024 + (k & 7) * 128 +
+                               ((((xi & 31) >> 2) ^ (k & 7)) << 4) + (xi & 3) * 4;
+              *reinterpret_cast<uint32_t*>(vrow + offt) = wv[e];
+            }
+          }
+        }
+        fence_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(v_full + 8 * vs);
+        continue;
+      }
+      // Scalar path: lane = bond index k (+32 h); each warp load reads one contiguous table row.
       int bo[kMaxTabs][KB / 32];
 #pragma unroll
       for (int q = 0; q < kMaxTabs; ++q)
 #pragma unroll
         for (int h = 0; h < KB / 32; ++h) bo[q][h] = (q < a.ntab && h * 32 + lane < a.K) ? a.boff[q][h * 32 + lane] : 0;
-      const uint32_t vmask = __ballot_sync(0xffffffffu, valid);
 #pragma unroll 4
       for (int i = 0; i < 32; ++i) {
         const int xi = xw + i;

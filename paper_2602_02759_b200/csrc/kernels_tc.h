@@ -33,6 +33,8 @@ struct TcArgs {
   int mode;                   // 0 update, 1 update + loss, 2 loss only
   float* debug;               // optional debug dump (first tile of CTA (0,0))
   int vt;                     // 1: numerator MMAs read a K-major V^T copy; 0: MN-major view of V
+  int vec4;                   // 1: every table has the bond contiguous (boff[k] = k), K % 4 == 0 and
+                              //    16-byte aligned rows -> float4 V generation
   int dbg;                    // diagnostics: 1 prefill N/D with 1 and always accumulate,
                               // 2 numerator B as K-major, 4 swap LBO/SBO of the MN-major view
 };
