@@ -7,12 +7,17 @@
 //   N  += P_a V,  D += P_b V  (TF32 MMAs, A operand = P in TMEM, accumulators in TMEM)
 // Y and the mask are streamed HBM -> smem by TMA exactly once; Yhat, a and b never leave the SM.
 //
-// CTA = 128 rows (TMEM lanes) x a contiguous range of 64-column tiles.  384 threads:
+// CTA = 128 rows (TMEM lanes) x a contiguous range of 64-column tiles.  512 threads:
 //   warp 0      TMA producer (Y / mask ring of NS stages)
 //   warp 1      TMEM allocator + single-thread MMA issuer
-//   warps 2-3   column-operand generator: V tile = prod of column tables (Khatri-Rao), TF32
-//               round-to-nearest, written in the UMMA SW128 K-major layout (NV stages)
-//   warps 4-11  elementwise: tcgen05.ld S -> a, b (+ loss) -> tcgen05.st P; epilogue N, D
+//   warps 2-3   idle
+//   warps 4-7   column operand: V tile = prod of column tables (Khatri-Rao), 16 columns per
+//               warp; rows constant across the tile are loaded once and broadcast; the next
+//               tile's table rows are in flight while the current tile is stored; TF32
+//               round-to-nearest, written twice in the UMMA SW128 K-major layout: V (rows = tile
+//               columns, K = bond) for the reconstruction MMA and V^T (rows = bond, K = tile
+//               columns) for the numerator / denominator MMAs
+//   warps 8-15  elementwise: tcgen05.ld S -> a, b (+ loss) -> tcgen05.st P; epilogue N, D
 // TMEM (512 columns): S[2] (2x64) | P_a, P_b (2x64) | N, D (2xKB) | U_hi, U_lo (2xKB)
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -31,7 +36,8 @@ namespace tc {
 constexpr int BM = 128, BN = 64;
 constexpr int NS = 3;        // Y / mask pipeline stages
 constexpr int NV = 3;        // V tile stages
-constexpr int NTHREADS = 384;
+constexpr int NTHREADS = 512;
+constexpr int NVG = 4;       // V-generator warps (16 tile columns each)
 constexpr int Y_STAGE = BM * BN * 4;      // 32 KB
 constexpr int M_STAGE = BM * BN;          // 8 KB
 constexpr int VT_OFF = BN * 64 * 4;       // V^T copy after V inside a stage
@@ -100,41 +106,33 @@ __device__ __forceinline__ void mma_commit(uint32_t bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar) : "memory");
 }
 
-#define NEF_R32(x)                                                                                                    \
-  "=r"(x[0]), "=r"(x[1]), "=r"(x[2]), "=r"(x[3]), "=r"(x[4]), "=r"(x[5]), "=r"(x[6]), "=r"(x[7]), "=r"(x[8]),      \
-      "=r"(x[9]), "=r"(x[10]), "=r"(x[11]), "=r"(x[12]), "=r"(x[13]), "=r"(x[14]), "=r"(x[15]), "=r"(x[16]),        \
-      "=r"(x[17]), "=r"(x[18]), "=r"(x[19]), "=r"(x[20]), "=r"(x[21]), "=r"(x[22]), "=r"(x[23]), "=r"(x[24]),       \
-      "=r"(x[25]), "=r"(x[26]), "=r"(x[27]), "=r"(x[28]), "=r"(x[29]), "=r"(x[30]), "=r"(x[31])
-#define NEF_W32(x)                                                                                                    \
-  "r"(x[0]), "r"(x[1]), "r"(x[2]), "r"(x[3]), "r"(x[4]), "r"(x[5]), "r"(x[6]), "r"(x[7]), "r"(x[8]), "r"(x[9]),     \
-      "r"(x[10]), "r"(x[11]), "r"(x[12]), "r"(x[13]), "r"(x[14]), "r"(x[15]), "r"(x[16]), "r"(x[17]), "r"(x[18]),   \
-      "r"(x[19]), "r"(x[20]), "r"(x[21]), "r"(x[22]), "r"(x[23]), "r"(x[24]), "r"(x[25]), "r"(x[26]), "r"(x[27]),   \
-      "r"(x[28]), "r"(x[29]), "r"(x[30]), "r"(x[31])
+#define NEF_R16(x)                                                                                              \
+  "=r"(x[0]), "=r"(x[1]), "=r"(x[2]), "=r"(x[3]), "=r"(x[4]), "=r"(x[5]), "=r"(x[6]), "=r"(x[7]), "=r"(x[8]), \
+      "=r"(x[9]), "=r"(x[10]), "=r"(x[11]), "=r"(x[12]), "=r"(x[13]), "=r"(x[14]), "=r"(x[15])
+#define NEF_P16(x)                                                                                              \
+  "+r"(x[0]), "+r"(x[1]), "+r"(x[2]), "+r"(x[3]), "+r"(x[4]), "+r"(x[5]), "+r"(x[6]), "+r"(x[7]), "+r"(x[8]), \
+      "+r"(x[9]), "+r"(x[10]), "+r"(x[11]), "+r"(x[12]), "+r"(x[13]), "+r"(x[14]), "+r"(x[15])
+#define NEF_W16(x)                                                                                                \
+  "r"(x[0]), "r"(x[1]), "r"(x[2]), "r"(x[3]), "r"(x[4]), "r"(x[5]), "r"(x[6]), "r"(x[7]), "r"(x[8]), "r"(x[9]), \
+      "r"(x[10]), "r"(x[11]), "r"(x[12]), "r"(x[13]), "r"(x[14]), "r"(x[15])
 
-// 32 consecutive TMEM columns of this thread's lane
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+// 16 / 32 consecutive TMEM columns of this thread's lane
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
   asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
-      "%16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"
-      : NEF_R32(r)
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15}, "
+      "[%16];"
+      : NEF_R16(r)
       : "r"(taddr));
 }
 // wait for tcgen05.ld; the registers are tied in so no use can be scheduled above the wait
-__device__ __forceinline__ void tmem_ld_wait(uint32_t (&r)[32]) {
-  asm volatile("tcgen05.wait::ld.sync.aligned;"
-               : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
-                 "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]), "+r"(r[15]),
-                 "+r"(r[16]), "+r"(r[17]), "+r"(r[18]), "+r"(r[19]), "+r"(r[20]), "+r"(r[21]), "+r"(r[22]),
-                 "+r"(r[23]), "+r"(r[24]), "+r"(r[25]), "+r"(r[26]), "+r"(r[27]), "+r"(r[28]), "+r"(r[29]),
-                 "+r"(r[30]), "+r"(r[31])
-               :
-               : "memory");
+__device__ __forceinline__ void tmem_ld_wait(uint32_t (&r)[16]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" : NEF_P16(r) : : "memory");
 }
-__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32]) {
+__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
   asm volatile(
-      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, "
-      "%15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31, %32};" ::"r"(taddr),
-      NEF_W32(r)
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, %13, %14, %15, "
+      "%16};" ::"r"(taddr),
+      NEF_W16(r)
       : "memory");
 }
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
@@ -155,10 +153,167 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t
   d |= (uint64_t)2 << 61;
   return d;
 }
-// instruction descriptor: kind::tf32, D f32, A/B tf32, A K-major, B K- or MN-major
-__host__ __device__ constexpr uint32_t idesc_tf32(int M, int N, int b_mn_major) {
-  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)b_mn_major << 16) | ((uint32_t)(N >> 3) << 17) |
-         ((uint32_t)(M >> 4) << 24);
+// instruction descriptor: kind::tf32, D f32, A/B tf32, A and B K-major
+__host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+
+// byte offset of element (row, k) in an SW128 K-major operand whose rows are 128-byte atoms,
+// `rows` rows per atom column block (atom column = 32 fp32 along K)
+__device__ __forceinline__ int sw128_off(int row, int k, int rows) {
+  return (k >> 5) * (rows * 128) + (row >> 3) * 1024 + (row & 7) * 128 + ((((k & 31) >> 2) ^ (row & 7)) << 4) +
+         (k & 3) * 4;
+}
+
+// ------------------------------------------------------------------ column operand generator
+// Table rows of one tile held in registers (software pipelining across tiles).
+template <int KB>
+struct VTile {
+  static constexpr int C = KB / 4;     // 16-byte chunks per padded row
+  static constexpr int RL = 32 / C;    // rows per warp load
+  static constexpr int NL = 16 / RL;   // loads per warp (16 rows per warp)
+  float4 ld[NL];                       // varying table rows (chunk c of row l*RL+rs)
+  float4 cst;                          // product of the tile-constant rows (chunk c)
+  uint32_t vmask;                      // valid tile columns of this warp (16 bits)
+  int mode;                            // 0 fast (<= 1 varying table), 1 general, 2 empty
+};
+
+template <int KB>
+__device__ __forceinline__ void vtile_issue(const TcArgs& a, int64_t tile, int xw, int lane, VTile<KB>& v,
+                                            int (&toff)[kMaxTabs]) {
+  using VT = VTile<KB>;
+  const int xl = lane & 15;
+  const int x = xw + xl;
+  int64_t col;
+  bool valid;
+  if (a.layout == 0) {
+    col = tile * BN + x;
+    valid = col < a.CO;
+  } else {
+    const int64_t ti = tile % a.tiles_inner, to = tile / a.tiles_inner;
+    const int64_t ci = ti * BN + x;
+    valid = ci < a.CI;
+    col = to * a.CI + ci;
+  }
+#pragma unroll
+  for (int q = 0; q < kMaxTabs; ++q) toff[q] = 0;
+  if (valid) {
+    int64_t rem = col;
+    for (int d = a.nc - 1; d >= 0; --d) {
+      const int64_t i = rem % a.cdim[d];
+      rem /= a.cdim[d];
+#pragma unroll
+      for (int q = 0; q < kMaxTabs; ++q)
+        if (q < a.ntab) toff[q] += (int)(i * a.tcs[q][d]);
+    }
+  }
+  v.vmask = __ballot_sync(0xffffffffu, valid) & 0xffffu;
+  if (v.vmask == 0u || !a.vec4) {
+    v.mode = v.vmask == 0u ? 2 : 1;
+    return;
+  }
+  const int first = __ffs(v.vmask) - 1;
+  const int rs = lane / VT::C, c = lane % VT::C;
+  const bool kok = c * 4 < a.K;
+  int nvar = 0, var_q = -1;
+  v.cst = make_float4(1.f, 1.f, 1.f, 1.f);
+#pragma unroll
+  for (int q = 0; q < kMaxTabs; ++q) {
+    if (q >= a.ntab) break;
+    const int t0 = __shfl_sync(0xffffffffu, toff[q], first);
+    const bool uni = __all_sync(0xffffffffu, !valid || toff[q] == t0);
+    if (uni) {
+      const float4 r = kok ? __ldg(reinterpret_cast<const float4*>(a.tab[q] + t0) + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+      v.cst.x *= r.x; v.cst.y *= r.y; v.cst.z *= r.z; v.cst.w *= r.w;
+    } else {
+      ++nvar;
+      var_q = q;
+    }
+  }
+  if (nvar > 1) {
+    v.mode = 1;
+    return;
+  }
+  v.mode = 0;
+  if (var_q < 0) {
+#pragma unroll
+    for (int l = 0; l < VT::NL; ++l) v.ld[l] = make_float4(1.f, 1.f, 1.f, 1.f);
+    return;
+  }
+  int tv = toff[0];
+#pragma unroll
+  for (int q = 1; q < kMaxTabs; ++q)
+    if (q == var_q) tv = toff[q];
+  const float4* tab = reinterpret_cast<const float4*>(a.tab[var_q]);
+#pragma unroll
+  for (int l = 0; l < VT::NL; ++l) {
+    const int xi = l * VT::RL + rs;
+    const int to = __shfl_sync(0xffffffffu, tv, xi);
+    v.ld[l] = (((v.vmask >> xi) & 1u) && kok) ? __ldg(tab + (to >> 2) + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+}
+
+template <int KB>
+__device__ __forceinline__ void vtile_store(const TcArgs& a, int xw, int lane, const VTile<KB>& v,
+                                            const int (&toff)[kMaxTabs], unsigned char* vrow) {
+  using VT = VTile<KB>;
+  const int rs = lane / VT::C, c = lane % VT::C;
+  const bool kok = c * 4 < a.K;
+  if (v.mode == 1 && a.vec4) {
+    // general vector path: several varying tables, product formed after all loads of a table
+#pragma unroll
+    for (int l = 0; l < VT::NL; ++l) {
+      const int xi = l * VT::RL + rs;
+      const bool ok = ((v.vmask >> xi) & 1u) && kok;
+      float4 p = make_float4(1.f, 1.f, 1.f, 1.f);
+      for (int q = 0; q < a.ntab; ++q) {
+        const int to = __shfl_sync(0xffffffffu, toff[q], xi);
+        const float4 r = ok ? __ldg(reinterpret_cast<const float4*>(a.tab[q] + to) + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+        p.x *= r.x; p.y *= r.y; p.z *= r.z; p.w *= r.w;
+      }
+      const int x = xw + xi;
+      const uint32_t w[4] = {ok ? tf32_rna(p.x) : 0u, ok ? tf32_rna(p.y) : 0u, ok ? tf32_rna(p.z) : 0u,
+                             ok ? tf32_rna(p.w) : 0u};
+      *reinterpret_cast<uint4*>(vrow + sw128_off(x, 4 * c, BN)) = make_uint4(w[0], w[1], w[2], w[3]);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) *reinterpret_cast<uint32_t*>(vrow + VT_OFF + sw128_off(4 * c + e, x, KB)) = w[e];
+    }
+    return;
+  }
+  if (v.mode == 1) {
+    // scalar path (bond not contiguous / unaligned rows): lane = bond index k (+32 h)
+#pragma unroll 1
+    for (int i = 0; i < 16; ++i) {
+      const int x = xw + i;
+      const bool vi = (v.vmask >> i) & 1u;
+#pragma unroll
+      for (int h = 0; h < KB / 32; ++h) {
+        const int k = h * 32 + lane;
+        float p = (vi && k < a.K) ? 1.f : 0.f;
+        for (int q = 0; q < a.ntab; ++q) {
+          const int to = __shfl_sync(0xffffffffu, toff[q], i);
+          if (p != 0.f) p *= __ldg(a.tab[q] + to + a.boff[q][k]);
+        }
+        const uint32_t w = tf32_rna(p);
+        *reinterpret_cast<uint32_t*>(vrow + sw128_off(x, k, BN)) = w;
+        *reinterpret_cast<uint32_t*>(vrow + VT_OFF + sw128_off(k, x, KB)) = w;
+      }
+    }
+    return;
+  }
+  // fast path (mode 0) and empty tiles (mode 2: all zeros)
+#pragma unroll
+  for (int l = 0; l < VT::NL; ++l) {
+    const int xi = l * VT::RL + rs;
+    const bool ok = v.mode == 0 && ((v.vmask >> xi) & 1u) && kok;
+    const float4 p = make_float4(v.cst.x * v.ld[l].x, v.cst.y * v.ld[l].y, v.cst.z * v.ld[l].z, v.cst.w * v.ld[l].w);
+    const int x = xw + xi;
+    const uint32_t w[4] = {ok ? tf32_rna(p.x) : 0u, ok ? tf32_rna(p.y) : 0u, ok ? tf32_rna(p.z) : 0u,
+                           ok ? tf32_rna(p.w) : 0u};
+    *reinterpret_cast<uint4*>(vrow + sw128_off(x, 4 * c, BN)) = make_uint4(w[0], w[1], w[2], w[3]);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) *reinterpret_cast<uint32_t*>(vrow + VT_OFF + sw128_off(4 * c + e, x, KB)) = w[e];
+  }
 }
 
 // ------------------------------------------------------------------ the kernel
@@ -176,7 +331,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
   unsigned char* gbase = smraw + (base - raw);
   const uint32_t sY = base;                                  // NS x 32 KB
   const uint32_t sM = sY + NS * Y_STAGE;                     // NS x 8 KB
-  const uint32_t sV = sM + NS * M_STAGE;                     // NV x V_STAGE
+  const uint32_t sV = sM + NS * M_STAGE;                     // NV x (V | V^T)
   const uint32_t sBar = sV + NV * V_STAGE_MAX;
   const uint32_t y_full = sBar, y_empty = sBar + 8 * NS, v_full = sBar + 16 * NS, v_empty = v_full + 8 * NV;
   const uint32_t s_full = v_empty + 8 * NV, s_empty = s_full + 16, p_full = s_empty + 16, p_empty = p_full + 8;
@@ -199,7 +354,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
 
   if (tid == 0) {
     for (int i = 0; i < NS; ++i) { mbar_init(y_full + 8 * i, 1); mbar_init(y_empty + 8 * i, 8); }
-    for (int i = 0; i < NV; ++i) { mbar_init(v_full + 8 * i, 2); mbar_init(v_empty + 8 * i, 1); }
+    for (int i = 0; i < NV; ++i) { mbar_init(v_full + 8 * i, NVG); mbar_init(v_empty + 8 * i, 1); }
     for (int i = 0; i < 2; ++i) { mbar_init(s_full + 8 * i, 1); mbar_init(s_empty + 8 * i, 8); }
     mbar_init(p_full, 8);
     mbar_init(p_empty, 1);
@@ -251,8 +406,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
   } else if (warp == 1) {
     // ------------------------------------------------------------ MMA issuer (one thread)
     if (lane == 0 && T > 0) {
-      constexpr uint32_t id1 = idesc_tf32(128, BN, 0);   // S = U V^T : N = 64 tile columns, B K-major
-      constexpr uint32_t id2 = idesc_tf32(128, KB, 1);   // N = P V   : N = bond, B MN-major
+      constexpr uint32_t id1 = idesc_tf32(128, BN);   // S = U V^T   : N = 64 tile columns
+      constexpr uint32_t id2 = idesc_tf32(128, KB);   // N = P V     : N = bond
       mbar_wait(u_ready, 0);
       tc_fence_after();
       for (int t = 0; t <= T; ++t) {
@@ -280,28 +435,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
           const int u = t - 1, vs = u % NV;
           mbar_wait(p_full, u & 1);
           tc_fence_after();
-          const uint32_t vb = sV + vs * V_STAGE_MAX;
-          const bool acc_all = (a.dbg & 1) != 0;
-          if (a.vt) {
-            // B = V^T copy, K-major SW128: rows = bond (N), K = tile columns (2 atoms of 32)
-            constexpr uint32_t id2k = idesc_tf32(128, KB, 0);
-            const uint32_t vtb = vb + VT_OFF;
+          // B = V^T, K-major SW128: rows = bond (N), K = tile columns (2 atoms of 32)
+          const uint32_t vtb = sV + vs * V_STAGE_MAX + VT_OFF;
 #pragma unroll
-            for (int kk = 0; kk < BN / 8; ++kk) {
-              const uint64_t bd = sdesc(vtb + (kk >> 2) * (KB * 128) + (kk & 3) * 32, 16, 1024);
-              const uint32_t acc = (acc_all || u > 0 || kk > 0) ? 1u : 0u;
-              mma_ts(tNa, tPa + kk * 8, bd, id2k, acc);
-              mma_ts(tNb, tPb + kk * 8, bd, id2k, acc);
-            }
-          } else {
-            const uint32_t idv = (a.dbg & 2) ? idesc_tf32(128, KB, 0) : id2;
-#pragma unroll
-            for (int kk = 0; kk < BN / 8; ++kk) {
-              const uint64_t bd = (a.dbg & 4) ? sdesc(vb + kk * 1024, 1024, BN * 128) : sdesc(vb + kk * 1024, BN * 128, 1024);
-              const uint32_t acc = (acc_all || u > 0 || kk > 0) ? 1u : 0u;
-              mma_ts(tNa, tPa + kk * 8, bd, idv, acc);
-              mma_ts(tNb, tPb + kk * 8, bd, idv, acc);
-            }
+          for (int kk = 0; kk < BN / 8; ++kk) {
+            const uint64_t bd = sdesc(vtb + (kk >> 2) * (KB * 128) + (kk & 3) * 32, 16, 1024);
+            const uint32_t acc = (u > 0 || kk > 0) ? 1u : 0u;
+            mma_ts(tNa, tPa + kk * 8, bd, id2, acc);
+            mma_ts(tNb, tPb + kk * 8, bd, id2, acc);
           }
           mma_commit(p_empty);
           mma_commit(v_empty + 8 * vs);
@@ -309,133 +450,28 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
       }
       mma_commit(nd_full);
     }
-  } else if (warp < 4) {
+  } else if (warp >= 4 && warp < 4 + NVG) {
     // ------------------------------------------------------------ column operand V (Khatri-Rao)
-    // Each warp owns 32 tile columns; lane = column slot for the offset arithmetic, then
-    // lane = bond index for the coalesced table-row loads and the swizzled stores.
-    const int xw = (warp - 2) * 32;
-    const int x = xw + lane;   // tile column slot whose offsets this lane computes
+    const int xw = (warp - 4) * 16;
+    VTile<KB> cur, nxt;
+    int toff_c[kMaxTabs], toff_n[kMaxTabs];
+    if (T > 0) vtile_issue<KB>(a, t_begin, xw, lane, cur, toff_c);
     for (int t = 0; t < T; ++t) {
+      if (t + 1 < T) vtile_issue<KB>(a, t_begin + t + 1, xw, lane, nxt, toff_n);   // next tile's rows in flight
       const int vs = t % NV;
       mbar_wait(v_empty + 8 * vs, ((t / NV) & 1) ^ 1);
-      const int64_t tile = t_begin + t;
-      int64_t col;
-      bool valid;
-      if (a.layout == 0) {
-        col = tile * BN + x;
-        valid = col < a.CO;
-      } else {
-        const int64_t ti = tile % a.tiles_inner, to = tile / a.tiles_inner;
-        const int64_t ci = ti * BN + x;
-        valid = ci < a.CI;
-        col = to * a.CI + ci;
-      }
-      int toff[kMaxTabs] = {0, 0, 0, 0};
-      if (valid) {
-        int64_t rem = col;
-        for (int d = a.nc - 1; d >= 0; --d) {
-          const int64_t i = rem % a.cdim[d];
-          rem /= a.cdim[d];
-          for (int q = 0; q < a.ntab; ++q) toff[q] += (int)(i * a.tcs[q][d]);
-        }
-      }
-      unsigned char* vrow = gV + vs * V_STAGE_MAX;
-      const uint32_t vmask = __ballot_sync(0xffffffffu, valid);
-      if (a.vec4) {
-        // Vector path (bond contiguous in every table, rows 16-byte aligned): lane = (row
-        // sub-index, 16-byte chunk); each warp load covers 32/C full table rows and all loads
-        // of a table are in flight together (L1 is small next to ~220 KB of smem).
-        constexpr int C = KB / 4;          // 16-byte chunks per padded row
-        constexpr int RL = 32 / C;         // rows per warp load
-        constexpr int NL = 32 / RL;        // loads per table per warp (= C)
-        const int rs = lane / C, c = lane % C;
-        const bool kok = c * 4 < a.K;
-        float4 acc[NL];
-#pragma unroll
-        for (int l = 0; l < NL; ++l) acc[l] = make_float4(1.f, 1.f, 1.f, 1.f);
-        for (int q = 0; q < a.ntab; ++q) {
-          float4 ld[NL];
-#pragma unroll
-          for (int l = 0; l < NL; ++l) {
-            const int xl = l * RL + rs;
-            const int to = __shfl_sync(0xffffffffu, toff[q], xl);
-            ld[l] = (((vmask >> xl) & 1u) && kok) ? __ldg(reinterpret_cast<const float4*>(a.tab[q] + to) + c)
-                                                  : make_float4(0.f, 0.f, 0.f, 0.f);
-          }
-#pragma unroll
-          for (int l = 0; l < NL; ++l) {
-            acc[l].x *= ld[l].x; acc[l].y *= ld[l].y; acc[l].z *= ld[l].z; acc[l].w *= ld[l].w;
-          }
-        }
-#pragma unroll
-        for (int l = 0; l < NL; ++l) {
-          const int xi = xw + l * RL + rs;
-          const bool ok = ((vmask >> (l * RL + rs)) & 1u) && kok && a.ntab > 0;
-          const uint32_t w0 = ok ? tf32_rna(acc[l].x) : 0u, w1 = ok ? tf32_rna(acc[l].y) : 0u;
-          const uint32_t w2 = ok ? tf32_rna(acc[l].z) : 0u, w3 = ok ? tf32_rna(acc[l].w) : 0u;
-          const int atom = c >> 3, chunk = c & 7;
-          const int off = atom * (BN * 128) + (xi >> 3) * 1024 + (xi & 7) * 128 + ((chunk ^ (xi & 7)) << 4);
-          *reinterpret_cast<uint4*>(vrow + off) = make_uint4(w0, w1, w2, w3);
-          if (a.vt) {
-            const uint32_t wv[4] = {w0, w1, w2, w3};
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-              const int k = 4 * c + e;
-              const int offt = VT_OFF + (xi >> 5) * (KB * 128) + (k >> 3) * 1024 + (k & 7) * 128 +
-                               ((((xi & 31) >> 2) ^ (k & 7)) << 4) + (xi & 3) * 4;
-              *reinterpret_cast<uint32_t*>(vrow + offt) = wv[e];
-            }
-          }
-        }
-        fence_async_smem();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(v_full + 8 * vs);
-        continue;
-      }
-      // Scalar path: lane = bond index k (+32 h); each warp load reads one contiguous table row.
-      int bo[kMaxTabs][KB / 32];
-#pragma unroll
-      for (int q = 0; q < kMaxTabs; ++q)
-#pragma unroll
-        for (int h = 0; h < KB / 32; ++h) bo[q][h] = (q < a.ntab && h * 32 + lane < a.K) ? a.boff[q][h * 32 + lane] : 0;
-#pragma unroll 4
-      for (int i = 0; i < 32; ++i) {
-        const int xi = xw + i;
-        const bool vi = (vmask >> i) & 1u;
-        float p[KB / 32];
-#pragma unroll
-        for (int h = 0; h < KB / 32; ++h) p[h] = (vi && h * 32 + lane < a.K) ? 1.f : 0.f;
-        for (int q = 0; q < a.ntab; ++q) {
-          const int to = __shfl_sync(0xffffffffu, toff[q], i);
-          const float* tp = a.tab[q] + to;
-#pragma unroll
-          for (int h = 0; h < KB / 32; ++h)
-            if (p[h] != 0.f) p[h] *= __ldg(tp + bo[q][h]);
-        }
-#pragma unroll
-        for (int h = 0; h < KB / 32; ++h) {
-          const uint32_t w = tf32_rna(p[h]);
-          const int k = h * 32 + lane;
-          // V: row xi, K = bond (SW128 K-major atoms of 32 bond elements)
-          const int off = h * (BN * 128) + (xi >> 3) * 1024 + (xi & 7) * 128 + ((((k & 31) >> 2) ^ (xi & 7)) << 4) +
-                          (k & 3) * 4;
-          *reinterpret_cast<uint32_t*>(vrow + off) = w;
-          if (a.vt) {
-            // V^T: row k (bond), K = tile column xi; SW128 K-major, 2 atoms of 32 columns
-            const int offt = VT_OFF + (xi >> 5) * (KB * 128) + (k >> 3) * 1024 + (k & 7) * 128 +
-                             ((((xi & 31) >> 2) ^ (k & 7)) << 4) + (xi & 3) * 4;
-            *reinterpret_cast<uint32_t*>(vrow + offt) = w;
-          }
-        }
-      }
+      vtile_store<KB>(a, xw, lane, cur, toff_c, gV + vs * V_STAGE_MAX);
       fence_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(v_full + 8 * vs);
+      cur = nxt;
+#pragma unroll
+      for (int q = 0; q < kMaxTabs; ++q) toff_c[q] = toff_n[q];
     }
-  } else {
+  } else if (warp >= 8) {
     // ------------------------------------------------------------ elementwise + epilogue
-    const int ew = tid - 128;
-    const int g = ew >> 7;                 // column half of the tile
+    const int ew = tid - 256;              // 0..255
+    const int g = ew >> 7;                 // column half of the tile (32 columns)
     const int qd = warp & 3;               // TMEM lane quarter
     const int m = qd * 32 + lane;          // row within the block (= TMEM lane)
     const uint32_t lane_off = (uint32_t)(qd * 32) << 16;
@@ -444,23 +480,16 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
     // U -> TMEM, split hi (g = 0) / lo (g = 1)
     {
 #pragma unroll 1
-      for (int h = 0; h < KB / 32; ++h) {
-        uint32_t r[32];
+      for (int h = 0; h < KB / 16; ++h) {
+        uint32_t r[16];
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const int k = h * 32 + j;
-          float u = (row_ok && k < a.K) ? __ldg(a.U + row * a.K + k) : 0.f;
+        for (int j = 0; j < 16; ++j) {
+          const int k = h * 16 + j;
+          const float u = (row_ok && k < a.K) ? __ldg(a.U + row * a.K + k) : 0.f;
           const uint32_t hi = tf32_rna(u);
           r[j] = g == 0 ? hi : tf32_rna(u - __uint_as_float(hi));
         }
-        tmem_st32((g == 0 ? tUh : tUl) + lane_off + h * 32, r);
-      }
-      if (a.dbg & 1) {   // diagnostic: prefill the N / D accumulators with 1.0
-        uint32_t one[32];
-#pragma unroll
-        for (int j = 0; j < 32; ++j) one[j] = __float_as_uint(1.f);
-#pragma unroll
-        for (int h = 0; h < KB / 32; ++h) tmem_st32((g == 0 ? tNa : tNb) + lane_off + h * 32, one);
+        tmem_st16((g == 0 ? tUh : tUl) + lane_off + h * 16, r);
       }
       tmem_st_wait();
       tc_fence_before();
@@ -481,102 +510,106 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
         const int64_t c = a.CI - ti * BN;
         cols_here = (int)(c < BN ? c : BN);
       }
+      const int st = t % NS;
       mbar_wait(s_full + 8 * s, (t >> 1) & 1);
       tc_fence_after();
-      uint32_t sv[32];
-      tmem_ld32(tS + 64 * s + lane_off + 32 * g, sv);
-      tmem_ld_wait(sv);
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(s_empty + 8 * s);
-      const int st = t % NS;
       mbar_wait(y_full + 8 * st, (t / NS) & 1);
-      // gather my row's 32 Y values and mask bytes
-      float yv[32];
-      uint32_t mk[8];   // 32 mask bytes packed
       const unsigned char* ys = gY + st * Y_STAGE;
       const unsigned char* ms = gM + st * M_STAGE;
-      if (a.layout == 0) {
+      float lsum = 0.f;
+#pragma unroll 1
+      for (int h = 0; h < 2; ++h) {
+        const int c0 = 32 * g + 16 * h;   // first tile column of this half-step
+        uint32_t sv[16];
+        tmem_ld16(tS + 64 * s + lane_off + c0, sv);
+        // my row's 16 Y values and mask bytes (missing values are never used)
+        float yv[16];
+        uint32_t mk[4];
+        if (a.layout == 0) {
 #pragma unroll
-        for (int j = 0; j < 32; ++j) yv[j] = reinterpret_cast<const float*>(ys)[(32 * g + j) * BM + m];
-        if (a.has_mask) {
+          for (int j = 0; j < 16; ++j) yv[j] = reinterpret_cast<const float*>(ys)[(c0 + j) * BM + m];
+          if (a.has_mask) {
 #pragma unroll
-          for (int j4 = 0; j4 < 8; ++j4) {
-            uint32_t w = 0;
+            for (int j4 = 0; j4 < 4; ++j4) {
+              uint32_t w = 0;
 #pragma unroll
-            for (int e = 0; e < 4; ++e) w |= (uint32_t)ms[(32 * g + 4 * j4 + e) * BM + m] << (8 * e);
-            mk[j4] = w;
+              for (int e = 0; e < 4; ++e) w |= (uint32_t)ms[(c0 + 4 * j4 + e) * BM + m] << (8 * e);
+              mk[j4] = w;
+            }
           }
-        }
-      } else {
-        const unsigned char* sub = ys + g * (Y_STAGE / 2) + m * 128;
+        } else {
+          const unsigned char* sub = ys + g * (Y_STAGE / 2) + m * 128;
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
-          const float4 f = *reinterpret_cast<const float4*>(sub + ((q ^ (m & 7)) << 4));
-          yv[4 * q] = f.x; yv[4 * q + 1] = f.y; yv[4 * q + 2] = f.z; yv[4 * q + 3] = f.w;
-        }
-        if (a.has_mask) {
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
+          for (int q = 0; q < 4; ++q) {
+            const float4 f = *reinterpret_cast<const float4*>(sub + (((4 * h + q) ^ (m & 7)) << 4));
+            yv[4 * q] = f.x; yv[4 * q + 1] = f.y; yv[4 * q + 2] = f.z; yv[4 * q + 3] = f.w;
+          }
+          if (a.has_mask) {
             const int q = 2 * g + h;
             const uint4 w = *reinterpret_cast<const uint4*>(ms + m * 64 + ((q ^ ((m >> 1) & 3)) << 4));
-            mk[4 * h] = w.x; mk[4 * h + 1] = w.y; mk[4 * h + 2] = w.z; mk[4 * h + 3] = w.w;
+            mk[0] = w.x; mk[1] = w.y; mk[2] = w.z; mk[3] = w.w;
           }
+        }
+        // observed-entry bits: row / column in range and mask byte nonzero (R5, R6)
+        const int cv = cols_here - c0;
+        uint32_t obs = (!row_ok || cv <= 0) ? 0u : (cv >= 16 ? 0xffffu : ((1u << cv) - 1u));
+        if (a.has_mask) {
+          uint32_t mb = 0;
+#pragma unroll
+          for (int j4 = 0; j4 < 4; ++j4) {
+            const uint32_t nz = __vcmpne4(mk[j4], 0u);   // 0xff per nonzero byte
+            mb |= ((nz & 1u) | ((nz >> 7) & 2u) | ((nz >> 14) & 4u) | ((nz >> 21) & 8u)) << (4 * j4);
+          }
+          obs &= mb;
+        }
+#pragma unroll
+        for (int j = 0; j < 16; ++j) yv[j] = ((obs >> j) & 1u) ? yv[j] : 1.f;
+        tmem_ld_wait(sv);
+        if (h == 1) {   // S buffer fully read
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(s_empty + 8 * s);
+        }
+        if (a.mode != 0) {   // loss of the iterate entering the sweep (uniform branch)
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const float l = Ew<KIND>::loss(yv[j], fmaxf(__uint_as_float(sv[j]), 1e-30f), a.dv);
+            lsum += ((obs >> j) & 1u) ? l : 0.f;
+          }
+          cnt += __popc(obs);
+        }
+        // in place: sv[] becomes P_a, pb[] P_b; branch-free selects
+        uint32_t pb[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const float yh = fmaxf(__uint_as_float(sv[j]), 1e-30f);
+          float av, bv;
+          Ew<KIND>::ab(yv[j], yh, a.dv, av, bv);
+          const bool o = (obs >> j) & 1u;
+          sv[j] = o ? tf32_rna(av) : 0u;
+          pb[j] = o ? tf32_rna(bv) : 0u;
+        }
+        if (a.mode != 2) {
+          if (h == 0) {
+            mbar_wait(p_empty, (t & 1) ^ 1);
+            tc_fence_after();
+          }
+          tmem_st16(tPa + lane_off + c0, sv);
+          tmem_st16(tPb + lane_off + c0, pb);
+        }
+        if (a.debug && blockIdx.x == 0 && blockIdx.y == 0 && t == 0) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) a.debug[m * 64 + c0 + j] = __uint_as_float(sv[j]);
         }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(y_empty + 8 * st);
-      // observed-entry bits: row / column in range and mask byte nonzero (R5, R6)
-      const int cv = cols_here - 32 * g;
-      uint32_t obs = (!row_ok || cv <= 0) ? 0u : (cv >= 32 ? 0xffffffffu : ((1u << cv) - 1u));
-      if (a.has_mask) {
-        uint32_t mb = 0;
-#pragma unroll
-        for (int j4 = 0; j4 < 8; ++j4) {
-          const uint32_t nz = __vcmpne4(mk[j4], 0u);   // 0xff per nonzero byte
-          mb |= ((nz & 1u) | ((nz >> 7) & 2u) | ((nz >> 14) & 4u) | ((nz >> 21) & 8u)) << (4 * j4);
-        }
-        obs &= mb;
-      }
-      // masked values are replaced before any arithmetic (never used, NaN-safe)
-#pragma unroll
-      for (int j = 0; j < 32; ++j) yv[j] = ((obs >> j) & 1u) ? yv[j] : 1.f;
-      if (a.mode != 0) {   // loss of the iterate entering the sweep (uniform branch)
-        float lsum = 0.f;
-#pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const float l = Ew<KIND>::loss(yv[j], fmaxf(__uint_as_float(sv[j]), 1e-30f), a.dv);
-          lsum += ((obs >> j) & 1u) ? l : 0.f;
-        }
-        loss_acc += (double)lsum;
-        cnt += __popc(obs);
-      }
-      // in place: sv[] becomes P_a, yb[] becomes P_b (register pressure); branch-free selects
-      uint32_t (&pa)[32] = sv;
-      uint32_t yb[32];
-      uint32_t (&pb)[32] = yb;
-#pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const float yh = fmaxf(__uint_as_float(sv[j]), 1e-30f);
-        float av, bv;
-        Ew<KIND>::ab(yv[j], yh, a.dv, av, bv);
-        const bool o = (obs >> j) & 1u;
-        pa[j] = o ? tf32_rna(av) : 0u;
-        pb[j] = o ? tf32_rna(bv) : 0u;
-      }
+      loss_acc += (double)lsum;
       if (a.mode != 2) {
-        mbar_wait(p_empty, (t & 1) ^ 1);
-        tc_fence_after();
-        tmem_st32(tPa + lane_off + 32 * g, pa);
-        tmem_st32(tPb + lane_off + 32 * g, pb);
         tmem_st_wait();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(p_full);
-      }
-      if (a.debug && blockIdx.x == 0 && blockIdx.y == 0 && t == 0) {
-#pragma unroll
-        for (int j = 0; j < 32; ++j) a.debug[m * 64 + 32 * g + j] = __uint_as_float(pa[j]);
       }
     }
     // epilogue: N (g = 0) / D (g = 1) for this lane -> split partials
@@ -587,14 +620,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
         mbar_wait(nd_full, 0);
         tc_fence_after();
 #pragma unroll 1
-        for (int h = 0; h < KB / 32; ++h) {
-          uint32_t r[32];
-          tmem_ld32((g == 0 ? tNa : tNb) + lane_off + h * 32, r);
+        for (int h = 0; h < KB / 16; ++h) {
+          uint32_t r[16];
+          tmem_ld16((g == 0 ? tNa : tNb) + lane_off + h * 16, r);
           tmem_ld_wait(r);
           if (row_ok) {
 #pragma unroll
-            for (int j = 0; j < 32; ++j)
-              if (h * 32 + j < a.K) out[row * a.K + h * 32 + j] = __uint_as_float(r[j]);
+            for (int j = 0; j < 16; ++j)
+              if (h * 16 + j < a.K) out[row * a.K + h * 16 + j] = __uint_as_float(r[j]);
           }
         }
       } else if (row_ok) {
