@@ -13,6 +13,30 @@
 
 namespace nef {
 
+// Single-instruction MUFU forms.  Every argument reaching them is a clamped Yhat (>= 1e-30,
+// a normal number) or a data value >= 0, so flush-to-zero never changes a result.
+__device__ __forceinline__ float frsqrt(float x) {
+  float r;
+  asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ float frcp(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ float fsqrt(float x) {
+  float r;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
+// fp32 -> TF32 bit pattern, round to nearest with ties away from zero (= cvt.rna.tf32.f32)
+// as two integer ops: add half a TF32 ulp to the magnitude bits, clear the low 13 bits.
+__device__ __forceinline__ uint32_t tf32_bits(float x) {
+  return (__float_as_uint(x) + 0x1000u) & 0xffffe000u;
+}
+
 __device__ __forceinline__ float powc(float y, int code, float p) {
   switch (code) {
     case POW_0: return 1.f;
@@ -132,7 +156,7 @@ struct Ew {
 template <>
 struct Ew<EW_KL> {   // (1, 0): a = x / y, b = 1
   static __device__ __forceinline__ void ab(float x, float yh, const DivParams&, float& av, float& bv) {
-    av = __fdividef(x, yh);
+    av = x * frcp(yh);
     bv = 1.f;
   }
   static __device__ __forceinline__ float loss(float x, float yh, const DivParams&) { return kl_loss(x, yh); }
@@ -153,13 +177,13 @@ struct Ew<EW_EUC> {  // (1, 1): a = x, b = y
 template <>
 struct Ew<EW_B_M05> {  // (1, -0.5): a = x y^-3/2, b = y^-1/2; L = 2 (sqrt x - sqrt y)^2 / sqrt y
   static __device__ __forceinline__ void ab(float x, float yh, const DivParams&, float& av, float& bv) {
-    const float r = rsqrtf(yh);
+    const float r = frsqrt(yh);
     bv = r;
     av = x * r * r * r;
   }
   static __device__ __forceinline__ float loss(float x, float yh, const DivParams&) {
-    const float r = rsqrtf(yh);
-    const float d = sqrtf(x) - yh * r;
+    const float r = frsqrt(yh);
+    const float d = fsqrt(x) - yh * r;
     return 2.f * d * d * r;
   }
 };
@@ -167,13 +191,13 @@ struct Ew<EW_B_M05> {  // (1, -0.5): a = x y^-3/2, b = y^-1/2; L = 2 (sqrt x - s
 template <>
 struct Ew<EW_A05_B0> {  // (0.5, 0): a = sqrt(x) / y, b = y^-1/2; L = 4 y^1/2 f(log(x/y)/2)
   static __device__ __forceinline__ void ab(float x, float yh, const DivParams&, float& av, float& bv) {
-    const float r = rsqrtf(yh);
+    const float r = frsqrt(yh);
     bv = r;
-    av = sqrtf(x) * r * r;
+    av = fsqrt(x) * r * r;
   }
   static __device__ __forceinline__ float loss(float x, float yh, const DivParams&) {
     // 4 [sqrt y - sqrt x + sqrt x v], v = log(x/y)/2 (= 4 sqrt(y) f(v)); series near v = 0
-    const float sy = sqrtf(yh), sx = sqrtf(x);
+    const float sy = fsqrt(yh), sx = fsqrt(x);
     const float v = 0.5f * logf(fmaxf(x, 1e-38f) / yh);
     const float l = fabsf(v) < 0.3f ? 4.f * sy * fser(v) : 4.f * (sy - sx + sx * v);
     return x > 0.f ? l : 4.f * sy;
@@ -183,7 +207,7 @@ struct Ew<EW_A05_B0> {  // (0.5, 0): a = sqrt(x) / y, b = y^-1/2; L = 4 y^1/2 f(
 template <>
 struct Ew<EW_B05> {  // (1, 0.5): a = x y^-1/2, b = y^1/2
   static __device__ __forceinline__ void ab(float x, float yh, const DivParams&, float& av, float& bv) {
-    const float r = rsqrtf(yh);
+    const float r = frsqrt(yh);
     av = x * r;
     bv = yh * r;
   }
@@ -202,8 +226,8 @@ struct Ew<EW_B2> {  // (1, 2): a = x y, b = y^2
 template <>
 struct Ew<EW_A05_B1> {  // (0.5, 1): a = sqrt(x), b = sqrt(y)
   static __device__ __forceinline__ void ab(float x, float yh, const DivParams&, float& av, float& bv) {
-    av = sqrtf(x);
-    bv = sqrtf(yh);
+    av = fsqrt(x);
+    bv = fsqrt(yh);
   }
   static __device__ __forceinline__ float loss(float x, float yh, const DivParams& d) { return loss_entry(x, yh, d); }
 };
