@@ -267,8 +267,8 @@ __device__ __forceinline__ void vtile_store(const TcArgs& a, int xw, int lane, c
         p.x *= r.x; p.y *= r.y; p.z *= r.z; p.w *= r.w;
       }
       const int x = xw + xi;
-      const uint32_t w[4] = {ok ? tf32_rna(p.x) : 0u, ok ? tf32_rna(p.y) : 0u, ok ? tf32_rna(p.z) : 0u,
-                             ok ? tf32_rna(p.w) : 0u};
+      const uint32_t w[4] = {ok ? tf32_bits(p.x) : 0u, ok ? tf32_bits(p.y) : 0u, ok ? tf32_bits(p.z) : 0u,
+                             ok ? tf32_bits(p.w) : 0u};
       *reinterpret_cast<uint4*>(vrow + sw128_off(x, 4 * c, BN)) = make_uint4(w[0], w[1], w[2], w[3]);
 #pragma unroll
       for (int e = 0; e < 4; ++e) *reinterpret_cast<uint32_t*>(vrow + VT_OFF + sw128_off(4 * c + e, x, KB)) = w[e];
@@ -289,7 +289,7 @@ __device__ __forceinline__ void vtile_store(const TcArgs& a, int xw, int lane, c
           const int to = __shfl_sync(0xffffffffu, toff[q], i);
           if (p != 0.f) p *= __ldg(a.tab[q] + to + a.boff[q][k]);
         }
-        const uint32_t w = tf32_rna(p);
+        const uint32_t w = tf32_bits(p);
         *reinterpret_cast<uint32_t*>(vrow + sw128_off(x, k, BN)) = w;
         *reinterpret_cast<uint32_t*>(vrow + VT_OFF + sw128_off(k, x, KB)) = w;
       }
@@ -303,8 +303,8 @@ __device__ __forceinline__ void vtile_store(const TcArgs& a, int xw, int lane, c
     const bool ok = v.mode == 0 && ((v.vmask >> xi) & 1u) && kok;
     const float4 p = make_float4(v.cst.x * v.ld[l].x, v.cst.y * v.ld[l].y, v.cst.z * v.ld[l].z, v.cst.w * v.ld[l].w);
     const int x = xw + xi;
-    const uint32_t w[4] = {ok ? tf32_rna(p.x) : 0u, ok ? tf32_rna(p.y) : 0u, ok ? tf32_rna(p.z) : 0u,
-                           ok ? tf32_rna(p.w) : 0u};
+    const uint32_t w[4] = {ok ? tf32_bits(p.x) : 0u, ok ? tf32_bits(p.y) : 0u, ok ? tf32_bits(p.z) : 0u,
+                           ok ? tf32_bits(p.w) : 0u};
     *reinterpret_cast<uint4*>(vrow + sw128_off(x, 4 * c, BN)) = make_uint4(w[0], w[1], w[2], w[3]);
 #pragma unroll
     for (int e = 0; e < 4; ++e) *reinterpret_cast<uint32_t*>(vrow + VT_OFF + sw128_off(4 * c + e, x, KB)) = w[e];
@@ -481,8 +481,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
         for (int j = 0; j < 16; ++j) {
           const int k = h * 16 + j;
           const float u = (row_ok && k < a.K) ? __ldg(a.U + row * a.K + k) : 0.f;
-          const uint32_t hi = tf32_rna(u);
-          r[j] = g == 0 ? hi : tf32_rna(u - __uint_as_float(hi));
+          const uint32_t hi = tf32_bits(u);
+          r[j] = g == 0 ? hi : tf32_bits(u - __uint_as_float(hi));
         }
         tmem_st16((g == 0 ? tUh : tUl) + lane_off + h * 16, r);
       }
@@ -581,8 +581,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
           float av, bv;
           Ew<KIND>::ab(yv[j], yh, a.dv, av, bv);
           const bool o = (obs >> j) & 1u;
-          sv[j] = o ? tf32_rna(av) : 0u;
-          pb[j] = o ? tf32_rna(bv) : 0u;
+          sv[j] = o ? tf32_bits(av) : 0u;
+          pb[j] = o ? tf32_bits(bv) : 0u;
         }
         if (a.mode != 2) {
           if (h == 0) {
