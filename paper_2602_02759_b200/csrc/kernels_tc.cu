@@ -62,19 +62,20 @@ __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
 __device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
   asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
 }
-// Bounded wait: a pipeline bug traps (kernel error) instead of hanging the GPU.
+// Wait with a suspend-time hint: the warp sleeps until the phase completes (no issue slots
+// burnt on polling).  Bounded: a pipeline bug traps (kernel error) instead of hanging the GPU.
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
   uint32_t done = 0;
   for (uint32_t it = 0;; ++it) {
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
         "selp.u32 %0, 1, 0, p;\n}"
         : "=r"(done)
-        : "r"(bar), "r"(parity)
+        : "r"(bar), "r"(parity), "r"(20000u)
         : "memory");
     if (done) return;
-    if (it > (1u << 26)) __trap();
+    if (it > (1u << 22)) __trap();
   }
 }
 __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* tm, int c0, int c1, uint32_t bar) {
@@ -164,21 +165,21 @@ __device__ __forceinline__ int sw128_off(int row, int k, int rows) {
 // Table rows of one tile held in registers (software pipelining across tiles).
 template <int KB>
 struct VTile {
-  static constexpr int C = KB / 4;     // 16-byte chunks per padded row
-  static constexpr int RL = 32 / C;    // rows per warp load
-  static constexpr int NL = 16 / RL;   // loads per warp (16 rows per warp)
-  float4 ld[NL];                       // varying table rows (chunk c of row l*RL+rs)
-  float4 cst;                          // product of the tile-constant rows (chunk c)
-  uint32_t vmask;                      // valid tile columns of this warp (16 bits)
-  int mode;                            // 0 fast (<= 1 varying table), 1 general, 2 empty
+  static constexpr int C = KB / 4;          // 16-byte chunks per padded row
+  static constexpr int NB = (4 * C) / 32;   // 4x4 blocks per lane (16 rows = 4 row groups per warp)
+  float4 ld[NB][4];                         // varying-table rows r of block i, chunk c
+  float4 cst;                               // product of the tile-constant rows (chunk c)
+  uint32_t vmask;                           // valid tile columns of this warp (16 bits)
+  int mode;                                 // 0 fast (<= 1 varying table), 1 general, 2 empty
 };
 
+// Column offsets of this warp's 16 tile columns (lane & 15), validity, and - on the vector
+// path - the loads of the next tile's table rows: lane owns 4x4 blocks (4 rows x 4 bonds).
 template <int KB>
 __device__ __forceinline__ void vtile_issue(const TcArgs& a, int64_t tile, int xw, int lane, VTile<KB>& v,
                                             int (&toff)[kMaxTabs]) {
   using VT = VTile<KB>;
-  const int xl = lane & 15;
-  const int x = xw + xl;
+  const int x = xw + (lane & 15);
   int64_t col;
   bool valid;
   if (a.layout == 0) {
@@ -208,7 +209,7 @@ __device__ __forceinline__ void vtile_issue(const TcArgs& a, int64_t tile, int x
     return;
   }
   const int first = __ffs(v.vmask) - 1;
-  const int rs = lane / VT::C, c = lane % VT::C;
+  const int c = lane % VT::C;
   const bool kok = c * 4 < a.K;
   int nvar = 0, var_q = -1;
   v.cst = make_float4(1.f, 1.f, 1.f, 1.f);
@@ -232,7 +233,9 @@ __device__ __forceinline__ void vtile_issue(const TcArgs& a, int64_t tile, int x
   v.mode = 0;
   if (var_q < 0) {
 #pragma unroll
-    for (int l = 0; l < VT::NL; ++l) v.ld[l] = make_float4(1.f, 1.f, 1.f, 1.f);
+    for (int i = 0; i < VT::NB; ++i)
+#pragma unroll
+      for (int r = 0; r < 4; ++r) v.ld[i][r] = make_float4(1.f, 1.f, 1.f, 1.f);
     return;
   }
   int tv = toff[0];
@@ -241,37 +244,62 @@ __device__ __forceinline__ void vtile_issue(const TcArgs& a, int64_t tile, int x
     if (q == var_q) tv = toff[q];
   const float4* tab = reinterpret_cast<const float4*>(a.tab[var_q]);
 #pragma unroll
-  for (int l = 0; l < VT::NL; ++l) {
-    const int xi = l * VT::RL + rs;
-    const int to = __shfl_sync(0xffffffffu, tv, xi);
-    v.ld[l] = (((v.vmask >> xi) & 1u) && kok) ? __ldg(tab + (to >> 2) + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int i = 0; i < VT::NB; ++i) {
+    const int rg = (lane + 32 * i) / VT::C;   // row group of block i
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const int xr = 4 * rg + r;
+      const int to = __shfl_sync(0xffffffffu, tv, xr);
+      v.ld[i][r] = (((v.vmask >> xr) & 1u) && kok) ? __ldg(tab + (to >> 2) + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
   }
+}
+
+// Store one 4x4 block (rows x0..x0+3, bonds 4c..4c+3): four 16-byte rows of V and four
+// 16-byte columns of V^T, TF32 round-to-nearest, zeros where invalid.
+template <int KB>
+__device__ __forceinline__ void vblock_store(unsigned char* vrow, int x0, int c, uint32_t okbits, const float4 (&p)[4]) {
+  uint32_t w[4][4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    const uint32_t m = ((okbits >> r) & 1u) ? 0xffffffffu : 0u;
+    w[r][0] = tf32_bits(p[r].x) & m;
+    w[r][1] = tf32_bits(p[r].y) & m;
+    w[r][2] = tf32_bits(p[r].z) & m;
+    w[r][3] = tf32_bits(p[r].w) & m;
+    *reinterpret_cast<uint4*>(vrow + sw128_off(x0 + r, 4 * c, BN)) = make_uint4(w[r][0], w[r][1], w[r][2], w[r][3]);
+  }
+#pragma unroll
+  for (int e = 0; e < 4; ++e)
+    *reinterpret_cast<uint4*>(vrow + VT_OFF + sw128_off(4 * c + e, x0, KB)) = make_uint4(w[0][e], w[1][e], w[2][e], w[3][e]);
 }
 
 template <int KB>
 __device__ __forceinline__ void vtile_store(const TcArgs& a, int xw, int lane, const VTile<KB>& v,
                                             const int (&toff)[kMaxTabs], unsigned char* vrow) {
   using VT = VTile<KB>;
-  const int rs = lane / VT::C, c = lane % VT::C;
+  const int c = lane % VT::C;
   const bool kok = c * 4 < a.K;
   if (v.mode == 1 && a.vec4) {
-    // general vector path: several varying tables, product formed after all loads of a table
+    // general vector path: several varying tables, rows multiplied table by table
 #pragma unroll
-    for (int l = 0; l < VT::NL; ++l) {
-      const int xi = l * VT::RL + rs;
-      const bool ok = ((v.vmask >> xi) & 1u) && kok;
-      float4 p = make_float4(1.f, 1.f, 1.f, 1.f);
+    for (int i = 0; i < VT::NB; ++i) {
+      const int rg = (lane + 32 * i) / VT::C;
+      float4 p[4];
+#pragma unroll
+      for (int r = 0; r < 4; ++r) p[r] = make_float4(1.f, 1.f, 1.f, 1.f);
       for (int q = 0; q < a.ntab; ++q) {
-        const int to = __shfl_sync(0xffffffffu, toff[q], xi);
-        const float4 r = ok ? __ldg(reinterpret_cast<const float4*>(a.tab[q] + to) + c) : make_float4(0.f, 0.f, 0.f, 0.f);
-        p.x *= r.x; p.y *= r.y; p.z *= r.z; p.w *= r.w;
-      }
-      const int x = xw + xi;
-      const uint32_t w[4] = {ok ? tf32_bits(p.x) : 0u, ok ? tf32_bits(p.y) : 0u, ok ? tf32_bits(p.z) : 0u,
-                             ok ? tf32_bits(p.w) : 0u};
-      *reinterpret_cast<uint4*>(vrow + sw128_off(x, 4 * c, BN)) = make_uint4(w[0], w[1], w[2], w[3]);
 #pragma unroll
-      for (int e = 0; e < 4; ++e) *reinterpret_cast<uint32_t*>(vrow + VT_OFF + sw128_off(4 * c + e, x, KB)) = w[e];
+        for (int r = 0; r < 4; ++r) {
+          const int xr = 4 * rg + r;
+          const int to = __shfl_sync(0xffffffffu, toff[q], xr);
+          const float4 t = (((v.vmask >> xr) & 1u) && kok) ? __ldg(reinterpret_cast<const float4*>(a.tab[q] + to) + c)
+                                                          : make_float4(0.f, 0.f, 0.f, 0.f);
+          p[r].x *= t.x; p[r].y *= t.y; p[r].z *= t.z; p[r].w *= t.w;
+        }
+      }
+      const uint32_t ok = kok ? ((v.vmask >> (4 * rg)) & 0xfu) : 0u;
+      vblock_store<KB>(vrow, xw + 4 * rg, c, ok, p);
     }
     return;
   }
@@ -296,18 +324,16 @@ __device__ __forceinline__ void vtile_store(const TcArgs& a, int xw, int lane, c
     }
     return;
   }
-  // fast path (mode 0) and empty tiles (mode 2: all zeros)
+  // fast path (mode 0: constant rows x one varying table) and empty tiles (mode 2: zeros)
 #pragma unroll
-  for (int l = 0; l < VT::NL; ++l) {
-    const int xi = l * VT::RL + rs;
-    const bool ok = v.mode == 0 && ((v.vmask >> xi) & 1u) && kok;
-    const float4 p = make_float4(v.cst.x * v.ld[l].x, v.cst.y * v.ld[l].y, v.cst.z * v.ld[l].z, v.cst.w * v.ld[l].w);
-    const int x = xw + xi;
-    const uint32_t w[4] = {ok ? tf32_bits(p.x) : 0u, ok ? tf32_bits(p.y) : 0u, ok ? tf32_bits(p.z) : 0u,
-                           ok ? tf32_bits(p.w) : 0u};
-    *reinterpret_cast<uint4*>(vrow + sw128_off(x, 4 * c, BN)) = make_uint4(w[0], w[1], w[2], w[3]);
+  for (int i = 0; i < VT::NB; ++i) {
+    const int rg = (lane + 32 * i) / VT::C;
+    float4 p[4];
 #pragma unroll
-    for (int e = 0; e < 4; ++e) *reinterpret_cast<uint32_t*>(vrow + VT_OFF + sw128_off(4 * c + e, x, KB)) = w[e];
+    for (int r = 0; r < 4; ++r)
+      p[r] = make_float4(v.cst.x * v.ld[i][r].x, v.cst.y * v.ld[i][r].y, v.cst.z * v.ld[i][r].z, v.cst.w * v.ld[i][r].w);
+    const uint32_t ok = (v.mode == 0 && kok) ? ((v.vmask >> (4 * rg)) & 0xfu) : 0u;
+    vblock_store<KB>(vrow, xw + 4 * rg, c, ok, p);
   }
 }
 
@@ -545,20 +571,21 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
             mk[0] = w.x; mk[1] = w.y; mk[2] = w.z; mk[3] = w.w;
           }
         }
-        // observed-entry bits: row / column in range and mask byte nonzero (R5, R6)
+        // observed-entry byte masks (0xff per observed entry): mask byte nonzero (R6) and
+        // row / column in range.  Missing entries' values are used only in discarded lanes
+        // of the arithmetic below and never reach a result (AND with 0, R5).
+        uint32_t nz[4];
+#pragma unroll
+        for (int j4 = 0; j4 < 4; ++j4) nz[j4] = a.has_mask ? __vcmpne4(mk[j4], 0u) : 0xffffffffu;
         const int cv = cols_here - c0;
-        uint32_t obs = (!row_ok || cv <= 0) ? 0u : (cv >= 16 ? 0xffffu : ((1u << cv) - 1u));
-        if (a.has_mask) {
-          uint32_t mb = 0;
+        const uint32_t vbits = (!row_ok || cv <= 0) ? 0u : (cv >= 16 ? 0xffffu : ((1u << cv) - 1u));
+        if (vbits != 0xffffu) {
 #pragma unroll
           for (int j4 = 0; j4 < 4; ++j4) {
-            const uint32_t nz = __vcmpne4(mk[j4], 0u);   // 0xff per nonzero byte
-            mb |= ((nz & 1u) | ((nz >> 7) & 2u) | ((nz >> 14) & 4u) | ((nz >> 21) & 8u)) << (4 * j4);
+            const uint32_t b = (vbits >> (4 * j4)) & 0xfu;
+            nz[j4] &= ((b * 0x00204081u) & 0x01010101u) * 0xffu;   // 4 bits -> 4 bytes of 0x00 / 0xff
           }
-          obs &= mb;
         }
-#pragma unroll
-        for (int j = 0; j < 16; ++j) yv[j] = ((obs >> j) & 1u) ? yv[j] : 1.f;
         tmem_ld_wait(sv);
         if (h == 1) {   // S buffer fully read
           tc_fence_before();
@@ -568,21 +595,23 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
         if (a.mode != 0) {   // loss of the iterate entering the sweep (uniform branch)
 #pragma unroll
           for (int j = 0; j < 16; ++j) {
-            const float l = Ew<KIND>::loss(yv[j], fmaxf(__uint_as_float(sv[j]), 1e-30f), a.dv);
-            lsum += ((obs >> j) & 1u) ? l : 0.f;
+            const bool o = (nz[j >> 2] >> (8 * (j & 3))) & 1u;
+            const float l = Ew<KIND>::loss(o ? yv[j] : 1.f, fmaxf(__uint_as_float(sv[j]), 1e-30f), a.dv);
+            lsum += o ? l : 0.f;
           }
-          cnt += __popc(obs);
+#pragma unroll
+          for (int j4 = 0; j4 < 4; ++j4) cnt += __popc(nz[j4]) >> 3;
         }
-        // in place: sv[] becomes P_a, pb[] P_b; branch-free selects
+        // in place: sv[] becomes P_a, pb[] P_b; TF32 rounding and masking fused (add, and)
         uint32_t pb[16];
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
           const float yh = fmaxf(__uint_as_float(sv[j]), 1e-30f);
           float av, bv;
           Ew<KIND>::ab(yv[j], yh, a.dv, av, bv);
-          const bool o = (obs >> j) & 1u;
-          sv[j] = o ? tf32_bits(av) : 0u;
-          pb[j] = o ? tf32_bits(bv) : 0u;
+          const uint32_t mw = __byte_perm(nz[j >> 2], 0u, (j & 3) * 0x1111u);   // replicate byte
+          sv[j] = tf32_bits(av) & mw;
+          pb[j] = tf32_bits(bv) & mw;
         }
         if (a.mode != 2) {
           if (h == 0) {
