@@ -173,11 +173,41 @@ struct VTile {
   int mode;                                 // 0 fast (<= 1 varying table), 1 general, 2 empty
 };
 
+// Mixed-radix odometer of a lane's linear column index over the column modes: advanced by
+// the (small, nonnegative) step between consecutive tiles; divides only when a digit wraps.
+struct Odo {
+  int64_t col = -1;
+  int64_t dig[kMaxModes];
+};
+
+__device__ __forceinline__ void odo_seek(const TcArgs& a, Odo& o, int64_t col) {
+  if (o.col < 0) {
+    int64_t rem = col;
+    for (int d = a.nc - 1; d >= 0; --d) {
+      o.dig[d] = d > 0 ? rem % a.cdim[d] : rem;
+      rem = d > 0 ? rem / a.cdim[d] : 0;
+    }
+  } else {
+    int64_t carry = col - o.col;
+    for (int d = a.nc - 1; d >= 0 && carry; --d) {
+      const int64_t v = o.dig[d] + carry;
+      if (d == 0 || v < a.cdim[d]) {
+        o.dig[d] = v;
+        carry = 0;
+      } else {
+        o.dig[d] = v % a.cdim[d];
+        carry = v / a.cdim[d];
+      }
+    }
+  }
+  o.col = col;
+}
+
 // Column offsets of this warp's 16 tile columns (lane & 15), validity, and - on the vector
 // path - the loads of the next tile's table rows: lane owns 4x4 blocks (4 rows x 4 bonds).
 template <int KB>
 __device__ __forceinline__ void vtile_issue(const TcArgs& a, int64_t tile, int xw, int lane, VTile<KB>& v,
-                                            int (&toff)[kMaxTabs]) {
+                                            int (&toff)[kMaxTabs], Odo& odo) {
   using VT = VTile<KB>;
   const int x = xw + (lane & 15);
   int64_t col;
@@ -191,17 +221,13 @@ __device__ __forceinline__ void vtile_issue(const TcArgs& a, int64_t tile, int x
     valid = ci < a.CI;
     col = to * a.CI + ci;
   }
+  odo_seek(a, odo, col);
 #pragma unroll
-  for (int q = 0; q < kMaxTabs; ++q) toff[q] = 0;
-  if (valid) {
-    int64_t rem = col;
-    for (int d = a.nc - 1; d >= 0; --d) {
-      const int64_t i = rem % a.cdim[d];
-      rem /= a.cdim[d];
-#pragma unroll
-      for (int q = 0; q < kMaxTabs; ++q)
-        if (q < a.ntab) toff[q] += (int)(i * a.tcs[q][d]);
-    }
+  for (int q = 0; q < kMaxTabs; ++q) {
+    int o = 0;
+    if (q < a.ntab)
+      for (int d = 0; d < a.nc; ++d) o += (int)(odo.dig[d] * a.tcs[q][d]);
+    toff[q] = valid ? o : 0;
   }
   v.vmask = __ballot_sync(0xffffffffu, valid) & 0xffffu;
   if (v.vmask == 0u || !a.vec4) {
@@ -255,10 +281,31 @@ __device__ __forceinline__ void vtile_issue(const TcArgs& a, int64_t tile, int x
   }
 }
 
+// Per-lane smem byte offsets of its 4x4 blocks inside a V stage (constant over tiles).
+template <int KB>
+struct VOff {
+  static constexpr int C = KB / 4, NB = (4 * C) / 32;
+  int v[NB][4];    // V rows x0 + r, chunk c
+  int vt[NB][4];   // V^T rows 4c + e, column chunk x0 / 4
+  __device__ __forceinline__ void init(int xw, int lane) {
+    const int c = lane % C;
+#pragma unroll
+    for (int i = 0; i < NB; ++i) {
+      const int x0 = xw + 4 * ((lane + 32 * i) / C);
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        v[i][r] = sw128_off(x0 + r, 4 * c, BN);
+        vt[i][r] = VT_OFF + sw128_off(4 * c + r, x0, KB);
+      }
+    }
+  }
+};
+
 // Store one 4x4 block (rows x0..x0+3, bonds 4c..4c+3): four 16-byte rows of V and four
 // 16-byte columns of V^T, TF32 round-to-nearest, zeros where invalid.
 template <int KB>
-__device__ __forceinline__ void vblock_store(unsigned char* vrow, int x0, int c, uint32_t okbits, const float4 (&p)[4]) {
+__device__ __forceinline__ void vblock_store(unsigned char* vrow, const int (&ov)[4], const int (&ovt)[4],
+                                             uint32_t okbits, const float4 (&p)[4]) {
   uint32_t w[4][4];
 #pragma unroll
   for (int r = 0; r < 4; ++r) {
@@ -267,16 +314,16 @@ __device__ __forceinline__ void vblock_store(unsigned char* vrow, int x0, int c,
     w[r][1] = tf32_bits(p[r].y) & m;
     w[r][2] = tf32_bits(p[r].z) & m;
     w[r][3] = tf32_bits(p[r].w) & m;
-    *reinterpret_cast<uint4*>(vrow + sw128_off(x0 + r, 4 * c, BN)) = make_uint4(w[r][0], w[r][1], w[r][2], w[r][3]);
+    *reinterpret_cast<uint4*>(vrow + ov[r]) = make_uint4(w[r][0], w[r][1], w[r][2], w[r][3]);
   }
 #pragma unroll
   for (int e = 0; e < 4; ++e)
-    *reinterpret_cast<uint4*>(vrow + VT_OFF + sw128_off(4 * c + e, x0, KB)) = make_uint4(w[0][e], w[1][e], w[2][e], w[3][e]);
+    *reinterpret_cast<uint4*>(vrow + ovt[e]) = make_uint4(w[0][e], w[1][e], w[2][e], w[3][e]);
 }
 
 template <int KB>
 __device__ __forceinline__ void vtile_store(const TcArgs& a, int xw, int lane, const VTile<KB>& v,
-                                            const int (&toff)[kMaxTabs], unsigned char* vrow) {
+                                            const int (&toff)[kMaxTabs], unsigned char* vrow, const VOff<KB>& vo) {
   using VT = VTile<KB>;
   const int c = lane % VT::C;
   const bool kok = c * 4 < a.K;
@@ -299,7 +346,7 @@ __device__ __forceinline__ void vtile_store(const TcArgs& a, int xw, int lane, c
         }
       }
       const uint32_t ok = kok ? ((v.vmask >> (4 * rg)) & 0xfu) : 0u;
-      vblock_store<KB>(vrow, xw + 4 * rg, c, ok, p);
+      vblock_store<KB>(vrow, vo.v[i], vo.vt[i], ok, p);
     }
     return;
   }
@@ -333,7 +380,7 @@ __device__ __forceinline__ void vtile_store(const TcArgs& a, int xw, int lane, c
     for (int r = 0; r < 4; ++r)
       p[r] = make_float4(v.cst.x * v.ld[i][r].x, v.cst.y * v.ld[i][r].y, v.cst.z * v.ld[i][r].z, v.cst.w * v.ld[i][r].w);
     const uint32_t ok = (v.mode == 0 && kok) ? ((v.vmask >> (4 * rg)) & 0xfu) : 0u;
-    vblock_store<KB>(vrow, xw + 4 * rg, c, ok, p);
+    vblock_store<KB>(vrow, vo.v[i], vo.vt[i], ok, p);
   }
 }
 
@@ -476,12 +523,15 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
     const int xw = (warp - 4) * 16;
     VTile<KB> cur, nxt;
     int toff_c[kMaxTabs], toff_n[kMaxTabs];
-    if (T > 0) vtile_issue<KB>(a, t_begin, xw, lane, cur, toff_c);
+    Odo odo;
+    VOff<KB> vo;
+    vo.init(xw, lane);
+    if (T > 0) vtile_issue<KB>(a, t_begin, xw, lane, cur, toff_c, odo);
     for (int t = 0; t < T; ++t) {
-      if (t + 1 < T) vtile_issue<KB>(a, t_begin + t + 1, xw, lane, nxt, toff_n);   // next tile's rows in flight
+      if (t + 1 < T) vtile_issue<KB>(a, t_begin + t + 1, xw, lane, nxt, toff_n, odo);   // next tile's rows in flight
       const int vs = t % NV;
       mbar_wait(v_empty + 8 * vs, ((t / NV) & 1) ^ 1);
-      vtile_store<KB>(a, xw, lane, cur, toff_c, gV + vs * V_STAGE_MAX);
+      vtile_store<KB>(a, xw, lane, cur, toff_c, gV + vs * V_STAGE_MAX, vo);
       fence_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(v_full + 8 * vs);
