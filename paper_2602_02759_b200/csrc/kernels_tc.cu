@@ -175,28 +175,38 @@ struct VTile {
 
 // Mixed-radix odometer of a lane's linear column index over the column modes: advanced by
 // the (small, nonnegative) step between consecutive tiles; divides only when a digit wraps.
+// Digits live in registers (loops fully unrolled over kMaxModes, guarded by nc).
 struct Odo {
   int64_t col = -1;
-  int64_t dig[kMaxModes];
+  int dig[kMaxModes];
 };
 
 __device__ __forceinline__ void odo_seek(const TcArgs& a, Odo& o, int64_t col) {
   if (o.col < 0) {
     int64_t rem = col;
-    for (int d = a.nc - 1; d >= 0; --d) {
-      o.dig[d] = d > 0 ? rem % a.cdim[d] : rem;
-      rem = d > 0 ? rem / a.cdim[d] : 0;
+#pragma unroll
+    for (int d = kMaxModes - 1; d >= 0; --d) {
+      if (d >= a.nc) { o.dig[d] = 0; continue; }
+      if (d > 0) {
+        o.dig[d] = (int)(rem % a.cdim[d]);
+        rem /= a.cdim[d];
+      } else {
+        o.dig[d] = (int)rem;
+      }
     }
   } else {
-    int64_t carry = col - o.col;
-    for (int d = a.nc - 1; d >= 0 && carry; --d) {
-      const int64_t v = o.dig[d] + carry;
-      if (d == 0 || v < a.cdim[d]) {
+    int carry = (int)(col - o.col);
+#pragma unroll
+    for (int d = kMaxModes - 1; d >= 0; --d) {
+      if (d >= a.nc || carry == 0) continue;
+      const int v = o.dig[d] + carry;
+      const int n = (int)a.cdim[d];
+      if (d == 0 || v < n) {
         o.dig[d] = v;
         carry = 0;
       } else {
-        o.dig[d] = v % a.cdim[d];
-        carry = v / a.cdim[d];
+        o.dig[d] = v % n;
+        carry = v / n;
       }
     }
   }
@@ -225,8 +235,9 @@ __device__ __forceinline__ void vtile_issue(const TcArgs& a, int64_t tile, int x
 #pragma unroll
   for (int q = 0; q < kMaxTabs; ++q) {
     int o = 0;
-    if (q < a.ntab)
-      for (int d = 0; d < a.nc; ++d) o += (int)(odo.dig[d] * a.tcs[q][d]);
+#pragma unroll
+    for (int d = 0; d < kMaxModes; ++d)
+      if (q < a.ntab && d < a.nc) o += odo.dig[d] * (int)a.tcs[q][d];
     toff[q] = valid ? o : 0;
   }
   v.vmask = __ballot_sync(0xffffffffu, valid) & 0xffffu;
@@ -282,21 +293,24 @@ __device__ __forceinline__ void vtile_issue(const TcArgs& a, int64_t tile, int x
 }
 
 // Per-lane smem byte offsets of its 4x4 blocks inside a V stage (constant over tiles).
+// Per-lane smem byte offsets of its 4x4 blocks inside a V stage (constant over tiles).  Rows
+// x0..x0+3 (x0 % 4 == 0) share one 8-row swizzle group, so row r of V sits at
+//   vb + r*128 + ((cx ^ r) << 4)   with cx = (c & 7) ^ (x0 & 7),
+// and bond 4c+e of V^T at  vtb + e*128 + ((xc ^ e) << 4)  with xc = ((x0 & 31) >> 2) ^ (4 (c & 1)).
 template <int KB>
 struct VOff {
   static constexpr int C = KB / 4, NB = (4 * C) / 32;
-  int v[NB][4];    // V rows x0 + r, chunk c
-  int vt[NB][4];   // V^T rows 4c + e, column chunk x0 / 4
+  int vb[NB], vtb[NB], cx[NB], xc[NB];
   __device__ __forceinline__ void init(int xw, int lane) {
     const int c = lane % C;
 #pragma unroll
     for (int i = 0; i < NB; ++i) {
       const int x0 = xw + 4 * ((lane + 32 * i) / C);
-#pragma unroll
-      for (int r = 0; r < 4; ++r) {
-        v[i][r] = sw128_off(x0 + r, 4 * c, BN);
-        vt[i][r] = VT_OFF + sw128_off(4 * c + r, x0, KB);
-      }
+      vb[i] = (c >> 3) * (BN * 128) + (x0 >> 3) * 1024 + (x0 & 7) * 128;
+      cx[i] = (c & 7) ^ (x0 & 7);
+      const int k0 = 4 * c;
+      vtb[i] = VT_OFF + (x0 >> 5) * (KB * 128) + (k0 >> 3) * 1024 + (k0 & 7) * 128;
+      xc[i] = ((x0 & 31) >> 2) ^ (k0 & 7);
     }
   }
 };
@@ -304,8 +318,8 @@ struct VOff {
 // Store one 4x4 block (rows x0..x0+3, bonds 4c..4c+3): four 16-byte rows of V and four
 // 16-byte columns of V^T, TF32 round-to-nearest, zeros where invalid.
 template <int KB>
-__device__ __forceinline__ void vblock_store(unsigned char* vrow, const int (&ov)[4], const int (&ovt)[4],
-                                             uint32_t okbits, const float4 (&p)[4]) {
+__device__ __forceinline__ void vblock_store(unsigned char* vrow, int vb, int cx, int vtb, int xc, uint32_t okbits,
+                                             const float4 (&p)[4]) {
   uint32_t w[4][4];
 #pragma unroll
   for (int r = 0; r < 4; ++r) {
@@ -314,20 +328,22 @@ __device__ __forceinline__ void vblock_store(unsigned char* vrow, const int (&ov
     w[r][1] = tf32_bits(p[r].y) & m;
     w[r][2] = tf32_bits(p[r].z) & m;
     w[r][3] = tf32_bits(p[r].w) & m;
-    *reinterpret_cast<uint4*>(vrow + ov[r]) = make_uint4(w[r][0], w[r][1], w[r][2], w[r][3]);
+    *reinterpret_cast<uint4*>(vrow + vb + r * 128 + ((cx ^ r) << 4)) = make_uint4(w[r][0], w[r][1], w[r][2], w[r][3]);
   }
 #pragma unroll
   for (int e = 0; e < 4; ++e)
-    *reinterpret_cast<uint4*>(vrow + ovt[e]) = make_uint4(w[0][e], w[1][e], w[2][e], w[3][e]);
+    *reinterpret_cast<uint4*>(vrow + vtb + e * 128 + ((xc ^ e) << 4)) = make_uint4(w[0][e], w[1][e], w[2][e], w[3][e]);
 }
 
+// Slow paths (several varying tables, or non-vectorisable tables), out of line so the fast
+// path keeps its registers.
 template <int KB>
-__device__ __forceinline__ void vtile_store(const TcArgs& a, int xw, int lane, const VTile<KB>& v,
-                                            const int (&toff)[kMaxTabs], unsigned char* vrow, const VOff<KB>& vo) {
+__device__ __noinline__ void vtile_store_slow(const TcArgs& a, int xw, int lane, const VTile<KB>& v,
+                                              const int (&toff)[kMaxTabs], unsigned char* vrow, const VOff<KB>& vo) {
   using VT = VTile<KB>;
   const int c = lane % VT::C;
   const bool kok = c * 4 < a.K;
-  if (v.mode == 1 && a.vec4) {
+  if (a.vec4) {
     // general vector path: several varying tables, rows multiplied table by table
 #pragma unroll
     for (int i = 0; i < VT::NB; ++i) {
@@ -346,11 +362,11 @@ __device__ __forceinline__ void vtile_store(const TcArgs& a, int xw, int lane, c
         }
       }
       const uint32_t ok = kok ? ((v.vmask >> (4 * rg)) & 0xfu) : 0u;
-      vblock_store<KB>(vrow, vo.v[i], vo.vt[i], ok, p);
+      vblock_store<KB>(vrow, vo.vb[i], vo.cx[i], vo.vtb[i], vo.xc[i], ok, p);
     }
     return;
   }
-  if (v.mode == 1) {
+  {
     // scalar path (bond not contiguous / unaligned rows): lane = bond index k (+32 h)
 #pragma unroll 1
     for (int i = 0; i < 16; ++i) {
@@ -369,6 +385,17 @@ __device__ __forceinline__ void vtile_store(const TcArgs& a, int xw, int lane, c
         *reinterpret_cast<uint32_t*>(vrow + VT_OFF + sw128_off(k, x, KB)) = w;
       }
     }
+  }
+}
+
+template <int KB>
+__device__ __forceinline__ void vtile_store(const TcArgs& a, int xw, int lane, const VTile<KB>& v,
+                                            const int (&toff)[kMaxTabs], unsigned char* vrow, const VOff<KB>& vo) {
+  using VT = VTile<KB>;
+  const int c = lane % VT::C;
+  const bool kok = c * 4 < a.K;
+  if (v.mode == 1) {
+    vtile_store_slow<KB>(a, xw, lane, v, toff, vrow, vo);
     return;
   }
   // fast path (mode 0: constant rows x one varying table) and empty tiles (mode 2: zeros)
@@ -380,7 +407,7 @@ __device__ __forceinline__ void vtile_store(const TcArgs& a, int xw, int lane, c
     for (int r = 0; r < 4; ++r)
       p[r] = make_float4(v.cst.x * v.ld[i][r].x, v.cst.y * v.ld[i][r].y, v.cst.z * v.ld[i][r].z, v.cst.w * v.ld[i][r].w);
     const uint32_t ok = (v.mode == 0 && kok) ? ((v.vmask >> (4 * rg)) & 0xfu) : 0u;
-    vblock_store<KB>(vrow, vo.v[i], vo.vt[i], ok, p);
+    vblock_store<KB>(vrow, vo.vb[i], vo.cx[i], vo.vtb[i], vo.xc[i], ok, p);
   }
 }
 
