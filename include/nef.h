@@ -153,6 +153,11 @@ int nef_set_kernel_policy(int policy);
  * floats (row-major) to it.  NULL disables. */
 int nef_debug_dump(float* device_buffer);
 
+/* Diagnostics hook: when device_buffer != NULL the tcgen05 streaming kernel records, for
+ * CTA (0,0) and its first 1024 column tiles, clock64() stamps of its pipeline hand-offs
+ * (TMA issue, V generation, MMA issues, elementwise waits) as int64 [tile][16]. */
+int nef_debug_trace(int64_t* device_buffer);
+
 void nef_plan_destroy(nef_plan_t plan);
 const char* nef_last_error(void);
 const char* nef_version(void);

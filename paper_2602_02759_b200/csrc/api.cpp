@@ -34,6 +34,7 @@ thread_local std::string g_err;
 thread_local int64_t g_launches = 0;
 int g_policy = 0;
 float* g_debug = nullptr;   // optional device dump of the tcgen05 kernel's first tile (tests)
+long long* g_trace = nullptr;   // optional pipeline timeline of the tcgen05 kernel (diagnostics)
 
 // live CUDA-event timing of the streaming kernel (nef_profile_*)
 struct Prof {
@@ -250,6 +251,7 @@ int stream_pass(const Ctx& c, const nef::Lowering& L, const float* Y, const uint
     t.dv = dv;
     t.mode = mode;
     t.debug = g_debug;
+    t.trace = g_trace;
     {
       const char* e = std::getenv("NEF_TC_VT");
       t.vt = e ? std::atoi(e) : 1;
@@ -409,6 +411,11 @@ int nef_profile_read(double* kernel_ms, int64_t* launches, double* algorithmic_b
 
 int nef_debug_dump(float* device_buffer) {
   g_debug = device_buffer;
+  return NEF_OK;
+}
+
+int nef_debug_trace(int64_t* device_buffer) {
+  g_trace = reinterpret_cast<long long*>(device_buffer);
   return NEF_OK;
 }
 

@@ -411,6 +411,88 @@ __device__ __forceinline__ void vtile_store(const TcArgs& a, int xw, int lane, c
   }
 }
 
+// ------------------------------------------------------------------ elementwise stage
+// Row m's 16 Y values and mask bytes of half-step h of column half g (missing values are
+// loaded but never used: they only feed discarded lanes of the arithmetic).
+__device__ __forceinline__ void ew_load_y(const TcArgs& a, const unsigned char* ys, const unsigned char* ms, int g,
+                                          int h, int m, float (&yv)[16], uint32_t (&mk)[4]) {
+  const int c0 = 32 * g + 16 * h;
+  if (a.layout == 0) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) yv[j] = reinterpret_cast<const float*>(ys)[(c0 + j) * BM + m];
+    if (a.has_mask) {
+#pragma unroll
+      for (int j4 = 0; j4 < 4; ++j4) {
+        uint32_t w = 0;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) w |= (uint32_t)ms[(c0 + 4 * j4 + e) * BM + m] << (8 * e);
+        mk[j4] = w;
+      }
+    }
+  } else {
+    const unsigned char* sub = ys + g * (Y_STAGE / 2) + m * 128;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const float4 f = *reinterpret_cast<const float4*>(sub + (((4 * h + q) ^ (m & 7)) << 4));
+      yv[4 * q] = f.x; yv[4 * q + 1] = f.y; yv[4 * q + 2] = f.z; yv[4 * q + 3] = f.w;
+    }
+    if (a.has_mask) {
+      const int q = 2 * g + h;
+      const uint4 w = *reinterpret_cast<const uint4*>(ms + m * 64 + ((q ^ ((m >> 1) & 3)) << 4));
+      mk[0] = w.x; mk[1] = w.y; mk[2] = w.z; mk[3] = w.w;
+    }
+  }
+}
+
+// a, b (and the loss) of 16 entries: sv (S on entry) becomes P_a, pb receives P_b, both
+// TF32-rounded and zero at missing / out-of-range entries.  cv = valid columns from c0.
+template <int KIND>
+__device__ __forceinline__ void ew_half(const TcArgs& a, uint32_t (&sv)[16], const float (&yv)[16],
+                                        const uint32_t (&mk)[4], int cv, bool row_ok, uint32_t (&pb)[16],
+                                        float& lsum, long long& cnt) {
+  // observed-entry byte masks (0xff per observed entry): mask byte nonzero (R6) and row /
+  // column in range; AND-ed into the results (R5: a select, never a multiply)
+  uint32_t nz[4];
+#pragma unroll
+  for (int j4 = 0; j4 < 4; ++j4) nz[j4] = a.has_mask ? __vcmpne4(mk[j4], 0u) : 0xffffffffu;
+  const uint32_t vbits = (!row_ok || cv <= 0) ? 0u : (cv >= 16 ? 0xffffu : ((1u << cv) - 1u));
+  if (vbits != 0xffffu) {
+#pragma unroll
+    for (int j4 = 0; j4 < 4; ++j4) {
+      const uint32_t b = (vbits >> (4 * j4)) & 0xfu;
+      nz[j4] &= ((b * 0x00204081u) & 0x01010101u) * 0xffu;   // 4 bits -> 4 bytes of 0x00 / 0xff
+    }
+  }
+  if (a.mode != 0) {   // loss of the iterate entering the sweep (uniform branch)
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const bool o = (nz[j >> 2] >> (8 * (j & 3))) & 1u;
+      const float l = Ew<KIND>::loss(o ? yv[j] : 1.f, fmaxf(__uint_as_float(sv[j]), 1e-30f), a.dv);
+      lsum += o ? l : 0.f;
+    }
+#pragma unroll
+    for (int j4 = 0; j4 < 4; ++j4) cnt += __popc(nz[j4]) >> 3;
+  }
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    const float yh = fmaxf(__uint_as_float(sv[j]), 1e-30f);
+    float av, bv;
+    Ew<KIND>::ab(yv[j], yh, a.dv, av, bv);
+    const uint32_t mw = __byte_perm(nz[j >> 2], 0u, (j & 3) * 0x1111u);   // replicate byte
+    sv[j] = tf32_bits(av) & mw;
+    pb[j] = tf32_bits(bv) & mw;
+  }
+}
+
+// pipeline timeline (diagnostics): event e of tile t in CTA (0,0)
+enum TraceEv : int {
+  EV_TMA_ISSUE = 0, EV_VG_START, EV_VG_DONE, EV_MMA1_ISSUE, EV_MMA23_ISSUE, EV_EW_S, EV_EW_Y, EV_EW_PEMPTY,
+  EV_EW_DONE, EV_VG_ISSUED
+};
+__device__ __forceinline__ void trace_ev(const TcArgs& a, int t, int e) {
+  if (a.trace && blockIdx.x == 0 && blockIdx.y == 0 && t < 1024) a.trace[t * 16 + e] = (long long)clock64();
+}
+
 // ------------------------------------------------------------------ the kernel
 template <int KB, int KIND>
 __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_constant__ Params P) {
@@ -477,6 +559,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
       for (int t = 0; t < T; ++t) {
         const int st = t % NS;
         mbar_wait(y_empty + 8 * st, ((t / NS) & 1) ^ 1);
+        trace_ev(a, t, EV_TMA_ISSUE);
         const int64_t tile = t_begin + t;
         const uint32_t bar = y_full + 8 * st;
         mbar_expect_tx(bar, bytes);
@@ -505,43 +588,50 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
       constexpr uint32_t id2 = idesc_tf32(128, KB);   // N = P V     : N = bond
       mbar_wait(u_ready, 0);
       tc_fence_after();
-      for (int t = 0; t <= T; ++t) {
-        if (t < T) {
-          const int vs = t % NV, s = t & 1;
-          mbar_wait(v_full + 8 * vs, (t / NV) & 1);
-          mbar_wait(s_empty + 8 * s, ((t >> 1) & 1) ^ 1);
-          tc_fence_after();
-          const uint32_t vb = sV + vs * V_STAGE_MAX;
-          const uint32_t d = tS + 64 * s;
+      // reconstruction MMAs only; the numerator / denominator MMAs have their own issuer
+      // (warp 2) so that neither waits behind the other's dependencies
+      for (int t = 0; t < T; ++t) {
+        const int vs = t % NV, s = t & 1;
+        mbar_wait(v_full + 8 * vs, (t / NV) & 1);
+        mbar_wait(s_empty + 8 * s, ((t >> 1) & 1) ^ 1);
+        tc_fence_after();
+        trace_ev(a, t, EV_MMA1_ISSUE);
+        const uint32_t vb = sV + vs * V_STAGE_MAX;
+        const uint32_t d = tS + 64 * s;
 #pragma unroll
-          for (int kk = 0; kk < KB / 8; ++kk) {
-            const uint64_t bd = sdesc(vb + (kk >> 2) * (BN * 128) + (kk & 3) * 32, 16, 1024);
-            mma_ts(d, tUh + kk * 8, bd, id1, kk > 0 ? 1u : 0u);
-          }
-#pragma unroll
-          for (int kk = 0; kk < KB / 8; ++kk) {
-            const uint64_t bd = sdesc(vb + (kk >> 2) * (BN * 128) + (kk & 3) * 32, 16, 1024);
-            mma_ts(d, tUl + kk * 8, bd, id1, 1u);
-          }
-          mma_commit(s_full + 8 * s);
-          if (a.mode == 2) mma_commit(v_empty + 8 * vs);
+        for (int kk = 0; kk < KB / 8; ++kk) {
+          const uint64_t bd = sdesc(vb + (kk >> 2) * (BN * 128) + (kk & 3) * 32, 16, 1024);
+          mma_ts(d, tUh + kk * 8, bd, id1, kk > 0 ? 1u : 0u);
         }
-        if (t >= 1 && a.mode != 2) {
-          const int u = t - 1, vs = u % NV;
-          mbar_wait(p_full, u & 1);
-          tc_fence_after();
-          // B = V^T, K-major SW128: rows = bond (N), K = tile columns (2 atoms of 32)
-          const uint32_t vtb = sV + vs * V_STAGE_MAX + VT_OFF;
 #pragma unroll
-          for (int kk = 0; kk < BN / 8; ++kk) {
-            const uint64_t bd = sdesc(vtb + (kk >> 2) * (KB * 128) + (kk & 3) * 32, 16, 1024);
-            const uint32_t acc = (u > 0 || kk > 0) ? 1u : 0u;
-            mma_ts(tNa, tPa + kk * 8, bd, id2, acc);
-            mma_ts(tNb, tPb + kk * 8, bd, id2, acc);
-          }
-          mma_commit(p_empty);
-          mma_commit(v_empty + 8 * vs);
+        for (int kk = 0; kk < KB / 8; ++kk) {
+          const uint64_t bd = sdesc(vb + (kk >> 2) * (BN * 128) + (kk & 3) * 32, 16, 1024);
+          mma_ts(d, tUl + kk * 8, bd, id1, 1u);
         }
+        mma_commit(s_full + 8 * s);
+        if (a.mode == 2) mma_commit(v_empty + 8 * vs);   // else released by the numerator issuer
+      }
+    }
+  } else if (warp == 2) {
+    // ------------------------------------------------------------ numerator / denominator MMAs
+    if (lane == 0 && T > 0 && a.mode != 2) {
+      constexpr uint32_t id2 = idesc_tf32(128, KB);   // N = P V : N = bond
+      for (int u = 0; u < T; ++u) {
+        const int vs = u % NV;
+        mbar_wait(p_full, u & 1);
+        tc_fence_after();
+        trace_ev(a, u, EV_MMA23_ISSUE);
+        // B = V^T, K-major SW128: rows = bond (N), K = tile columns (2 atoms of 32)
+        const uint32_t vtb = sV + vs * V_STAGE_MAX + VT_OFF;
+#pragma unroll
+        for (int kk = 0; kk < BN / 8; ++kk) {
+          const uint64_t bd = sdesc(vtb + (kk >> 2) * (KB * 128) + (kk & 3) * 32, 16, 1024);
+          const uint32_t acc = (u > 0 || kk > 0) ? 1u : 0u;
+          mma_ts(tNa, tPa + kk * 8, bd, id2, acc);
+          mma_ts(tNb, tPb + kk * 8, bd, id2, acc);
+        }
+        mma_commit(p_empty);
+        mma_commit(v_empty + 8 * vs);
       }
       mma_commit(nd_full);
     }
@@ -556,12 +646,15 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
     if (T > 0) vtile_issue<KB>(a, t_begin, xw, lane, cur, toff_c, odo);
     for (int t = 0; t < T; ++t) {
       if (t + 1 < T) vtile_issue<KB>(a, t_begin + t + 1, xw, lane, nxt, toff_n, odo);   // next tile's rows in flight
+      if (warp == 4 && lane == 0) trace_ev(a, t, EV_VG_ISSUED);
       const int vs = t % NV;
       mbar_wait(v_empty + 8 * vs, ((t / NV) & 1) ^ 1);
+      if (warp == 4 && lane == 0) trace_ev(a, t, EV_VG_START);
       vtile_store<KB>(a, xw, lane, cur, toff_c, gV + vs * V_STAGE_MAX, vo);
       fence_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(v_full + 8 * vs);
+      if (warp == 4 && lane == 0) trace_ev(a, t, EV_VG_DONE);
       cur = nxt;
 #pragma unroll
       for (int q = 0; q < kMaxTabs; ++q) toff_c[q] = toff_n[q];
@@ -610,107 +703,54 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
       }
       const int st = t % NS;
       mbar_wait(s_full + 8 * s, (t >> 1) & 1);
+      if (warp == 8 && lane == 0) trace_ev(a, t, EV_EW_S);
       tc_fence_after();
       mbar_wait(y_full + 8 * st, (t / NS) & 1);
+      if (warp == 8 && lane == 0) trace_ev(a, t, EV_EW_Y);
       const unsigned char* ys = gY + st * Y_STAGE;
       const unsigned char* ms = gM + st * M_STAGE;
       float lsum = 0.f;
-#pragma unroll 1
+      // issue both halves' TMEM loads and smem loads before any arithmetic (latency overlap)
+      uint32_t sv[2][16];
+      float yv[2][16];
+      uint32_t mk[2][4];
+      tmem_ld16(tS + 64 * s + lane_off + 32 * g, sv[0]);
+      tmem_ld16(tS + 64 * s + lane_off + 32 * g + 16, sv[1]);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) ew_load_y(a, ys, ms, g, h, m, yv[h], mk[h]);
+      tmem_ld_wait(sv[0]);
+      tmem_ld_wait(sv[1]);
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(s_empty + 8 * s);   // S buffer fully read
+      __syncwarp();
+      if (lane == 0) mbar_arrive(y_empty + 8 * st);  // Y / mask stage fully read
+#pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int c0 = 32 * g + 16 * h;   // first tile column of this half-step
-        uint32_t sv[16];
-        tmem_ld16(tS + 64 * s + lane_off + c0, sv);
-        // my row's 16 Y values and mask bytes (missing values are never used)
-        float yv[16];
-        uint32_t mk[4];
-        if (a.layout == 0) {
-#pragma unroll
-          for (int j = 0; j < 16; ++j) yv[j] = reinterpret_cast<const float*>(ys)[(c0 + j) * BM + m];
-          if (a.has_mask) {
-#pragma unroll
-            for (int j4 = 0; j4 < 4; ++j4) {
-              uint32_t w = 0;
-#pragma unroll
-              for (int e = 0; e < 4; ++e) w |= (uint32_t)ms[(c0 + 4 * j4 + e) * BM + m] << (8 * e);
-              mk[j4] = w;
-            }
-          }
-        } else {
-          const unsigned char* sub = ys + g * (Y_STAGE / 2) + m * 128;
-#pragma unroll
-          for (int q = 0; q < 4; ++q) {
-            const float4 f = *reinterpret_cast<const float4*>(sub + (((4 * h + q) ^ (m & 7)) << 4));
-            yv[4 * q] = f.x; yv[4 * q + 1] = f.y; yv[4 * q + 2] = f.z; yv[4 * q + 3] = f.w;
-          }
-          if (a.has_mask) {
-            const int q = 2 * g + h;
-            const uint4 w = *reinterpret_cast<const uint4*>(ms + m * 64 + ((q ^ ((m >> 1) & 3)) << 4));
-            mk[0] = w.x; mk[1] = w.y; mk[2] = w.z; mk[3] = w.w;
-          }
-        }
-        // observed-entry byte masks (0xff per observed entry): mask byte nonzero (R6) and
-        // row / column in range.  Missing entries' values are used only in discarded lanes
-        // of the arithmetic below and never reach a result (AND with 0, R5).
-        uint32_t nz[4];
-#pragma unroll
-        for (int j4 = 0; j4 < 4; ++j4) nz[j4] = a.has_mask ? __vcmpne4(mk[j4], 0u) : 0xffffffffu;
-        const int cv = cols_here - c0;
-        const uint32_t vbits = (!row_ok || cv <= 0) ? 0u : (cv >= 16 ? 0xffffu : ((1u << cv) - 1u));
-        if (vbits != 0xffffu) {
-#pragma unroll
-          for (int j4 = 0; j4 < 4; ++j4) {
-            const uint32_t b = (vbits >> (4 * j4)) & 0xfu;
-            nz[j4] &= ((b * 0x00204081u) & 0x01010101u) * 0xffu;   // 4 bits -> 4 bytes of 0x00 / 0xff
-          }
-        }
-        tmem_ld_wait(sv);
-        if (h == 1) {   // S buffer fully read
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) mbar_arrive(s_empty + 8 * s);
-        }
-        if (a.mode != 0) {   // loss of the iterate entering the sweep (uniform branch)
-#pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            const bool o = (nz[j >> 2] >> (8 * (j & 3))) & 1u;
-            const float l = Ew<KIND>::loss(o ? yv[j] : 1.f, fmaxf(__uint_as_float(sv[j]), 1e-30f), a.dv);
-            lsum += o ? l : 0.f;
-          }
-#pragma unroll
-          for (int j4 = 0; j4 < 4; ++j4) cnt += __popc(nz[j4]) >> 3;
-        }
-        // in place: sv[] becomes P_a, pb[] P_b; TF32 rounding and masking fused (add, and)
         uint32_t pb[16];
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          const float yh = fmaxf(__uint_as_float(sv[j]), 1e-30f);
-          float av, bv;
-          Ew<KIND>::ab(yv[j], yh, a.dv, av, bv);
-          const uint32_t mw = __byte_perm(nz[j >> 2], 0u, (j & 3) * 0x1111u);   // replicate byte
-          sv[j] = tf32_bits(av) & mw;
-          pb[j] = tf32_bits(bv) & mw;
-        }
+        ew_half<KIND>(a, sv[h], yv[h], mk[h], cols_here - c0, row_ok, pb, lsum, cnt);
         if (a.mode != 2) {
           if (h == 0) {
             mbar_wait(p_empty, (t & 1) ^ 1);
+            if (warp == 8 && lane == 0) trace_ev(a, t, EV_EW_PEMPTY);
             tc_fence_after();
           }
-          tmem_st16(tPa + lane_off + c0, sv);
+          tmem_st16(tPa + lane_off + c0, sv[h]);
           tmem_st16(tPb + lane_off + c0, pb);
         }
         if (a.debug && blockIdx.x == 0 && blockIdx.y == 0 && t == 0) {
 #pragma unroll
-          for (int j = 0; j < 16; ++j) a.debug[m * 64 + c0 + j] = __uint_as_float(sv[j]);
+          for (int j = 0; j < 16; ++j) a.debug[m * 64 + c0 + j] = __uint_as_float(sv[h][j]);
         }
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(y_empty + 8 * st);
       loss_acc += (double)lsum;
       if (a.mode != 2) {
         tmem_st_wait();
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(p_full);
+        if (warp == 8 && lane == 0) trace_ev(a, t, EV_EW_DONE);
       }
     }
     // epilogue: N (g = 0) / D (g = 1) for this lane -> split partials

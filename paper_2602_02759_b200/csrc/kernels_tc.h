@@ -32,6 +32,7 @@ struct TcArgs {
   DivParams dv;
   int mode;                   // 0 update, 1 update + loss, 2 loss only
   float* debug;               // optional debug dump (first tile of CTA (0,0))
+  long long* trace;           // optional pipeline timeline of CTA (0,0): [tile][16] clock64 stamps
   int vt;                     // 1: numerator MMAs read a K-major V^T copy; 0: MN-major view of V
   int vec4;                   // 1: every table has the bond contiguous (boff[k] = k), K % 4 == 0 and
                               //    16-byte aligned rows -> float4 V generation

@@ -55,6 +55,7 @@ def _load():
         "nef_set_kernel_policy": (ctypes.c_int, [ctypes.c_int]),
         "nef_profile_enable": (ctypes.c_int, [ctypes.c_int]),
         "nef_debug_dump": (ctypes.c_int, [vp]),
+        "nef_debug_trace": (ctypes.c_int, [vp]),
         "nef_profile_read": (ctypes.c_int, [ctypes.POINTER(d), i64p, ctypes.POINTER(d)]),
         "nef_plan_destroy": (None, [vp]),
         "nef_last_error": (ctypes.c_char_p, []),
@@ -71,7 +72,7 @@ LIB = _load()
 EXPORTED = ("nef_plan", "nef_plan_info", "nef_factor_shape", "nef_local_shape", "nef_plan_describe", "nef_fit",
             "nef_update", "nef_num_den", "nef_apply_update", "nef_loss", "nef_host_scratch_bytes", "nef_fit_host",
             "nef_nccl_unique_id", "nef_plan_shard", "nef_last_launch_count", "nef_set_kernel_policy",
-            "nef_profile_enable", "nef_profile_read", "nef_debug_dump",
+            "nef_profile_enable", "nef_profile_read", "nef_debug_dump", "nef_debug_trace",
             "nef_plan_destroy", "nef_last_error", "nef_version")
 
 
@@ -223,6 +224,10 @@ def nef_profile_read():
 
 def nef_debug_dump(buf):
     _check(LIB.nef_debug_dump(_ptr(buf)))
+
+
+def nef_debug_trace(buf):
+    _check(LIB.nef_debug_trace(_ptr(buf)))
 
 
 def nef_version() -> str:

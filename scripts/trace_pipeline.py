@@ -1,0 +1,42 @@
+"""Print the tcgen05 kernel's per-tile pipeline timeline (CTA (0,0)) for one factor update."""
+import argparse
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, ".")
+from nef_inputs import CONFIGS, generate_torch  # noqa: E402
+from paper_2602_02759_b200 import nef  # noqa: E402
+
+EV = ["TMA", "VG_START", "VG_DONE", "MMA1", "MMA23", "EW_S", "EW_Y", "EW_PEMPTY", "EW_DONE", "VG_ISSUED"]
+ap = argparse.ArgumentParser()
+ap.add_argument("--config", default="c5")
+ap.add_argument("--ell", type=int, default=0)
+ap.add_argument("--first", type=int, default=200)
+ap.add_argument("--n", type=int, default=8)
+args = ap.parse_args()
+cfg = CONFIGS[args.config]
+d = generate_torch(args.config, torch.device("cuda"))
+plan = nef.Plan(cfg.model, cfg.shape, cfg.ranks)
+F = [f.clone() for f in d["init"]]
+plan.update(args.ell, d["Y"], d["mask"], cfg.alpha, cfg.beta, F)
+tr = torch.zeros(1024 * 16, dtype=torch.int64, device="cuda")
+nef.nef_debug_trace(tr)
+plan.update(args.ell, d["Y"], d["mask"], cfg.alpha, cfg.beta, F)
+torch.cuda.synchronize()
+nef.nef_debug_trace(None)
+t = tr.cpu().numpy().reshape(1024, 16)[:, :len(EV)].astype(np.int64)
+valid = (t[:, EV.index("EW_DONE")] > 0).sum()
+print("tiles traced", valid)
+lo, hi = args.first, min(args.first + args.n, valid - 1)
+base = t[lo, EV.index("MMA1")]
+print("tile " + " ".join("%9s" % e for e in EV))
+for i in range(lo, hi):
+    print("%4d " % i + " ".join("%9d" % (t[i, j] - base) for j in range(len(EV))))
+per = np.diff(t[lo:hi + 1, EV.index("EW_DONE")])
+print("cycles per tile (EW_DONE to EW_DONE): median %d" % np.median(per))
+for a_, b_ in [("MMA1", "EW_S"), ("EW_S", "EW_PEMPTY"), ("EW_PEMPTY", "EW_DONE"), ("EW_DONE", "MMA23"),
+               ("VG_START", "VG_DONE"), ("VG_DONE", "MMA1"), ("TMA", "EW_Y")]:
+    dd = t[lo:hi, EV.index(b_)] - t[lo:hi, EV.index(a_)]
+    print("%10s -> %-10s median %7d" % (a_, b_, np.median(dd)))
