@@ -243,6 +243,22 @@ int stream_pass(const Ctx& c, const nef::Lowering& L, const float* Y, const uint
         for (int k = 0; k < L.K; ++k) v4 = v4 && (boff[(size_t)q * L.K + k] == k);
       }
       t.vec4 = v4 && a.ntab > 0 ? 1 : 0;
+      // direct V: the innermost column mode (last column mode) has an extent divisible by 64,
+      // exactly one table carries it, with one table row per column (row stride = K)
+      t.vdirect = 0;
+      const int inner = a.nc - 1;
+      const char* dv = std::getenv("NEF_TC_VDIRECT");
+      const bool allow = !dv || std::atoi(dv) != 0;
+      if (allow && t.vec4 && inner >= 0 && a.cdim[inner] % 64 == 0) {
+        int nvar = 0, vq = -1;
+        for (int q = 0; q < a.ntab; ++q)
+          if (a.tcs[q][inner] != 0) { ++nvar; vq = q; }
+        if (nvar == 1 && a.tcs[vq][inner] == L.K) {
+          t.vdirect = 1;
+          t.var_tab = vq;
+          t.var_rows = L.tabs[vq].prog.result.elems / L.K;
+        }
+      }
     }
     t.Qpart = reinterpret_cast<float*>(c.ws + L.ws_tc_Qpart);
     t.losspart = reinterpret_cast<double*>(c.ws + L.ws_tc_losspart);

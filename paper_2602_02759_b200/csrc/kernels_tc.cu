@@ -46,6 +46,7 @@ constexpr int V_STAGE_MAX = 2 * VT_OFF;   // V (16 KB) + V^T (16 KB) for KB = 64
 struct __align__(64) Params {
   CUtensorMap tmY;
   CUtensorMap tmM;
+  CUtensorMap tmV;   // direct-V table rows (2-D {K, var_rows}, box {32, 64}, SW128)
   TcArgs a;
 };
 
@@ -484,6 +485,13 @@ __device__ __forceinline__ void ew_half(const TcArgs& a, uint32_t (&sv)[16], con
   }
 }
 
+// linear column index of the first column of a tile
+__device__ __forceinline__ int64_t tile_col0(const TcArgs& a, int64_t tile) {
+  if (a.layout == 0) return tile * BN;
+  const int64_t ti = tile % a.tiles_inner, to = tile / a.tiles_inner;
+  return to * a.CI + ti * BN;
+}
+
 // pipeline timeline (diagnostics): event e of tile t in CTA (0,0)
 enum TraceEv : int {
   EV_TMA_ISSUE = 0, EV_VG_START, EV_VG_DONE, EV_MMA1_ISSUE, EV_MMA23_ISSUE, EV_EW_S, EV_EW_Y, EV_EW_PEMPTY,
@@ -513,7 +521,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
   const uint32_t y_full = sBar, y_empty = sBar + 8 * NS, v_full = sBar + 16 * NS, v_empty = v_full + 8 * NV;
   const uint32_t s_full = v_empty + 8 * NV, s_empty = s_full + 16, p_full = s_empty + 16, p_empty = p_full + 8;
   const uint32_t nd_full = p_empty + 8, u_ready = nd_full + 8;
-  const uint32_t sTmem = u_ready + 8;
+  const uint32_t vraw_full = u_ready + 8;   // NV barriers: direct-V rows landed (TMA)
+  const uint32_t sTmem = vraw_full + 8 * NV;
   unsigned char* gY = gbase;
   unsigned char* gM = gbase + NS * Y_STAGE;
   unsigned char* gV = gM + NS * M_STAGE;
@@ -537,6 +546,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
     mbar_init(p_empty, 1);
     mbar_init(nd_full, 1);
     mbar_init(u_ready, 8);
+    for (int i = 0; i < NV; ++i) mbar_init(vraw_full + 8 * i, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&P.tmY)) : "memory");
     if (a.has_mask) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&P.tmM)) : "memory");
@@ -634,6 +644,77 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
         mma_commit(v_empty + 8 * vs);
       }
       mma_commit(nd_full);
+    }
+  } else if (warp == 3) {
+    // ------------------------------------------------------------ direct-V row loads (TMA)
+    if (lane == 0 && a.vdirect) {
+      Odo o;
+      for (int t = 0; t < T; ++t) {
+        const int vs = t % NV;
+        mbar_wait(v_empty + 8 * vs, ((t / NV) & 1) ^ 1);
+        odo_seek(a, o, tile_col0(a, t_begin + t));
+        int off = 0;
+#pragma unroll
+        for (int d = 0; d < kMaxModes; ++d)
+          if (d < a.nc) off += o.dig[d] * (int)a.tcs[a.var_tab][d];
+        const int rowv = off / a.K;
+        const uint32_t bar = vraw_full + 8 * vs;
+        mbar_expect_tx(bar, (uint32_t)(KB * BN * 4));
+#pragma unroll
+        for (int h = 0; h < KB / 32; ++h) tma_load_2d(sV + vs * V_STAGE_MAX + h * (BN * 128), &P.tmV, 32 * h, rowv, bar);
+      }
+    }
+  } else if (warp >= 4 && warp < 4 + NVG && a.vdirect) {
+    // ------------------------------------------------------------ direct V: scale rows in place
+    // V[x][k] = T_var[row0 + x][k] * prod_{q != var} T_q[const row][k]; V^T written alongside.
+    const int xw = (warp - 4) * 16;
+    constexpr int C = KB / 4, NB = (4 * C) / 32;
+    const int c = lane % C;
+    const bool kok = c * 4 < a.K;
+    VOff<KB> vo;
+    vo.init(xw, lane);
+    Odo o;
+    float4 cn[kMaxTabs];
+    auto fetch_const = [&](int t, float4 (&cr)[kMaxTabs]) {
+      odo_seek(a, o, tile_col0(a, t_begin + t));
+#pragma unroll
+      for (int q = 0; q < kMaxTabs; ++q) {
+        cr[q] = make_float4(1.f, 1.f, 1.f, 1.f);
+        if (q < a.ntab && q != a.var_tab) {
+          int off = 0;
+#pragma unroll
+          for (int d = 0; d < kMaxModes; ++d)
+            if (d < a.nc) off += o.dig[d] * (int)a.tcs[q][d];
+          cr[q] = kok ? __ldg(reinterpret_cast<const float4*>(a.tab[q] + off) + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      }
+    };
+    if (T > 0) fetch_const(0, cn);
+    for (int t = 0; t < T; ++t) {
+      float4 cst = make_float4(1.f, 1.f, 1.f, 1.f);
+#pragma unroll
+      for (int q = 0; q < kMaxTabs; ++q) {
+        cst.x *= cn[q].x; cst.y *= cn[q].y; cst.z *= cn[q].z; cst.w *= cn[q].w;
+      }
+      if (t + 1 < T) fetch_const(t + 1, cn);   // next tile's constant rows in flight
+      const int vs = t % NV;
+      mbar_wait(vraw_full + 8 * vs, (t / NV) & 1);
+      if (warp == 4 && lane == 0) trace_ev(a, t, EV_VG_START);
+      unsigned char* vrow = gV + vs * V_STAGE_MAX;
+#pragma unroll
+      for (int i = 0; i < NB; ++i) {
+        float4 p[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+          const float4 f = *reinterpret_cast<const float4*>(vrow + vo.vb[i] + r * 128 + ((vo.cx[i] ^ r) << 4));
+          p[r] = make_float4(f.x * cst.x, f.y * cst.y, f.z * cst.z, f.w * cst.w);
+        }
+        vblock_store<KB>(vrow, vo.vb[i], vo.cx[i], vo.vtb[i], vo.xc[i], kok ? 0xfu : 0u, p);
+      }
+      fence_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(v_full + 8 * vs);
+      if (warp == 4 && lane == 0) trace_ev(a, t, EV_VG_DONE);
     }
   } else if (warp >= 4 && warp < 4 + NVG) {
     // ------------------------------------------------------------ column operand V (Khatri-Rao)
@@ -880,6 +961,14 @@ cudaError_t launch(const TcArgs& args, const float* Y, const uint8_t* M, int64_t
       uint32_t bm[3] = {64, 128, 1};
       ok = encode(&P.tmM, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, M, d, sm, bm, CU_TENSOR_MAP_SWIZZLE_64B);
     }
+  }
+  if (ok && args.vdirect) {
+    // table rows [var_rows][K] -> V stage, two 32-float SW128 boxes (K beyond the row: zeros)
+    uint64_t d[2] = {(uint64_t)args.K, (uint64_t)args.var_rows};
+    uint64_t sv[1] = {(uint64_t)args.K * 4};
+    uint32_t bv[2] = {32, 64};
+    ok = encode(&P.tmV, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, args.tab[args.var_tab], d, sv, bv,
+                CU_TENSOR_MAP_SWIZZLE_128B);
   }
   if (!ok) return cudaErrorInvalidValue;
   P.a.has_mask = M ? 1 : 0;

@@ -36,6 +36,12 @@ struct TcArgs {
   int vt;                     // 1: numerator MMAs read a K-major V^T copy; 0: MN-major view of V
   int vec4;                   // 1: every table has the bond contiguous (boff[k] = k), K % 4 == 0 and
                               //    16-byte aligned rows -> float4 V generation
+  // direct V: the 64 columns of every tile are 64 consecutive rows of ONE
+  // column table (the one holding the innermost column mode; every other table is constant
+  // across a tile); those rows are TMA-loaded into the V stage and scaled in place.
+  int vdirect;
+  int var_tab;                // index of that table
+  int64_t var_rows;           // its number of rows (row length = K)
   int dbg;                    // diagnostics: 1 prefill N/D with 1 and always accumulate,
                               // 2 numerator B as K-major, 4 swap LBO/SBO of the MN-major view
 };

@@ -21,6 +21,11 @@ TC_CASES = [
     ("ik,jk,tl,dl,kl->ijtd", (32, 48, 24, 40), (20, 10), (0.5, 0.0), 0.0, "poisson"),  # c4-like
     ("ir,jr,kr->ijk", (130, 96, 64), (40,), (1.0, 0.5), 0.0, "gamma"),            # literal c5 reading, K=40
     ("ir,jr,kr->ijk", (256, 128, 64), (17,), (0.5, 0.5), 0.1, "gamma"),           # Hellinger, odd bond
+    # inner column extents divisible by 64: direct-V path (table rows TMA-loaded into the V stage)
+    ("ir,jr,kr->ijk", (130, 128, 192), (32,), (1.0, 0.0), 0.2, "poisson"),
+    ("ir,jr,kr->ijk", (96, 192, 128), (64,), (1.0, -0.5), 0.05, "gamma"),
+    ("ia,jb,kc,abc->ijk", (80, 128, 64), (16, 16, 16), (1.0, 1.0), 0.1, "absnormal"),
+    ("ir,jr,kr->ijk", (64, 64, 128), (24,), (0.5, 0.0), 0.0, "poisson"),
 ]
 
 
@@ -140,7 +145,40 @@ def test_tc_matches_ffma_and_n_observed(nef, case):
     assert abs(s_tc - rs) <= 1e-4 * abs(rs) and abs(s_ff - rs) <= 1e-5 * abs(rs)
 
 
-@pytest.mark.parametrize("case", [TC_CASES[0], TC_CASES[1]], ids=["c3like", "c5like"])
+def test_direct_v_matches_generated_v(nef):
+    """The direct-V path (TMA rows scaled in place) and the generated-V path form the same
+    TF32-rounded V tiles, hence bit-identical numerators / denominators."""
+    import subprocess
+    import sys
+    code = r'''
+import sys, numpy as np, torch
+sys.path.insert(0, ".")
+from paper_2602_02759_b200 import nef
+from tests.test_gpu_tc import TC_CASES, _data, _dev
+out = []
+for ci in (6, 7, 8):
+    ms, shape, ranks, (al, be), pm, law = TC_CASES[ci]
+    Y, M, init = _data(ms, shape, ranks, pm, law)
+    plan = nef.Plan(ms, shape, ranks)
+    Yd, Md, F = _dev(Y, M, init)
+    for ell in range(len(F)):
+        n, d = plan.num_den(ell, Yd, Md, al, be, F)
+        out.append(torch.cat([n.flatten(), d.flatten()]).cpu().numpy())
+np.save(sys.argv[1], np.concatenate(out))
+'''
+    import os
+    import tempfile
+    res = []
+    for flag in ("1", "0"):
+        f = tempfile.mktemp(suffix=".npy")
+        env = dict(os.environ, NEF_TC_VDIRECT=flag)
+        subprocess.run([sys.executable, "-c", code, f], env=env, check=True, timeout=300,
+                       cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+        res.append(np.load(f))
+    assert np.array_equal(res[0], res[1])
+
+
+@pytest.mark.parametrize("case", [TC_CASES[0], TC_CASES[1], TC_CASES[7]], ids=["c3like", "c5like", "c5direct"])
 def test_tc_mask_garbage_and_determinism(nef, case):
     ms, shape, ranks, (al, be), pm, law = case
     Y, M, init = _data(ms, shape, ranks, pm, law)
