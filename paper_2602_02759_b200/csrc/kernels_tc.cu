@@ -806,24 +806,33 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
       if (lane == 0) mbar_arrive(s_empty + 8 * s);   // S buffer fully read
       __syncwarp();
       if (lane == 0) mbar_arrive(y_empty + 8 * st);  // Y / mask stage fully read
-#pragma unroll
+      // one code instance for both half-steps (instruction cache): half 1's registers are
+      // handed over to the working set at the end of half 0
+#pragma unroll 1
       for (int h = 0; h < 2; ++h) {
         const int c0 = 32 * g + 16 * h;   // first tile column of this half-step
         uint32_t pb[16];
-        ew_half<KIND>(a, sv[h], yv[h], mk[h], cols_here - c0, row_ok, pb, lsum, cnt);
+        ew_half<KIND>(a, sv[0], yv[0], mk[0], cols_here - c0, row_ok, pb, lsum, cnt);
         if (a.mode != 2) {
           if (h == 0) {
             mbar_wait(p_empty, (t & 1) ^ 1);
             if (warp == 8 && lane == 0) trace_ev(a, t, EV_EW_PEMPTY);
             tc_fence_after();
           }
-          tmem_st16(tPa + lane_off + c0, sv[h]);
+          tmem_st16(tPa + lane_off + c0, sv[0]);
           tmem_st16(tPb + lane_off + c0, pb);
         }
         if (a.debug && blockIdx.x == 0 && blockIdx.y == 0 && t == 0) {
 #pragma unroll
-          for (int j = 0; j < 16; ++j) a.debug[m * 64 + c0 + j] = __uint_as_float(sv[h][j]);
+          for (int j = 0; j < 16; ++j) a.debug[m * 64 + c0 + j] = __uint_as_float(sv[0][j]);
         }
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          sv[0][j] = sv[1][j];
+          yv[0][j] = yv[1][j];
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) mk[0][j] = mk[1][j];
       }
       loss_acc += (double)lsum;
       if (a.mode != 2) {
