@@ -143,12 +143,18 @@ __device__ __forceinline__ float kl_loss(float x, float y) {
 
 // Compile-time specialisations of (a, b, L) for the (alpha, beta) pairs of the configs
 // (paper convention; EW_* in kernels.h).  Ew<EW_GENERIC> defers to the runtime codes.
+// ab2 evaluates two entries at once; the specialisations use the packed fp32x2 multiplies of
+// sm_100 (FMUL2: one issue slot for two products).
 template <int KIND>
 struct Ew {
   static __device__ __forceinline__ void ab(float x, float yh, const DivParams& d, float& av, float& bv) {
     const float2 r = ab_entry_ool(x, yh, d);
     av = r.x;
     bv = r.y;
+  }
+  static __device__ __forceinline__ void ab2(float2 x, float2 yh, const DivParams& d, float2& av, float2& bv) {
+    ab(x.x, yh.x, d, av.x, bv.x);
+    ab(x.y, yh.y, d, av.y, bv.y);
   }
   static __device__ __forceinline__ float loss(float x, float yh, const DivParams& d) { return loss_entry(x, yh, d); }
 };
@@ -159,12 +165,20 @@ struct Ew<EW_KL> {   // (1, 0): a = x / y, b = 1
     av = x * frcp(yh);
     bv = 1.f;
   }
+  static __device__ __forceinline__ void ab2(float2 x, float2 yh, const DivParams&, float2& av, float2& bv) {
+    av = __fmul2_rn(x, make_float2(frcp(yh.x), frcp(yh.y)));
+    bv = make_float2(1.f, 1.f);
+  }
   static __device__ __forceinline__ float loss(float x, float yh, const DivParams&) { return kl_loss(x, yh); }
 };
 
 template <>
 struct Ew<EW_EUC> {  // (1, 1): a = x, b = y
   static __device__ __forceinline__ void ab(float x, float yh, const DivParams&, float& av, float& bv) {
+    av = x;
+    bv = yh;
+  }
+  static __device__ __forceinline__ void ab2(float2 x, float2 yh, const DivParams&, float2& av, float2& bv) {
     av = x;
     bv = yh;
   }
@@ -181,6 +195,11 @@ struct Ew<EW_B_M05> {  // (1, -0.5): a = x y^-3/2, b = y^-1/2; L = 2 (sqrt x - s
     bv = r;
     av = x * r * r * r;
   }
+  static __device__ __forceinline__ void ab2(float2 x, float2 yh, const DivParams&, float2& av, float2& bv) {
+    const float2 r = make_float2(frsqrt(yh.x), frsqrt(yh.y));
+    bv = r;
+    av = __fmul2_rn(__fmul2_rn(x, r), __fmul2_rn(r, r));
+  }
   static __device__ __forceinline__ float loss(float x, float yh, const DivParams&) {
     const float r = frsqrt(yh);
     const float d = fsqrt(x) - yh * r;
@@ -194,6 +213,11 @@ struct Ew<EW_A05_B0> {  // (0.5, 0): a = sqrt(x) / y, b = y^-1/2; L = 4 y^1/2 f(
     const float r = frsqrt(yh);
     bv = r;
     av = fsqrt(x) * r * r;
+  }
+  static __device__ __forceinline__ void ab2(float2 x, float2 yh, const DivParams&, float2& av, float2& bv) {
+    const float2 r = make_float2(frsqrt(yh.x), frsqrt(yh.y));
+    bv = r;
+    av = __fmul2_rn(make_float2(fsqrt(x.x), fsqrt(x.y)), __fmul2_rn(r, r));
   }
   static __device__ __forceinline__ float loss(float x, float yh, const DivParams&) {
     // 4 [sqrt y - sqrt x + sqrt x v], v = log(x/y)/2 (= 4 sqrt(y) f(v)); series near v = 0
@@ -211,6 +235,10 @@ struct Ew<EW_B05> {  // (1, 0.5): a = x y^-1/2, b = y^1/2
     av = x * r;
     bv = yh * r;
   }
+  static __device__ __forceinline__ void ab2(float2 x, float2 yh, const DivParams& d, float2& av, float2& bv) {
+    ab(x.x, yh.x, d, av.x, bv.x);
+    ab(x.y, yh.y, d, av.y, bv.y);
+  }
   static __device__ __forceinline__ float loss(float x, float yh, const DivParams& d) { return loss_entry(x, yh, d); }
 };
 
@@ -220,6 +248,10 @@ struct Ew<EW_B2> {  // (1, 2): a = x y, b = y^2
     av = x * yh;
     bv = yh * yh;
   }
+  static __device__ __forceinline__ void ab2(float2 x, float2 yh, const DivParams& d, float2& av, float2& bv) {
+    ab(x.x, yh.x, d, av.x, bv.x);
+    ab(x.y, yh.y, d, av.y, bv.y);
+  }
   static __device__ __forceinline__ float loss(float x, float yh, const DivParams& d) { return loss_entry(x, yh, d); }
 };
 
@@ -228,6 +260,10 @@ struct Ew<EW_A05_B1> {  // (0.5, 1): a = sqrt(x), b = sqrt(y)
   static __device__ __forceinline__ void ab(float x, float yh, const DivParams&, float& av, float& bv) {
     av = fsqrt(x);
     bv = fsqrt(yh);
+  }
+  static __device__ __forceinline__ void ab2(float2 x, float2 yh, const DivParams& d, float2& av, float2& bv) {
+    ab(x.x, yh.x, d, av.x, bv.x);
+    ab(x.y, yh.y, d, av.y, bv.y);
   }
   static __device__ __forceinline__ float loss(float x, float yh, const DivParams& d) { return loss_entry(x, yh, d); }
 };

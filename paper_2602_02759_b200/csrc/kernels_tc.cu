@@ -9,8 +9,9 @@
 //
 // CTA = 128 rows (TMEM lanes) x a contiguous range of 64-column tiles.  512 threads:
 //   warp 0      TMA producer (Y / mask ring of NS stages)
-//   warp 1      TMEM allocator + single-thread MMA issuer
-//   warps 2-3   idle
+//   warp 1      TMEM allocator + single-thread MMA issuer (reconstruction and N/D MMAs)
+//   warp 2      idle
+//   warp 3      direct-V row loads (TMA) when the tile's V rows are rows of one table
 //   warps 4-7   column operand: V tile = prod of column tables (Khatri-Rao), 16 columns per
 //               warp; rows constant across the tile are loaded once and broadcast; the next
 //               tile's table rows are in flight while the current tile is stored; TF32
@@ -18,7 +19,7 @@
 //               columns, K = bond) for the reconstruction MMA and V^T (rows = bond, K = tile
 //               columns) for the numerator / denominator MMAs
 //   warps 8-15  elementwise: tcgen05.ld S -> a, b (+ loss) -> tcgen05.st P; epilogue N, D
-// TMEM (512 columns): S[2] (2x64) | P_a, P_b (2x64) | N, D (2xKB) | U_hi, U_lo (2xKB)
+// TMEM (512 columns): tile buffer[2] (S -> P_a in place | P_b, 2 x 128) | N, D (2xKB) | U_hi, U_lo (2xKB)
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
@@ -102,6 +103,22 @@ __device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a, uint64_t bdesc, u
       "setp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}" ::"r"(d),
       "r"(a), "l"(bdesc), "r"(idesc), "r"(acc)
+      : "memory");
+}
+// the same, issued by one elected lane of a converged warp (warp-uniform operands)
+__device__ __forceinline__ void mma_ts_elect(uint32_t d, uint32_t a, uint64_t bdesc, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n}" ::"r"(d),
+      "r"(a), "l"(bdesc), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit_elect(uint32_t bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n}" ::"r"(bar)
       : "memory");
 }
 __device__ __forceinline__ void mma_commit(uint32_t bar) {
@@ -413,24 +430,29 @@ __device__ __forceinline__ void vtile_store(const TcArgs& a, int xw, int lane, c
 }
 
 // ------------------------------------------------------------------ elementwise stage
-// Row m's 16 Y values and mask bytes of half-step h of column half g (missing values are
-// loaded but never used: they only feed discarded lanes of the arithmetic).
+// Row m's 16 Y values of half-step h of column half g (tile columns [32g + 16h, +16)) and
+// their mask bytes, four per word (missing values are loaded but only ever feed discarded
+// lanes).  h is a runtime value: one code instance serves both half-steps (I-cache).
 __device__ __forceinline__ void ew_load_y(const TcArgs& a, const unsigned char* ys, const unsigned char* ms, int g,
                                           int h, int m, float (&yv)[16], uint32_t (&mk)[4]) {
   const int c0 = 32 * g + 16 * h;
   if (a.layout == 0) {
+    // [64 columns][128 rows] fp32 / uint8, rows contiguous: lane = row, conflict-free
+    const float* yf = reinterpret_cast<const float*>(ys) + c0 * BM + m;
 #pragma unroll
-    for (int j = 0; j < 16; ++j) yv[j] = reinterpret_cast<const float*>(ys)[(c0 + j) * BM + m];
+    for (int j = 0; j < 16; ++j) yv[j] = yf[j * BM];
     if (a.has_mask) {
+      const unsigned char* mb = ms + c0 * BM + m;
 #pragma unroll
       for (int j4 = 0; j4 < 4; ++j4) {
         uint32_t w = 0;
 #pragma unroll
-        for (int e = 0; e < 4; ++e) w |= (uint32_t)ms[(c0 + 4 * j4 + e) * BM + m] << (8 * e);
+        for (int e = 0; e < 4; ++e) w |= (uint32_t)mb[(4 * j4 + e) * BM] << (8 * e);
         mk[j4] = w;
       }
     }
   } else {
+    // SW128 boxes of [128 rows][32 columns] fp32 (one per column half); SW64 [128][64] uint8
     const unsigned char* sub = ys + g * (Y_STAGE / 2) + m * 128;
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
@@ -445,14 +467,14 @@ __device__ __forceinline__ void ew_load_y(const TcArgs& a, const unsigned char* 
   }
 }
 
-// a, b (and the loss) of 16 entries: sv (S on entry) becomes P_a, pb receives P_b, both
-// TF32-rounded and zero at missing / out-of-range entries.  cv = valid columns from c0.
+// a, b (and, in loss mode, the loss) of 16 entries: sv holds S on entry and P_a on exit, pb
+// receives P_b; both TF32-rounded (RN) and zero at missing or out-of-range entries (R5: an
+// AND with an all-ones / all-zeros word, never a multiply).  cv = valid tile columns from the
+// half-step's first column.
 template <int KIND>
 __device__ __forceinline__ void ew_half(const TcArgs& a, uint32_t (&sv)[16], const float (&yv)[16],
                                         const uint32_t (&mk)[4], int cv, bool row_ok, uint32_t (&pb)[16],
                                         float& lsum, long long& cnt) {
-  // observed-entry byte masks (0xff per observed entry): mask byte nonzero (R6) and row /
-  // column in range; AND-ed into the results (R5: a select, never a multiply)
   uint32_t nz[4];
 #pragma unroll
   for (int j4 = 0; j4 < 4; ++j4) nz[j4] = a.has_mask ? __vcmpne4(mk[j4], 0u) : 0xffffffffu;
@@ -475,13 +497,16 @@ __device__ __forceinline__ void ew_half(const TcArgs& a, uint32_t (&sv)[16], con
     for (int j4 = 0; j4 < 4; ++j4) cnt += __popc(nz[j4]) >> 3;
   }
 #pragma unroll
-  for (int j = 0; j < 16; ++j) {
-    const float yh = fmaxf(__uint_as_float(sv[j]), 1e-30f);
-    float av, bv;
-    Ew<KIND>::ab(yv[j], yh, a.dv, av, bv);
-    const uint32_t mw = __byte_perm(nz[j >> 2], 0u, (j & 3) * 0x1111u);   // replicate byte
-    sv[j] = tf32_bits(av) & mw;
-    pb[j] = tf32_bits(bv) & mw;
+  for (int j = 0; j < 16; j += 2) {
+    const float2 yh = make_float2(fmaxf(__uint_as_float(sv[j]), 1e-30f), fmaxf(__uint_as_float(sv[j + 1]), 1e-30f));
+    float2 av, bv;
+    Ew<KIND>::ab2(make_float2(yv[j], yv[j + 1]), yh, a.dv, av, bv);
+    const uint32_t m0 = __byte_perm(nz[j >> 2], 0u, (j & 3) * 0x1111u);   // replicate byte
+    const uint32_t m1 = __byte_perm(nz[j >> 2], 0u, ((j + 1) & 3) * 0x1111u);
+    sv[j] = tf32_bits(av.x) & m0;
+    sv[j + 1] = tf32_bits(av.y) & m1;
+    pb[j] = tf32_bits(bv.x) & m0;
+    pb[j + 1] = tf32_bits(bv.y) & m1;
   }
 }
 
@@ -492,9 +517,40 @@ __device__ __forceinline__ int64_t tile_col0(const TcArgs& a, int64_t tile) {
   return to * a.CI + ti * BN;
 }
 
+// Direct V: consecutive tiles of a chunk advance the linear column index by 64
+// inside the innermost column mode (its extent is a multiple of 64), so the variable table's
+// row advances by 64 and the tile-constant rows change only when that mode wraps.  The two
+// functions below recompute from scratch at a wrap (cold, out of line).
+__device__ __noinline__ int direct_var_row(const TcArgs& a, int64_t col) {
+  int off = 0;
+  for (int d = a.nc - 1; d >= 0; --d) {
+    const int64_t dig = d > 0 ? col % a.cdim[d] : col;
+    col = d > 0 ? col / a.cdim[d] : 0;
+    off += (int)dig * (int)a.tcs[a.var_tab][d];
+  }
+  return off / a.K;
+}
+// product of the tile-constant table rows, bond chunk c (4 values) of this lane
+__device__ __noinline__ float4 direct_cst(const TcArgs& a, int64_t col, int c) {
+  int off[kMaxTabs] = {0, 0, 0, 0};
+  for (int d = a.nc - 1; d >= 0; --d) {
+    const int64_t dig = d > 0 ? col % a.cdim[d] : col;
+    col = d > 0 ? col / a.cdim[d] : 0;
+    for (int q = 0; q < a.ntab; ++q) off[q] += (int)dig * (int)a.tcs[q][d];
+  }
+  float4 p = make_float4(1.f, 1.f, 1.f, 1.f);
+  if (c * 4 >= a.K) return make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int q = 0; q < a.ntab; ++q) {
+    if (q == a.var_tab) continue;
+    const float4 r = __ldg(reinterpret_cast<const float4*>(a.tab[q] + off[q]) + c);
+    p.x *= r.x; p.y *= r.y; p.z *= r.z; p.w *= r.w;
+  }
+  return p;
+}
+
 // pipeline timeline (diagnostics): event e of tile t in CTA (0,0)
 enum TraceEv : int {
-  EV_TMA_ISSUE = 0, EV_VG_START, EV_VG_DONE, EV_MMA1_ISSUE, EV_MMA23_ISSUE, EV_EW_S, EV_EW_Y, EV_EW_PEMPTY,
+  EV_TMA_ISSUE = 0, EV_VG_START, EV_VG_DONE, EV_MMA1_ISSUE, EV_MMA23_ISSUE, EV_EW_S, EV_EW_Y, EV_EW_HALF,
   EV_EW_DONE, EV_VG_ISSUED
 };
 __device__ __forceinline__ void trace_ev(const TcArgs& a, int t, int e) {
@@ -502,6 +558,13 @@ __device__ __forceinline__ void trace_ev(const TcArgs& a, int t, int e) {
 }
 
 // ------------------------------------------------------------------ the kernel
+// TMEM (512 columns x 128 lanes): two tile buffers of 128 columns, each holding S in its first
+// 64 columns; the elementwise warps overwrite S in place with P_a and put P_b in the other 64
+// (so a tile needs no second buffer and the elementwise stage never waits for the numerator
+// MMAs of the previous tile); then N, D (KB each) and U_hi, U_lo (KB each).
+//
+// Tile t uses buffer t & 1.  Single MMA issuer, in order:
+//   S(0), S(1), then for each t: [P(t) ready] N,D += P(t) V(t); [buffer t&1 retired] S(t+2)
 template <int KB, int KIND>
 __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_constant__ Params P) {
   extern __shared__ unsigned char smraw[];
@@ -518,10 +581,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
   const uint32_t sM = sY + NS * Y_STAGE;                     // NS x 8 KB
   const uint32_t sV = sM + NS * M_STAGE;                     // NV x (V | V^T)
   const uint32_t sBar = sV + NV * V_STAGE_MAX;
-  const uint32_t y_full = sBar, y_empty = sBar + 8 * NS, v_full = sBar + 16 * NS, v_empty = v_full + 8 * NV;
-  const uint32_t s_full = v_empty + 8 * NV, s_empty = s_full + 16, p_full = s_empty + 16, p_empty = p_full + 8;
-  const uint32_t nd_full = p_empty + 8, u_ready = nd_full + 8;
-  const uint32_t vraw_full = u_ready + 8;   // NV barriers: direct-V rows landed (TMA)
+  const uint32_t y_full = sBar, y_empty = y_full + 8 * NS;
+  const uint32_t v_full = y_empty + 8 * NS, v_empty = v_full + 8 * NV;
+  const uint32_t s_full = v_empty + 8 * NV;                  // [2] S(t) in buffer t & 1 (MMA commit)
+  const uint32_t p_full = s_full + 16;                       // [2] P(t) written (8 elementwise warps)
+  const uint32_t buf_free = p_full + 16;                     // [2] N,D MMAs of tile t retired (commit)
+  const uint32_t nd_full = buf_free + 16, u_ready = nd_full + 8;
+  const uint32_t vraw_full = u_ready + 8;                    // NV barriers: direct-V rows landed (TMA)
   const uint32_t sTmem = vraw_full + 8 * NV;
   unsigned char* gY = gbase;
   unsigned char* gM = gbase + NS * Y_STAGE;
@@ -541,9 +607,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
   if (tid == 0) {
     for (int i = 0; i < NS; ++i) { mbar_init(y_full + 8 * i, 1); mbar_init(y_empty + 8 * i, 8); }
     for (int i = 0; i < NV; ++i) { mbar_init(v_full + 8 * i, NVG); mbar_init(v_empty + 8 * i, 1); }
-    for (int i = 0; i < 2; ++i) { mbar_init(s_full + 8 * i, 1); mbar_init(s_empty + 8 * i, 8); }
-    mbar_init(p_full, 8);
-    mbar_init(p_empty, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(s_full + 8 * i, 1);
+      mbar_init(p_full + 8 * i, 8);
+      mbar_init(buf_free + 8 * i, 1);
+    }
     mbar_init(nd_full, 1);
     mbar_init(u_ready, 8);
     for (int i = 0; i < NV; ++i) mbar_init(vraw_full + 8 * i, 1);
@@ -559,7 +627,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *gTmem;
-  const uint32_t tS = tmem, tPa = tmem + 128, tPb = tmem + 192, tNa = tmem + 256, tNb = tmem + 256 + KB;
+  const uint32_t tNa = tmem + 256, tNb = tmem + 256 + KB;
   const uint32_t tUh = tmem + 256 + 2 * KB, tUl = tmem + 256 + 3 * KB;
 
   if (warp == 0) {
@@ -592,72 +660,78 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
       }
     }
   } else if (warp == 1) {
-    // ------------------------------------------------------------ MMA issuer (one thread)
-    if (lane == 0 && T > 0) {
+    // ------------------------------------------------------------ MMA issuer
+    // The whole warp runs the issue loop (warp-uniform control flow, so descriptors and TMEM
+    // addresses stay in uniform registers and every tcgen05.mma is one elected issue; a
+    // lane-0-only loop measured ~3x slower issue, starving the N = 64 MMAs).
+    if (T > 0) {
       constexpr uint32_t id1 = idesc_tf32(128, BN);   // S = U V^T   : N = 64 tile columns
       constexpr uint32_t id2 = idesc_tf32(128, KB);   // N = P V     : N = bond
+      const bool war_wait = !(a.dbg & 8);
       mbar_wait(u_ready, 0);
       tc_fence_after();
-      // reconstruction MMAs only; the numerator / denominator MMAs have their own issuer
-      // (warp 2) so that neither waits behind the other's dependencies
-      for (int t = 0; t < T; ++t) {
-        const int vs = t % NV, s = t & 1;
+      // S(t) = U_hi V(t)^T + U_lo V(t)^T into buffer t & 1 (split reconstruction)
+      auto mma_s = [&](int t) {
+        const int vs = t % NV, b = t & 1;
         mbar_wait(v_full + 8 * vs, (t / NV) & 1);
-        mbar_wait(s_empty + 8 * s, ((t >> 1) & 1) ^ 1);
+        if (t >= 2 && war_wait) mbar_wait(buf_free + 8 * b, ((t >> 1) - 1) & 1);
         tc_fence_after();
-        trace_ev(a, t, EV_MMA1_ISSUE);
-        const uint32_t vb = sV + vs * V_STAGE_MAX;
-        const uint32_t d = tS + 64 * s;
+        if (lane == 0) trace_ev(a, t, EV_MMA1_ISSUE);
+        __syncwarp();
+        const uint64_t vd = sdesc(sV + vs * V_STAGE_MAX, 16, 1024);
+        const uint32_t d = tmem + 128 * b;
 #pragma unroll
-        for (int kk = 0; kk < KB / 8; ++kk) {
-          const uint64_t bd = sdesc(vb + (kk >> 2) * (BN * 128) + (kk & 3) * 32, 16, 1024);
-          mma_ts(d, tUh + kk * 8, bd, id1, kk > 0 ? 1u : 0u);
-        }
+        for (int kk = 0; kk < KB / 8; ++kk)
+          mma_ts_elect(d, tUh + kk * 8, vd + (uint64_t)(((kk >> 2) * (BN * 128) + (kk & 3) * 32) >> 4), id1, kk > 0 ? 1u : 0u);
 #pragma unroll
-        for (int kk = 0; kk < KB / 8; ++kk) {
-          const uint64_t bd = sdesc(vb + (kk >> 2) * (BN * 128) + (kk & 3) * 32, 16, 1024);
-          mma_ts(d, tUl + kk * 8, bd, id1, 1u);
-        }
-        mma_commit(s_full + 8 * s);
-        if (a.mode == 2) mma_commit(v_empty + 8 * vs);   // else released by the numerator issuer
-      }
-    }
-  } else if (warp == 2) {
-    // ------------------------------------------------------------ numerator / denominator MMAs
-    if (lane == 0 && T > 0 && a.mode != 2) {
-      constexpr uint32_t id2 = idesc_tf32(128, KB);   // N = P V : N = bond
+        for (int kk = 0; kk < KB / 8; ++kk)
+          mma_ts_elect(d, tUl + kk * 8, vd + (uint64_t)(((kk >> 2) * (BN * 128) + (kk & 3) * 32) >> 4), id1, 1u);
+        mma_commit_elect(s_full + 8 * b);
+      };
+      mma_s(0);
+      if (T > 1) mma_s(1);
       for (int u = 0; u < T; ++u) {
-        const int vs = u % NV;
-        mbar_wait(p_full, u & 1);
+        const int vs = u % NV, b = u & 1;
+        mbar_wait(p_full + 8 * b, (u >> 1) & 1);
         tc_fence_after();
-        trace_ev(a, u, EV_MMA23_ISSUE);
-        // B = V^T, K-major SW128: rows = bond (N), K = tile columns (2 atoms of 32)
-        const uint32_t vtb = sV + vs * V_STAGE_MAX + VT_OFF;
+        if (lane == 0) trace_ev(a, u, EV_MMA23_ISSUE);
+        __syncwarp();
+        if (a.mode != 2) {
+          // B = V^T, K-major SW128: rows = bond (N), K = tile columns (2 atoms of 32)
+          const uint64_t vtd = sdesc(sV + vs * V_STAGE_MAX + VT_OFF, 16, 1024);
+          const uint32_t pa = tmem + 128 * b, pbb = pa + 64;
 #pragma unroll
-        for (int kk = 0; kk < BN / 8; ++kk) {
-          const uint64_t bd = sdesc(vtb + (kk >> 2) * (KB * 128) + (kk & 3) * 32, 16, 1024);
-          const uint32_t acc = (u > 0 || kk > 0) ? 1u : 0u;
-          mma_ts(tNa, tPa + kk * 8, bd, id2, acc);
-          mma_ts(tNb, tPb + kk * 8, bd, id2, acc);
+          for (int kk = 0; kk < BN / 8; ++kk) {
+            const uint64_t bd = vtd + (uint64_t)(((kk >> 2) * (KB * 128) + (kk & 3) * 32) >> 4);
+            const uint32_t acc = (u > 0 || kk > 0) ? 1u : 0u;
+            mma_ts_elect(tNa, pa + kk * 8, bd, id2, acc);
+            mma_ts_elect(tNb, pbb + kk * 8, bd, id2, acc);
+          }
         }
-        mma_commit(p_empty);
-        mma_commit(v_empty + 8 * vs);
+        mma_commit_elect(v_empty + 8 * vs);
+        mma_commit_elect(buf_free + 8 * b);
+        if (u + 2 < T) mma_s(u + 2);
       }
-      mma_commit(nd_full);
+      mma_commit_elect(nd_full);
     }
   } else if (warp == 3) {
     // ------------------------------------------------------------ direct-V row loads (TMA)
-    if (lane == 0 && a.vdirect) {
-      Odo o;
+    if (lane == 0 && a.vdirect && T > 0) {
+      const int e_in = (int)a.cdim[a.nc - 1];
+      int64_t col = tile_col0(a, t_begin);
+      int inner = (int)(col % e_in);
+      int rowv = direct_var_row(a, col);
       for (int t = 0; t < T; ++t) {
+        if (t > 0) {
+          inner += BN;
+          rowv += BN;
+          if (inner >= e_in) {
+            inner = 0;
+            rowv = direct_var_row(a, tile_col0(a, t_begin + t));
+          }
+        }
         const int vs = t % NV;
         mbar_wait(v_empty + 8 * vs, ((t / NV) & 1) ^ 1);
-        odo_seek(a, o, tile_col0(a, t_begin + t));
-        int off = 0;
-#pragma unroll
-        for (int d = 0; d < kMaxModes; ++d)
-          if (d < a.nc) off += o.dig[d] * (int)a.tcs[a.var_tab][d];
-        const int rowv = off / a.K;
         const uint32_t bar = vraw_full + 8 * vs;
         mbar_expect_tx(bar, (uint32_t)(KB * BN * 4));
 #pragma unroll
@@ -666,37 +740,29 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
     }
   } else if (warp >= 4 && warp < 4 + NVG && a.vdirect) {
     // ------------------------------------------------------------ direct V: scale rows in place
-    // V[x][k] = T_var[row0 + x][k] * prod_{q != var} T_q[const row][k]; V^T written alongside.
+    // V[x][k] = T_var[row + x][k] * prod_{q != var} T_q[const row][k]; V^T written alongside.
     const int xw = (warp - 4) * 16;
     constexpr int C = KB / 4, NB = (4 * C) / 32;
     const int c = lane % C;
     const bool kok = c * 4 < a.K;
     VOff<KB> vo;
     vo.init(xw, lane);
-    Odo o;
-    float4 cn[kMaxTabs];
-    auto fetch_const = [&](int t, float4 (&cr)[kMaxTabs]) {
-      odo_seek(a, o, tile_col0(a, t_begin + t));
-#pragma unroll
-      for (int q = 0; q < kMaxTabs; ++q) {
-        cr[q] = make_float4(1.f, 1.f, 1.f, 1.f);
-        if (q < a.ntab && q != a.var_tab) {
-          int off = 0;
-#pragma unroll
-          for (int d = 0; d < kMaxModes; ++d)
-            if (d < a.nc) off += o.dig[d] * (int)a.tcs[q][d];
-          cr[q] = kok ? __ldg(reinterpret_cast<const float4*>(a.tab[q] + off) + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+    const int e_in = (int)a.cdim[a.nc - 1];
+    int inner = 0;
+    float4 cst = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (T > 0) {
+      const int64_t col = tile_col0(a, t_begin);
+      inner = (int)(col % e_in);
+      cst = direct_cst(a, col, c);
+    }
+    for (int t = 0; t < T; ++t) {
+      if (t > 0) {
+        inner += BN;
+        if (inner >= e_in) {
+          inner = 0;
+          cst = direct_cst(a, tile_col0(a, t_begin + t), c);
         }
       }
-    };
-    if (T > 0) fetch_const(0, cn);
-    for (int t = 0; t < T; ++t) {
-      float4 cst = make_float4(1.f, 1.f, 1.f, 1.f);
-#pragma unroll
-      for (int q = 0; q < kMaxTabs; ++q) {
-        cst.x *= cn[q].x; cst.y *= cn[q].y; cst.z *= cn[q].z; cst.w *= cn[q].w;
-      }
-      if (t + 1 < T) fetch_const(t + 1, cn);   // next tile's constant rows in flight
       const int vs = t % NV;
       mbar_wait(vraw_full + 8 * vs, (t / NV) & 1);
       if (warp == 4 && lane == 0) trace_ev(a, t, EV_VG_START);
@@ -707,7 +773,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
           const float4 f = *reinterpret_cast<const float4*>(vrow + vo.vb[i] + r * 128 + ((vo.cx[i] ^ r) << 4));
-          p[r] = make_float4(f.x * cst.x, f.y * cst.y, f.z * cst.z, f.w * cst.w);
+          const float2 lo = __fmul2_rn(make_float2(f.x, f.y), make_float2(cst.x, cst.y));
+          const float2 hi = __fmul2_rn(make_float2(f.z, f.w), make_float2(cst.z, cst.w));
+          p[r] = make_float4(lo.x, lo.y, hi.x, hi.y);
         }
         vblock_store<KB>(vrow, vo.vb[i], vo.cx[i], vo.vtb[i], vo.xc[i], kok ? 0xfu : 0u, p);
       }
@@ -770,78 +838,55 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
     }
     double loss_acc = 0.0;
     long long cnt = 0;
-    for (int t = 0; t < T; ++t) {
-      const int s = t & 1;
-      const int64_t tile = t_begin + t;
-      int cols_here;
-      if (a.layout == 0) {
-        const int64_t c = a.CO - tile * BN;
-        cols_here = (int)(c < BN ? c : BN);
-      } else {
-        const int64_t ti = tile % a.tiles_inner;
-        const int64_t c = a.CI - ti * BN;
-        cols_here = (int)(c < BN ? c : BN);
-      }
+    // valid columns of a tile: the tile's offset inside its column block, advanced per tile
+    // (no 64-bit division in the loop)
+    const int64_t cext = a.layout == 0 ? a.CO : a.CI;
+    const int tiles_blk = (int)(a.layout == 0 ? a.tiles : a.tiles_inner);
+    int tin = (int)(a.layout == 0 ? t_begin : t_begin % a.tiles_inner);
+    for (int t = 0; t < T; ++t, ++tin) {
+      const int b = t & 1;
+      if (tin >= tiles_blk) tin = 0;
+      const int64_t crem = cext - (int64_t)tin * BN;
+      const int cols_here = (int)(crem < BN ? crem : BN);
       const int st = t % NS;
-      mbar_wait(s_full + 8 * s, (t >> 1) & 1);
+      const uint32_t tb = tmem + 128 * b + lane_off + 32 * g;   // S / P_a columns of this thread
+      mbar_wait(s_full + 8 * b, (t >> 1) & 1);
       if (warp == 8 && lane == 0) trace_ev(a, t, EV_EW_S);
       tc_fence_after();
+      float lsum = 0.f;
       mbar_wait(y_full + 8 * st, (t / NS) & 1);
       if (warp == 8 && lane == 0) trace_ev(a, t, EV_EW_Y);
-      const unsigned char* ys = gY + st * Y_STAGE;
-      const unsigned char* ms = gM + st * M_STAGE;
-      float lsum = 0.f;
-      // issue both halves' TMEM loads and smem loads before any arithmetic (latency overlap)
-      uint32_t sv[2][16];
-      float yv[2][16];
-      uint32_t mk[2][4];
-      tmem_ld16(tS + 64 * s + lane_off + 32 * g, sv[0]);
-      tmem_ld16(tS + 64 * s + lane_off + 32 * g + 16, sv[1]);
-#pragma unroll
-      for (int h = 0; h < 2; ++h) ew_load_y(a, ys, ms, g, h, m, yv[h], mk[h]);
-      tmem_ld_wait(sv[0]);
-      tmem_ld_wait(sv[1]);
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(s_empty + 8 * s);   // S buffer fully read
-      __syncwarp();
-      if (lane == 0) mbar_arrive(y_empty + 8 * st);  // Y / mask stage fully read
-      // one code instance for both half-steps (instruction cache): half 1's registers are
-      // handed over to the working set at the end of half 0
+      // two half-steps of 16 columns through ONE code instance (I-cache)
 #pragma unroll 1
       for (int h = 0; h < 2; ++h) {
-        const int c0 = 32 * g + 16 * h;   // first tile column of this half-step
-        uint32_t pb[16];
-        ew_half<KIND>(a, sv[0], yv[0], mk[0], cols_here - c0, row_ok, pb, lsum, cnt);
+        const uint32_t tc = tb + 16 * h;
+        uint32_t sv[16], pb[16];
+        float yv[16];
+        uint32_t mk[4];
+        tmem_ld16(tc, sv);
+        ew_load_y(a, gY + st * Y_STAGE, gM + st * M_STAGE, g, h, m, yv, mk);
+        tmem_ld_wait(sv);
+        if (h == 1) {
+          __syncwarp();
+          if (lane == 0) mbar_arrive(y_empty + 8 * st);  // Y / mask stage fully read
+        }
+        ew_half<KIND>(a, sv, yv, mk, cols_here - 32 * g - 16 * h, row_ok, pb, lsum, cnt);
         if (a.mode != 2) {
-          if (h == 0) {
-            mbar_wait(p_empty, (t & 1) ^ 1);
-            if (warp == 8 && lane == 0) trace_ev(a, t, EV_EW_PEMPTY);
-            tc_fence_after();
-          }
-          tmem_st16(tPa + lane_off + c0, sv[0]);
-          tmem_st16(tPb + lane_off + c0, pb);
+          tmem_st16(tc, sv);
+          tmem_st16(tc + 64, pb);
         }
         if (a.debug && blockIdx.x == 0 && blockIdx.y == 0 && t == 0) {
 #pragma unroll
-          for (int j = 0; j < 16; ++j) a.debug[m * 64 + c0 + j] = __uint_as_float(sv[0][j]);
+          for (int j = 0; j < 16; ++j) a.debug[m * 64 + 32 * g + 16 * h + j] = __uint_as_float(sv[j]);
         }
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          sv[0][j] = sv[1][j];
-          yv[0][j] = yv[1][j];
-        }
-#pragma unroll
-        for (int j = 0; j < 4; ++j) mk[0][j] = mk[1][j];
       }
+      if (warp == 8 && lane == 0) trace_ev(a, t, EV_EW_HALF);
+      if (a.mode != 2) tmem_st_wait();
       loss_acc += (double)lsum;
-      if (a.mode != 2) {
-        tmem_st_wait();
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(p_full);
-        if (warp == 8 && lane == 0) trace_ev(a, t, EV_EW_DONE);
-      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(p_full + 8 * b);      // P(t) in TMEM (or, loss only: S(t) consumed)
+      if (warp == 8 && lane == 0) trace_ev(a, t, EV_EW_DONE);
     }
     // epilogue: N (g = 0) / D (g = 1) for this lane -> split partials
     if (a.mode != 2) {
@@ -864,6 +909,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
       } else if (row_ok) {
         for (int k = 0; k < a.K; ++k) out[row * a.K + k] = 0.f;
       }
+    } else if (T > 0) {
+      mbar_wait(nd_full, 0);
     }
     if (a.mode != 0) {
       gRed[ew] = loss_acc;
