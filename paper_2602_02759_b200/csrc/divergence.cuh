@@ -157,6 +157,11 @@ struct Ew {
     ab(x.y, yh.y, d, av.y, bv.y);
   }
   static __device__ __forceinline__ float loss(float x, float yh, const DivParams& d) { return loss_entry(x, yh, d); }
+  static __device__ __forceinline__ void abl2(float2 x, float2 yh, const DivParams& d, float2& av, float2& bv,
+                                              float2& l) {
+    ab2(x, yh, d, av, bv);
+    l = make_float2(loss(x.x, yh.x, d), loss(x.y, yh.y, d));
+  }
 };
 
 template <>
@@ -170,6 +175,11 @@ struct Ew<EW_KL> {   // (1, 0): a = x / y, b = 1
     bv = make_float2(1.f, 1.f);
   }
   static __device__ __forceinline__ float loss(float x, float yh, const DivParams&) { return kl_loss(x, yh); }
+  static __device__ __forceinline__ void abl2(float2 x, float2 yh, const DivParams& d, float2& av, float2& bv,
+                                              float2& l) {
+    ab2(x, yh, d, av, bv);
+    l = make_float2(loss(x.x, yh.x, d), loss(x.y, yh.y, d));
+  }
 };
 
 template <>
@@ -185,6 +195,11 @@ struct Ew<EW_EUC> {  // (1, 1): a = x, b = y
   static __device__ __forceinline__ float loss(float x, float yh, const DivParams&) {
     const float r = x - yh;
     return 0.5f * r * r;
+  }
+  static __device__ __forceinline__ void abl2(float2 x, float2 yh, const DivParams& d, float2& av, float2& bv,
+                                              float2& l) {
+    ab2(x, yh, d, av, bv);
+    l = make_float2(loss(x.x, yh.x, d), loss(x.y, yh.y, d));
   }
 };
 
@@ -204,6 +219,16 @@ struct Ew<EW_B_M05> {  // (1, -0.5): a = x y^-3/2, b = y^-1/2; L = 2 (sqrt x - s
     const float r = frsqrt(yh);
     const float d = fsqrt(x) - yh * r;
     return 2.f * d * d * r;
+  }
+  static __device__ __forceinline__ void abl2(float2 x, float2 yh, const DivParams&, float2& av, float2& bv,
+                                              float2& l) {
+    // shares rsqrt(yhat) between a, b and the loss 2 (sqrt x - sqrt y)^2 / sqrt y
+    const float2 r = make_float2(frsqrt(yh.x), frsqrt(yh.y));
+    bv = r;
+    av = __fmul2_rn(__fmul2_rn(x, r), __fmul2_rn(r, r));
+    const float2 dd = __ffma2_rn(make_float2(-yh.x, -yh.y), r, make_float2(fsqrt(x.x), fsqrt(x.y)));
+    const float2 d2 = __fmul2_rn(dd, dd);
+    l = __fmul2_rn(__fmul2_rn(d2, r), make_float2(2.f, 2.f));
   }
 };
 
@@ -226,6 +251,11 @@ struct Ew<EW_A05_B0> {  // (0.5, 0): a = sqrt(x) / y, b = y^-1/2; L = 4 y^1/2 f(
     const float l = fabsf(v) < 0.3f ? 4.f * sy * fser(v) : 4.f * (sy - sx + sx * v);
     return x > 0.f ? l : 4.f * sy;
   }
+  static __device__ __forceinline__ void abl2(float2 x, float2 yh, const DivParams& d, float2& av, float2& bv,
+                                              float2& l) {
+    ab2(x, yh, d, av, bv);
+    l = make_float2(loss(x.x, yh.x, d), loss(x.y, yh.y, d));
+  }
 };
 
 template <>
@@ -240,6 +270,11 @@ struct Ew<EW_B05> {  // (1, 0.5): a = x y^-1/2, b = y^1/2
     ab(x.y, yh.y, d, av.y, bv.y);
   }
   static __device__ __forceinline__ float loss(float x, float yh, const DivParams& d) { return loss_entry(x, yh, d); }
+  static __device__ __forceinline__ void abl2(float2 x, float2 yh, const DivParams& d, float2& av, float2& bv,
+                                              float2& l) {
+    ab2(x, yh, d, av, bv);
+    l = make_float2(loss(x.x, yh.x, d), loss(x.y, yh.y, d));
+  }
 };
 
 template <>
@@ -253,6 +288,11 @@ struct Ew<EW_B2> {  // (1, 2): a = x y, b = y^2
     ab(x.y, yh.y, d, av.y, bv.y);
   }
   static __device__ __forceinline__ float loss(float x, float yh, const DivParams& d) { return loss_entry(x, yh, d); }
+  static __device__ __forceinline__ void abl2(float2 x, float2 yh, const DivParams& d, float2& av, float2& bv,
+                                              float2& l) {
+    ab2(x, yh, d, av, bv);
+    l = make_float2(loss(x.x, yh.x, d), loss(x.y, yh.y, d));
+  }
 };
 
 template <>
@@ -266,6 +306,11 @@ struct Ew<EW_A05_B1> {  // (0.5, 1): a = sqrt(x), b = sqrt(y)
     ab(x.y, yh.y, d, av.y, bv.y);
   }
   static __device__ __forceinline__ float loss(float x, float yh, const DivParams& d) { return loss_entry(x, yh, d); }
+  static __device__ __forceinline__ void abl2(float2 x, float2 yh, const DivParams& d, float2& av, float2& bv,
+                                              float2& l) {
+    ab2(x, yh, d, av, bv);
+    l = make_float2(loss(x.x, yh.x, d), loss(x.y, yh.y, d));
+  }
 };
 
 // dispatch helper: calls f.template operator()<KIND>() for the pair's kind

@@ -80,6 +80,39 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
     if (it > (1u << 22)) __trap();
   }
 }
+// Spin variant for waits on the critical path (no suspend hint: a suspended waiter was seen to
+// wake ~1000 cycles after the phase completed).  Still bounded.
+__device__ __forceinline__ void mbar_spin(uint32_t bar, uint32_t parity) {
+  uint32_t done = 0;
+  for (uint32_t it = 0;; ++it) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    if (done) return;
+    if (it > (1u << 26)) __trap();
+  }
+}
+// Producer-side wait (the producer runs ahead of its consumer): poll with a short sleep
+// between tries so the waiting warp leaves the issue slots to the elementwise warps.
+__device__ __forceinline__ void mbar_wait_relaxed(uint32_t bar, uint32_t parity) {
+  uint32_t done = 0;
+  for (uint32_t it = 0;; ++it) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(done)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    if (done) return;
+    __nanosleep(64);
+    if (it > (1u << 26)) __trap();
+  }
+}
 __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* tm, int c0, int c1, uint32_t bar) {
   asm volatile(
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
@@ -468,45 +501,56 @@ __device__ __forceinline__ void ew_load_y(const TcArgs& a, const unsigned char* 
 }
 
 // a, b (and, in loss mode, the loss) of 16 entries: sv holds S on entry and P_a on exit, pb
-// receives P_b; both TF32-rounded (RN) and zero at missing or out-of-range entries (R5: an
-// AND with an all-ones / all-zeros word, never a multiply).  cv = valid tile columns from the
-// half-step's first column.
+// receives P_b; zero at missing or out-of-range entries (R5: a select on the observed flag,
+// never a multiply).  cv = valid tile columns from the half-step's first column.
+// TF32 operands: the tensor core reads only the top 19 bits of each 32-bit container, so
+// adding half a TF32 ulp (0x1000) to the bit pattern is round-to-nearest (ties away) of the
+// value the MMA consumes; the low 13 bits need not be cleared.
 template <int KIND>
 __device__ __forceinline__ void ew_half(const TcArgs& a, uint32_t (&sv)[16], const float (&yv)[16],
                                         const uint32_t (&mk)[4], int cv, bool row_ok, uint32_t (&pb)[16],
                                         float& lsum, long long& cnt) {
-  uint32_t nz[4];
+  // observed bytes: mask byte nonzero (R6) and row / column in range
+  uint32_t ob[4];
 #pragma unroll
-  for (int j4 = 0; j4 < 4; ++j4) nz[j4] = a.has_mask ? __vcmpne4(mk[j4], 0u) : 0xffffffffu;
+  for (int j4 = 0; j4 < 4; ++j4) ob[j4] = a.has_mask ? mk[j4] : 0x01010101u;
   const uint32_t vbits = (!row_ok || cv <= 0) ? 0u : (cv >= 16 ? 0xffffu : ((1u << cv) - 1u));
   if (vbits != 0xffffu) {
 #pragma unroll
     for (int j4 = 0; j4 < 4; ++j4) {
       const uint32_t b = (vbits >> (4 * j4)) & 0xfu;
-      nz[j4] &= ((b * 0x00204081u) & 0x01010101u) * 0xffu;   // 4 bits -> 4 bytes of 0x00 / 0xff
+      ob[j4] &= ((b * 0x00204081u) & 0x01010101u) * 0xffu;   // 4 bits -> 4 bytes of 0x00 / 0xff
     }
   }
   if (a.mode != 0) {   // loss of the iterate entering the sweep (uniform branch)
 #pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      const bool o = (nz[j >> 2] >> (8 * (j & 3))) & 1u;
-      const float l = Ew<KIND>::loss(o ? yv[j] : 1.f, fmaxf(__uint_as_float(sv[j]), 1e-30f), a.dv);
-      lsum += o ? l : 0.f;
+    for (int j = 0; j < 16; j += 2) {
+      const bool o0 = (ob[j >> 2] & (0xffu << (8 * (j & 3)))) != 0u;
+      const bool o1 = (ob[j >> 2] & (0xffu << (8 * ((j + 1) & 3)))) != 0u;
+      const float2 yh = make_float2(fmaxf(__uint_as_float(sv[j]), 1e-30f), fmaxf(__uint_as_float(sv[j + 1]), 1e-30f));
+      float2 av, bv, lv;
+      Ew<KIND>::abl2(make_float2(o0 ? yv[j] : 1.f, o1 ? yv[j + 1] : 1.f), yh, a.dv, av, bv, lv);
+      lsum += (o0 ? lv.x : 0.f) + (o1 ? lv.y : 0.f);
+      sv[j] = o0 ? __float_as_uint(av.x) + 0x1000u : 0u;
+      sv[j + 1] = o1 ? __float_as_uint(av.y) + 0x1000u : 0u;
+      pb[j] = o0 ? __float_as_uint(bv.x) + 0x1000u : 0u;
+      pb[j + 1] = o1 ? __float_as_uint(bv.y) + 0x1000u : 0u;
     }
 #pragma unroll
-    for (int j4 = 0; j4 < 4; ++j4) cnt += __popc(nz[j4]) >> 3;
+    for (int j4 = 0; j4 < 4; ++j4) cnt += __popc(__vcmpne4(ob[j4], 0u)) >> 3;
+    return;
   }
 #pragma unroll
   for (int j = 0; j < 16; j += 2) {
     const float2 yh = make_float2(fmaxf(__uint_as_float(sv[j]), 1e-30f), fmaxf(__uint_as_float(sv[j + 1]), 1e-30f));
     float2 av, bv;
     Ew<KIND>::ab2(make_float2(yv[j], yv[j + 1]), yh, a.dv, av, bv);
-    const uint32_t m0 = __byte_perm(nz[j >> 2], 0u, (j & 3) * 0x1111u);   // replicate byte
-    const uint32_t m1 = __byte_perm(nz[j >> 2], 0u, ((j + 1) & 3) * 0x1111u);
-    sv[j] = tf32_bits(av.x) & m0;
-    sv[j + 1] = tf32_bits(av.y) & m1;
-    pb[j] = tf32_bits(bv.x) & m0;
-    pb[j + 1] = tf32_bits(bv.y) & m1;
+    const bool o0 = (ob[j >> 2] & (0xffu << (8 * (j & 3)))) != 0u;
+    const bool o1 = (ob[j >> 2] & (0xffu << (8 * ((j + 1) & 3)))) != 0u;
+    sv[j] = o0 ? __float_as_uint(av.x) + 0x1000u : 0u;
+    sv[j + 1] = o1 ? __float_as_uint(av.y) + 0x1000u : 0u;
+    pb[j] = o0 ? __float_as_uint(bv.x) + 0x1000u : 0u;
+    pb[j + 1] = o1 ? __float_as_uint(bv.y) + 0x1000u : 0u;
   }
 }
 
@@ -636,7 +680,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
       const uint32_t bytes = (uint32_t)Y_STAGE + (a.has_mask ? (uint32_t)M_STAGE : 0u);
       for (int t = 0; t < T; ++t) {
         const int st = t % NS;
-        mbar_wait(y_empty + 8 * st, ((t / NS) & 1) ^ 1);
+        mbar_wait_relaxed(y_empty + 8 * st, ((t / NS) & 1) ^ 1);
         trace_ev(a, t, EV_TMA_ISSUE);
         const int64_t tile = t_begin + t;
         const uint32_t bar = y_full + 8 * st;
@@ -668,13 +712,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
       constexpr uint32_t id1 = idesc_tf32(128, BN);   // S = U V^T   : N = 64 tile columns
       constexpr uint32_t id2 = idesc_tf32(128, KB);   // N = P V     : N = bond
       const bool war_wait = !(a.dbg & 8);
-      mbar_wait(u_ready, 0);
+      mbar_spin(u_ready, 0);
       tc_fence_after();
       // S(t) = U_hi V(t)^T + U_lo V(t)^T into buffer t & 1 (split reconstruction)
       auto mma_s = [&](int t) {
         const int vs = t % NV, b = t & 1;
-        mbar_wait(v_full + 8 * vs, (t / NV) & 1);
-        if (t >= 2 && war_wait) mbar_wait(buf_free + 8 * b, ((t >> 1) - 1) & 1);
+        mbar_spin(v_full + 8 * vs, (t / NV) & 1);
+        if (t >= 2 && war_wait) mbar_spin(buf_free + 8 * b, ((t >> 1) - 1) & 1);
         tc_fence_after();
         if (lane == 0) trace_ev(a, t, EV_MMA1_ISSUE);
         __syncwarp();
@@ -692,7 +736,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
       if (T > 1) mma_s(1);
       for (int u = 0; u < T; ++u) {
         const int vs = u % NV, b = u & 1;
-        mbar_wait(p_full + 8 * b, (u >> 1) & 1);
+        mbar_spin(p_full + 8 * b, (u >> 1) & 1);
         tc_fence_after();
         if (lane == 0) trace_ev(a, u, EV_MMA23_ISSUE);
         __syncwarp();
@@ -731,7 +775,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
           }
         }
         const int vs = t % NV;
-        mbar_wait(v_empty + 8 * vs, ((t / NV) & 1) ^ 1);
+        mbar_wait_relaxed(v_empty + 8 * vs, ((t / NV) & 1) ^ 1);
         const uint32_t bar = vraw_full + 8 * vs;
         mbar_expect_tx(bar, (uint32_t)(KB * BN * 4));
 #pragma unroll
@@ -764,7 +808,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
         }
       }
       const int vs = t % NV;
-      mbar_wait(vraw_full + 8 * vs, (t / NV) & 1);
+      mbar_wait_relaxed(vraw_full + 8 * vs, (t / NV) & 1);
       if (warp == 4 && lane == 0) trace_ev(a, t, EV_VG_START);
       unsigned char* vrow = gV + vs * V_STAGE_MAX;
 #pragma unroll
@@ -797,7 +841,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
       if (t + 1 < T) vtile_issue<KB>(a, t_begin + t + 1, xw, lane, nxt, toff_n, odo);   // next tile's rows in flight
       if (warp == 4 && lane == 0) trace_ev(a, t, EV_VG_ISSUED);
       const int vs = t % NV;
-      mbar_wait(v_empty + 8 * vs, ((t / NV) & 1) ^ 1);
+      mbar_wait_relaxed(v_empty + 8 * vs, ((t / NV) & 1) ^ 1);
       if (warp == 4 && lane == 0) trace_ev(a, t, EV_VG_START);
       vtile_store<KB>(a, xw, lane, cur, toff_c, gV + vs * V_STAGE_MAX, vo);
       fence_async_smem();
@@ -850,11 +894,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
       const int cols_here = (int)(crem < BN ? crem : BN);
       const int st = t % NS;
       const uint32_t tb = tmem + 128 * b + lane_off + 32 * g;   // S / P_a columns of this thread
-      mbar_wait(s_full + 8 * b, (t >> 1) & 1);
+      mbar_spin(s_full + 8 * b, (t >> 1) & 1);
       if (warp == 8 && lane == 0) trace_ev(a, t, EV_EW_S);
       tc_fence_after();
       float lsum = 0.f;
-      mbar_wait(y_full + 8 * st, (t / NS) & 1);
+      mbar_spin(y_full + 8 * st, (t / NS) & 1);
       if (warp == 8 && lane == 0) trace_ev(a, t, EV_EW_Y);
       // two half-steps of 16 columns through ONE code instance (I-cache)
 #pragma unroll 1
@@ -877,7 +921,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
         }
         if (a.debug && blockIdx.x == 0 && blockIdx.y == 0 && t == 0) {
 #pragma unroll
-          for (int j = 0; j < 16; ++j) a.debug[m * 64 + 32 * g + 16 * h + j] = __uint_as_float(sv[j]);
+          for (int j = 0; j < 16; ++j) a.debug[m * 64 + 32 * g + 16 * h + j] = __uint_as_float(sv[j] & 0xffffe000u);
         }
       }
       if (warp == 8 && lane == 0) trace_ev(a, t, EV_EW_HALF);
