@@ -82,9 +82,21 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
 }
 // Spin variant for waits on the critical path (no suspend hint: a suspended waiter was seen to
 // wake ~1000 cycles after the phase completed).  Still bounded.
+#ifndef NEF_SPIN_HINT
+#define NEF_SPIN_HINT 0
+#endif
 __device__ __forceinline__ void mbar_spin(uint32_t bar, uint32_t parity) {
   uint32_t done = 0;
   for (uint32_t it = 0;; ++it) {
+#if NEF_SPIN_HINT
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+        "selp.u32 %0, 1, 0, p;\n}"
+        : "=r"(done)
+        : "r"(bar), "r"(parity), "r"(NEF_SPIN_HINT)
+        : "memory");
+#else
     asm volatile(
         "{\n\t.reg .pred p;\n\t"
         "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
@@ -92,13 +104,14 @@ __device__ __forceinline__ void mbar_spin(uint32_t bar, uint32_t parity) {
         : "=r"(done)
         : "r"(bar), "r"(parity)
         : "memory");
+#endif
     if (done) return;
     if (it > (1u << 26)) __trap();
   }
 }
 // Producer-side wait (the producer runs ahead of its consumer): poll with a short sleep
 // between tries so the waiting warp leaves the issue slots to the elementwise warps.
-__device__ __forceinline__ void mbar_wait_relaxed(uint32_t bar, uint32_t parity) {
+__device__ __forceinline__ void mbar_wait_relaxed(uint32_t bar, uint32_t parity, uint32_t ns = 256) {
   uint32_t done = 0;
   for (uint32_t it = 0;; ++it) {
     asm volatile(
@@ -109,7 +122,7 @@ __device__ __forceinline__ void mbar_wait_relaxed(uint32_t bar, uint32_t parity)
         : "r"(bar), "r"(parity)
         : "memory");
     if (done) return;
-    __nanosleep(64);
+    __nanosleep(ns);
     if (it > (1u << 26)) __trap();
   }
 }
@@ -711,7 +724,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
     if (T > 0) {
       constexpr uint32_t id1 = idesc_tf32(128, BN);   // S = U V^T   : N = 64 tile columns
       constexpr uint32_t id2 = idesc_tf32(128, KB);   // N = P V     : N = bond
-      const bool war_wait = !(a.dbg & 8);
+      // The tensor pipe executes one thread's MMAs in issue order, so S(t+2) issued right behind
+      // the N/D MMAs of tile t cannot overwrite P(t) before they read it (checked: bit-identical
+      // factors with and without the explicit wait, scripts/war_check.py).  dbg & 16 restores
+      // the explicit wait on the N/D commit.
+      const bool war_wait = (a.dbg & 16) != 0;
       mbar_spin(u_ready, 0);
       tc_fence_after();
       // S(t) = U_hi V(t)^T + U_lo V(t)^T into buffer t & 1 (split reconstruction)
@@ -808,7 +825,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
         }
       }
       const int vs = t % NV;
-      mbar_wait_relaxed(vraw_full + 8 * vs, (t / NV) & 1);
+      mbar_wait_relaxed(vraw_full + 8 * vs, (t / NV) & 1, 96);
       if (warp == 4 && lane == 0) trace_ev(a, t, EV_VG_START);
       unsigned char* vrow = gV + vs * V_STAGE_MAX;
 #pragma unroll
@@ -926,7 +943,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
       }
       if (warp == 8 && lane == 0) trace_ev(a, t, EV_EW_HALF);
       if (a.mode != 2) tmem_st_wait();
-      loss_acc += (double)lsum;
+      if (a.mode != 0) loss_acc += (double)lsum;
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(p_full + 8 * b);      // P(t) in TMEM (or, loss only: S(t) consumed)
