@@ -243,20 +243,31 @@ int stream_pass(const Ctx& c, const nef::Lowering& L, const float* Y, const uint
         for (int k = 0; k < L.K; ++k) v4 = v4 && (boff[(size_t)q * L.K + k] == k);
       }
       t.vec4 = v4 && a.ntab > 0 ? 1 : 0;
-      // direct V: the innermost column mode (last column mode) has an extent divisible by 64,
-      // exactly one table carries it, with one table row per column (row stride = K)
+      // direct V (planner: Lowering::vd_tab): the tile's V rows are consecutive rows of one
+      // table, TMA-loaded; a K % 4 != 0 table is first copied to a 16-byte row pitch
       t.vdirect = 0;
-      const int inner = a.nc - 1;
       const char* dv = std::getenv("NEF_TC_VDIRECT");
       const bool allow = !dv || std::atoi(dv) != 0;
-      if (allow && t.vec4 && inner >= 0 && a.cdim[inner] % 64 == 0) {
-        int nvar = 0, vq = -1;
-        for (int q = 0; q < a.ntab; ++q)
-          if (a.tcs[q][inner] != 0) { ++nvar; vq = q; }
-        if (nvar == 1 && a.tcs[vq][inner] == L.K) {
-          t.vdirect = 1;
-          t.var_tab = vq;
-          t.var_rows = L.tabs[vq].prog.result.elems / L.K;
+      if (allow && L.vd_tab >= 0) {
+        t.vdirect = 1;
+        t.var_tab = L.vd_tab;
+        t.var_rows = L.vd_rows;
+        t.vd_E = L.vd_E;
+        // tiles per run: runs are whole column blocks (E a multiple of the block extent, or
+        // E == block) or E / 64 aligned tiles
+        {
+          const int64_t blk = L.tc_layout == 0 ? L.tc_CO : L.tc_CI;
+          const int64_t tiles_blk = (blk + 63) / 64;
+          if (L.vd_E % blk == 0) t.vd_tpr = (L.vd_E / blk) * tiles_blk;
+          else t.vd_tpr = L.vd_E / 64;
+        }
+        t.vd_pitch = L.vd_Kp;
+        t.vd_rows_ptr = a.tab[L.vd_tab];
+        if (L.ws_vpad >= 0) {
+          float* pad = reinterpret_cast<float*>(c.ws + L.ws_vpad);
+          CK(nef::launch_pad_rows(a.tab[L.vd_tab], pad, L.vd_rows, L.K, L.vd_Kp, c.s));
+          ++g_launches;
+          t.vd_rows_ptr = pad;
         }
       }
     }

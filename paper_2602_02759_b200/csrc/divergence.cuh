@@ -31,6 +31,25 @@ __device__ __forceinline__ float fsqrt(float x) {
   return r;
 }
 
+// natural log via MUFU.LG2 (abs. error ~1e-7 in the result; arguments are positive normals or
+// are discarded by the callers' selects)
+__device__ __forceinline__ float flog(float x) {
+  float r;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r * 0.69314718055994531f;
+}
+
+// f(u) = e^u... series helper on pairs: s(v) with f(v) = v^2 s(v) (see fser below)
+__device__ __forceinline__ float2 fser_poly2(float2 v) {
+  float2 s = make_float2(1.f / 840.f, 1.f / 840.f);
+  s = __ffma2_rn(s, v, make_float2(1.f / 144.f, 1.f / 144.f));
+  s = __ffma2_rn(s, v, make_float2(1.f / 30.f, 1.f / 30.f));
+  s = __ffma2_rn(s, v, make_float2(1.f / 8.f, 1.f / 8.f));
+  s = __ffma2_rn(s, v, make_float2(1.f / 3.f, 1.f / 3.f));
+  s = __ffma2_rn(s, v, make_float2(0.5f, 0.5f));
+  return __fmul2_rn(__fmul2_rn(v, v), s);
+}
+
 // fp32 -> TF32 bit pattern, round to nearest with ties away from zero (= cvt.rna.tf32.f32)
 // as two integer ops: add half a TF32 ulp to the magnitude bits, clear the low 13 bits.
 __device__ __forceinline__ uint32_t tf32_bits(float x) {
@@ -175,10 +194,16 @@ struct Ew<EW_KL> {   // (1, 0): a = x / y, b = 1
     bv = make_float2(1.f, 1.f);
   }
   static __device__ __forceinline__ float loss(float x, float yh, const DivParams&) { return kl_loss(x, yh); }
-  static __device__ __forceinline__ void abl2(float2 x, float2 yh, const DivParams& d, float2& av, float2& bv,
+  // a, b and the loss y f(u), u = log(x/y) = log(a): one rcp and one lg2 per entry
+  static __device__ __forceinline__ void abl2(float2 x, float2 yh, const DivParams&, float2& av, float2& bv,
                                               float2& l) {
-    ab2(x, yh, d, av, bv);
-    l = make_float2(loss(x.x, yh.x, d), loss(x.y, yh.y, d));
+    av = __fmul2_rn(x, make_float2(frcp(yh.x), frcp(yh.y)));
+    bv = make_float2(1.f, 1.f);
+    const float2 u = make_float2(flog(fmaxf(av.x, 1e-38f)), flog(fmaxf(av.y, 1e-38f)));
+    const float2 ser = __fmul2_rn(yh, fser_poly2(u));
+    const float2 dir = __ffma2_rn(x, u, make_float2(yh.x - x.x, yh.y - x.y));
+    l.x = x.x > 0.f ? (fabsf(u.x) < 0.3f ? ser.x : dir.x) : yh.x;
+    l.y = x.y > 0.f ? (fabsf(u.y) < 0.3f ? ser.y : dir.y) : yh.y;
   }
 };
 
@@ -251,10 +276,21 @@ struct Ew<EW_A05_B0> {  // (0.5, 0): a = sqrt(x) / y, b = y^-1/2; L = 4 y^1/2 f(
     const float l = fabsf(v) < 0.3f ? 4.f * sy * fser(v) : 4.f * (sy - sx + sx * v);
     return x > 0.f ? l : 4.f * sy;
   }
-  static __device__ __forceinline__ void abl2(float2 x, float2 yh, const DivParams& d, float2& av, float2& bv,
+  // shares rsqrt(y), sqrt(x) between a, b and the loss; v = log(x r^2) / 2
+  static __device__ __forceinline__ void abl2(float2 x, float2 yh, const DivParams&, float2& av, float2& bv,
                                               float2& l) {
-    ab2(x, yh, d, av, bv);
-    l = make_float2(loss(x.x, yh.x, d), loss(x.y, yh.y, d));
+    const float2 r = make_float2(frsqrt(yh.x), frsqrt(yh.y));
+    const float2 sx = make_float2(fsqrt(x.x), fsqrt(x.y));
+    const float2 r2 = __fmul2_rn(r, r);
+    bv = r;
+    av = __fmul2_rn(sx, r2);
+    const float2 q = __fmul2_rn(x, r2);   // x / y
+    const float2 v = make_float2(0.5f * flog(fmaxf(q.x, 1e-38f)), 0.5f * flog(fmaxf(q.y, 1e-38f)));
+    const float2 sy = __fmul2_rn(yh, r);
+    const float2 ser = __fmul2_rn(__fmul2_rn(sy, make_float2(4.f, 4.f)), fser_poly2(v));
+    const float2 dir = __fmul2_rn(make_float2(4.f, 4.f), __ffma2_rn(sx, v, make_float2(sy.x - sx.x, sy.y - sx.y)));
+    l.x = x.x > 0.f ? (fabsf(v.x) < 0.3f ? ser.x : dir.x) : 4.f * sy.x;
+    l.y = x.y > 0.f ? (fabsf(v.y) < 0.3f ? ser.y : dir.y) : 4.f * sy.y;
   }
 };
 

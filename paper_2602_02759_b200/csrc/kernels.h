@@ -56,6 +56,9 @@ cudaError_t launch_fused_ffma(const FusedArgs& a, cudaStream_t s);
 // Small einsum step (C = sum A*B, optional B), fp64 accumulation
 cudaError_t launch_einstep(const EinStep& st, const float* A, const float* B, float* C, cudaStream_t s);
 
+// dst[r][0..Kp) = src[r][0..K) padded with zeros (16-byte row pitch for TMA)
+cudaError_t launch_pad_rows(const float* src, float* dst, int64_t rows, int64_t K, int64_t Kp, cudaStream_t s);
+
 // Q[2][n_rows][K] = sum over chunks of Qpart (fixed order)
 cudaError_t launch_reduce_q(const float* Qpart, float* Q, int64_t n_chunks, int64_t elems2, cudaStream_t s);
 

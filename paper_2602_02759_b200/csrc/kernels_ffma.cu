@@ -402,6 +402,15 @@ cudaError_t launch_einstep(const EinStep& st, const float* A, const float* B, fl
 }
 
 // --------------------------------------------------------------------------------------
+__global__ void pad_rows_kernel(const float* __restrict__ src, float* __restrict__ dst, long long rows, int K, int Kp) {
+  const long long n = rows * Kp;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    const long long r = i / Kp;
+    const int k = (int)(i - r * Kp);
+    dst[i] = k < K ? src[r * K + k] : 0.f;
+  }
+}
+
 __global__ void reduce_q_kernel(const float* __restrict__ part, float* __restrict__ Q, long long n_chunks,
                                 long long elems) {
   for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < elems; e += (long long)gridDim.x * blockDim.x) {
@@ -461,6 +470,13 @@ __global__ void loss_reduce_kernel(const double* __restrict__ part, const long l
 cudaError_t launch_loss_reduce(const double* part, const long long* cpart, int64_t n, double* slot, long long* cslot,
                                cudaStream_t s) {
   loss_reduce_kernel<<<1, 256, 0, s>>>(part, cpart, n, slot, cslot);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_pad_rows(const float* src, float* dst, int64_t rows, int64_t K, int64_t Kp, cudaStream_t s) {
+  const long long n = rows * Kp;
+  const int blocks = (int)std::min<long long>((n + 255) / 256, 148 * 8);
+  pad_rows_kernel<<<blocks > 0 ? blocks : 1, 256, 0, s>>>(src, dst, rows, (int)K, (int)Kp);
   return cudaGetLastError();
 }
 

@@ -574,10 +574,11 @@ __device__ __forceinline__ int64_t tile_col0(const TcArgs& a, int64_t tile) {
   return to * a.CI + ti * BN;
 }
 
-// Direct V: consecutive tiles of a chunk advance the linear column index by 64
-// inside the innermost column mode (its extent is a multiple of 64), so the variable table's
-// row advances by 64 and the tile-constant rows change only when that mode wraps.  The two
-// functions below recompute from scratch at a wrap (cold, out of line).
+// Direct V: inside a run of vd_E columns (the trailing column modes one table
+// stores as consecutive rows), consecutive tiles advance the table row by 64 and the
+// tile-constant rows do not change; tiles never straddle runs (vd_E % 64 == 0, or the run is
+// the whole column block).  The two functions below recompute from scratch when a new run
+// starts (cold, out of line).
 __device__ __noinline__ int direct_var_row(const TcArgs& a, int64_t col) {
   int off = 0;
   for (int d = a.nc - 1; d >= 0; --d) {
@@ -587,23 +588,80 @@ __device__ __noinline__ int direct_var_row(const TcArgs& a, int64_t col) {
   }
   return off / a.K;
 }
-// product of the tile-constant table rows, bond chunk c (4 values) of this lane
-__device__ __noinline__ float4 direct_cst(const TcArgs& a, int64_t col, int c) {
-  int off[kMaxTabs] = {0, 0, 0, 0};
+// element offsets of every table's row at linear column col (out of line: divisions)
+struct TabOffs { int o[kMaxTabs]; };
+__device__ __noinline__ TabOffs direct_offs(const TcArgs& a, int64_t col) {
+  TabOffs r;
+  for (int q = 0; q < kMaxTabs; ++q) r.o[q] = 0;
   for (int d = a.nc - 1; d >= 0; --d) {
     const int64_t dig = d > 0 ? col % a.cdim[d] : col;
     col = d > 0 ? col / a.cdim[d] : 0;
-    for (int q = 0; q < a.ntab; ++q) off[q] += (int)dig * (int)a.tcs[q][d];
+    for (int q = 0; q < a.ntab; ++q) r.o[q] += (int)dig * (int)a.tcs[q][d];
   }
-  float4 p = make_float4(1.f, 1.f, 1.f, 1.f);
-  if (c * 4 >= a.K) return make_float4(0.f, 0.f, 0.f, 0.f);
-  for (int q = 0; q < a.ntab; ++q) {
-    if (q == a.var_tab) continue;
-    const float4 r = __ldg(reinterpret_cast<const float4*>(a.tab[q] + off[q]) + c);
-    p.x *= r.x; p.y *= r.y; p.z *= r.z; p.w *= r.w;
-  }
-  return p;
+  return r;
 }
+// Tile-constant rows of a run, bond chunk c (4 values) of this lane: loads issued here (all in
+// flight together), product formed by cst_product when needed (software-pipelined by the caller).
+struct CstLoad { float v[kMaxTabs][4]; };
+__device__ __forceinline__ void cst_issue(const TcArgs& a, int64_t col, int c, CstLoad& L) {
+  const TabOffs off = direct_offs(a, col);
+#pragma unroll
+  for (int q = 0; q < kMaxTabs; ++q)
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int k = 4 * c + e;
+      const bool use = q < a.ntab && q != a.var_tab && k < a.K;
+      L.v[q][e] = use ? __ldg(a.tab[q] + off.o[q] + k) : 1.f;   // bond stride 1 (planner)
+    }
+}
+__device__ __forceinline__ float4 cst_product(const TcArgs& a, int c, const CstLoad& L) {
+  float p[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    p[e] = 4 * c + e < a.K ? 1.f : 0.f;
+#pragma unroll
+    for (int q = 0; q < kMaxTabs; ++q) p[e] *= L.v[q][e];
+  }
+  return make_float4(p[0], p[1], p[2], p[3]);
+}
+
+// Walk over a chunk's tiles for the direct-V path.  Runs are a fixed number of tiles
+// (vd_tpr, host-computed), so a new run is a counter wrap; inside a run the column offset
+// advances by 64 per tile, or to the next CI block after a block's (ragged) last tile.  Only
+// init (once per CTA) and the callers' work at a new run divide.
+struct RunCursor {
+  int k, ti, tin, tpr;
+  int64_t off, blk_off, tile, ci;
+  __device__ __forceinline__ void init(const TcArgs& a, int64_t t0) {
+    tpr = (int)a.vd_tpr;
+    tin = (int)(a.layout == 0 ? a.tiles : a.tiles_inner);
+    ci = a.layout == 0 ? 0 : a.CI;
+    tile = t0;
+    k = (int)(t0 % tpr);
+    ti = (int)(t0 % tin);
+    off = tile_col0(a, t0) - tile_col0(a, t0 - k);
+    blk_off = off - (int64_t)ti * BN;
+  }
+  // advance to the next tile; true when it starts a new run (then off = 0)
+  __device__ __forceinline__ bool next() {
+    ++tile;
+    const bool wrap = ++ti == tin;
+    if (wrap) ti = 0;
+    if (++k == tpr) {
+      k = 0;
+      off = 0;
+      blk_off = 0;
+      return true;
+    }
+    if (wrap) {
+      blk_off += ci;
+      off = blk_off;
+    } else {
+      off += BN;
+    }
+    return false;
+  }
+};
 
 // pipeline timeline (diagnostics): event e of tile t in CTA (0,0)
 enum TraceEv : int {
@@ -778,19 +836,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
   } else if (warp == 3) {
     // ------------------------------------------------------------ direct-V row loads (TMA)
     if (lane == 0 && a.vdirect && T > 0) {
-      const int e_in = (int)a.cdim[a.nc - 1];
-      int64_t col = tile_col0(a, t_begin);
-      int inner = (int)(col % e_in);
-      int rowv = direct_var_row(a, col);
+      RunCursor rc;
+      rc.init(a, t_begin);
+      int run_row = direct_var_row(a, tile_col0(a, t_begin) - rc.off);
       for (int t = 0; t < T; ++t) {
-        if (t > 0) {
-          inner += BN;
-          rowv += BN;
-          if (inner >= e_in) {
-            inner = 0;
-            rowv = direct_var_row(a, tile_col0(a, t_begin + t));
-          }
-        }
+        if (t > 0 && rc.next()) run_row = direct_var_row(a, tile_col0(a, rc.tile));
+        const int rowv = run_row + (int)rc.off;
         const int vs = t % NV;
         mbar_wait_relaxed(v_empty + 8 * vs, ((t / NV) & 1) ^ 1);
         const uint32_t bar = vraw_full + 8 * vs;
@@ -808,21 +859,25 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
     const bool kok = c * 4 < a.K;
     VOff<KB> vo;
     vo.init(xw, lane);
-    const int e_in = (int)a.cdim[a.nc - 1];
-    int inner = 0;
+    // the next tile's run is looked up one tile ahead so that a new run's constant rows are in
+    // flight while the current tile is scaled
+    RunCursor rn;
+    CstLoad ld;
     float4 cst = make_float4(0.f, 0.f, 0.f, 0.f);
+    bool pend = false;
     if (T > 0) {
-      const int64_t col = tile_col0(a, t_begin);
-      inner = (int)(col % e_in);
-      cst = direct_cst(a, col, c);
+      rn.init(a, t_begin);
+      cst_issue(a, tile_col0(a, t_begin), c, ld);
+      cst = cst_product(a, c, ld);
     }
     for (int t = 0; t < T; ++t) {
-      if (t > 0) {
-        inner += BN;
-        if (inner >= e_in) {
-          inner = 0;
-          cst = direct_cst(a, tile_col0(a, t_begin + t), c);
-        }
+      if (pend) {
+        cst = cst_product(a, c, ld);
+        pend = false;
+      }
+      if (t + 1 < T && rn.next()) {
+        cst_issue(a, tile_col0(a, rn.tile), c, ld);
+        pend = true;
       }
       const int vs = t % NV;
       mbar_wait_relaxed(vraw_full + 8 * vs, (t / NV) & 1, 96);
@@ -1082,9 +1137,9 @@ cudaError_t launch(const TcArgs& args, const float* Y, const uint8_t* M, int64_t
   if (ok && args.vdirect) {
     // table rows [var_rows][K] -> V stage, two 32-float SW128 boxes (K beyond the row: zeros)
     uint64_t d[2] = {(uint64_t)args.K, (uint64_t)args.var_rows};
-    uint64_t sv[1] = {(uint64_t)args.K * 4};
+    uint64_t sv[1] = {(uint64_t)args.vd_pitch * 4};
     uint32_t bv[2] = {32, 64};
-    ok = encode(&P.tmV, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, args.tab[args.var_tab], d, sv, bv,
+    ok = encode(&P.tmV, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, args.vd_rows_ptr, d, sv, bv,
                 CU_TENSOR_MAP_SWIZZLE_128B);
   }
   if (!ok) return cudaErrorInvalidValue;

@@ -42,6 +42,10 @@ struct TcArgs {
   int vdirect;
   int var_tab;                // index of that table
   int64_t var_rows;           // its number of rows (row length = K)
+  int64_t vd_E;               // run length: columns per run of consecutive table rows
+  int64_t vd_tpr;             // tiles per run
+  int64_t vd_pitch;           // row pitch (elements) of vd_rows_ptr (K rounded up to 4)
+  const float* vd_rows_ptr;   // the table rows the TMA reads (the table, or its padded copy)
   int dbg;                    // diagnostics: 1 prefill N/D with 1 and always accumulate,
                               // 2 numerator B as K-major, 4 swap LBO/SBO of the MN-major view
 };

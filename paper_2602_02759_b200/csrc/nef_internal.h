@@ -92,6 +92,15 @@ struct Lowering {
   int64_t tc_row_blocks = 0;    // 128-row blocks
   int64_t ws_tc_Qpart = 0;      // partial buffer for the tcgen05 path
   int64_t ws_tc_losspart = 0;   // per-CTA loss / count partials of the tcgen05 path
+  // direct V: one table vd_tab holds the trailing column modes as consecutive
+  // rows (row pitch K), every other table is constant over them; runs of vd_E columns map to
+  // consecutive table rows, and no 64-column tile straddles two runs
+  int vd_tab = -1;
+  int64_t vd_E = 0;
+  int64_t vd_rows = 0;          // rows of that table
+  int64_t vd_Kp = 0;            // TMA row pitch (elements): K rounded up to 4
+  int64_t ws_vpad = -1;         // padded copy of the table when K % 4 != 0 (else -1)
+  bool tabs_merged = false;     // all column factors merged into one table (small column space)
 };
 
 struct Plan {

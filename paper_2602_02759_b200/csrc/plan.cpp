@@ -271,6 +271,11 @@ bool lower_candidate(const Plan& p, int ell, unsigned rowmask, unsigned pure_ass
   return true;
 }
 
+void build_tables(const Plan& p, Lowering& L, Bump& bump, bool merge);
+void direct_run(Lowering& L);
+void tc_geometry(const Plan& p, Lowering& L);
+void finish_workspace(const Plan& p, Lowering& L, Bump& bump, const std::string& uidx);
+
 // Fill programs, tables and workspace of a chosen candidate.
 void finish_lowering(const Plan& p, Lowering& L, Bump& bump) {
   // U[row, bond] from the row-side factors
@@ -278,9 +283,37 @@ void finish_lowering(const Plan& p, Lowering& L, Bump& bump) {
   for (int f : L.row_factors) rin.push_back({factor_buf(p, f), p.ops[f]});
   std::string uidx = L.row_idx + L.bond;
   L.uprog = compile_einsum(p, rin, uidx, bump, nullptr);
-  // column tables: connected components of col factors via non-bond contracted letters
+  build_tables(p, L, bump, false);
+  // tcgen05 geometry first (the direct-V analysis needs the column blocks)
+  tc_geometry(p, L);
+  if (L.tc_ok) {
+    direct_run(L);
+    // no direct-V run with the component tables: merge every column factor into ONE table
+    // over all column modes (consecutive rows for every tile) when that table is small
+    // (L2-resident; its generation is a few microseconds)
+    if (L.vd_tab < 0 && L.tabs.size() >= 1 && L.n_cols * L.K <= ((int64_t)4 << 20)) {
+      build_tables(p, L, bump, true);
+      direct_run(L);
+    }
+  }
+  if (L.vd_tab >= 0) {
+    L.vd_Kp = (L.K + 3) / 4 * 4;
+    if (L.vd_Kp != L.K) L.ws_vpad = bump.take(L.vd_rows * L.vd_Kp * 4 + 256);
+  }
+  finish_workspace(p, L, bump, uidx);
+}
+
+// Column tables: connected components of the column factors via non-bond contracted letters,
+// or (merge) one table over all column factors.
+void build_tables(const Plan& p, Lowering& L, Bump& bump, bool merge) {
+  L.tabs.clear();
+  L.tabs_merged = merge;
   std::vector<int> comp(L.col_factors.size(), -1);
   int ncomp = 0;
+  if (merge) {
+    for (auto& c : comp) c = 0;
+    ncomp = L.col_factors.empty() ? 0 : 1;
+  }
   for (size_t i = 0; i < L.col_factors.size(); ++i) {
     if (comp[i] >= 0) continue;
     comp[i] = ncomp;
@@ -329,44 +362,49 @@ void finish_lowering(const Plan& p, Lowering& L, Bump& bump) {
     }
     L.tabs.push_back(T);
   }
-  // workspace for the streaming pass
-  const int64_t BM = 64, BN = 64;
-  int64_t row_blocks = (L.n_rows + BM - 1) / BM;
-  int64_t col_tiles = (L.n_cols + BN - 1) / BN;
-  int64_t target = (int64_t)p.num_sms * 4;
-  int64_t chunks = std::max<int64_t>(1, (target + row_blocks - 1) / row_blocks);
-  chunks = std::min(chunks, col_tiles);
-  int64_t qelems = L.n_rows * L.K;
-  while (chunks > 1 && chunks * qelems * 8 > (int64_t)512 << 20) chunks /= 2;
-  L.n_chunks = chunks;
-  L.ws_boff = bump.take((int64_t)L.tabs.size() * L.K * 4);
-  L.ws_Qpart = bump.take(chunks * qelems * 2 * 4);
-  L.ws_Q = bump.take(qelems * 2 * 4);
-  int64_t felems = prod_idx(p, p.ops[L.ell]);
-  L.ws_num = bump.take(2 * felems * 4);   // num | den adjacent (one all-reduce)
-  L.ws_den = L.ws_num + felems * 4;
-  L.ws_losspart = bump.take(row_blocks * chunks * 16);
-  // epilogue: Num (ell's layout) = einsum(Q[row_idx + bond], row factors except ell)
-  std::string qidx = uidx;
-  if (L.row_factors.size() == 1 && p.ops[L.ell] == qidx) {
-    L.epi_identity = true;
-  } else {
-    BufRef qa;
-    qa.kind = BUF_WS;
-    qa.id = L.ws_Q;
-    qa.elems = qelems;
-    std::vector<Operand> ein;
-    ein.push_back({qa, qidx});
-    for (int f : L.row_factors)
-      if (f != L.ell) ein.push_back({factor_buf(p, f), p.ops[f]});
-    BufRef tgt;
-    tgt.kind = BUF_WS;
-    tgt.id = L.ws_num;
-    tgt.elems = felems;
-    L.epi = compile_einsum(p, ein, p.ops[L.ell], bump, &tgt);
+}
+
+// Direct-V analysis (see Lowering::vd_tab): the longest trailing run of column modes that one
+// table stores as consecutive rows of pitch K while the other tables are constant over it.
+void direct_run(Lowering& L) {
+  L.vd_tab = -1;
+  L.vd_E = 0;
+  const int nc = (int)L.col_modes.size();
+  if (nc == 0 || L.tabs.empty()) return;
+  const int64_t blk = L.tc_layout == 0 ? L.n_cols : L.tc_CI;
+  for (size_t q = 0; q < L.tabs.size(); ++q) {
+    const ColTable& T = L.tabs[q];
+    bool unit = true;
+    for (int64_t b = 0; b < L.K; ++b) unit &= T.boff[(size_t)b] == b;
+    if (!unit) continue;
+    int64_t want = L.K, E = 1;
+    int m = nc;
+    for (int d = nc - 1; d >= 0; --d) {
+      bool ok = T.cstride[d] == want;
+      for (size_t q2 = 0; q2 < L.tabs.size() && ok; ++q2)
+        if (q2 != q) ok = L.tabs[q2].cstride[d] == 0;
+      if (!ok) break;
+      want *= L.cdim[d];
+      E *= L.cdim[d];
+      m = d;
+    }
+    if (m == nc) continue;
+    // no 64-column tile may straddle two runs: tiles are 64-aligned inside each column block
+    // (layout 0 / 1: one block of n_cols / CI columns; layout 2: CO blocks of CI columns)
+    bool fits;
+    if (L.tc_layout == 2) fits = (E % 64 == 0 && L.tc_CI % 64 == 0) || E % L.tc_CI == 0;
+    else fits = E % 64 == 0 || E == blk;
+    if (!fits) continue;
+    L.vd_tab = (int)q;
+    L.vd_E = E;
+    L.vd_rows = T.prog.result.elems / L.K;
+    return;
   }
-  // tcgen05 / TMA geometry: the row modes must be one adjacent block of Y modes; the column
-  // modes then split into an outer block (before) and an inner block (after).
+}
+
+// tcgen05 / TMA geometry: the row modes must be one adjacent block of Y modes; the column
+// modes then split into an outer block (before) and an inner block (after).
+void tc_geometry(const Plan& p, Lowering& L) {
   L.tc_ok = false;
   bool adjacent = !L.row_modes.empty();
   for (size_t k = 1; k < L.row_modes.size(); ++k) adjacent &= L.row_modes[k] == L.row_modes[k - 1] + 1;
@@ -406,10 +444,52 @@ void finish_lowering(const Plan& p, Lowering& L, Bump& bump) {
       int64_t ch = std::max<int64_t>(1, p.num_sms / L.tc_row_blocks);
       ch = std::min(ch, L.tc_tiles);
       L.tc_chunks = ch;
-      L.ws_tc_Qpart = bump.take(ch * L.tc_row_blocks * 128 * L.K * 2 * 4);
-      int64_t nparts = L.tc_row_blocks * ch;
-      L.ws_tc_losspart = bump.take(nparts * 16);
     }
+  }
+}
+
+// Workspace of the streaming pass and the epilogue program.
+void finish_workspace(const Plan& p, Lowering& L, Bump& bump, const std::string& uidx) {
+  // workspace for the streaming pass
+  const int64_t BM = 64, BN = 64;
+  int64_t row_blocks = (L.n_rows + BM - 1) / BM;
+  int64_t col_tiles = (L.n_cols + BN - 1) / BN;
+  int64_t target = (int64_t)p.num_sms * 4;
+  int64_t chunks = std::max<int64_t>(1, (target + row_blocks - 1) / row_blocks);
+  chunks = std::min(chunks, col_tiles);
+  int64_t qelems = L.n_rows * L.K;
+  while (chunks > 1 && chunks * qelems * 8 > (int64_t)512 << 20) chunks /= 2;
+  L.n_chunks = chunks;
+  L.ws_boff = bump.take((int64_t)L.tabs.size() * L.K * 4);
+  L.ws_Qpart = bump.take(chunks * qelems * 2 * 4);
+  L.ws_Q = bump.take(qelems * 2 * 4);
+  int64_t felems = prod_idx(p, p.ops[L.ell]);
+  L.ws_num = bump.take(2 * felems * 4);   // num | den adjacent (one all-reduce)
+  L.ws_den = L.ws_num + felems * 4;
+  L.ws_losspart = bump.take(row_blocks * chunks * 16);
+  // epilogue: Num (ell's layout) = einsum(Q[row_idx + bond], row factors except ell)
+  std::string qidx = uidx;
+  if (L.row_factors.size() == 1 && p.ops[L.ell] == qidx) {
+    L.epi_identity = true;
+  } else {
+    BufRef qa;
+    qa.kind = BUF_WS;
+    qa.id = L.ws_Q;
+    qa.elems = qelems;
+    std::vector<Operand> ein;
+    ein.push_back({qa, qidx});
+    for (int f : L.row_factors)
+      if (f != L.ell) ein.push_back({factor_buf(p, f), p.ops[f]});
+    BufRef tgt;
+    tgt.kind = BUF_WS;
+    tgt.id = L.ws_num;
+    tgt.elems = felems;
+    L.epi = compile_einsum(p, ein, p.ops[L.ell], bump, &tgt);
+  }
+  if (L.tc_ok) {
+    L.ws_tc_Qpart = bump.take(L.tc_chunks * L.tc_row_blocks * 128 * L.K * 2 * 4);
+    int64_t nparts = L.tc_row_blocks * L.tc_chunks;
+    L.ws_tc_losspart = bump.take(nparts * 16);
   }
   L.ws_end = bump.off;
 }
@@ -586,7 +666,7 @@ std::string describe_plan(const Plan& p) {
       << ",\"row_fast\":" << (L.row_fast ? "true" : "false") << ",\"n_chunks\":" << L.n_chunks
       << ",\"tc\":" << (L.tc_ok ? "true" : "false") << ",\"tc_layout\":" << L.tc_layout << ",\"tc_R\":" << L.tc_R
       << ",\"tc_CI\":" << L.tc_CI << ",\"tc_CO\":" << L.tc_CO << ",\"tc_KB\":" << L.tc_KB
-      << ",\"tc_tiles\":" << L.tc_tiles << ",\"tc_chunks\":" << L.tc_chunks << ",\"row_factors\":[";
+      << ",\"tc_tiles\":" << L.tc_tiles << ",\"tc_chunks\":" << L.tc_chunks << ",\"vd_tab\":" << L.vd_tab << ",\"vd_E\":" << L.vd_E << ",\"tabs_merged\":" << (L.tabs_merged ? "true" : "false") << ",\"row_factors\":[";
     for (size_t k = 0; k < L.row_factors.size(); ++k) o << (k ? "," : "") << L.row_factors[k];
     o << "],\"col_factors\":[";
     for (size_t k = 0; k < L.col_factors.size(); ++k) o << (k ? "," : "") << L.col_factors[k];

@@ -248,7 +248,10 @@ class Plan:
     def __del__(self):
         h = getattr(self, "h", None)
         if h:
-            nef_plan_destroy(h)
+            try:
+                nef_plan_destroy(h)
+            except TypeError:   # interpreter shutdown: module globals already cleared
+                pass
             self.h = None
 
     @property

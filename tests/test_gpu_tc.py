@@ -26,6 +26,10 @@ TC_CASES = [
     ("ir,jr,kr->ijk", (96, 192, 128), (64,), (1.0, -0.5), 0.05, "gamma"),
     ("ia,jb,kc,abc->ijk", (80, 128, 64), (16, 16, 16), (1.0, 1.0), 0.1, "absnormal"),
     ("ir,jr,kr->ijk", (64, 64, 128), (24,), (0.5, 0.0), 0.0, "poisson"),
+    # layout 2 with a ragged 40-column inner block: direct-V runs spanning whole blocks
+    ("ia,jb,kc,abc->ijk", (64, 72, 40), (8, 8, 8), (1.0, 1.0), 0.0, "absnormal"),
+    # small column space merged into one table (K = 10: padded 16-byte row pitch)
+    ("ik,jk,tl,dl,kl->ijtd", (40, 48, 16, 36), (12, 10), (0.5, 0.0), 0.0, "poisson"),
 ]
 
 
