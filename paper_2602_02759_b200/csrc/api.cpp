@@ -34,7 +34,8 @@ thread_local std::string g_err;
 thread_local int64_t g_launches = 0;
 int g_policy = 0;
 float* g_debug = nullptr;   // optional device dump of the tcgen05 kernel's first tile (tests)
-long long* g_trace = nullptr;   // optional pipeline timeline of the tcgen05 kernel (diagnostics)
+long long* g_trace = nullptr;
+bool g_no_sentinel = std::getenv("NEF_NO_SENTINEL") != nullptr;   // diagnostics: stream the uint8 mask   // optional pipeline timeline of the tcgen05 kernel (diagnostics)
 
 // live CUDA-event timing of the streaming kernel (nef_profile_*)
 struct Prof {
@@ -119,6 +120,7 @@ struct Ctx {
   char* ws;
   size_t ws_bytes;
   cudaStream_t s;
+  const float* ysent = nullptr;   // NaN-sentinel copy of Y (mask folded in), when prepared
 };
 
 float* resolve(const Ctx& c, const nef::BufRef& b) {
@@ -201,8 +203,8 @@ struct StreamOut {
   int64_t nparts = 0;
 };
 
-bool use_tc(const nef::Lowering& L, const uint8_t* M) {
-  return g_policy == 0 && L.tc_ok && (!M || (L.tc_mask_ok && (reinterpret_cast<uintptr_t>(M) & 15) == 0));
+bool use_tc(const nef::Lowering& L, const uint8_t* M, bool sentinel = false) {
+  return g_policy == 0 && L.tc_ok && (!M || sentinel || (L.tc_mask_ok && (reinterpret_cast<uintptr_t>(M) & 15) == 0));
 }
 
 // One streaming pass over Y (+mask) for lowering L: the tcgen05 kernel where the planner
@@ -212,7 +214,12 @@ int stream_pass(const Ctx& c, const nef::Lowering& L, const float* Y, const uint
   std::vector<int32_t> boff;
   nef::FusedArgs a = fused_args(c, L, Y, M, mode, dv, boff);
   const double bytes = (double)c.p->n_local * (M ? 5.0 : 4.0);
-  if (use_tc(L, M)) {
+  const bool sent = M && c.ysent;
+  if (use_tc(L, M, sent)) {
+    if (sent) {   // stream the NaN-sentinel copy: no mask stream (4 B / entry)
+      Y = c.ysent;
+      M = nullptr;
+    }
     nef::tc::TcArgs t{};
     t.layout = L.tc_layout;
     t.R = L.tc_R;
@@ -524,6 +531,18 @@ int nef_fit(nef_plan_t plan, const float* Y, const uint8_t* mask, double alpha, 
   Ctx c{&p, factors, static_cast<char*>(workspace), ws_bytes, static_cast<cudaStream_t>(stream)};
   nef::DivParams dv = nef::make_div(alpha, beta);
   nef::UpdArgs u = nef::make_upd(alpha, beta, eps);
+  // a1 precompute (once per fit): fold the mask into a NaN-sentinel copy of Y for the tcgen05
+  // passes (R5: missing values are never used, whatever Y holds there)
+  if (mask && g_policy == 0 && !g_no_sentinel) {
+    bool any_tc = false;
+    for (const auto& L : p.low) any_tc |= L.tc_ok;
+    if (any_tc) {
+      float* ys = reinterpret_cast<float*>(c.ws + p.ws_sent);
+      CK(nef::launch_sentinel(Y, mask, ys, p.n_local, c.s));
+      ++g_launches;
+      c.ysent = ys;
+    }
+  }
   double* slots = reinterpret_cast<double*>(c.ws + p.ws_trace);
   long long* cslots = reinterpret_cast<long long*>(c.ws + p.ws_trace + 8 * 2048);
   const int kSlots = 2048;

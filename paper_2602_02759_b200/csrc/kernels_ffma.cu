@@ -402,6 +402,27 @@ cudaError_t launch_einstep(const EinStep& st, const float* A, const float* B, fl
 }
 
 // --------------------------------------------------------------------------------------
+// 4 entries per thread and iteration: one 4-byte mask load and one 16-byte Y load / store, all
+// fully coalesced across the warp
+__global__ void sentinel_kernel(const float* __restrict__ Y, const uint8_t* __restrict__ M, float* __restrict__ out,
+                                long long n4) {
+  const float nan = __uint_as_float(0x7fc00000u);
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4; i += (long long)gridDim.x * blockDim.x) {
+    const uint32_t w = __ldcs(reinterpret_cast<const unsigned int*>(M) + i);
+    float4 y = __ldcs(reinterpret_cast<const float4*>(Y) + i);
+    y.x = (w & 0xffu) ? y.x : nan;
+    y.y = (w & 0xff00u) ? y.y : nan;
+    y.z = (w & 0xff0000u) ? y.z : nan;
+    y.w = (w & 0xff000000u) ? y.w : nan;
+    __stcs(reinterpret_cast<float4*>(out) + i, y);
+  }
+}
+__global__ void sentinel_tail_kernel(const float* __restrict__ Y, const uint8_t* __restrict__ M, float* __restrict__ out,
+                                     long long from, long long n) {
+  for (long long i = from + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    out[i] = M[i] ? Y[i] : __uint_as_float(0x7fc00000u);
+}
+
 __global__ void pad_rows_kernel(const float* __restrict__ src, float* __restrict__ dst, long long rows, int K, int Kp) {
   const long long n = rows * Kp;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
@@ -477,6 +498,14 @@ cudaError_t launch_pad_rows(const float* src, float* dst, int64_t rows, int64_t 
   const long long n = rows * Kp;
   const int blocks = (int)std::min<long long>((n + 255) / 256, 148 * 8);
   pad_rows_kernel<<<blocks > 0 ? blocks : 1, 256, 0, s>>>(src, dst, rows, (int)K, (int)Kp);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_sentinel(const float* Y, const uint8_t* M, float* out, int64_t n, cudaStream_t s) {
+  const bool vec = (((reinterpret_cast<uintptr_t>(Y) | reinterpret_cast<uintptr_t>(out)) & 15) | (reinterpret_cast<uintptr_t>(M) & 3)) == 0;
+  const long long n4 = vec ? n / 4 : 0;
+  if (n4 > 0) sentinel_kernel<<<148 * 16, 256, 0, s>>>(Y, M, out, n4);
+  if (n4 * 4 < n) sentinel_tail_kernel<<<148, 256, 0, s>>>(Y, M, out, n4 * 4, n);
   return cudaGetLastError();
 }
 

@@ -36,9 +36,16 @@ namespace tc {
 
 constexpr int BM = 128, BN = 64;
 constexpr int NS = 3;        // Y / mask pipeline stages
-constexpr int NV = 3;        // V tile stages
-constexpr int NTHREADS = 512;
+// V tile stages: 3 with a uint8 mask stream (its stages take the smem), else 4
+template <int MM> struct VStages { static constexpr int value = MM == 1 ? 3 : 4; };
+// warp roles: 16 elementwise warps, 4 V generators, direct-V row loads, TMA producer, MMA
+// issuer.  The warp schedulers favour higher warp ids, so the producers whose latency is on the
+// critical path sit above the elementwise warps (with the producers below, the V generators
+// and the MMA issuer starved during the elementwise phase of every tile).
+constexpr int W_EW0 = 0, W_VG0 = 16, W_DV = 20, W_TMA = 21, W_MMA = 22;
 constexpr int NVG = 4;       // V-generator warps (16 tile columns each)
+constexpr int NEW = 16;      // elementwise warps: 4 TMEM lane quarters x 4 groups of 16 columns
+constexpr int NTHREADS = 23 * 32;   // 736
 constexpr int Y_STAGE = BM * BN * 4;      // 32 KB
 constexpr int M_STAGE = BM * BN;          // 8 KB
 constexpr int VT_OFF = BN * 64 * 4;       // V^T copy after V inside a stage
@@ -125,6 +132,18 @@ __device__ __forceinline__ void mbar_wait_relaxed(uint32_t bar, uint32_t parity,
     __nanosleep(ns);
     if (it > (1u << 26)) __trap();
   }
+}
+// MMA-issuer wait: it shares its SM sub-partition with two elementwise warps, so it backs off
+// between polls (NEF_MMA_WAIT: 0 spin, else nanoseconds of sleep per failed poll)
+#ifndef NEF_MMA_WAIT
+#define NEF_MMA_WAIT 32
+#endif
+__device__ __forceinline__ void mbar_wait_mma(uint32_t bar, uint32_t parity) {
+#if NEF_MMA_WAIT
+  mbar_wait_relaxed(bar, parity, NEF_MMA_WAIT);
+#else
+  mbar_spin(bar, parity);
+#endif
 }
 __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* tm, int c0, int c1, uint32_t bar) {
   asm volatile(
@@ -567,6 +586,48 @@ __device__ __forceinline__ void ew_half(const TcArgs& a, uint32_t (&sv)[16], con
   }
 }
 
+// The same without a mask stream: a missing entry carries NaN in Y (the NaN-sentinel copy nef_fit
+// makes once per fit, R5), and every NaN propagates through a (which has a factor of x)
+// and through b' = x * 0 + b, so max(., 0) - which returns 0 for NaN - zeroes both.  Entries
+// outside the tile's valid rows / columns (TMA zero fill) are turned into NaN first.
+template <int KIND>
+__device__ __forceinline__ void ew_half_sent(const TcArgs& a, uint32_t (&sv)[16], float (&yv)[16], int cv, bool row_ok,
+                                             uint32_t (&pb)[16], float& lsum, long long& cnt) {
+  const uint32_t vbits = (!row_ok || cv <= 0) ? 0u : (cv >= 16 ? 0xffffu : ((1u << cv) - 1u));
+  if (vbits != 0xffffu) {
+#pragma unroll
+    for (int j = 0; j < 16; ++j) yv[j] = ((vbits >> j) & 1u) ? yv[j] : __uint_as_float(0x7fc00000u);
+  }
+  if (a.mode != 0) {   // loss of the iterate entering the sweep (uniform branch)
+#pragma unroll
+    for (int j = 0; j < 16; j += 2) {
+      const bool o0 = yv[j] == yv[j], o1 = yv[j + 1] == yv[j + 1];
+      const float2 yh = make_float2(fmaxf(__uint_as_float(sv[j]), 1e-30f), fmaxf(__uint_as_float(sv[j + 1]), 1e-30f));
+      float2 av, bv, lv;
+      Ew<KIND>::abl2(make_float2(o0 ? yv[j] : 1.f, o1 ? yv[j + 1] : 1.f), yh, a.dv, av, bv, lv);
+      lsum += (o0 ? lv.x : 0.f) + (o1 ? lv.y : 0.f);
+      cnt += (o0 ? 1 : 0) + (o1 ? 1 : 0);
+      sv[j] = o0 ? __float_as_uint(av.x) + 0x1000u : 0u;
+      sv[j + 1] = o1 ? __float_as_uint(av.y) + 0x1000u : 0u;
+      pb[j] = o0 ? __float_as_uint(bv.x) + 0x1000u : 0u;
+      pb[j + 1] = o1 ? __float_as_uint(bv.y) + 0x1000u : 0u;
+    }
+    return;
+  }
+#pragma unroll
+  for (int j = 0; j < 16; j += 2) {
+    const float2 x = make_float2(yv[j], yv[j + 1]);
+    const float2 yh = make_float2(fmaxf(__uint_as_float(sv[j]), 1e-30f), fmaxf(__uint_as_float(sv[j + 1]), 1e-30f));
+    float2 av, bv;
+    Ew<KIND>::ab2(x, yh, a.dv, av, bv);
+    bv = __ffma2_rn(x, make_float2(0.f, 0.f), bv);   // NaN at missing entries
+    sv[j] = __float_as_uint(fmaxf(av.x, 0.f)) + 0x1000u;
+    sv[j + 1] = __float_as_uint(fmaxf(av.y, 0.f)) + 0x1000u;
+    pb[j] = __float_as_uint(fmaxf(bv.x, 0.f)) + 0x1000u;
+    pb[j + 1] = __float_as_uint(fmaxf(bv.y, 0.f)) + 0x1000u;
+  }
+}
+
 // linear column index of the first column of a tile
 __device__ __forceinline__ int64_t tile_col0(const TcArgs& a, int64_t tile) {
   if (a.layout == 0) return tile * BN;
@@ -669,7 +730,7 @@ enum TraceEv : int {
   EV_EW_DONE, EV_VG_ISSUED
 };
 __device__ __forceinline__ void trace_ev(const TcArgs& a, int t, int e) {
-  if (a.trace && blockIdx.x == 0 && blockIdx.y == 0 && t < 1024) a.trace[t * 16 + e] = (long long)clock64();
+  if (a.trace && blockIdx.x == 0 && blockIdx.y == 0 && t < 1024) a.trace[t * 32 + e] = (long long)clock64();
 }
 
 // ------------------------------------------------------------------ the kernel
@@ -680,8 +741,10 @@ __device__ __forceinline__ void trace_ev(const TcArgs& a, int t, int e) {
 //
 // Tile t uses buffer t & 1.  Single MMA issuer, in order:
 //   S(0), S(1), then for each t: [P(t) ready] N,D += P(t) V(t); [buffer t&1 retired] S(t+2)
-template <int KB, int KIND>
+// MM: 1 = uint8 mask streamed alongside Y; 0 = no mask stream (no mask, or the NaN-sentinel Y)
+template <int KB, int KIND, int MM>
 __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_constant__ Params P) {
+  constexpr int NV = VStages<MM>::value;
   extern __shared__ unsigned char smraw[];
   const TcArgs& a = P.a;
   const int tid = threadIdx.x;
@@ -694,7 +757,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
   unsigned char* gbase = smraw + (base - raw);
   const uint32_t sY = base;                                  // NS x 32 KB
   const uint32_t sM = sY + NS * Y_STAGE;                     // NS x 8 KB
-  const uint32_t sV = sM + NS * M_STAGE;                     // NV x (V | V^T)
+  const uint32_t sV = sM + (MM == 1 ? NS * M_STAGE : 0);     // NV x (V | V^T)
   const uint32_t sBar = sV + NV * V_STAGE_MAX;
   const uint32_t y_full = sBar, y_empty = y_full + 8 * NS;
   const uint32_t v_full = y_empty + 8 * NS, v_empty = v_full + 8 * NV;
@@ -706,10 +769,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
   const uint32_t sTmem = vraw_full + 8 * NV;
   unsigned char* gY = gbase;
   unsigned char* gM = gbase + NS * Y_STAGE;
-  unsigned char* gV = gM + NS * M_STAGE;
+  unsigned char* gV = gbase + (sV - base);
   uint32_t* gTmem = reinterpret_cast<uint32_t*>(gbase + (sTmem - base));
-  double* gRed = reinterpret_cast<double*>(gbase + (sTmem - base) + 64);
-  long long* gRedC = reinterpret_cast<long long*>(gbase + (sTmem - base) + 64 + 256 * 8);
+  // loss reduction scratch: aliases Y stage 0, free once every tile has been consumed
+  double* gRed = reinterpret_cast<double*>(gbase);
+  long long* gRedC = reinterpret_cast<long long*>(gbase + NEW * 32 * 8);
 
   const int64_t rb = blockIdx.x;
   const int64_t ch = blockIdx.y;
@@ -720,21 +784,21 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
   const int rows_here = (int)((a.n_rows - row0) < BM ? (a.n_rows - row0) : BM);
 
   if (tid == 0) {
-    for (int i = 0; i < NS; ++i) { mbar_init(y_full + 8 * i, 1); mbar_init(y_empty + 8 * i, 8); }
+    for (int i = 0; i < NS; ++i) { mbar_init(y_full + 8 * i, 1); mbar_init(y_empty + 8 * i, NEW); }
     for (int i = 0; i < NV; ++i) { mbar_init(v_full + 8 * i, NVG); mbar_init(v_empty + 8 * i, 1); }
     for (int i = 0; i < 2; ++i) {
       mbar_init(s_full + 8 * i, 1);
-      mbar_init(p_full + 8 * i, 8);
+      mbar_init(p_full + 8 * i, NEW);
       mbar_init(buf_free + 8 * i, 1);
     }
     mbar_init(nd_full, 1);
-    mbar_init(u_ready, 8);
+    mbar_init(u_ready, NEW);
     for (int i = 0; i < NV; ++i) mbar_init(vraw_full + 8 * i, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&P.tmY)) : "memory");
     if (a.has_mask) asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&P.tmM)) : "memory");
   }
-  if (warp == 1) {
+  if (warp == W_MMA) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(sTmem) : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
@@ -745,7 +809,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
   const uint32_t tNa = tmem + 256, tNb = tmem + 256 + KB;
   const uint32_t tUh = tmem + 256 + 2 * KB, tUl = tmem + 256 + 3 * KB;
 
-  if (warp == 0) {
+  if (warp == W_TMA) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
       const uint32_t bytes = (uint32_t)Y_STAGE + (a.has_mask ? (uint32_t)M_STAGE : 0u);
@@ -774,7 +838,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
         }
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == W_MMA) {
     // ------------------------------------------------------------ MMA issuer
     // The whole warp runs the issue loop (warp-uniform control flow, so descriptors and TMEM
     // addresses stay in uniform registers and every tcgen05.mma is one elected issue; a
@@ -787,13 +851,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
       // factors with and without the explicit wait, scripts/war_check.py).  dbg & 16 restores
       // the explicit wait on the N/D commit.
       const bool war_wait = (a.dbg & 16) != 0;
-      mbar_spin(u_ready, 0);
+      mbar_wait_mma(u_ready, 0);
       tc_fence_after();
       // S(t) = U_hi V(t)^T + U_lo V(t)^T into buffer t & 1 (split reconstruction)
       auto mma_s = [&](int t) {
         const int vs = t % NV, b = t & 1;
-        mbar_spin(v_full + 8 * vs, (t / NV) & 1);
-        if (t >= 2 && war_wait) mbar_spin(buf_free + 8 * b, ((t >> 1) - 1) & 1);
+        mbar_wait_mma(v_full + 8 * vs, (t / NV) & 1);
+        if (t >= 2 && war_wait) mbar_wait_mma(buf_free + 8 * b, ((t >> 1) - 1) & 1);
         tc_fence_after();
         if (lane == 0) trace_ev(a, t, EV_MMA1_ISSUE);
         __syncwarp();
@@ -802,20 +866,22 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
 #pragma unroll
         for (int kk = 0; kk < KB / 8; ++kk)
           mma_ts_elect(d, tUh + kk * 8, vd + (uint64_t)(((kk >> 2) * (BN * 128) + (kk & 3) * 32) >> 4), id1, kk > 0 ? 1u : 0u);
+        if (!(a.dbg & 32)) {   // dbg 32: timing experiment without the U_lo half of the split
 #pragma unroll
-        for (int kk = 0; kk < KB / 8; ++kk)
-          mma_ts_elect(d, tUl + kk * 8, vd + (uint64_t)(((kk >> 2) * (BN * 128) + (kk & 3) * 32) >> 4), id1, 1u);
+          for (int kk = 0; kk < KB / 8; ++kk)
+            mma_ts_elect(d, tUl + kk * 8, vd + (uint64_t)(((kk >> 2) * (BN * 128) + (kk & 3) * 32) >> 4), id1, 1u);
+        }
         mma_commit_elect(s_full + 8 * b);
       };
       mma_s(0);
       if (T > 1) mma_s(1);
       for (int u = 0; u < T; ++u) {
         const int vs = u % NV, b = u & 1;
-        mbar_spin(p_full + 8 * b, (u >> 1) & 1);
+        mbar_wait_mma(p_full + 8 * b, (u >> 1) & 1);
         tc_fence_after();
         if (lane == 0) trace_ev(a, u, EV_MMA23_ISSUE);
         __syncwarp();
-        if (a.mode != 2) {
+        if (a.mode != 2 && !(a.dbg & 64)) {   // dbg 64: timing experiment without N/D MMAs
           // B = V^T, K-major SW128: rows = bond (N), K = tile columns (2 atoms of 32)
           const uint64_t vtd = sdesc(sV + vs * V_STAGE_MAX + VT_OFF, 16, 1024);
           const uint32_t pa = tmem + 128 * b, pbb = pa + 64;
@@ -833,7 +899,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
       }
       mma_commit_elect(nd_full);
     }
-  } else if (warp == 3) {
+  } else if (warp == W_DV) {
     // ------------------------------------------------------------ direct-V row loads (TMA)
     if (lane == 0 && a.vdirect && T > 0) {
       RunCursor rc;
@@ -850,10 +916,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
         for (int h = 0; h < KB / 32; ++h) tma_load_2d(sV + vs * V_STAGE_MAX + h * (BN * 128), &P.tmV, 32 * h, rowv, bar);
       }
     }
-  } else if (warp >= 4 && warp < 4 + NVG && a.vdirect) {
+  } else if (warp >= W_VG0 && warp < W_VG0 + NVG && a.vdirect) {
     // ------------------------------------------------------------ direct V: scale rows in place
     // V[x][k] = T_var[row + x][k] * prod_{q != var} T_q[const row][k]; V^T written alongside.
-    const int xw = (warp - 4) * 16;
+    const int xw = (warp - W_VG0) * 16;
     constexpr int C = KB / 4, NB = (4 * C) / 32;
     const int c = lane % C;
     const bool kok = c * 4 < a.K;
@@ -881,7 +947,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
       }
       const int vs = t % NV;
       mbar_wait_relaxed(vraw_full + 8 * vs, (t / NV) & 1, 96);
-      if (warp == 4 && lane == 0) trace_ev(a, t, EV_VG_START);
+      if (warp == W_VG0 && lane == 0) trace_ev(a, t, EV_VG_START);
       unsigned char* vrow = gV + vs * V_STAGE_MAX;
 #pragma unroll
       for (int i = 0; i < NB; ++i) {
@@ -893,16 +959,18 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
           const float2 hi = __fmul2_rn(make_float2(f.z, f.w), make_float2(cst.z, cst.w));
           p[r] = make_float4(lo.x, lo.y, hi.x, hi.y);
         }
-        vblock_store<KB>(vrow, vo.vb[i], vo.cx[i], vo.vtb[i], vo.xc[i], kok ? 0xfu : 0u, p);
+        if (!(a.dbg & 128))   // dbg 128: timing experiment without the V / V^T stores
+          vblock_store<KB>(vrow, vo.vb[i], vo.cx[i], vo.vtb[i], vo.xc[i], kok ? 0xfu : 0u, p);
       }
+      if (warp == W_VG0 && lane == 0) trace_ev(a, t, EV_VG_ISSUED);
       fence_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(v_full + 8 * vs);
-      if (warp == 4 && lane == 0) trace_ev(a, t, EV_VG_DONE);
+      if (warp == W_VG0 && lane == 0) trace_ev(a, t, EV_VG_DONE);
     }
-  } else if (warp >= 4 && warp < 4 + NVG) {
+  } else if (warp >= W_VG0 && warp < W_VG0 + NVG) {
     // ------------------------------------------------------------ column operand V (Khatri-Rao)
-    const int xw = (warp - 4) * 16;
+    const int xw = (warp - W_VG0) * 16;
     VTile<KB> cur, nxt;
     int toff_c[kMaxTabs], toff_n[kMaxTabs];
     Odo odo;
@@ -911,41 +979,44 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
     if (T > 0) vtile_issue<KB>(a, t_begin, xw, lane, cur, toff_c, odo);
     for (int t = 0; t < T; ++t) {
       if (t + 1 < T) vtile_issue<KB>(a, t_begin + t + 1, xw, lane, nxt, toff_n, odo);   // next tile's rows in flight
-      if (warp == 4 && lane == 0) trace_ev(a, t, EV_VG_ISSUED);
+      if (warp == W_VG0 && lane == 0) trace_ev(a, t, EV_VG_ISSUED);
       const int vs = t % NV;
       mbar_wait_relaxed(v_empty + 8 * vs, ((t / NV) & 1) ^ 1);
-      if (warp == 4 && lane == 0) trace_ev(a, t, EV_VG_START);
+      if (warp == W_VG0 && lane == 0) trace_ev(a, t, EV_VG_START);
       vtile_store<KB>(a, xw, lane, cur, toff_c, gV + vs * V_STAGE_MAX, vo);
       fence_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(v_full + 8 * vs);
-      if (warp == 4 && lane == 0) trace_ev(a, t, EV_VG_DONE);
+      if (warp == W_VG0 && lane == 0) trace_ev(a, t, EV_VG_DONE);
       cur = nxt;
 #pragma unroll
       for (int q = 0; q < kMaxTabs; ++q) toff_c[q] = toff_n[q];
     }
-  } else if (warp >= 8) {
+  } else if (warp >= W_EW0 && warp < W_EW0 + NEW) {
     // ------------------------------------------------------------ elementwise + epilogue
-    const int ew = tid - 256;              // 0..255
-    const int g = ew >> 7;                 // column half of the tile (32 columns)
+    const int ew = tid - W_EW0 * 32;       // 0..511
+    const int cg = (warp - W_EW0) >> 2;    // column group: tile columns [16 cg, 16 cg + 16)
     const int qd = warp & 3;               // TMEM lane quarter
     const int m = qd * 32 + lane;          // row within the block (= TMEM lane)
     const uint32_t lane_off = (uint32_t)(qd * 32) << 16;
     const int64_t row = row0 + m;
     const bool row_ok = m < rows_here;
-    // U -> TMEM, split hi (g = 0) / lo (g = 1)
+    constexpr int NCH = KB / 16;           // 16-column chunks of U_hi (and of U_lo, N, D)
+    // U -> TMEM, split hi / lo: the 2 NCH chunks are shared out among the 4 column groups
     {
 #pragma unroll 1
-      for (int h = 0; h < KB / 16; ++h) {
+      for (int c = cg * (2 * NCH / 4); c < (cg + 1) * (2 * NCH / 4); ++c) {
+        const bool lo = c >= NCH;
+        const int h = lo ? c - NCH : c;
         uint32_t r[16];
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
           const int k = h * 16 + j;
           const float u = (row_ok && k < a.K) ? __ldg(a.U + row * a.K + k) : 0.f;
           const uint32_t hi = tf32_bits(u);
-          r[j] = g == 0 ? hi : tf32_bits(u - __uint_as_float(hi));
+          r[j] = lo ? tf32_bits(u - __uint_as_float(hi)) : hi;
         }
-        tmem_st16((g == 0 ? tUh : tUl) + lane_off + h * 16, r);
+        tmem_st16((lo ? tUl : tUh) + lane_off + h * 16, r);
       }
       tmem_st_wait();
       tc_fence_before();
@@ -965,76 +1036,82 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
       const int64_t crem = cext - (int64_t)tin * BN;
       const int cols_here = (int)(crem < BN ? crem : BN);
       const int st = t % NS;
-      const uint32_t tb = tmem + 128 * b + lane_off + 32 * g;   // S / P_a columns of this thread
+      const uint32_t tc = tmem + 128 * b + lane_off + 16 * cg;   // S / P_a columns of this warp
       mbar_spin(s_full + 8 * b, (t >> 1) & 1);
-      if (warp == 8 && lane == 0) trace_ev(a, t, EV_EW_S);
+      if (warp == W_EW0 && lane == 0) trace_ev(a, t, EV_EW_S);
       tc_fence_after();
       float lsum = 0.f;
+      uint32_t sv[16], pb[16];
+      float yv[16];
+      uint32_t mk[4] = {0u, 0u, 0u, 0u};
+      tmem_ld16(tc, sv);
       mbar_spin(y_full + 8 * st, (t / NS) & 1);
-      if (warp == 8 && lane == 0) trace_ev(a, t, EV_EW_Y);
-      // two half-steps of 16 columns through ONE code instance (I-cache)
-#pragma unroll 1
-      for (int h = 0; h < 2; ++h) {
-        const uint32_t tc = tb + 16 * h;
-        uint32_t sv[16], pb[16];
-        float yv[16];
-        uint32_t mk[4];
-        tmem_ld16(tc, sv);
-        ew_load_y(a, gY + st * Y_STAGE, gM + st * M_STAGE, g, h, m, yv, mk);
-        tmem_ld_wait(sv);
-        if (h == 1) {
-          __syncwarp();
-          if (lane == 0) mbar_arrive(y_empty + 8 * st);  // Y / mask stage fully read
-        }
-        ew_half<KIND>(a, sv, yv, mk, cols_here - 32 * g - 16 * h, row_ok, pb, lsum, cnt);
-        if (a.mode != 2) {
-          tmem_st16(tc, sv);
-          tmem_st16(tc + 64, pb);
-        }
-        if (a.debug && blockIdx.x == 0 && blockIdx.y == 0 && t == 0) {
+      if (warp == W_EW0 && lane == 0) trace_ev(a, t, EV_EW_Y);
+      ew_load_y(a, gY + st * Y_STAGE, gM + st * M_STAGE, cg >> 1, cg & 1, m, yv, mk);   // (MM == 0: a.has_mask = 0)
+      tmem_ld_wait(sv);
+      __syncwarp();
+      if (lane == 0) mbar_arrive(y_empty + 8 * st);  // Y / mask stage read by this warp
+      if (!(a.dbg & 256)) {
+        if (MM == 1) ew_half<KIND>(a, sv, yv, mk, cols_here - 16 * cg, row_ok, pb, lsum, cnt);
+        else ew_half_sent<KIND>(a, sv, yv, cols_here - 16 * cg, row_ok, pb, lsum, cnt);
+      } else {   // dbg 256: timing experiment without the elementwise math (P_b = S + Y)
 #pragma unroll
-          for (int j = 0; j < 16; ++j) a.debug[m * 64 + 32 * g + 16 * h + j] = __uint_as_float(sv[j] & 0xffffe000u);
-        }
+        for (int j = 0; j < 16; ++j) pb[j] = sv[j] + __float_as_uint(yv[j]) + mk[j >> 2];
       }
-      if (warp == 8 && lane == 0) trace_ev(a, t, EV_EW_HALF);
+      if (a.mode != 2) {
+        tmem_st16(tc, sv);
+        tmem_st16(tc + 64, pb);
+      }
+      if (a.debug && blockIdx.x == 0 && blockIdx.y == 0 && t == 0) {
+#pragma unroll
+        for (int j = 0; j < 16; ++j) a.debug[m * 64 + 16 * cg + j] = __uint_as_float(sv[j] & 0xffffe000u);
+      }
+      if (warp == W_EW0 && lane == 0) trace_ev(a, t, EV_EW_HALF);
       if (a.mode != 2) tmem_st_wait();
       if (a.mode != 0) loss_acc += (double)lsum;
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(p_full + 8 * b);      // P(t) in TMEM (or, loss only: S(t) consumed)
-      if (warp == 8 && lane == 0) trace_ev(a, t, EV_EW_DONE);
+      if (warp == W_EW0 && lane == 0) trace_ev(a, t, EV_EW_DONE);
+      if (lane == 0) trace_ev(a, t, 16 + warp - W_EW0);     // per-warp arrival (diagnostics)
     }
-    // epilogue: N (g = 0) / D (g = 1) for this lane -> split partials
+    // epilogue: N | D (2 NCH chunks of 16 columns, shared out among the column groups) -> split
+    // partials
     if (a.mode != 2) {
       const int64_t elems = a.n_rows * (int64_t)a.K;
-      float* out = a.Qpart + ch * 2 * elems + (int64_t)g * elems;
       if (T > 0) {
-        mbar_wait(nd_full, 0);
+        mbar_spin(nd_full, 0);
         tc_fence_after();
+      }
 #pragma unroll 1
-        for (int h = 0; h < KB / 16; ++h) {
-          uint32_t r[16];
-          tmem_ld16((g == 0 ? tNa : tNb) + lane_off + h * 16, r);
+      for (int c = cg * (2 * NCH / 4); c < (cg + 1) * (2 * NCH / 4); ++c) {
+        const int which = c >= NCH ? 1 : 0;
+        const int h = which ? c - NCH : c;
+        float* out = a.Qpart + ch * 2 * elems + (int64_t)which * elems;
+        uint32_t r[16];
+        if (T > 0) {
+          tmem_ld16((which ? tNb : tNa) + lane_off + h * 16, r);
           tmem_ld_wait(r);
-          if (row_ok) {
+        } else {
 #pragma unroll
-            for (int j = 0; j < 16; ++j)
-              if (h * 16 + j < a.K) out[row * a.K + h * 16 + j] = __uint_as_float(r[j]);
-          }
+          for (int j = 0; j < 16; ++j) r[j] = 0u;
         }
-      } else if (row_ok) {
-        for (int k = 0; k < a.K; ++k) out[row * a.K + k] = 0.f;
+        if (row_ok) {
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            if (h * 16 + j < a.K) out[row * a.K + h * 16 + j] = __uint_as_float(r[j]);
+        }
       }
     } else if (T > 0) {
-      mbar_wait(nd_full, 0);
+      mbar_spin(nd_full, 0);
     }
     if (a.mode != 0) {
       gRed[ew] = loss_acc;
       gRedC[ew] = cnt;
-      asm volatile("bar.sync 1, 256;" ::: "memory");
-      for (int w = 128; w > 0; w >>= 1) {
+      asm volatile("bar.sync 1, %0;" ::"n"(NEW * 32) : "memory");
+      for (int w = NEW * 16; w > 0; w >>= 1) {
         if (ew < w) { gRed[ew] += gRed[ew + w]; gRedC[ew] += gRedC[ew + w]; }
-        asm volatile("bar.sync 1, 256;" ::: "memory");
+        asm volatile("bar.sync 1, %0;" ::"n"(NEW * 32) : "memory");
       }
       if (ew == 0) {
         const int64_t id = (int64_t)blockIdx.y * gridDim.x + blockIdx.x;
@@ -1045,7 +1122,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 1) {
+  if (warp == W_MMA) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
   }
@@ -1075,26 +1152,28 @@ static bool encode(CUtensorMap* tm, CUtensorMapDataType dt, int rank, const void
 struct TcLauncher {
   const Params& P;
   dim3 grid;
-  size_t smem;
   cudaStream_t s;
   int KB;
+  int MM;
+  template <int KB_, int KIND, int MM_>
+  cudaError_t go() const {
+    const size_t smem = smem_bytes(MM_);
+    cudaError_t e = cudaFuncSetAttribute(fused_tc_kernel<KB_, KIND, MM_>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    fused_tc_kernel<KB_, KIND, MM_><<<grid, NTHREADS, smem, s>>>(P);
+    return cudaGetLastError();
+  }
   template <int KIND>
   cudaError_t operator()() const {
-    cudaError_t e;
-    if (KB == 32) {
-      e = cudaFuncSetAttribute(fused_tc_kernel<32, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      if (e != cudaSuccess) return e;
-      fused_tc_kernel<32, KIND><<<grid, NTHREADS, smem, s>>>(P);
-    } else {
-      e = cudaFuncSetAttribute(fused_tc_kernel<64, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      if (e != cudaSuccess) return e;
-      fused_tc_kernel<64, KIND><<<grid, NTHREADS, smem, s>>>(P);
-    }
-    return cudaGetLastError();
+    if (KB == 32) return MM ? go<32, KIND, 1>() : go<32, KIND, 0>();
+    return MM ? go<64, KIND, 1>() : go<64, KIND, 0>();
   }
 };
 
-size_t smem_bytes() { return 1024 + NS * (Y_STAGE + M_STAGE) + NV * V_STAGE_MAX + 256 + 64 + 256 * 16; }
+size_t smem_bytes(int mm) {
+  const int nv = mm == 1 ? VStages<1>::value : VStages<0>::value;
+  return 1024 + NS * Y_STAGE + (mm == 1 ? NS * M_STAGE : 0) + nv * V_STAGE_MAX + 256 + 64;
+}
 
 cudaError_t launch(const TcArgs& args, const float* Y, const uint8_t* M, int64_t row_blocks, int64_t chunks,
                    cudaStream_t s) {
@@ -1144,9 +1223,8 @@ cudaError_t launch(const TcArgs& args, const float* Y, const uint8_t* M, int64_t
   }
   if (!ok) return cudaErrorInvalidValue;
   P.a.has_mask = M ? 1 : 0;
-  const size_t smem = smem_bytes();
   dim3 grid((unsigned)row_blocks, (unsigned)chunks);
-  return dispatch_ew(args.dv.kind, TcLauncher{P, grid, smem, s, args.KB});
+  return dispatch_ew(args.dv.kind, TcLauncher{P, grid, s, args.KB, M ? 1 : 0});
 }
 
 }  // namespace tc

@@ -50,7 +50,7 @@ struct TcArgs {
                               // 2 numerator B as K-major, 4 swap LBO/SBO of the MN-major view
 };
 
-size_t smem_bytes();
+size_t smem_bytes(int mm);   // mm: 1 = uint8 mask stream, 0 = none / NaN-sentinel Y
 cudaError_t launch(const TcArgs& args, const float* Y, const uint8_t* M, int64_t row_blocks, int64_t chunks,
                    cudaStream_t s);
 

@@ -116,6 +116,7 @@ struct Plan {
   int64_t n_local = 0;               // local entries
   size_t ws_bytes = 0;
   int64_t ws_trace = 0;              // fp64 trace accumulators
+  int64_t ws_sent = 0;               // NaN-sentinel copy of Y (nef_fit with a mask)
   // sharding
   int shard_mode = -1, rank = 0, world = 1;
   int64_t local_begin = 0, local_len = 0;

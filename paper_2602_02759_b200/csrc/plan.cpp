@@ -558,7 +558,9 @@ int lower_all(Plan& p, std::string& err) {
     p.low[ell] = std::move(L);
   }
   p.ws_trace = (ws + 255) / 256 * 256;
-  p.ws_bytes = (size_t)(p.ws_trace + (int64_t)8 * 4096 + 256);
+  // NaN-sentinel copy of the local Y (nef_fit with a mask, R5): 4 B per local entry
+  p.ws_sent = (p.ws_trace + (int64_t)8 * 4096 + 256 + 255) / 256 * 256;
+  p.ws_bytes = (size_t)(p.ws_sent + p.n_local * 4 + 256);
   return NEF_OK;
 }
 

@@ -13,12 +13,13 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="c3")
 ap.add_argument("--policies", default="0,1")
 ap.add_argument("--reps", type=int, default=3)
+ap.add_argument("--nomask", action="store_true")
 args = ap.parse_args()
 cfg = CONFIGS[args.config]
 d = generate_torch(args.config, torch.device("cuda"))
 plan = nef.Plan(cfg.model, cfg.shape, cfg.ranks)
 desc = plan.describe()
-Y, M, F = d["Y"], d["mask"], d["init"]
+Y, M, F = d["Y"], (None if args.nomask else d["mask"]), d["init"]
 res = {}
 for pol in [int(p) for p in args.policies.split(",")]:
     nef.nef_set_kernel_policy(pol)

@@ -21,12 +21,13 @@ d = generate_torch(args.config, torch.device("cuda"))
 plan = nef.Plan(cfg.model, cfg.shape, cfg.ranks)
 F = [f.clone() for f in d["init"]]
 plan.update(args.ell, d["Y"], d["mask"], cfg.alpha, cfg.beta, F)
-tr = torch.zeros(1024 * 16, dtype=torch.int64, device="cuda")
+tr = torch.zeros(1024 * 32, dtype=torch.int64, device="cuda")
 nef.nef_debug_trace(tr)
 plan.update(args.ell, d["Y"], d["mask"], cfg.alpha, cfg.beta, F)
 torch.cuda.synchronize()
 nef.nef_debug_trace(None)
-t = tr.cpu().numpy().reshape(1024, 16)[:, :len(EV)].astype(np.int64)
+full = tr.cpu().numpy().reshape(1024, 32).astype(np.int64)
+t = full[:, :len(EV)]
 valid = (t[:, EV.index("EW_DONE")] > 0).sum()
 print("tiles traced", valid)
 lo, hi = args.first, min(args.first + args.n, valid - 1)
@@ -37,6 +38,13 @@ for i in range(lo, hi):
 per = np.diff(t[lo:hi + 1, EV.index("EW_DONE")])
 print("cycles per tile (EW_DONE to EW_DONE): median %d" % np.median(per))
 for a_, b_ in [("MMA1", "EW_S"), ("EW_S", "EW_PEMPTY"), ("EW_PEMPTY", "EW_DONE"), ("EW_DONE", "MMA23"),
-               ("VG_START", "VG_DONE"), ("VG_DONE", "MMA1"), ("TMA", "EW_Y")]:
+               ("VG_START", "VG_DONE"), ("VG_START", "VG_ISSUED"), ("VG_ISSUED", "VG_DONE"), ("VG_DONE", "MMA1"),
+               ("TMA", "EW_Y")]:
     dd = t[lo:hi, EV.index(b_)] - t[lo:hi, EV.index(a_)]
     print("%10s -> %-10s median %7d" % (a_, b_, np.median(dd)))
+
+ew = full[lo:hi, 16:24]
+print("per-EW-warp arrival on p_full relative to warp 8 (rows = tiles, cols = warps 8..15):")
+for i in range(ew.shape[0]):
+    print("%4d " % (lo + i) + " ".join("%6d" % (ew[i, j] - ew[i, 0]) for j in range(8)))
+print("median lag per warp:", [int(np.median(ew[:, j] - ew[:, 0])) for j in range(8)])
