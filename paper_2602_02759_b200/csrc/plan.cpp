@@ -291,7 +291,7 @@ void finish_lowering(const Plan& p, Lowering& L, Bump& bump) {
     // no direct-V run with the component tables: merge every column factor into ONE table
     // over all column modes (consecutive rows for every tile) when that table is small
     // (L2-resident; its generation is a few microseconds)
-    if (L.vd_tab < 0 && L.tabs.size() >= 1 && L.n_cols * L.K <= ((int64_t)4 << 20)) {
+    if (L.vd_tab < 0 && L.tabs.size() >= 1 && L.n_cols * L.K <= ((int64_t)8 << 20)) {
       build_tables(p, L, bump, true);
       direct_run(L);
     }

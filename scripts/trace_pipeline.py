@@ -43,8 +43,8 @@ for a_, b_ in [("MMA1", "EW_S"), ("EW_S", "EW_PEMPTY"), ("EW_PEMPTY", "EW_DONE")
     dd = t[lo:hi, EV.index(b_)] - t[lo:hi, EV.index(a_)]
     print("%10s -> %-10s median %7d" % (a_, b_, np.median(dd)))
 
-ew = full[lo:hi, 16:24]
-print("per-EW-warp arrival on p_full relative to warp 8 (rows = tiles, cols = warps 8..15):")
+ew = full[lo:hi, 16:32]
+print("per-EW-warp arrival on p_full relative to EW warp 0 (rows = tiles, cols = EW warps 0..15):")
 for i in range(ew.shape[0]):
-    print("%4d " % (lo + i) + " ".join("%6d" % (ew[i, j] - ew[i, 0]) for j in range(8)))
-print("median lag per warp:", [int(np.median(ew[:, j] - ew[:, 0])) for j in range(8)])
+    print("%4d " % (lo + i) + " ".join("%5d" % (ew[i, j] - ew[i, 0]) for j in range(16)))
+print("median lag per warp:", [int(np.median(ew[:, j] - ew[:, 0])) for j in range(16)])
