@@ -166,6 +166,7 @@ __device__ __forceinline__ float kl_loss(float x, float y) {
 // sm_100 (FMUL2: one issue slot for two products).
 template <int KIND>
 struct Ew {
+  static constexpr bool kLinX = false;   // a = x * (positive factor)
   static __device__ __forceinline__ void ab(float x, float yh, const DivParams& d, float& av, float& bv) {
     const float2 r = ab_entry_ool(x, yh, d);
     av = r.x;
@@ -184,7 +185,8 @@ struct Ew {
 };
 
 template <>
-struct Ew<EW_KL> {   // (1, 0): a = x / y, b = 1
+struct Ew<EW_KL> {  // (1, 0): a = x / y, b = 1
+  static constexpr bool kLinX = true;   // a = x * (positive factor)
   static __device__ __forceinline__ void ab(float x, float yh, const DivParams&, float& av, float& bv) {
     av = x * frcp(yh);
     bv = 1.f;
@@ -209,6 +211,7 @@ struct Ew<EW_KL> {   // (1, 0): a = x / y, b = 1
 
 template <>
 struct Ew<EW_EUC> {  // (1, 1): a = x, b = y
+  static constexpr bool kLinX = true;   // a = x * (positive factor)
   static __device__ __forceinline__ void ab(float x, float yh, const DivParams&, float& av, float& bv) {
     av = x;
     bv = yh;
@@ -230,6 +233,7 @@ struct Ew<EW_EUC> {  // (1, 1): a = x, b = y
 
 template <>
 struct Ew<EW_B_M05> {  // (1, -0.5): a = x y^-3/2, b = y^-1/2; L = 2 (sqrt x - sqrt y)^2 / sqrt y
+  static constexpr bool kLinX = true;   // a = x * (positive factor)
   static __device__ __forceinline__ void ab(float x, float yh, const DivParams&, float& av, float& bv) {
     const float r = frsqrt(yh);
     bv = r;
@@ -259,6 +263,7 @@ struct Ew<EW_B_M05> {  // (1, -0.5): a = x y^-3/2, b = y^-1/2; L = 2 (sqrt x - s
 
 template <>
 struct Ew<EW_A05_B0> {  // (0.5, 0): a = sqrt(x) / y, b = y^-1/2; L = 4 y^1/2 f(log(x/y)/2)
+  static constexpr bool kLinX = false;   // a = x * (positive factor)
   static __device__ __forceinline__ void ab(float x, float yh, const DivParams&, float& av, float& bv) {
     const float r = frsqrt(yh);
     bv = r;
@@ -296,6 +301,7 @@ struct Ew<EW_A05_B0> {  // (0.5, 0): a = sqrt(x) / y, b = y^-1/2; L = 4 y^1/2 f(
 
 template <>
 struct Ew<EW_B05> {  // (1, 0.5): a = x y^-1/2, b = y^1/2
+  static constexpr bool kLinX = true;   // a = x * (positive factor)
   static __device__ __forceinline__ void ab(float x, float yh, const DivParams&, float& av, float& bv) {
     const float r = frsqrt(yh);
     av = x * r;
@@ -315,6 +321,7 @@ struct Ew<EW_B05> {  // (1, 0.5): a = x y^-1/2, b = y^1/2
 
 template <>
 struct Ew<EW_B2> {  // (1, 2): a = x y, b = y^2
+  static constexpr bool kLinX = true;   // a = x * (positive factor)
   static __device__ __forceinline__ void ab(float x, float yh, const DivParams&, float& av, float& bv) {
     av = x * yh;
     bv = yh * yh;
@@ -333,6 +340,7 @@ struct Ew<EW_B2> {  // (1, 2): a = x y, b = y^2
 
 template <>
 struct Ew<EW_A05_B1> {  // (0.5, 1): a = sqrt(x), b = sqrt(y)
+  static constexpr bool kLinX = false;   // a = x * (positive factor)
   static __device__ __forceinline__ void ab(float x, float yh, const DivParams&, float& av, float& bv) {
     av = fsqrt(x);
     bv = fsqrt(yh);

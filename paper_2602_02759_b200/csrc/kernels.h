@@ -56,7 +56,7 @@ cudaError_t launch_fused_ffma(const FusedArgs& a, cudaStream_t s);
 // Small einsum step (C = sum A*B, optional B), fp64 accumulation
 cudaError_t launch_einstep(const EinStep& st, const float* A, const float* B, float* C, cudaStream_t s);
 
-// out[i] = M[i] ? Y[i] : NaN  (the NaN-sentinel copy of Y; M nonzero = observed)
+// out[i] = M[i] ? Y[i] + 0 : -1  (the sentinel copy of Y; M nonzero = observed; observed data >= 0)
 cudaError_t launch_sentinel(const float* Y, const uint8_t* M, float* out, int64_t n, cudaStream_t s);
 
 // dst[r][0..Kp) = src[r][0..K) padded with zeros (16-byte row pitch for TMA)

@@ -406,21 +406,21 @@ cudaError_t launch_einstep(const EinStep& st, const float* A, const float* B, fl
 // fully coalesced across the warp
 __global__ void sentinel_kernel(const float* __restrict__ Y, const uint8_t* __restrict__ M, float* __restrict__ out,
                                 long long n4) {
-  const float nan = __uint_as_float(0x7fc00000u);
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4; i += (long long)gridDim.x * blockDim.x) {
     const uint32_t w = __ldcs(reinterpret_cast<const unsigned int*>(M) + i);
     float4 y = __ldcs(reinterpret_cast<const float4*>(Y) + i);
-    y.x = (w & 0xffu) ? y.x : nan;
-    y.y = (w & 0xff00u) ? y.y : nan;
-    y.z = (w & 0xff0000u) ? y.z : nan;
-    y.w = (w & 0xff000000u) ? y.w : nan;
+    // observed: + 0 turns -0 into +0 (the kernel reads the sign); missing: -1
+    y.x = (w & 0xffu) ? y.x + 0.f : -1.f;
+    y.y = (w & 0xff00u) ? y.y + 0.f : -1.f;
+    y.z = (w & 0xff0000u) ? y.z + 0.f : -1.f;
+    y.w = (w & 0xff000000u) ? y.w + 0.f : -1.f;
     __stcs(reinterpret_cast<float4*>(out) + i, y);
   }
 }
 __global__ void sentinel_tail_kernel(const float* __restrict__ Y, const uint8_t* __restrict__ M, float* __restrict__ out,
                                      long long from, long long n) {
   for (long long i = from + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
-    out[i] = M[i] ? Y[i] : __uint_as_float(0x7fc00000u);
+    out[i] = M[i] ? Y[i] + 0.f : -1.f;
 }
 
 __global__ void pad_rows_kernel(const float* __restrict__ src, float* __restrict__ dst, long long rows, int K, int Kp) {

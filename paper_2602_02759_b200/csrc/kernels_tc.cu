@@ -145,6 +145,21 @@ __device__ __forceinline__ void mbar_wait_mma(uint32_t bar, uint32_t parity) {
   mbar_spin(bar, parity);
 #endif
 }
+// Elementwise warps waiting for S: sixteen of them polling would take the issue slots the V
+// generator and the other elementwise warps need (NEF_EW_WAIT: 0 spin, 1 suspend-hint wait,
+// else nanoseconds of sleep between polls)
+#ifndef NEF_EW_WAIT
+#define NEF_EW_WAIT 32
+#endif
+__device__ __forceinline__ void mbar_wait_ew(uint32_t bar, uint32_t parity) {
+#if NEF_EW_WAIT == 0
+  mbar_spin(bar, parity);
+#elif NEF_EW_WAIT == 1
+  mbar_wait(bar, parity);
+#else
+  mbar_wait_relaxed(bar, parity, NEF_EW_WAIT);
+#endif
+}
 __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* tm, int c0, int c1, uint32_t bar) {
   asm volatile(
       "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
@@ -418,6 +433,25 @@ __device__ __forceinline__ void vblock_store(unsigned char* vrow, int vb, int cx
     *reinterpret_cast<uint4*>(vrow + vtb + e * 128 + ((xc ^ e) << 4)) = make_uint4(w[0][e], w[1][e], w[2][e], w[3][e]);
 }
 
+// Direct path: bonds beyond K are TMA zero fill times a zero constant row, rows beyond the
+// table are zero fill, so no masking; + half a TF32 ulp = RN of what the tensor core truncates
+template <int KB>
+__device__ __forceinline__ void vblock_store_direct(unsigned char* vrow, int vb, int cx, int vtb, int xc,
+                                                    const float4 (&p)[4]) {
+  uint32_t w[4][4];
+#pragma unroll
+  for (int r = 0; r < 4; ++r) {
+    w[r][0] = __float_as_uint(p[r].x) + 0x1000u;
+    w[r][1] = __float_as_uint(p[r].y) + 0x1000u;
+    w[r][2] = __float_as_uint(p[r].z) + 0x1000u;
+    w[r][3] = __float_as_uint(p[r].w) + 0x1000u;
+    *reinterpret_cast<uint4*>(vrow + vb + r * 128 + ((cx ^ r) << 4)) = make_uint4(w[r][0], w[r][1], w[r][2], w[r][3]);
+  }
+#pragma unroll
+  for (int e = 0; e < 4; ++e)
+    *reinterpret_cast<uint4*>(vrow + vtb + e * 128 + ((xc ^ e) << 4)) = make_uint4(w[0][e], w[1][e], w[2][e], w[3][e]);
+}
+
 // Slow paths (several varying tables, or non-vectorisable tables), out of line so the fast
 // path keeps its registers.
 template <int KB>
@@ -586,22 +620,24 @@ __device__ __forceinline__ void ew_half(const TcArgs& a, uint32_t (&sv)[16], con
   }
 }
 
-// The same without a mask stream: a missing entry carries NaN in Y (the NaN-sentinel copy nef_fit
-// makes once per fit, R5), and every NaN propagates through a (which has a factor of x)
-// and through b' = x * 0 + b, so max(., 0) - which returns 0 for NaN - zeroes both.  Entries
-// outside the tile's valid rows / columns (TMA zero fill) are turned into NaN first.
+// The same without a mask stream: a missing entry carries -1 in Y (the sentinel copy nef_fit
+// makes once per fit, R5; observed data are >= +0).  a has the sign of x (directly, or
+// by a copysign for the sqrt forms) and b gets it by a copysign, so one add-then-max per value,
+// max(bits + 0x1000, 0), both rounds (TF32 RN of the value the tensor core truncates) and zeroes
+// the missing entries.  Entries outside the tile's valid rows / columns (TMA zero fill) are
+// turned into -1 first.
 template <int KIND>
 __device__ __forceinline__ void ew_half_sent(const TcArgs& a, uint32_t (&sv)[16], float (&yv)[16], int cv, bool row_ok,
                                              uint32_t (&pb)[16], float& lsum, long long& cnt) {
   const uint32_t vbits = (!row_ok || cv <= 0) ? 0u : (cv >= 16 ? 0xffffu : ((1u << cv) - 1u));
   if (vbits != 0xffffu) {
 #pragma unroll
-    for (int j = 0; j < 16; ++j) yv[j] = ((vbits >> j) & 1u) ? yv[j] : __uint_as_float(0x7fc00000u);
+    for (int j = 0; j < 16; ++j) yv[j] = ((vbits >> j) & 1u) ? yv[j] : -1.f;
   }
   if (a.mode != 0) {   // loss of the iterate entering the sweep (uniform branch)
 #pragma unroll
     for (int j = 0; j < 16; j += 2) {
-      const bool o0 = yv[j] == yv[j], o1 = yv[j + 1] == yv[j + 1];
+      const bool o0 = yv[j] >= 0.f, o1 = yv[j + 1] >= 0.f;
       const float2 yh = make_float2(fmaxf(__uint_as_float(sv[j]), 1e-30f), fmaxf(__uint_as_float(sv[j + 1]), 1e-30f));
       float2 av, bv, lv;
       Ew<KIND>::abl2(make_float2(o0 ? yv[j] : 1.f, o1 ? yv[j + 1] : 1.f), yh, a.dv, av, bv, lv);
@@ -619,12 +655,16 @@ __device__ __forceinline__ void ew_half_sent(const TcArgs& a, uint32_t (&sv)[16]
     const float2 x = make_float2(yv[j], yv[j + 1]);
     const float2 yh = make_float2(fmaxf(__uint_as_float(sv[j]), 1e-30f), fmaxf(__uint_as_float(sv[j + 1]), 1e-30f));
     float2 av, bv;
-    Ew<KIND>::ab2(x, yh, a.dv, av, bv);
-    bv = __ffma2_rn(x, make_float2(0.f, 0.f), bv);   // NaN at missing entries
-    sv[j] = __float_as_uint(fmaxf(av.x, 0.f)) + 0x1000u;
-    sv[j + 1] = __float_as_uint(fmaxf(av.y, 0.f)) + 0x1000u;
-    pb[j] = __float_as_uint(fmaxf(bv.x, 0.f)) + 0x1000u;
-    pb[j + 1] = __float_as_uint(fmaxf(bv.y, 0.f)) + 0x1000u;
+    if (Ew<KIND>::kLinX) {
+      Ew<KIND>::ab2(x, yh, a.dv, av, bv);   // a = x * (positive): carries the sign of x
+    } else {
+      Ew<KIND>::ab2(make_float2(fabsf(x.x), fabsf(x.y)), yh, a.dv, av, bv);
+      av = make_float2(copysignf(av.x, x.x), copysignf(av.y, x.y));
+    }
+    sv[j] = (uint32_t)__viaddmax_s32(__float_as_int(av.x), 0x1000, 0);
+    sv[j + 1] = (uint32_t)__viaddmax_s32(__float_as_int(av.y), 0x1000, 0);
+    pb[j] = (uint32_t)__viaddmax_s32(__float_as_int(copysignf(bv.x, x.x)), 0x1000, 0);
+    pb[j + 1] = (uint32_t)__viaddmax_s32(__float_as_int(copysignf(bv.y, x.y)), 0x1000, 0);
   }
 }
 
@@ -729,8 +769,14 @@ enum TraceEv : int {
   EV_TMA_ISSUE = 0, EV_VG_START, EV_VG_DONE, EV_MMA1_ISSUE, EV_MMA23_ISSUE, EV_EW_S, EV_EW_Y, EV_EW_HALF,
   EV_EW_DONE, EV_VG_ISSUED
 };
+// compiled in only with -DNEF_TRACE=1 (scripts/build_variants.sh): the checks cost issue slots
+#ifndef NEF_TRACE
+#define NEF_TRACE 0
+#endif
 __device__ __forceinline__ void trace_ev(const TcArgs& a, int t, int e) {
+#if NEF_TRACE
   if (a.trace && blockIdx.x == 0 && blockIdx.y == 0 && t < 1024) a.trace[t * 32 + e] = (long long)clock64();
+#endif
 }
 
 // ------------------------------------------------------------------ the kernel
@@ -922,7 +968,6 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
     const int xw = (warp - W_VG0) * 16;
     constexpr int C = KB / 4, NB = (4 * C) / 32;
     const int c = lane % C;
-    const bool kok = c * 4 < a.K;
     VOff<KB> vo;
     vo.init(xw, lane);
     // the next tile's run is looked up one tile ahead so that a new run's constant rows are in
@@ -960,7 +1005,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
           p[r] = make_float4(lo.x, lo.y, hi.x, hi.y);
         }
         if (!(a.dbg & 128))   // dbg 128: timing experiment without the V / V^T stores
-          vblock_store<KB>(vrow, vo.vb[i], vo.cx[i], vo.vtb[i], vo.xc[i], kok ? 0xfu : 0u, p);
+          vblock_store_direct<KB>(vrow, vo.vb[i], vo.cx[i], vo.vtb[i], vo.xc[i], p);
       }
       if (warp == W_VG0 && lane == 0) trace_ev(a, t, EV_VG_ISSUED);
       fence_async_smem();
@@ -1037,7 +1082,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
       const int cols_here = (int)(crem < BN ? crem : BN);
       const int st = t % NS;
       const uint32_t tc = tmem + 128 * b + lane_off + 16 * cg;   // S / P_a columns of this warp
-      mbar_spin(s_full + 8 * b, (t >> 1) & 1);
+      mbar_wait_ew(s_full + 8 * b, (t >> 1) & 1);
       if (warp == W_EW0 && lane == 0) trace_ev(a, t, EV_EW_S);
       tc_fence_after();
       float lsum = 0.f;

@@ -14,7 +14,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libnef.so")
+LIB_PATH = os.environ.get("NEF_LIB") or os.path.join(_HERE, "libnef.so")   # NEF_LIB: diagnostic builds
 
 NEF_STATUS = {0: "OK", 1: "PARSE", 2: "SHAPE", 3: "DOMAIN", 4: "DATA", 5: "ARG", 6: "CUDA", 7: "NCCL",
               8: "UNSUPPORTED"}

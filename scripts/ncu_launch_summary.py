@@ -1,5 +1,6 @@
-"""Summarise an ncu launch list (--metrics gpu__time_duration.sum --csv) per kernel:
-launches, total and mean device time, share of all libnef kernels and of everything.
+"""Summarise an ncu launch list (--metrics gpu__time_duration.sum[,dram__bytes_read.sum,
+dram__bytes_write.sum] --csv) per kernel: launches, total / mean device time, share of all libnef
+kernels, mean DRAM bytes per launch.
 
     python scripts/ncu_launch_summary.py gpurun_out/launches.csv > profiles/rNN_launches.txt
 """
@@ -10,19 +11,32 @@ import sys
 path = sys.argv[1]
 rows = list(csv.reader(l for l in open(path) if not l.startswith("==")))
 hdr = rows[0]
-ki, vi, ui = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
-scale = {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "second": 1e3}
-agg = collections.defaultdict(list)
+ki, mi, vi, ui, ii = (hdr.index(x) for x in ("Kernel Name", "Metric Name", "Metric Value", "Metric Unit", "ID"))
+scale = {"nsecond": 1e-6, "usecond": 1e-3, "msecond": 1.0, "second": 1e3, "ns": 1e-6, "us": 1e-3, "ms": 1.0}
+launch = collections.OrderedDict()
 for r in rows[1:]:
-    agg[r[ki]].append(float(r[vi].replace(",", "")) * scale.get(r[ui], 1e-6))
-ours = {k: v for k, v in agg.items() if k.startswith(("nef::", "tc::", "void tc::", "void nef::"))}
-tot_ours = sum(sum(v) for v in ours.values())
-tot_all = sum(sum(v) for v in agg.values())
+    m = launch.setdefault((int(r[ii]), r[ki]), {})
+    v = float(r[vi].replace(",", ""))
+    if r[mi] == "gpu__time_duration.sum":
+        v *= scale.get(r[ui], 1e-6)
+    elif r[ui] in ("Gbyte", "Mbyte", "Kbyte"):
+        v *= {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3}[r[ui]]
+    m[r[mi]] = v
+agg = collections.defaultdict(list)
+for (i, k), m in launch.items():
+    agg[k].append(m)
+ours = {k for k in agg if k.startswith(("nef::", "tc::", "void tc::", "void nef::")) or "sentinel" in k or "pad_rows" in k}
+t = lambda ms: sum(x.get("gpu__time_duration.sum", 0.0) for x in ms)
+tot_ours = sum(t(v) for k, v in agg.items() if k in ours)
+tot_all = sum(t(v) for v in agg.values())
 print("# %s: %d launches, %.3f ms total; libnef kernels %d launches, %.3f ms" % (
-    path, sum(len(v) for v in agg.values()), tot_all, sum(len(v) for v in ours.values()), tot_ours))
+    path, len(launch), tot_all, sum(len(v) for k, v in agg.items() if k in ours), tot_ours))
 print("# (cold-cache, serialised ncu times: compare shares, not absolutes; non-libnef kernels = "
       "torch input generation outside the timed region)")
-print("%-8s %12s %12s %10s  %s" % ("launches", "total_ms", "mean_ms", "share_nef", "kernel"))
-for k, v in sorted(agg.items(), key=lambda x: -sum(x[1])):
-    share = "%.4f" % (sum(v) / tot_ours) if k in ours else "-"
-    print("%-8d %12.4f %12.5f %10s  %s" % (len(v), sum(v), sum(v) / len(v), share, k[:110]))
+print("%-8s %12s %12s %10s %14s %14s  %s" % ("launches", "total_ms", "mean_ms", "share_nef", "dram_rd_B/launch",
+                                              "dram_wr_B/launch", "kernel"))
+for k, v in sorted(agg.items(), key=lambda x: -t(x[1])):
+    share = "%.4f" % (t(v) / tot_ours) if k in ours else "-"
+    rd = sum(x.get("dram__bytes_read.sum", 0.0) for x in v) / len(v)
+    wr = sum(x.get("dram__bytes_write.sum", 0.0) for x in v) / len(v)
+    print("%-8d %12.4f %12.5f %10s %14.4g %14.4g  %s" % (len(v), t(v), t(v) / len(v), share, rd, wr, k[:100]))

@@ -1,4 +1,6 @@
-"""Print the tcgen05 kernel's per-tile pipeline timeline (CTA (0,0)) for one factor update."""
+"""Print the tcgen05 kernel's per-tile pipeline timeline (CTA (0,0)) for one factor update.
+Needs the -DNEF_TRACE=1 build: scripts/build_variants.sh trace="-DNEF_TRACE=1", then run with
+NEF_LIB=paper_2602_02759_b200/libnef_trace.so (or copy it over libnef.so)."""
 import argparse
 import sys
 
