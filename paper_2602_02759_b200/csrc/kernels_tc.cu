@@ -42,10 +42,23 @@ template <int MM> struct VStages { static constexpr int value = MM == 1 ? 3 : 4;
 // issuer.  The warp schedulers favour higher warp ids, so the producers whose latency is on the
 // critical path sit above the elementwise warps (with the producers below, the V generators
 // and the MMA issuer starved during the elementwise phase of every tile).
+#ifndef NEF_WARP_MAP
+#define NEF_WARP_MAP 0
+#endif
+#if NEF_WARP_MAP == 0
 constexpr int W_EW0 = 0, W_VG0 = 16, W_DV = 20, W_TMA = 21, W_MMA = 22;
+__device__ __forceinline__ int vg_index(int warp) { return warp >= 16 && warp < 20 ? warp - 16 : -1; }
+#else
+// the MMA issuer's sub-partition (2) hosts no V generator: V generators on warps 16, 17, 19, 20
+// (sub-partitions 0, 1, 3, 0), TMA producer 21 (1), MMA issuer 22 (2), V-row loads 23 (3)
+constexpr int W_EW0 = 0, W_VG0 = 16, W_DV = 23, W_TMA = 21, W_MMA = 22;
+__device__ __forceinline__ int vg_index(int warp) {
+  return warp == 16 ? 0 : warp == 17 ? 1 : warp == 19 ? 2 : warp == 20 ? 3 : -1;
+}
+#endif
 constexpr int NVG = 4;       // V-generator warps (16 tile columns each)
 constexpr int NEW = 16;      // elementwise warps: 4 TMEM lane quarters x 4 groups of 16 columns
-constexpr int NTHREADS = 23 * 32;   // 736
+constexpr int NTHREADS = (NEF_WARP_MAP == 0 ? 23 : 24) * 32;
 constexpr int Y_STAGE = BM * BN * 4;      // 32 KB
 constexpr int M_STAGE = BM * BN;          // 8 KB
 constexpr int VT_OFF = BN * 64 * 4;       // V^T copy after V inside a stage
@@ -118,7 +131,17 @@ __device__ __forceinline__ void mbar_spin(uint32_t bar, uint32_t parity) {
 }
 // Producer-side wait (the producer runs ahead of its consumer): poll with a short sleep
 // between tries so the waiting warp leaves the issue slots to the elementwise warps.
+#ifndef NEF_PROD_HINT
+#define NEF_PROD_HINT 1
+#endif
 __device__ __forceinline__ void mbar_wait_relaxed(uint32_t bar, uint32_t parity, uint32_t ns = 256) {
+#if NEF_PROD_HINT
+  // suspend-hint try_wait: the waiting thread sleeps until the phase completes (or the hint
+  // elapses) without polling
+  (void)ns;
+  mbar_wait(bar, parity);
+  return;
+#endif
   uint32_t done = 0;
   for (uint32_t it = 0;; ++it) {
     asm volatile(
@@ -962,10 +985,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
         for (int h = 0; h < KB / 32; ++h) tma_load_2d(sV + vs * V_STAGE_MAX + h * (BN * 128), &P.tmV, 32 * h, rowv, bar);
       }
     }
-  } else if (warp >= W_VG0 && warp < W_VG0 + NVG && a.vdirect) {
+  } else if (vg_index(warp) >= 0 && a.vdirect) {
     // ------------------------------------------------------------ direct V: scale rows in place
     // V[x][k] = T_var[row + x][k] * prod_{q != var} T_q[const row][k]; V^T written alongside.
-    const int xw = (warp - W_VG0) * 16;
+    const int xw = vg_index(warp) * 16;
     constexpr int C = KB / 4, NB = (4 * C) / 32;
     const int c = lane % C;
     VOff<KB> vo;
@@ -1013,9 +1036,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
       if (lane == 0) mbar_arrive(v_full + 8 * vs);
       if (warp == W_VG0 && lane == 0) trace_ev(a, t, EV_VG_DONE);
     }
-  } else if (warp >= W_VG0 && warp < W_VG0 + NVG) {
+  } else if (vg_index(warp) >= 0) {
     // ------------------------------------------------------------ column operand V (Khatri-Rao)
-    const int xw = (warp - W_VG0) * 16;
+    const int xw = vg_index(warp) * 16;
     VTile<KB> cur, nxt;
     int toff_c[kMaxTabs], toff_n[kMaxTabs];
     Odo odo;
