@@ -133,6 +133,14 @@ int nef_fit_host(nef_plan_t plan, const float* Y_host, const uint8_t* mask_host,
 int nef_nccl_unique_id(void* out128);
 int nef_plan_shard(nef_plan_t plan, int rank, int world, const void* nccl_unique_id);
 
+/* The same split without a communicator (host planning only): the plan describes this rank's
+ * local tensor (nef_plan_info: local_begin / local_len; nef_plan_describe: "factor_has_shard",
+ * false = the factor's A|B must be summed over ranks).  nef_num_den then returns this rank's
+ * partial A|B, which the caller all-reduces (e.g. torch.distributed) before nef_apply_update;
+ * nef_fit / nef_update / nef_loss on such a plan with world > 1 return NEF_E_NCCL.
+ * Errors: NEF_E_ARG (bad rank / world, already sharded), NEF_E_SHAPE (largest mode < world). */
+int nef_plan_shard_host(nef_plan_t plan, int rank, int world);
+
 /* Number of kernel launches the last nef_fit / nef_loss / nef_update call enqueued. */
 int64_t nef_last_launch_count(void);
 

@@ -358,6 +358,9 @@ int num_den(const Ctx& c, int ell, const float* Y, const uint8_t* M, const nef::
 
 int allreduce(const nef::Plan& p, void* buf, size_t count, int dtype, cudaStream_t s) {
   if (p.world <= 1) return NEF_OK;
+  if (!p.nccl_comm)
+    return fail(NEF_E_NCCL, "plan sharded without a communicator (nef_plan_shard_host): use nef_num_den, an "
+                            "external all-reduce and nef_apply_update");
   int r = g_nccl.AllReduce(buf, buf, count, dtype, kNcclSum, p.nccl_comm, s);
   if (r != 0) return fail(NEF_E_NCCL, std::string("ncclAllReduce: ") + (g_nccl.GetErrorString ? g_nccl.GetErrorString(r) : "?"));
   return NEF_OK;
@@ -709,7 +712,15 @@ int nef_nccl_unique_id(void* out128) {
   return NEF_OK;
 }
 
+static int shard_impl(nef_plan_t plan, int rank, int world, const void* uid, bool host_only);
+
 int nef_plan_shard(nef_plan_t plan, int rank, int world, const void* uid) {
+  return shard_impl(plan, rank, world, uid, false);
+}
+
+int nef_plan_shard_host(nef_plan_t plan, int rank, int world) { return shard_impl(plan, rank, world, nullptr, true); }
+
+static int shard_impl(nef_plan_t plan, int rank, int world, const void* uid, bool host_only) {
   if (!plan) return fail(NEF_E_ARG, "null plan");
   if (world < 1 || rank < 0 || rank >= world) return fail(NEF_E_ARG, "bad rank/world");
   nef::Plan& p = plan->p;
@@ -723,7 +734,7 @@ int nef_plan_shard(nef_plan_t plan, int rank, int world, const void* uid) {
   int64_t q = n / world, r = n % world;
   int64_t begin = rank * q + std::min<int64_t>(rank, r);
   int64_t len = q + (rank < r ? 1 : 0);
-  if (world > 1) {
+  if (world > 1 && !host_only) {
     if (!uid) return fail(NEF_E_ARG, "null NCCL unique id");
     std::string err;
     if (!load_nccl(err)) return fail(NEF_E_NCCL, err);

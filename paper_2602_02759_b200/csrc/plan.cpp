@@ -660,7 +660,10 @@ std::string describe_plan(const Plan& p) {
   for (size_t l = 0; l < p.einstr.size(); ++l) o << (l ? "," : "") << "\"" << p.einstr[l] << "\"";
   o << "],\"shape\":[";
   for (size_t m = 0; m < p.shape.size(); ++m) o << (m ? "," : "") << p.shape[m];
-  o << "],\"shard_mode\":" << p.shard_mode << ",\"workspace_bytes\":" << p.ws_bytes << ",\"lowerings\":[";
+  o << "],\"shard_mode\":" << p.shard_mode << ",\"rank\":" << p.rank << ",\"world\":" << p.world
+    << ",\"local_begin\":" << p.local_begin << ",\"local_len\":" << p.local_len << ",\"factor_has_shard\":[";
+  for (size_t l = 0; l < p.factor_has_shard.size(); ++l) o << (l ? "," : "") << (p.factor_has_shard[l] ? "true" : "false");
+  o << "],\"workspace_bytes\":" << p.ws_bytes << ",\"lowerings\":[";
   for (size_t l = 0; l < p.low.size(); ++l) {
     const Lowering& L = p.low[l];
     o << (l ? "," : "") << "{\"ell\":" << L.ell << ",\"row_idx\":\"" << L.row_idx << "\",\"col_idx\":\"" << L.col_idx

@@ -51,6 +51,7 @@ def _load():
                                         vp]),
         "nef_nccl_unique_id": (ctypes.c_int, [vp]),
         "nef_plan_shard": (ctypes.c_int, [vp, ctypes.c_int, ctypes.c_int, vp]),
+        "nef_plan_shard_host": (ctypes.c_int, [vp, ctypes.c_int, ctypes.c_int]),
         "nef_last_launch_count": (ctypes.c_int64, []),
         "nef_set_kernel_policy": (ctypes.c_int, [ctypes.c_int]),
         "nef_profile_enable": (ctypes.c_int, [ctypes.c_int]),
@@ -71,7 +72,8 @@ def _load():
 LIB = _load()
 EXPORTED = ("nef_plan", "nef_plan_info", "nef_factor_shape", "nef_local_shape", "nef_plan_describe", "nef_fit",
             "nef_update", "nef_num_den", "nef_apply_update", "nef_loss", "nef_host_scratch_bytes", "nef_fit_host",
-            "nef_nccl_unique_id", "nef_plan_shard", "nef_last_launch_count", "nef_set_kernel_policy",
+            "nef_nccl_unique_id", "nef_plan_shard", "nef_plan_shard_host", "nef_last_launch_count",
+            "nef_set_kernel_policy",
             "nef_profile_enable", "nef_profile_read", "nef_debug_dump", "nef_debug_trace",
             "nef_plan_destroy", "nef_last_error", "nef_version")
 
@@ -202,6 +204,10 @@ def nef_plan_shard(h, rank, world, uid: bytes | None):
     _check(LIB.nef_plan_shard(h, int(rank), int(world), ub))
 
 
+def nef_plan_shard_host(h, rank, world):
+    _check(LIB.nef_plan_shard_host(h, int(rank), int(world)))
+
+
 def nef_last_launch_count() -> int:
     return int(LIB.nef_last_launch_count())
 
@@ -277,6 +283,11 @@ class Plan:
 
     def shard(self, rank, world, uid=None):
         nef_plan_shard(self.h, rank, world, uid)
+        self._ws = None
+
+    def shard_host(self, rank, world):
+        """Host-side split only (no communicator): nef_num_den then returns local partials."""
+        nef_plan_shard_host(self.h, rank, world)
         self._ws = None
 
     def workspace(self, device=None):
