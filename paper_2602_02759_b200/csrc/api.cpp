@@ -291,13 +291,15 @@ int stream_pass(const Ctx& c, const nef::Lowering& L, const float* Y, const uint
       t.vt = e ? std::atoi(e) : 1;
       e = std::getenv("NEF_TC_DBG");
       t.dbg = e ? std::atoi(e) : 0;
+      t.drain_tiles = nef::kDrainTiles;
+      t.n_groups = (tpc + nef::kDrainTiles - 1) / nef::kDrainTiles;
     }
     prof_begin(c.s);
     CK(nef::tc::launch(t, Y, M, L.tc_row_blocks, chunks, c.s));
     prof_end(c.s, bytes);
     ++g_launches;
     o.Qpart = t.Qpart;
-    o.n_chunks = chunks;
+    o.n_chunks = chunks * t.n_groups;
     o.losspart = t.losspart;
     o.countpart = t.countpart;
     return NEF_OK;

@@ -835,7 +835,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
   const uint32_t buf_free = p_full + 16;                     // [2] N,D MMAs of tile t retired (commit)
   const uint32_t nd_full = buf_free + 16, u_ready = nd_full + 8;
   const uint32_t vraw_full = u_ready + 8;                    // NV barriers: direct-V rows landed (TMA)
-  const uint32_t sTmem = vraw_full + 8 * NV;
+  const uint32_t drain_ready = vraw_full + 8 * NV;           // N/D of a drain group retired (commit)
+  const uint32_t sTmem = drain_ready + 8;
   unsigned char* gY = gbase;
   unsigned char* gM = gbase + NS * Y_STAGE;
   unsigned char* gV = gbase + (sV - base);
@@ -851,6 +852,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
   const int T = (int)(t_end > t_begin ? t_end - t_begin : 0);
   const int64_t row0 = rb * BM;
   const int rows_here = (int)((a.n_rows - row0) < BM ? (a.n_rows - row0) : BM);
+  // The tensor core's fp32 accumulation truncates (ubench/acc_round.cu), a bias growing with the
+  // number of accumulation steps; N and D are therefore drained into the (RN, fp32) partials
+  // every G tiles and restarted.
+  const int G = a.drain_tiles > 0 ? a.drain_tiles : (1 << 30);
 
   if (tid == 0) {
     for (int i = 0; i < NS; ++i) { mbar_init(y_full + 8 * i, 1); mbar_init(y_empty + 8 * i, NEW); }
@@ -861,6 +866,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
       mbar_init(buf_free + 8 * i, 1);
     }
     mbar_init(nd_full, 1);
+    mbar_init(drain_ready, 1);
     mbar_init(u_ready, NEW);
     for (int i = 0; i < NV; ++i) mbar_init(vraw_full + 8 * i, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -957,13 +963,15 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
 #pragma unroll
           for (int kk = 0; kk < BN / 8; ++kk) {
             const uint64_t bd = vtd + (uint64_t)(((kk >> 2) * (KB * 128) + (kk & 3) * 32) >> 4);
-            const uint32_t acc = (u > 0 || kk > 0) ? 1u : 0u;
+            // the accumulators restart at every drain group (see the elementwise loop)
+            const uint32_t acc = ((u % G) != 0 || kk > 0) ? 1u : 0u;
             mma_ts_elect(tNa, pa + kk * 8, bd, id2, acc);
             mma_ts_elect(tNb, pbb + kk * 8, bd, id2, acc);
           }
         }
         mma_commit_elect(v_empty + 8 * vs);
         mma_commit_elect(buf_free + 8 * b);
+        if (u % G == G - 1 && u != T - 1) mma_commit_elect(drain_ready);
         if (u + 2 < T) mma_s(u + 2);
       }
       mma_commit_elect(nd_full);
@@ -1091,6 +1099,36 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
       __syncwarp();
       if (lane == 0) mbar_arrive(u_ready);
     }
+    // N | D (2 NCH chunks of 16 columns, shared out among the column groups) -> this CTA's split
+    // partial of drain group grp (zeros when zero: a chunk with fewer tiles than others)
+    auto drain_nd = [&](int64_t grp, bool zero) {
+      const int64_t elems = a.n_rows * (int64_t)a.K;
+#pragma unroll 1
+      for (int c = cg * (2 * NCH / 4); c < (cg + 1) * (2 * NCH / 4); ++c) {
+        const int which = c >= NCH ? 1 : 0;
+        const int h = which ? c - NCH : c;
+        float* out = a.Qpart + ((ch * a.n_groups + grp) * 2 + which) * elems + row * a.K + h * 16;
+        uint32_t r[16];
+        if (!zero) {
+          tmem_ld16((which ? tNb : tNa) + lane_off + h * 16, r);
+          tmem_ld_wait(r);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 16; ++j) r[j] = 0u;
+        }
+        if (row_ok && h * 16 < a.K) {
+          if (h * 16 + 16 <= a.K && (a.K & 3) == 0) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              reinterpret_cast<uint4*>(out)[q] = make_uint4(r[4 * q], r[4 * q + 1], r[4 * q + 2], r[4 * q + 3]);
+          } else {
+#pragma unroll
+            for (int j = 0; j < 16; ++j)
+              if (h * 16 + j < a.K) out[j] = __uint_as_float(r[j]);
+          }
+        }
+      }
+    };
     double loss_acc = 0.0;
     long long cnt = 0;
     // valid columns of a tile: the tile's offset inside its column block, advanced per tile
@@ -1142,34 +1180,24 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
       if (lane == 0) mbar_arrive(p_full + 8 * b);      // P(t) in TMEM (or, loss only: S(t) consumed)
       if (warp == W_EW0 && lane == 0) trace_ev(a, t, EV_EW_DONE);
       if (lane == 0) trace_ev(a, t, 16 + warp - W_EW0);     // per-warp arrival (diagnostics)
+      if (a.mode != 2 && t % G == G - 1 && t != T - 1) {
+        // drain the group's N / D before any warp can contribute P(t+1) (the N/D MMAs of tile
+        // t+1 wait for every warp's P(t+1) and restart the accumulators)
+        mbar_wait(drain_ready, (t / G) & 1);
+        tc_fence_after();
+        drain_nd(t / G, false);
+      }
     }
-    // epilogue: N | D (2 NCH chunks of 16 columns, shared out among the column groups) -> split
-    // partials
+    // epilogue: the last group's N | D -> split partials (added to the earlier groups' drains)
     if (a.mode != 2) {
-      const int64_t elems = a.n_rows * (int64_t)a.K;
+      int64_t g0 = 0;
       if (T > 0) {
         mbar_spin(nd_full, 0);
         tc_fence_after();
+        drain_nd((T - 1) / G, false);
+        g0 = (T - 1) / G + 1;
       }
-#pragma unroll 1
-      for (int c = cg * (2 * NCH / 4); c < (cg + 1) * (2 * NCH / 4); ++c) {
-        const int which = c >= NCH ? 1 : 0;
-        const int h = which ? c - NCH : c;
-        float* out = a.Qpart + ch * 2 * elems + (int64_t)which * elems;
-        uint32_t r[16];
-        if (T > 0) {
-          tmem_ld16((which ? tNb : tNa) + lane_off + h * 16, r);
-          tmem_ld_wait(r);
-        } else {
-#pragma unroll
-          for (int j = 0; j < 16; ++j) r[j] = 0u;
-        }
-        if (row_ok) {
-#pragma unroll
-          for (int j = 0; j < 16; ++j)
-            if (h * 16 + j < a.K) out[row * a.K + h * 16 + j] = __uint_as_float(r[j]);
-        }
-      }
+      for (int64_t grp = g0; grp < a.n_groups; ++grp) drain_nd(grp, true);
     } else if (T > 0) {
       mbar_spin(nd_full, 0);
     }

@@ -26,7 +26,7 @@ struct TcArgs {
   const float* tab[kMaxTabs];
   int64_t tcs[kMaxTabs][kMaxModes];
   int32_t boff[kMaxTabs][64];
-  float* Qpart;               // [chunks][2][n_rows][K]
+  float* Qpart;               // [chunks][n_groups][2][n_rows][K]
   double* losspart;           // [row_blocks * chunks]
   long long* countpart;
   DivParams dv;
@@ -46,6 +46,8 @@ struct TcArgs {
   int64_t vd_tpr;             // tiles per run
   int64_t vd_pitch;           // row pitch (elements) of vd_rows_ptr (K rounded up to 4)
   const float* vd_rows_ptr;   // the table rows the TMA reads (the table, or its padded copy)
+  int drain_tiles;            // N / D drained into a separate split partial every this many tiles
+  int64_t n_groups;           // drain groups per chunk: Qpart is [chunks][n_groups][2][n_rows][K]
   int dbg;                    // diagnostics: 1 prefill N/D with 1 and always accumulate,
                               // 2 numerator B as K-major, 4 swap LBO/SBO of the MN-major view
 };

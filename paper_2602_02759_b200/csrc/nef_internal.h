@@ -12,6 +12,10 @@ namespace nef {
 constexpr int kMaxDims = 8;      // max indices per operand / per einsum step side
 constexpr int kMaxTabs = 4;      // max KR tables on the column side of a lowering
 constexpr int kMaxModes = 8;     // max observed modes
+// tcgen05 path: the tensor core's fp32 accumulation truncates, so the numerator / denominator
+// accumulators are drained to separate split partials every kDrainTiles tiles (<= 2048
+// truncating accumulation steps per partial; summed in fp64 by reduce_q)
+constexpr int kDrainTiles = 256;
 
 // ---------------------------------------------------------------------------------
 // Small einsum engine: C[out] = sum_{sum} A[...] * B[...]   (B optional)
@@ -90,6 +94,7 @@ struct Lowering {
   int64_t tc_tiles = 0;         // column tiles (64 wide)
   int64_t tc_chunks = 1;        // split of the tile range per row block
   int64_t tc_row_blocks = 0;    // 128-row blocks
+  int64_t tc_groups = 1;        // drain groups per chunk (kDrainTiles tiles each)
   int64_t ws_tc_Qpart = 0;      // partial buffer for the tcgen05 path
   int64_t ws_tc_losspart = 0;   // per-CTA loss / count partials of the tcgen05 path
   // direct V: one table vd_tab holds the trailing column modes as consecutive

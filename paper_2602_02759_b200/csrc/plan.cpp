@@ -444,6 +444,8 @@ void tc_geometry(const Plan& p, Lowering& L) {
       int64_t ch = std::max<int64_t>(1, p.num_sms / L.tc_row_blocks);
       ch = std::min(ch, L.tc_tiles);
       L.tc_chunks = ch;
+      const int64_t tpc = (L.tc_tiles + ch - 1) / ch;
+      L.tc_groups = std::max<int64_t>(1, (tpc + kDrainTiles - 1) / kDrainTiles);
     }
   }
 }
@@ -487,7 +489,7 @@ void finish_workspace(const Plan& p, Lowering& L, Bump& bump, const std::string&
     L.epi = compile_einsum(p, ein, p.ops[L.ell], bump, &tgt);
   }
   if (L.tc_ok) {
-    L.ws_tc_Qpart = bump.take(L.tc_chunks * L.tc_row_blocks * 128 * L.K * 2 * 4);
+    L.ws_tc_Qpart = bump.take(L.tc_chunks * L.tc_groups * L.tc_row_blocks * 128 * L.K * 2 * 4);
     int64_t nparts = L.tc_row_blocks * L.tc_chunks;
     L.ws_tc_losspart = bump.take(nparts * 16);
   }
@@ -671,7 +673,7 @@ std::string describe_plan(const Plan& p) {
       << ",\"row_fast\":" << (L.row_fast ? "true" : "false") << ",\"n_chunks\":" << L.n_chunks
       << ",\"tc\":" << (L.tc_ok ? "true" : "false") << ",\"tc_layout\":" << L.tc_layout << ",\"tc_R\":" << L.tc_R
       << ",\"tc_CI\":" << L.tc_CI << ",\"tc_CO\":" << L.tc_CO << ",\"tc_KB\":" << L.tc_KB
-      << ",\"tc_tiles\":" << L.tc_tiles << ",\"tc_chunks\":" << L.tc_chunks << ",\"vd_tab\":" << L.vd_tab << ",\"vd_E\":" << L.vd_E << ",\"tabs_merged\":" << (L.tabs_merged ? "true" : "false") << ",\"row_factors\":[";
+      << ",\"tc_tiles\":" << L.tc_tiles << ",\"tc_chunks\":" << L.tc_chunks << ",\"tc_groups\":" << L.tc_groups << ",\"vd_tab\":" << L.vd_tab << ",\"vd_E\":" << L.vd_E << ",\"tabs_merged\":" << (L.tabs_merged ? "true" : "false") << ",\"row_factors\":[";
     for (size_t k = 0; k < L.row_factors.size(); ++k) o << (k ? "," : "") << L.row_factors[k];
     o << "],\"col_factors\":[";
     for (size_t k = 0; k < L.col_factors.size(); ++k) o << (k ? "," : "") << L.col_factors[k];
