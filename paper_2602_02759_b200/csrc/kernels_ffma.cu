@@ -14,6 +14,7 @@
 //   * loss_reduce    : fixed-order fp64 sum of per-CTA loss partials
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdint>
 
@@ -353,34 +354,60 @@ struct EinStepDev {
   long long out_size, sum_size;
 };
 
+// Small einsum step C[out] = sum A[..] (* B[..]).  Templated on the index type (32-bit when
+// every offset fits) and on the parallelisation: L lanes share one output, each summing a
+// contiguous slice of the summed indices (odometer started by one decomposition), partials
+// combined with warp shuffles in fp64.  L = 1 for many outputs, 32 for few outputs with long sums
+// (e.g. the Tucker core's epilogue: 4096 outputs x 65536 terms).
+template <typename I, int L>
 __global__ void einstep_kernel(const __grid_constant__ EinStepDev st, const float* __restrict__ A,
                                const float* __restrict__ B, float* __restrict__ C) {
-  for (long long o = (long long)blockIdx.x * blockDim.x + threadIdx.x; o < st.out_size;
-       o += (long long)gridDim.x * blockDim.x) {
-    long long rem = o, ao = 0, bo = 0;
+  const long long gt = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = (int)(gt % L);
+  const long long stride = ((long long)gridDim.x * blockDim.x) / L;
+  const I chunk = (I)((st.sum_size + L - 1) / L);
+  const I s0 = (I)lane * chunk;
+  const I s1 = (I)((long long)s0 + chunk < st.sum_size ? (long long)s0 + chunk : st.sum_size);
+  // the loop bound is uniform across the L lanes of an output (L divides the block size)
+  for (long long o = gt / L; o < st.out_size; o += stride) {
+    I rem = (I)o, ao = 0, bo = 0;
     for (int d = st.nout - 1; d >= 0; --d) {
-      long long i = rem % st.odim[d];
-      rem /= st.odim[d];
-      ao += i * st.as_o[d];
-      bo += i * st.bs_o[d];
+      const I od = (I)st.odim[d];
+      const I i = rem % od;
+      rem /= od;
+      ao += i * (I)st.as_o[d];
+      bo += i * (I)st.bs_o[d];
     }
-    long long sidx[kMaxDims];
-    for (int d = 0; d < kMaxDims; ++d) sidx[d] = 0;
+    I sidx[kMaxDims];
+    {
+      I r = s0;
+      for (int d = st.nsum - 1; d >= 0; --d) {
+        const I sd = (I)st.sdim[d];
+        sidx[d] = r % sd;
+        r /= sd;
+        ao += sidx[d] * (I)st.as_s[d];
+        bo += sidx[d] * (I)st.bs_s[d];
+      }
+    }
     double acc = 0.0;
-    for (long long s = 0; s < st.sum_size; ++s) {
-      double v = (double)A[ao];
-      if (B) v *= (double)B[bo];
+    for (I s = s0; s < s1; ++s) {
+      double v = (double)__ldg(A + ao);
+      if (B) v *= (double)__ldg(B + bo);
       acc += v;
       for (int d = st.nsum - 1; d >= 0; --d) {
-        ao += st.as_s[d];
-        bo += st.bs_s[d];
-        if (++sidx[d] < st.sdim[d]) break;
-        ao -= st.as_s[d] * st.sdim[d];
-        bo -= st.bs_s[d] * st.sdim[d];
+        ao += (I)st.as_s[d];
+        bo += (I)st.bs_s[d];
+        if (++sidx[d] < (I)st.sdim[d]) break;
+        ao -= (I)(st.as_s[d] * st.sdim[d]);
+        bo -= (I)(st.bs_s[d] * st.sdim[d]);
         sidx[d] = 0;
       }
     }
-    C[o] = (float)acc;
+    if (L > 1) {
+#pragma unroll
+      for (int w = L / 2; w > 0; w >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, w);
+    }
+    if (lane == 0) C[o] = (float)acc;
   }
 }
 
@@ -388,16 +415,27 @@ cudaError_t launch_einstep(const EinStep& st, const float* A, const float* B, fl
   EinStepDev d{};
   d.nout = st.nout;
   d.nsum = st.nsum;
+  long long span = 1;   // largest offset reached in A or B (bounds the index type)
+  long long sa = 0, sb = 0;
   for (int k = 0; k < kMaxDims; ++k) {
     d.odim[k] = st.odim[k]; d.as_o[k] = st.as_o[k]; d.bs_o[k] = st.bs_o[k];
     d.sdim[k] = st.sdim[k]; d.as_s[k] = st.as_s[k]; d.bs_s[k] = st.bs_s[k];
+    if (k < st.nout) { sa += (st.odim[k] - 1) * st.as_o[k]; sb += (st.odim[k] - 1) * st.bs_o[k]; }
+    if (k < st.nsum) { sa += (st.sdim[k] - 1) * st.as_s[k]; sb += (st.sdim[k] - 1) * st.bs_s[k]; }
   }
+  span = std::max(std::max(sa, sb), std::max<long long>(st.out_size, st.sum_size));
   d.out_size = st.out_size;
   d.sum_size = st.sum_size;
-  long long blocks = (st.out_size + 255) / 256;
+  const bool split = st.out_size < 148 * 256 && st.sum_size >= 128;
+  const bool small = span < (1ll << 30);
+  const int L = split ? 32 : 1;
+  long long blocks = (st.out_size * L + 255) / 256;
   if (blocks > 148 * 32) blocks = 148 * 32;
   if (blocks < 1) blocks = 1;
-  einstep_kernel<<<(unsigned)blocks, 256, 0, s>>>(d, A, B, C);
+  if (split && small) einstep_kernel<int, 32><<<(unsigned)blocks, 256, 0, s>>>(d, A, B, C);
+  else if (split) einstep_kernel<long long, 32><<<(unsigned)blocks, 256, 0, s>>>(d, A, B, C);
+  else if (small) einstep_kernel<int, 1><<<(unsigned)blocks, 256, 0, s>>>(d, A, B, C);
+  else einstep_kernel<long long, 1><<<(unsigned)blocks, 256, 0, s>>>(d, A, B, C);
   return cudaGetLastError();
 }
 

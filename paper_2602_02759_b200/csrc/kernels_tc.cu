@@ -7,19 +7,18 @@
 //   N  += P_a V,  D += P_b V  (TF32 MMAs, A operand = P in TMEM, accumulators in TMEM)
 // Y and the mask are streamed HBM -> smem by TMA exactly once; Yhat, a and b never leave the SM.
 //
-// CTA = 128 rows (TMEM lanes) x a contiguous range of 64-column tiles.  512 threads:
-//   warp 0      TMA producer (Y / mask ring of NS stages)
-//   warp 1      TMEM allocator + single-thread MMA issuer (reconstruction and N/D MMAs)
-//   warp 2      idle
-//   warp 3      direct-V row loads (TMA) when the tile's V rows are rows of one table
-//   warps 4-7   column operand: V tile = prod of column tables (Khatri-Rao), 16 columns per
-//               warp; rows constant across the tile are loaded once and broadcast; the next
-//               tile's table rows are in flight while the current tile is stored; TF32
-//               round-to-nearest, written twice in the UMMA SW128 K-major layout: V (rows = tile
-//               columns, K = bond) for the reconstruction MMA and V^T (rows = bond, K = tile
-//               columns) for the numerator / denominator MMAs
-//   warps 8-15  elementwise: tcgen05.ld S -> a, b (+ loss) -> tcgen05.st P; epilogue N, D
+// CTA = 128 rows (TMEM lanes) x a contiguous range of 64-column tiles, 23 warps:
+//   warps 0-15  elementwise: tcgen05.ld S -> a, b (+ loss) -> tcgen05.st P_a over S, P_b beside
+//               it (lane quarter = warp % 4, 16-column group = warp / 4); N / D drains, epilogue
+//   warps 16-19 V generators: the tile's 64 direct-V table rows (TMA-loaded) scaled in place by
+//               the run's constant-row product, TF32 RN, plus the transposed copy V^T (both in
+//               the UMMA SW128 K-major layout: V for the reconstruction, V^T for N / D)
+//   warp 20     TMA of the direct-V table rows
+//   warp 21     TMA producer of the Y (and mask) tiles
+//   warp 22     TMEM allocator + MMA issuer (whole warp, elect.sync)
 // TMEM (512 columns): tile buffer[2] (S -> P_a in place | P_b, 2 x 128) | N, D (2xKB) | U_hi, U_lo (2xKB)
+// The generated-V path (Khatri-Rao products per tile, warps 16-19) remains for lowerings without
+// a direct-V table; the planner routes those to the CUDA-core kernel, so it is not exercised.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
