@@ -657,19 +657,24 @@ __device__ __forceinline__ void ew_half_sent(const TcArgs& a, uint32_t (&sv)[16]
     for (int j = 0; j < 16; ++j) yv[j] = ((vbits >> j) & 1u) ? yv[j] : -1.f;
   }
   if (a.mode != 0) {   // loss of the iterate entering the sweep (uniform branch)
+    // a, b and the loss from |x| (a missing entry's -1 becomes a harmless 1), then the sign of x
+    // selects: the loss of a missing entry is dropped, a and b are zeroed by the add-then-max.
+    // The observed count is constant over a fit: only the loss-only pass (mode 2) counts.
+    float2 l2 = make_float2(0.f, 0.f);
 #pragma unroll
     for (int j = 0; j < 16; j += 2) {
-      const bool o0 = yv[j] >= 0.f, o1 = yv[j + 1] >= 0.f;
+      const float2 x = make_float2(yv[j], yv[j + 1]);
       const float2 yh = make_float2(fmaxf(__uint_as_float(sv[j]), 1e-30f), fmaxf(__uint_as_float(sv[j + 1]), 1e-30f));
       float2 av, bv, lv;
-      Ew<KIND>::abl2(make_float2(o0 ? yv[j] : 1.f, o1 ? yv[j + 1] : 1.f), yh, a.dv, av, bv, lv);
-      lsum += (o0 ? lv.x : 0.f) + (o1 ? lv.y : 0.f);
-      cnt += (o0 ? 1 : 0) + (o1 ? 1 : 0);
-      sv[j] = o0 ? __float_as_uint(av.x) + 0x1000u : 0u;
-      sv[j + 1] = o1 ? __float_as_uint(av.y) + 0x1000u : 0u;
-      pb[j] = o0 ? __float_as_uint(bv.x) + 0x1000u : 0u;
-      pb[j + 1] = o1 ? __float_as_uint(bv.y) + 0x1000u : 0u;
+      Ew<KIND>::abl2(make_float2(fabsf(x.x), fabsf(x.y)), yh, a.dv, av, bv, lv);
+      l2 = __fadd2_rn(l2, make_float2(x.x >= 0.f ? lv.x : 0.f, x.y >= 0.f ? lv.y : 0.f));
+      if (a.mode == 2) cnt += (x.x >= 0.f ? 1 : 0) + (x.y >= 0.f ? 1 : 0);
+      sv[j] = (uint32_t)__viaddmax_s32(__float_as_int(copysignf(av.x, x.x)), 0x1000, 0);
+      sv[j + 1] = (uint32_t)__viaddmax_s32(__float_as_int(copysignf(av.y, x.y)), 0x1000, 0);
+      pb[j] = (uint32_t)__viaddmax_s32(__float_as_int(copysignf(bv.x, x.x)), 0x1000, 0);
+      pb[j + 1] = (uint32_t)__viaddmax_s32(__float_as_int(copysignf(bv.y, x.y)), 0x1000, 0);
     }
+    lsum += l2.x + l2.y;
     return;
   }
 #pragma unroll
