@@ -284,6 +284,25 @@ __device__ __forceinline__ int sw128_off(int row, int k, int rows) {
 // ------------------------------------------------------------------ column operand generator
 // Table rows of one tile held in registers (software pipelining across tiles).
 template <int KB>
+struct VTile;
+
+// Lane -> 4x4 block assignment of the V generators.  Lane owns bond chunk c (bonds 4c..4c+3) and,
+// for block i, row group rg (rows 4 rg..4 rg+3 of the warp's 16).  A 16-byte shared access is
+// served per quarter warp (8 lanes); the 8 lanes of a quarter hit 8 distinct 16-byte chunk slots
+// both in V (slot (c & 7) ^ (x0 & 7)) and in V^T (slot (x0 >> 2 & 7) ^ 4 (c & 1)): with q = lane & 3,
+// p = lane >> 2 & 1, a quarter with rotation g takes c & 7 = p + 2 ((q + g) & 3) and rg = q ^ 2i.
+// (c = lane % C with rg = lane / C would put 8 lanes of one quarter on two V^T slots.)
+template <int KB>
+__device__ __forceinline__ int vl_c(int lane) {
+  static_assert(KB == 32 || KB == 64, "V lane map: KB 32 or 64");
+  const int qq = lane >> 3, p = (lane >> 2) & 1, q = lane & 3;
+  const int g = KB == 64 ? (qq & 1) : qq;
+  const int h = KB == 64 ? (qq >> 1) : 0;
+  return 8 * h + p + 2 * ((q + g) & 3);
+}
+__device__ __forceinline__ int vl_rg(int lane, int i) { return (lane & 3) ^ (2 * i); }
+
+template <int KB>
 struct VTile {
   static constexpr int C = KB / 4;          // 16-byte chunks per padded row
   static constexpr int NB = (4 * C) / 32;   // 4x4 blocks per lane (16 rows = 4 row groups per warp)
@@ -366,7 +385,7 @@ __device__ __forceinline__ void vtile_issue(const TcArgs& a, int64_t tile, int x
     return;
   }
   const int first = __ffs(v.vmask) - 1;
-  const int c = lane % VT::C;
+  const int c = vl_c<KB>(lane);
   const bool kok = c * 4 < a.K;
   int nvar = 0, var_q = -1;
   v.cst = make_float4(1.f, 1.f, 1.f, 1.f);
@@ -402,7 +421,7 @@ __device__ __forceinline__ void vtile_issue(const TcArgs& a, int64_t tile, int x
   const float4* tab = reinterpret_cast<const float4*>(a.tab[var_q]);
 #pragma unroll
   for (int i = 0; i < VT::NB; ++i) {
-    const int rg = (lane + 32 * i) / VT::C;   // row group of block i
+    const int rg = vl_rg(lane, i);   // row group of block i
 #pragma unroll
     for (int r = 0; r < 4; ++r) {
       const int xr = 4 * rg + r;
@@ -422,10 +441,10 @@ struct VOff {
   static constexpr int C = KB / 4, NB = (4 * C) / 32;
   int vb[NB], vtb[NB], cx[NB], xc[NB];
   __device__ __forceinline__ void init(int xw, int lane) {
-    const int c = lane % C;
+    const int c = vl_c<KB>(lane);
 #pragma unroll
     for (int i = 0; i < NB; ++i) {
-      const int x0 = xw + 4 * ((lane + 32 * i) / C);
+      const int x0 = xw + 4 * vl_rg(lane, i);
       vb[i] = (c >> 3) * (BN * 128) + (x0 >> 3) * 1024 + (x0 & 7) * 128;
       cx[i] = (c & 7) ^ (x0 & 7);
       const int k0 = 4 * c;
@@ -480,13 +499,13 @@ template <int KB>
 __device__ __noinline__ void vtile_store_slow(const TcArgs& a, int xw, int lane, const VTile<KB>& v,
                                               const int (&toff)[kMaxTabs], unsigned char* vrow, const VOff<KB>& vo) {
   using VT = VTile<KB>;
-  const int c = lane % VT::C;
+  const int c = vl_c<KB>(lane);
   const bool kok = c * 4 < a.K;
   if (a.vec4) {
     // general vector path: several varying tables, rows multiplied table by table
 #pragma unroll
     for (int i = 0; i < VT::NB; ++i) {
-      const int rg = (lane + 32 * i) / VT::C;
+      const int rg = vl_rg(lane, i);
       float4 p[4];
 #pragma unroll
       for (int r = 0; r < 4; ++r) p[r] = make_float4(1.f, 1.f, 1.f, 1.f);
@@ -531,7 +550,7 @@ template <int KB>
 __device__ __forceinline__ void vtile_store(const TcArgs& a, int xw, int lane, const VTile<KB>& v,
                                             const int (&toff)[kMaxTabs], unsigned char* vrow, const VOff<KB>& vo) {
   using VT = VTile<KB>;
-  const int c = lane % VT::C;
+  const int c = vl_c<KB>(lane);
   const bool kok = c * 4 < a.K;
   if (v.mode == 1) {
     vtile_store_slow<KB>(a, xw, lane, v, toff, vrow, vo);
@@ -540,7 +559,7 @@ __device__ __forceinline__ void vtile_store(const TcArgs& a, int xw, int lane, c
   // fast path (mode 0: constant rows x one varying table) and empty tiles (mode 2: zeros)
 #pragma unroll
   for (int i = 0; i < VT::NB; ++i) {
-    const int rg = (lane + 32 * i) / VT::C;
+    const int rg = vl_rg(lane, i);
     float4 p[4];
 #pragma unroll
     for (int r = 0; r < 4; ++r)
@@ -1001,8 +1020,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
     // ------------------------------------------------------------ direct V: scale rows in place
     // V[x][k] = T_var[row + x][k] * prod_{q != var} T_q[const row][k]; V^T written alongside.
     const int xw = vg_index(warp) * 16;
-    constexpr int C = KB / 4, NB = (4 * C) / 32;
-    const int c = lane % C;
+    const int c = vl_c<KB>(lane);
     VOff<KB> vo;
     vo.init(xw, lane);
     // the next tile's run is looked up one tile ahead so that a new run's constant rows are in
@@ -1030,7 +1048,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
       if (warp == W_VG0 && lane == 0) trace_ev(a, t, EV_VG_START);
       unsigned char* vrow = gV + vs * V_STAGE_MAX;
 #pragma unroll
-      for (int i = 0; i < NB; ++i) {
+      for (int i = 0; i < VOff<KB>::NB; ++i) {
         float4 p[4];
 #pragma unroll
         for (int r = 0; r < 4; ++r) {

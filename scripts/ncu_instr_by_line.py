@@ -16,6 +16,7 @@ rows = list(csv.reader(io.StringIO(src)))
 hdr = rows[1]
 ie = hdr.index("Instructions Executed")
 isamp = hdr.index("Warp Stall Sampling (All Samples)")
+iexc = hdr.index("L1 Wavefronts Shared Excessive") if "L1 Wavefronts Shared Excessive" in hdr else None
 txt = subprocess.run(["nvdisasm", "--print-line-info-inline", cubin], capture_output=True, text=True).stdout
 line_of, cur, inside = {}, None, False
 for l in txt.split("\n"):
@@ -35,16 +36,23 @@ for l in txt.split("\n"):
 data = []
 for r in rows[2:]:
     try:
-        data.append((int(r[0], 16), int(r[ie] or 0), int(r[isamp] or 0)))
+        data.append((int(r[0], 16), int(r[ie] or 0), int(r[isamp] or 0),
+                     int(float(r[iexc] or 0)) if iexc is not None else 0))
     except (ValueError, IndexError):
         pass
-base = min(a for a, _, _ in data)
-ins, smp = collections.Counter(), collections.Counter()
-for a, n, s in data:
+base = min(d[0] for d in data)
+ins, smp, exc = collections.Counter(), collections.Counter(), collections.Counter()
+for a, n, s, x in data:
     k = line_of.get(a - base, "?")
     ins[k] += n
     smp[k] += s
+    exc[k] += x
 ti, ts = sum(ins.values()), sum(smp.values())
 print("warp instr per tile %.0f   samples %d" % (ti / tiles, ts))
 for k, v in ins.most_common(top):
     print("%7.0f instr/tile %5.1f%%   stall %5.1f%%   %s" % (v / tiles, 100 * v / ti, 100 * smp[k] / ts, k))
+tx = sum(exc.values())
+if tx:
+    print("# shared-memory excessive wavefronts (bank conflicts) per tile %.0f, by line" % (tx / tiles))
+    for k, v in exc.most_common(8):
+        print("%7.0f excess wavefronts/tile %5.1f%%   %s" % (v / tiles, 100 * v / tx, k))
