@@ -34,8 +34,9 @@ thread_local std::string g_err;
 thread_local int64_t g_launches = 0;
 int g_policy = 0;
 float* g_debug = nullptr;   // optional device dump of the tcgen05 kernel's first tile (tests)
-long long* g_trace = nullptr;
-bool g_no_sentinel = std::getenv("NEF_NO_SENTINEL") != nullptr;   // diagnostics: stream the uint8 mask   // optional pipeline timeline of the tcgen05 kernel (diagnostics)
+long long* g_trace = nullptr;   // optional pipeline timeline of the tcgen05 kernel (diagnostics)
+bool g_no_sentinel = std::getenv("NEF_NO_SENTINEL") != nullptr;   // diagnostics: stream the uint8 mask
+bool g_no_lconst = std::getenv("NEF_NO_LCONST") != nullptr;     // diagnostics: loss passes compute the whole divergence (R25 off)
 
 // live CUDA-event timing of the streaming kernel (nef_profile_*)
 struct Prof {
@@ -121,6 +122,8 @@ struct Ctx {
   size_t ws_bytes;
   cudaStream_t s;
   const float* ysent = nullptr;   // NaN-sentinel copy of Y (mask folded in), when prepared
+  const double* loff = nullptr;   // R25: [data-only loss sum][observed count] of the sentinel pass
+  double lscale = 1.0;            //      loss = lscale * (streamed part) + loff[0]
 };
 
 float* resolve(const Ctx& c, const nef::BufRef& b) {
@@ -201,6 +204,7 @@ struct StreamOut {
   double* losspart = nullptr;
   long long* countpart = nullptr;
   int64_t nparts = 0;
+  bool lconst = false;            // loss partials hold only the factor-dependent part (R25)
 };
 
 bool use_tc(const nef::Lowering& L, const uint8_t* M, bool sentinel = false) {
@@ -284,6 +288,7 @@ int stream_pass(const Ctx& c, const nef::Lowering& L, const float* Y, const uint
     t.countpart = reinterpret_cast<long long*>(c.ws + L.ws_tc_losspart + o.nparts * 8);
     t.dv = dv;
     t.mode = mode;
+    t.lconst = (sent && c.loff && mode != 0) ? 1 : 0;
     t.debug = g_debug;
     t.trace = g_trace;
     {
@@ -302,6 +307,7 @@ int stream_pass(const Ctx& c, const nef::Lowering& L, const float* Y, const uint
     o.n_chunks = chunks * t.n_groups;
     o.losspart = t.losspart;
     o.countpart = t.countpart;
+    o.lconst = t.lconst != 0;
     return NEF_OK;
   }
   prof_begin(c.s);
@@ -323,7 +329,8 @@ int loss_pass(const Ctx& c, const float* Y, const uint8_t* M, const nef::DivPara
   if (st) return st;
   StreamOut o;
   if ((st = stream_pass(c, L, Y, M, 2, dv, o))) return st;
-  CK(nef::launch_loss_reduce(o.losspart, o.countpart, o.nparts, slot, cslot, c.s));
+  CK(nef::launch_loss_reduce(o.losspart, o.countpart, o.nparts, slot, cslot, c.s, o.lconst ? c.lscale : 1.0,
+                             o.lconst ? c.loff : nullptr));
   ++g_launches;
   return NEF_OK;
 }
@@ -337,7 +344,8 @@ int num_den(const Ctx& c, int ell, const float* Y, const uint8_t* M, const nef::
   StreamOut o;
   if ((st = stream_pass(c, L, Y, M, mode, dv, o))) return st;
   if (mode == 1) {
-    CK(nef::launch_loss_reduce(o.losspart, o.countpart, o.nparts, slot, cslot, c.s));
+    CK(nef::launch_loss_reduce(o.losspart, o.countpart, o.nparts, slot, cslot, c.s, o.lconst ? c.lscale : 1.0,
+                               o.lconst ? c.loff : nullptr));
     ++g_launches;
   }
   const int64_t qe = L.n_rows * L.K;
@@ -543,9 +551,19 @@ int nef_fit(nef_plan_t plan, const float* Y, const uint8_t* mask, double alpha, 
     for (const auto& L : p.low) any_tc |= L.tc_ok;
     if (any_tc) {
       float* ys = reinterpret_cast<float*>(c.ws + p.ws_sent);
-      CK(nef::launch_sentinel(Y, mask, ys, p.n_local, c.s));
-      ++g_launches;
+      // R25: the data-only part of the loss summed once here for the pairs that split it off
+      const int dterm = g_no_lconst ? 0 : dv.kind == nef::EW_B_M05 ? 1 : dv.kind == nef::EW_KL ? 2 : 0;
+      double* dslot = reinterpret_cast<double*>(c.ws + p.ws_dterm);
+      double* dpart = reinterpret_cast<double*>(c.ws + p.ws_dpart);
+      CK(nef::launch_sentinel(Y, mask, ys, p.n_local, dterm, dpart,
+                              reinterpret_cast<long long*>(dpart + nef::kSentParts), dslot,
+                              reinterpret_cast<long long*>(dslot + 1), c.s));
+      g_launches += 3;
       c.ysent = ys;
+      if (dterm) {
+        c.loff = dslot;
+        c.lscale = dterm == 1 ? 2.0 : 1.0;
+      }
     }
   }
   double* slots = reinterpret_cast<double*>(c.ws + p.ws_trace);

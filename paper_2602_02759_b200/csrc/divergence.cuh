@@ -357,6 +357,40 @@ struct Ew<EW_A05_B1> {  // (0.5, 1): a = sqrt(x), b = sqrt(y)
   }
 };
 
+// Loss with its data-only part split off (R25).  For the pairs below the per-entry divergence
+// is  L(x, y) = scale * rem(x, y) + c(x),  with c depending on the data alone:
+//   (1, -0.5): 2 (sqrt x - sqrt y)^2 / sqrt y = 2 (x + y) / sqrt y - 4 sqrt x
+//   (1, 0)   : x log(x / y) - x + y           = (y - x log y) + (x log x - x)
+// C = sum_observed c(x) is constant over a fit and is summed once by the sentinel pass
+// (launch_sentinel, dterm_c below); the streaming passes then accumulate rem only.  abr2
+// takes the SIGNED sentinel value (a carries its sign; rem of a missing entry is discarded by
+// the caller's select).
+template <int KIND>
+struct LossOff {
+  static constexpr bool value = false;
+  static __device__ __forceinline__ void abr2(float2, float2, float2&, float2&, float2&) {}
+};
+template <>
+struct LossOff<EW_B_M05> {
+  static constexpr bool value = true;
+  static __device__ __forceinline__ void abr2(float2 x, float2 yh, float2& av, float2& bv, float2& rem) {
+    const float2 r = make_float2(frsqrt(yh.x), frsqrt(yh.y));
+    bv = r;
+    const float2 xr = __fmul2_rn(x, r);
+    av = __fmul2_rn(xr, __fmul2_rn(r, r));
+    rem = __ffma2_rn(yh, r, xr);   // (x + y) / sqrt y; scale 2
+  }
+};
+template <>
+struct LossOff<EW_KL> {
+  static constexpr bool value = true;
+  static __device__ __forceinline__ void abr2(float2 x, float2 yh, float2& av, float2& bv, float2& rem) {
+    av = __fmul2_rn(x, make_float2(frcp(yh.x), frcp(yh.y)));
+    bv = make_float2(1.f, 1.f);
+    rem = __ffma2_rn(make_float2(-x.x, -x.y), make_float2(flog(yh.x), flog(yh.y)), yh);   // y - x log y; scale 1
+  }
+};
+
 // dispatch helper: calls f.template operator()<KIND>() for the pair's kind
 template <typename F>
 inline cudaError_t dispatch_ew(int kind, F&& f) {

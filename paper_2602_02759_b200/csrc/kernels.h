@@ -56,8 +56,13 @@ cudaError_t launch_fused_ffma(const FusedArgs& a, cudaStream_t s);
 // Small einsum step (C = sum A*B, optional B), fp64 accumulation
 cudaError_t launch_einstep(const EinStep& st, const float* A, const float* B, float* C, cudaStream_t s);
 
-// out[i] = M[i] ? Y[i] + 0 : -1  (the sentinel copy of Y; M nonzero = observed; observed data >= 0)
-cudaError_t launch_sentinel(const float* Y, const uint8_t* M, float* out, int64_t n, cudaStream_t s);
+// out[i] = M[i] ? Y[i] + 0 : -1  (the sentinel copy of Y; M nonzero = observed; observed data >= 0).
+// With dpart (kSentBlocks + 1 partials each of dpart / dcpart): also *dslot = sum over observed
+// entries of the data-only loss term c(x) (dterm 1: (1,-0.5), 2: (1,0), 0: none; R25) and
+// *dcslot = the observed count, summed in fixed order.
+constexpr int kSentBlocks = 148 * 16;
+cudaError_t launch_sentinel(const float* Y, const uint8_t* M, float* out, int64_t n, int dterm, double* dpart,
+                            long long* dcpart, double* dslot, long long* dcslot, cudaStream_t s);
 
 // dst[r][0..Kp) = src[r][0..K) padded with zeros (16-byte row pitch for TMA)
 cudaError_t launch_pad_rows(const float* src, float* dst, int64_t rows, int64_t K, int64_t Kp, cudaStream_t s);
@@ -74,9 +79,10 @@ struct UpdArgs {
 UpdArgs make_upd(double alpha, double beta, double eps);
 cudaError_t launch_update(float* theta, const float* num, const float* den, int64_t n, UpdArgs u, cudaStream_t s);
 
-// Sum CTA loss partials (fixed order) into slot[0] (double) and count into cslot[0]
+// Sum CTA loss partials (fixed order) into slot[0] (double) and count into cslot[0].  With off
+// (R25): slot[0] = scale * sum + off[0] and cslot[0] = ((long long*)off)[1].
 cudaError_t launch_loss_reduce(const double* part, const long long* cpart, int64_t n, double* slot,
-                               long long* cslot, cudaStream_t s);
+                               long long* cslot, cudaStream_t s, double scale = 1.0, const double* off = nullptr);
 
 // Loss sum via the planner's lowering 0 (no update)
 }  // namespace nef

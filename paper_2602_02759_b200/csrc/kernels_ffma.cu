@@ -442,11 +442,49 @@ cudaError_t launch_einstep(const EinStep& st, const float* A, const float* B, fl
 // --------------------------------------------------------------------------------------
 // 4 entries per thread and iteration: one 4-byte mask load and one 16-byte Y load / store, all
 // fully coalesced across the warp
+// Data-only loss term c(x) of an observed entry (R25, LossOff in divergence.cuh)
+__device__ __forceinline__ double dterm_c(int dterm, float x) {
+  if (dterm == 1) return -4.0 * (double)sqrtf(x);                    // (1, -0.5)
+  if (dterm == 2) return x > 0.f ? (double)x * (double)logf(x) - (double)x : 0.0;   // (1, 0)
+  return 0.0;
+}
+
+// Block sum (fixed order) of (acc, cnt) into dpart[blockIdx.x] / dcpart[blockIdx.x] + slot_off
+__device__ __forceinline__ void sent_block_sum(double acc, long long cnt, double* dpart, long long* dcpart, int slot) {
+  __shared__ double ra[32];
+  __shared__ long long rc[32];
+  for (int o = 16; o > 0; o >>= 1) {
+    acc += __shfl_down_sync(0xffffffffu, acc, o);
+    cnt += __shfl_down_sync(0xffffffffu, cnt, o);
+  }
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  if (l == 0) { ra[w] = acc; rc[w] = cnt; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0.0;
+    long long c = 0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) { a += ra[i]; c += rc[i]; }
+    dpart[slot] = a;
+    dcpart[slot] = c;
+  }
+}
+
 __global__ void sentinel_kernel(const float* __restrict__ Y, const uint8_t* __restrict__ M, float* __restrict__ out,
-                                long long n4) {
+                                long long n4, int dterm, double* dpart, long long* dcpart) {
+  double acc = 0.0;
+  long long cnt = 0;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4; i += (long long)gridDim.x * blockDim.x) {
     const uint32_t w = __ldcs(reinterpret_cast<const unsigned int*>(M) + i);
     float4 y = __ldcs(reinterpret_cast<const float4*>(Y) + i);
+    if (dpart) {
+      cnt += __popc(__vcmpne4(w, 0u)) >> 3;
+      if (dterm) {
+        if (w & 0xffu) acc += dterm_c(dterm, y.x);
+        if (w & 0xff00u) acc += dterm_c(dterm, y.y);
+        if (w & 0xff0000u) acc += dterm_c(dterm, y.z);
+        if (w & 0xff000000u) acc += dterm_c(dterm, y.w);
+      }
+    }
     // observed: + 0 turns -0 into +0 (the kernel reads the sign); missing: -1
     y.x = (w & 0xffu) ? y.x + 0.f : -1.f;
     y.y = (w & 0xff00u) ? y.y + 0.f : -1.f;
@@ -454,11 +492,17 @@ __global__ void sentinel_kernel(const float* __restrict__ Y, const uint8_t* __re
     y.w = (w & 0xff000000u) ? y.w + 0.f : -1.f;
     __stcs(reinterpret_cast<float4*>(out) + i, y);
   }
+  if (dpart) sent_block_sum(acc, cnt, dpart, dcpart, blockIdx.x);
 }
 __global__ void sentinel_tail_kernel(const float* __restrict__ Y, const uint8_t* __restrict__ M, float* __restrict__ out,
-                                     long long from, long long n) {
-  for (long long i = from + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+                                     long long from, long long n, int dterm, double* dpart, long long* dcpart, int slot) {
+  double acc = 0.0;
+  long long cnt = 0;
+  for (long long i = from + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
+    if (M[i]) { ++cnt; acc += dterm_c(dterm, Y[i]); }
     out[i] = M[i] ? Y[i] + 0.f : -1.f;
+  }
+  if (dpart) sent_block_sum(acc, cnt, dpart, dcpart, slot + blockIdx.x);
 }
 
 __global__ void pad_rows_kernel(const float* __restrict__ src, float* __restrict__ dst, long long rows, int K, int Kp) {
@@ -510,7 +554,7 @@ cudaError_t launch_update(float* theta, const float* num, const float* den, int6
 }
 
 __global__ void loss_reduce_kernel(const double* __restrict__ part, const long long* __restrict__ cpart, long long n,
-                                   double* slot, long long* cslot) {
+                                   double* slot, long long* cslot, double scale, const double* off) {
   __shared__ double red[256];
   __shared__ long long redc[256];
   double acc = 0.0;
@@ -523,12 +567,16 @@ __global__ void loss_reduce_kernel(const double* __restrict__ part, const long l
     if ((int)threadIdx.x < w) { red[threadIdx.x] += red[threadIdx.x + w]; redc[threadIdx.x] += redc[threadIdx.x + w]; }
     __syncthreads();
   }
-  if (threadIdx.x == 0) { *slot = red[0]; *cslot = redc[0]; }
+  if (threadIdx.x == 0) {
+    // off (R25): [data-only loss sum][observed count] of the sentinel pass
+    *slot = off ? scale * red[0] + off[0] : red[0];
+    *cslot = off ? reinterpret_cast<const long long*>(off)[1] : redc[0];
+  }
 }
 
 cudaError_t launch_loss_reduce(const double* part, const long long* cpart, int64_t n, double* slot, long long* cslot,
-                               cudaStream_t s) {
-  loss_reduce_kernel<<<1, 256, 0, s>>>(part, cpart, n, slot, cslot);
+                               cudaStream_t s, double scale, const double* off) {
+  loss_reduce_kernel<<<1, 256, 0, s>>>(part, cpart, n, slot, cslot, scale, off);
   return cudaGetLastError();
 }
 
@@ -539,11 +587,19 @@ cudaError_t launch_pad_rows(const float* src, float* dst, int64_t rows, int64_t 
   return cudaGetLastError();
 }
 
-cudaError_t launch_sentinel(const float* Y, const uint8_t* M, float* out, int64_t n, cudaStream_t s) {
+cudaError_t launch_sentinel(const float* Y, const uint8_t* M, float* out, int64_t n, int dterm, double* dpart,
+                            long long* dcpart, double* dslot, long long* dcslot, cudaStream_t s) {
   const bool vec = (((reinterpret_cast<uintptr_t>(Y) | reinterpret_cast<uintptr_t>(out)) & 15) | (reinterpret_cast<uintptr_t>(M) & 3)) == 0;
   const long long n4 = vec ? n / 4 : 0;
-  if (n4 > 0) sentinel_kernel<<<148 * 16, 256, 0, s>>>(Y, M, out, n4);
-  if (n4 * 4 < n) sentinel_tail_kernel<<<148, 256, 0, s>>>(Y, M, out, n4 * 4, n);
+  // every one of the kSentBlocks + 1 partials is written (fixed grids), then summed in fixed order
+  if (vec) {
+    sentinel_kernel<<<kSentBlocks, 256, 0, s>>>(Y, M, out, n4, dterm, dpart, dcpart);
+    sentinel_tail_kernel<<<1, 256, 0, s>>>(Y, M, out, n4 * 4, n, dterm, dpart, dcpart, kSentBlocks);
+  } else {
+    sentinel_tail_kernel<<<kSentBlocks, 256, 0, s>>>(Y, M, out, 0, n, dterm, dpart, dcpart, 0);
+    sentinel_tail_kernel<<<1, 256, 0, s>>>(Y, M, out, n, n, dterm, dpart, dcpart, kSentBlocks);
+  }
+  if (dpart) loss_reduce_kernel<<<1, 256, 0, s>>>(dpart, dcpart, kSentBlocks + 1, dslot, dcslot, 1.0, nullptr);
   return cudaGetLastError();
 }
 

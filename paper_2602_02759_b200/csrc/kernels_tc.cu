@@ -24,6 +24,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 
 #include "divergence.cuh"
@@ -572,9 +573,17 @@ __device__ __forceinline__ void vtile_store(const TcArgs& a, int xw, int lane, c
 // ------------------------------------------------------------------ elementwise stage
 // Row m's 16 Y values of half-step h of column half g (tile columns [32g + 16h, +16)) and
 // their mask bytes, four per word (missing values are loaded but only ever feed discarded
-// lanes).  h is a runtime value: one code instance serves both half-steps (I-cache).
+// lanes).  Layouts 1 / 2 keep Y in SW128 128-byte lines of 32 columns: line yl at byte yoff,
+// 16-byte chunk j stored at chunk j ^ (yl & 7) - two [128 rows][32] boxes (line m of half g)
+// or, with a.y3d, one [128 rows][2 halves][32] box (line 2m + g); yoff / yswz are per-warp
+// constants computed once (ew_y_line).
+__device__ __forceinline__ void ew_y_line(const TcArgs& a, int g, int m, int& yoff, int& yswz) {
+  const int yl = a.y3d ? 2 * m + g : m;
+  yoff = a.y3d ? yl * 128 : g * (Y_STAGE / 2) + m * 128;
+  yswz = yl & 7;
+}
 __device__ __forceinline__ void ew_load_y(const TcArgs& a, const unsigned char* ys, const unsigned char* ms, int g,
-                                          int h, int m, float (&yv)[16], uint32_t (&mk)[4]) {
+                                          int h, int m, int yoff, int yswz, float (&yv)[16], uint32_t (&mk)[4]) {
   const int c0 = 32 * g + 16 * h;
   if (a.layout == 0) {
     // [64 columns][128 rows] fp32 / uint8, rows contiguous: lane = row, conflict-free
@@ -592,14 +601,16 @@ __device__ __forceinline__ void ew_load_y(const TcArgs& a, const unsigned char* 
       }
     }
   } else {
-    // SW128 boxes of [128 rows][32 columns] fp32 (one per column half); SW64 [128][64] uint8
-    const unsigned char* sub = ys + g * (Y_STAGE / 2) + m * 128;
+    // (a.y3d: rows m and m + 4 share a swizzle phase -> 2-way bank conflict, cheaper than
+    // reading the chunk pairs swapped and selecting them back)
+    const unsigned char* sub = ys + yoff;
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      const float4 f = *reinterpret_cast<const float4*>(sub + (((4 * h + q) ^ (m & 7)) << 4));
+      const float4 f = *reinterpret_cast<const float4*>(sub + (((4 * h + q) ^ yswz) << 4));
       yv[4 * q] = f.x; yv[4 * q + 1] = f.y; yv[4 * q + 2] = f.z; yv[4 * q + 3] = f.w;
     }
     if (a.has_mask) {
+      // SW64 [128 rows][64] uint8
       const int q = 2 * g + h;
       const uint4 w = *reinterpret_cast<const uint4*>(ms + m * 64 + ((q ^ ((m >> 1) & 3)) << 4));
       mk[0] = w.x; mk[1] = w.y; mk[2] = w.z; mk[3] = w.w;
@@ -674,6 +685,25 @@ __device__ __forceinline__ void ew_half_sent(const TcArgs& a, uint32_t (&sv)[16]
   if (vbits != 0xffffu) {
 #pragma unroll
     for (int j = 0; j < 16; ++j) yv[j] = ((vbits >> j) & 1u) ? yv[j] : -1.f;
+  }
+  if constexpr (LossOff<KIND>::value) {
+    if (a.mode != 0 && a.lconst) {   // loss without its data-only part (R25; count from the sentinel pass)
+      float2 l2 = make_float2(0.f, 0.f);
+#pragma unroll
+      for (int j = 0; j < 16; j += 2) {
+        const float2 x = make_float2(yv[j], yv[j + 1]);
+        const float2 yh = make_float2(fmaxf(__uint_as_float(sv[j]), 1e-30f), fmaxf(__uint_as_float(sv[j + 1]), 1e-30f));
+        float2 av, bv, rv;
+        LossOff<KIND>::abr2(x, yh, av, bv, rv);
+        l2 = __fadd2_rn(l2, make_float2(x.x >= 0.f ? rv.x : 0.f, x.y >= 0.f ? rv.y : 0.f));
+        sv[j] = (uint32_t)__viaddmax_s32(__float_as_int(av.x), 0x1000, 0);
+        sv[j + 1] = (uint32_t)__viaddmax_s32(__float_as_int(av.y), 0x1000, 0);
+        pb[j] = (uint32_t)__viaddmax_s32(__float_as_int(copysignf(bv.x, x.x)), 0x1000, 0);
+        pb[j + 1] = (uint32_t)__viaddmax_s32(__float_as_int(copysignf(bv.y, x.y)), 0x1000, 0);
+      }
+      lsum += l2.x + l2.y;
+      return;
+    }
   }
   if (a.mode != 0) {   // loss of the iterate entering the sweep (uniform branch)
     // a, b and the loss from |x| (a missing entry's -1 becomes a harmless 1), then the sign of x
@@ -925,8 +955,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
         } else {
           const int64_t ti = tile % a.tiles_inner, to = tile / a.tiles_inner;
           if (a.layout == 1) {
-            tma_load_2d(dY, &P.tmY, (int)(ti * BN), (int)row0, bar);
-            tma_load_2d(dY + Y_STAGE / 2, &P.tmY, (int)(ti * BN + 32), (int)row0, bar);
+            if (a.y3d) {
+              tma_load_3d(dY, &P.tmY, 0, (int)(ti * 2), (int)row0, bar);
+            } else {
+              tma_load_2d(dY, &P.tmY, (int)(ti * BN), (int)row0, bar);
+              tma_load_2d(dY + Y_STAGE / 2, &P.tmY, (int)(ti * BN + 32), (int)row0, bar);
+            }
             if (a.has_mask) tma_load_2d(dM, &P.tmM, (int)(ti * BN), (int)row0, bar);
           } else {
             tma_load_3d(dY, &P.tmY, (int)(ti * BN), (int)row0, (int)to, bar);
@@ -1097,6 +1131,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
     const int qd = warp & 3;               // TMEM lane quarter
     const int m = qd * 32 + lane;          // row within the block (= TMEM lane)
     const uint32_t lane_off = (uint32_t)(qd * 32) << 16;
+    int yoff, yswz;
+    ew_y_line(a, cg >> 1, m, yoff, yswz);
     const int64_t row = row0 + m;
     const bool row_ok = m < rows_here;
     constexpr int NCH = KB / 16;           // 16-column chunks of U_hi (and of U_lo, N, D)
@@ -1175,7 +1211,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
       tmem_ld16(tc, sv);
       mbar_spin(y_full + 8 * st, (t / NS) & 1);
       if (warp == W_EW0 && lane == 0) trace_ev(a, t, EV_EW_Y);
-      ew_load_y(a, gY + st * Y_STAGE, gM + st * M_STAGE, cg >> 1, cg & 1, m, yv, mk);   // (MM == 0: a.has_mask = 0)
+      ew_load_y(a, gY + st * Y_STAGE, gM + st * M_STAGE, cg >> 1, cg & 1, m, yoff, yswz, yv, mk);   // (MM == 0: a.has_mask = 0)
       tmem_ld_wait(sv);
       __syncwarp();
       if (lane == 0) mbar_arrive(y_empty + 8 * st);  // Y / mask stage read by this warp
@@ -1248,6 +1284,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
 
 // ------------------------------------------------------------------ host side
 static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+// NEF_NO_Y3D=1 (diagnostics): layout 1 with two 2-D boxes per tile
+static const bool g_no_y3d = [] { const char* e = std::getenv("NEF_NO_Y3D"); return e && e[0] == '1'; }();
 
 static bool get_encode() {
   if (g_encode) return true;
@@ -1311,14 +1349,25 @@ cudaError_t launch(const TcArgs& args, const float* Y, const uint8_t* M, int64_t
       ok = encode(&P.tmM, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, M, d, sm, by, CU_TENSOR_MAP_SWIZZLE_NONE);
     }
   } else if (L == 1) {
-    uint64_t d[2] = {(uint64_t)args.CI, (uint64_t)args.R};
-    uint64_t sy[1] = {(uint64_t)args.CI * 4};
-    uint32_t by[2] = {32, 128};
-    ok = encode(&P.tmY, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, Y, d, sy, by, CU_TENSOR_MAP_SWIZZLE_128B);
+    P.a.y3d = (args.CI % 32 == 0 && !g_no_y3d) ? 1 : 0;
+    if (P.a.y3d) {
+      // {32, CI/32, R}: a box {32, 2, 128} fetches both 128-byte halves of each row back to back
+      // (ubench/tma_stream: 7.0 TB/s streaming vs 4.5 TB/s for two {32, 128} boxes per tile)
+      uint64_t d[3] = {32, (uint64_t)args.CI / 32, (uint64_t)args.R};
+      uint64_t sy[2] = {128, (uint64_t)args.CI * 4};
+      uint32_t by[3] = {32, 2, 128};
+      ok = encode(&P.tmY, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, Y, d, sy, by, CU_TENSOR_MAP_SWIZZLE_128B);
+    } else {
+      uint64_t d[2] = {(uint64_t)args.CI, (uint64_t)args.R};
+      uint64_t sy[1] = {(uint64_t)args.CI * 4};
+      uint32_t by[2] = {32, 128};
+      ok = encode(&P.tmY, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, Y, d, sy, by, CU_TENSOR_MAP_SWIZZLE_128B);
+    }
     if (ok && M) {
+      uint64_t dm[2] = {(uint64_t)args.CI, (uint64_t)args.R};
       uint64_t sm[1] = {(uint64_t)args.CI};
       uint32_t bm[2] = {64, 128};
-      ok = encode(&P.tmM, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, M, d, sm, bm, CU_TENSOR_MAP_SWIZZLE_64B);
+      ok = encode(&P.tmM, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, M, dm, sm, bm, CU_TENSOR_MAP_SWIZZLE_64B);
     }
   } else {
     uint64_t d[3] = {(uint64_t)args.CI, (uint64_t)args.R, (uint64_t)args.CO};

@@ -46,6 +46,11 @@ struct TcArgs {
   int64_t vd_tpr;             // tiles per run
   int64_t vd_pitch;           // row pitch (elements) of vd_rows_ptr (K rounded up to 4)
   const float* vd_rows_ptr;   // the table rows the TMA reads (the table, or its padded copy)
+  int y3d;                    // layout 1 with CI % 32 == 0: Y tile = ONE 3-D TMA box {32, 2, 128}
+                              //   over the view {32, CI/32, R} (both 128-byte halves of a row
+                              //   requested back to back), smem [row][half][32] SW128
+  int lconst;                 // loss passes accumulate only the factor-dependent part (R25):
+                              //   LossOff<KIND>, the data-only sum comes from the sentinel pass
   int drain_tiles;            // N / D drained into a separate split partial every this many tiles
   int64_t n_groups;           // drain groups per chunk: Qpart is [chunks][n_groups][2][n_rows][K]
   int dbg;                    // diagnostics: 1 prefill N/D with 1 and always accumulate,

@@ -12,6 +12,7 @@ namespace nef {
 constexpr int kMaxDims = 8;      // max indices per operand / per einsum step side
 constexpr int kMaxTabs = 4;      // max KR tables on the column side of a lowering
 constexpr int kMaxModes = 8;     // max observed modes
+constexpr int kSentParts = 148 * 16 + 1;   // sentinel pass block partials (kernels.h kSentBlocks + 1)
 // tcgen05 path: the tensor core's fp32 accumulation truncates, so the numerator / denominator
 // accumulators are drained to separate split partials every kDrainTiles tiles (<= 2048
 // truncating accumulation steps per partial; summed in fp64 by reduce_q)
@@ -121,6 +122,8 @@ struct Plan {
   int64_t n_local = 0;               // local entries
   size_t ws_bytes = 0;
   int64_t ws_trace = 0;              // fp64 trace accumulators
+  int64_t ws_dterm = 0;              // [double][long long]: data-only loss sum, observed count (R25)
+  int64_t ws_dpart = 0;              // their kSentParts block partials (doubles, then counts)
   int64_t ws_sent = 0;               // NaN-sentinel copy of Y (nef_fit with a mask)
   // sharding
   int shard_mode = -1, rank = 0, world = 1;

@@ -560,8 +560,11 @@ int lower_all(Plan& p, std::string& err) {
     p.low[ell] = std::move(L);
   }
   p.ws_trace = (ws + 255) / 256 * 256;
+  // sentinel pass sums (R25): [data-only loss sum][observed count], then its block partials
+  p.ws_dterm = p.ws_trace + (int64_t)8 * 4096;
+  p.ws_dpart = p.ws_dterm + 256;
   // NaN-sentinel copy of the local Y (nef_fit with a mask, R5): 4 B per local entry
-  p.ws_sent = (p.ws_trace + (int64_t)8 * 4096 + 256 + 255) / 256 * 256;
+  p.ws_sent = (p.ws_dpart + (int64_t)16 * (kSentParts) + 255) / 256 * 256;
   p.ws_bytes = (size_t)(p.ws_sent + p.n_local * 4 + 256);
   return NEF_OK;
 }
@@ -671,7 +674,7 @@ std::string describe_plan(const Plan& p) {
     o << (l ? "," : "") << "{\"ell\":" << L.ell << ",\"row_idx\":\"" << L.row_idx << "\",\"col_idx\":\"" << L.col_idx
       << "\",\"bond\":\"" << L.bond << "\",\"K\":" << L.K << ",\"n_rows\":" << L.n_rows << ",\"n_cols\":" << L.n_cols
       << ",\"row_fast\":" << (L.row_fast ? "true" : "false") << ",\"n_chunks\":" << L.n_chunks
-      << ",\"tc\":" << (L.tc_ok ? "true" : "false") << ",\"tc_layout\":" << L.tc_layout << ",\"tc_R\":" << L.tc_R
+      << ",\"tc\":" << (L.tc_ok ? "true" : "false") << ",\"tc_mask_ok\":" << (L.tc_mask_ok ? "true" : "false") << ",\"tc_layout\":" << L.tc_layout << ",\"tc_R\":" << L.tc_R
       << ",\"tc_CI\":" << L.tc_CI << ",\"tc_CO\":" << L.tc_CO << ",\"tc_KB\":" << L.tc_KB
       << ",\"tc_tiles\":" << L.tc_tiles << ",\"tc_chunks\":" << L.tc_chunks << ",\"tc_groups\":" << L.tc_groups << ",\"vd_tab\":" << L.vd_tab << ",\"vd_E\":" << L.vd_E << ",\"tabs_merged\":" << (L.tabs_merged ? "true" : "false") << ",\"row_factors\":[";
     for (size_t k = 0; k < L.row_factors.size(); ++k) o << (k ? "," : "") << L.row_factors[k];

@@ -111,6 +111,24 @@ def test_n_observed_exact_and_loss(nef, name):
     assert abs(s - rs) <= 1e-4 * abs(rs)
 
 
+@pytest.mark.parametrize("name", ["c3", "c5", "c2"])
+def test_fit_loss_of_final_factors(nef, name):
+    """The final loss of a masked fit comes from the loss pass over the sentinel copy; for
+    (1,0) and (1,-0.5) (c3, c5) its data-only part is summed once by the sentinel pass and the
+    streamed part carries the rest (R25).  Pinned tightly against the oracle's loss
+    of the GPU's own final factors (no trajectory drift in the comparison).  c2 (Euclidean, whole
+    divergence per entry) is the control: x - yhat in fp32 of a close fit costs it ~4e-5."""
+    tol = 1e-4 if name == "c2" else 1e-5
+    d = generate_numpy(name)
+    Y, M, F = _dev(d)
+    plan = nef.Plan(d["model"], d["shape"], d["ranks"])
+    tr = plan.fit(Y, M, d["alpha"], d["beta"], F, 3)
+    rs, _ = O.loss(d["model"], d["Y"], d["mask"], [f.cpu().numpy() for f in F], d["alpha"], d["beta"])
+    assert abs(tr[-1] - rs) <= tol * abs(rs), (name, tr[-1], rs)
+    r0, _ = O.loss(d["model"], d["Y"], d["mask"], d["init"], d["alpha"], d["beta"])
+    assert abs(tr[0] - r0) <= tol * abs(r0), (name, tr[0], r0)
+
+
 def test_deterministic(nef):
     d = generate_numpy("c3")
     Y, M, F0 = _dev(d)

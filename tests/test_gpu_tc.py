@@ -30,6 +30,10 @@ TC_CASES = [
     ("ia,jb,kc,abc->ijk", (64, 72, 40), (8, 8, 8), (1.0, 1.0), 0.0, "absnormal"),
     # small column space merged into one table (K = 10: padded 16-byte row pitch)
     ("ik,jk,tl,dl,kl->ijtd", (40, 48, 16, 36), (12, 10), (0.5, 0.0), 0.0, "poisson"),
+    # layout 1, CI % 32 != 0: two 2-D Y boxes per tile (the 3-D single-box view needs CI % 32 == 0)
+    ("ir,jr,kr->ijk", (96, 130, 36), (32,), (1.0, -0.5), 0.05, "gamma"),
+    # layout 1, CI % 64 == 32: the last tile's second 32-column half is out of bounds (zero fill)
+    ("ir,jr,kr->ijk", (96, 104, 44), (32,), (1.0, 0.0), 0.2, "poisson"),
 ]
 
 
@@ -87,8 +91,8 @@ def test_first_tile_pa(nef, case):
     yhat = np.maximum(O.contract(ms, init), O.EPS_Y)
     _, out = O.parse(ms)
     for L in d["lowerings"]:
-        if not L["tc"]:
-            continue
+        if not L["tc"] or (M is not None and not L["tc_mask_ok"]):
+            continue   # (num_den streams the uint8 mask: its TMA view needs 16-byte strides)
         buf = torch.full((128 * 64,), -1.0, device="cuda")
         nef.nef_debug_dump(buf)
         try:
