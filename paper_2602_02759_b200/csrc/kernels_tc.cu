@@ -218,6 +218,7 @@ __device__ __forceinline__ void mma_ts_elect(uint32_t d, uint32_t a, uint64_t bd
       "r"(a), "l"(bdesc), "r"(idesc), "r"(acc)
       : "memory");
 }
+#include "mma_blocks.inc"
 __device__ __forceinline__ void mma_commit_elect(uint32_t bar) {
   asm volatile(
       "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
@@ -995,14 +996,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
         __syncwarp();
         const uint64_t vd = sdesc(sV + vs * V_STAGE_MAX, 16, 1024);
         const uint32_t d = tmem + 128 * b;
-#pragma unroll
-        for (int kk = 0; kk < KB / 8; ++kk)
-          mma_ts_elect(d, tUh + kk * 8, vd + (uint64_t)(((kk >> 2) * (BN * 128) + (kk & 3) * 32) >> 4), id1, kk > 0 ? 1u : 0u);
-        if (!(a.dbg & 32)) {   // dbg 32: timing experiment without the U_lo half of the split
-#pragma unroll
-          for (int kk = 0; kk < KB / 8; ++kk)
-            mma_ts_elect(d, tUl + kk * 8, vd + (uint64_t)(((kk >> 2) * (BN * 128) + (kk & 3) * 32) >> 4), id1, 1u);
-        }
+        // one asm block, one elect: U_hi and U_lo steps interleaved (tUl = tUh + KB)
+        if (KB == 64) mma_s_block_64(d, tUh, vd, id1, 0u);
+        else mma_s_block_32(d, tUh, vd, id1, 0u);
         mma_commit_elect(s_full + 8 * b);
       };
       mma_s(0);
@@ -1016,15 +1012,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
         if (a.mode != 2 && !(a.dbg & 64)) {   // dbg 64: timing experiment without N/D MMAs
           // B = V^T, K-major SW128: rows = bond (N), K = tile columns (2 atoms of 32)
           const uint64_t vtd = sdesc(sV + vs * V_STAGE_MAX + VT_OFF, 16, 1024);
-          const uint32_t pa = tmem + 128 * b, pbb = pa + 64;
-#pragma unroll
-          for (int kk = 0; kk < BN / 8; ++kk) {
-            const uint64_t bd = vtd + (uint64_t)(((kk >> 2) * (KB * 128) + (kk & 3) * 32) >> 4);
-            // the accumulators restart at every drain group (see the elementwise loop)
-            const uint32_t acc = ((u % G) != 0 || kk > 0) ? 1u : 0u;
-            mma_ts_elect(tNa, pa + kk * 8, bd, id2, acc);
-            mma_ts_elect(tNb, pbb + kk * 8, bd, id2, acc);
-          }
+          const uint32_t pa = tmem + 128 * b;   // P_a; P_b at pa + 64
+          // the accumulators restart at every drain group (see the elementwise loop)
+          const uint32_t acc = (u % G) != 0 ? 1u : 0u;
+          if (KB == 64) mma_nd_block_64(tNa, tNb, pa, vtd, id2, acc);
+          else mma_nd_block_32(tNa, tNb, pa, vtd, id2, acc);
         }
         mma_commit_elect(v_empty + 8 * vs);
         mma_commit_elect(buf_free + 8 * b);
