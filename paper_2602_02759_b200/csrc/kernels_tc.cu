@@ -35,7 +35,10 @@ namespace nef {
 namespace tc {
 
 constexpr int BM = 128, BN = 64;
-constexpr int NS = 3;        // Y / mask pipeline stages
+#ifndef NEF_NS
+#define NEF_NS 3
+#endif
+constexpr int NS = NEF_NS;   // Y / mask pipeline stages
 // V tile stages: 3 with a uint8 mask stream (its stages take the smem), else 4
 template <int MM> struct VStages { static constexpr int value = MM == 1 ? 3 : 4; };
 // warp roles: 16 elementwise warps, 4 V generators, direct-V row loads, TMA producer, MMA

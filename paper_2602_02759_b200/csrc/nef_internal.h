@@ -17,6 +17,8 @@ constexpr int kSentParts = 148 * 16 + 1;   // sentinel pass block partials (kern
 // accumulators are drained to separate split partials every kDrainTiles tiles (<= 2048
 // truncating accumulation steps per partial; summed in fp64 by reduce_q)
 constexpr int kDrainTiles = 256;
+// tcgen05 path only for factors whose entries each sum at least this many Y entries (R26)
+constexpr int64_t kTcMinSlab = 2048;
 
 // ---------------------------------------------------------------------------------
 // Small einsum engine: C[out] = sum_{sum} A[...] * B[...]   (B optional)

@@ -436,6 +436,15 @@ void tc_geometry(const Plan& p, Lowering& L) {
     // useful width: at least half of every 64-wide column box / 128-row box must be real data
     if (L.tc_layout == 0) ok = ok && R >= 64 && CO >= 32;
     else ok = ok && CI >= 32 && R >= 64;
+    // TF32 operand rounding (R26): an entry of factor ell's numerator / denominator sums the Y
+    // entries of its slab (Y with ell's observed indices fixed), whose RN errors (<= 2^-11
+    // relative each) average as 1/sqrt(slab); small slabs stay on the fp32 FFMA path
+    {
+      int64_t slab = 1;
+      for (size_t m = 0; m < p.out.size(); ++m)
+        if (p.ops[L.ell].find(p.out[m]) == std::string::npos) slab *= p.shape[m];
+      ok = ok && slab >= kTcMinSlab;
+    }
     if (ok) {
       L.tc_ok = true;
       L.tc_row_blocks = (R + 127) / 128;

@@ -1,0 +1,126 @@
+"""Degenerate and edge cases of the CUDA path against the float64 oracle (-m gpu), on shapes
+routed to the tcgen05 kernel and to the CUDA-core kernel:
+
+* a factor row / slab with no observed entry: numerator = denominator = 0, multiplier 1
+  (R10) - the row must come back bit-identical, everything else at the parity bar;
+* an all-missing mask: loss 0, n_observed 0, factors untouched;
+* rank 1 (K = 1: padded 16-byte table rows) and unit modes;
+* mostly-zero data (x = 0 entries: a = 0, loss terms of the x -> 0 limit).
+"""
+import numpy as np
+import pytest
+
+from oracle import nef_oracle as O
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+FACTOR_RTOL = 1e-4
+TRACE_RTOL = 1e-3
+
+
+@pytest.fixture(scope="module")
+def nef():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2602_02759_b200 import nef as n
+    n.nef_set_kernel_policy(0)
+    return n
+
+
+def _rel(a, b):
+    a = np.asarray(a, dtype=np.float64)
+    b = np.asarray(b, dtype=np.float64)
+    return float(np.max(np.abs(a - b) / np.maximum(np.abs(b), 1e-30)))
+
+
+def _problem(ms, shape, ranks, seed, zero_frac=0.0):
+    rng = np.random.default_rng(seed)
+    fs = O.factor_shapes(ms, shape, ranks)
+    truth = [rng.gamma(1.0, 1.0, s) for s in fs]
+    Y = rng.poisson(O.contract(ms, truth)).astype(np.float32) + 0.25
+    if zero_frac > 0:
+        Y[rng.random(shape) < zero_frac] = 0.0
+    init = [rng.uniform(0.1, 1, s).astype(np.float32) for s in fs]
+    return Y, init
+
+
+def _fit(nef, ms, shape, ranks, Y, M, init, ab, iters):
+    plan = nef.Plan(ms, shape, ranks)
+    F = [torch.from_numpy(f.copy()).cuda() for f in init]
+    Md = torch.from_numpy(M).cuda() if M is not None else None
+    tr = plan.fit(torch.from_numpy(Y).cuda(), Md, ab[0], ab[1], F, iters)
+    torch.cuda.synchronize()
+    return plan, [f.cpu().numpy() for f in F], tr
+
+
+# (model, shape, ranks, (alpha, beta)): tcgen05-routed CP shapes and a CUDA-core one
+SLAB_CASES = [
+    ("ir,jr,kr->ijk", (144, 80, 112), (64,), (1.0, -0.5)),   # c5-like, tcgen05
+    ("ir,jr,kr->ijk", (160, 144, 96), (32,), (1.0, 0.0)),    # c3-like, tcgen05
+    ("ir,jr,kr->ijk", (50, 40, 30), (5,), (1.0, 0.0)),       # c1 shape, CUDA-core
+]
+
+
+@pytest.mark.parametrize("case", SLAB_CASES, ids=lambda c: "x".join(map(str, c[1])))
+def test_unobserved_slabs_keep_their_rows(nef, case):
+    ms, shape, ranks, ab = case
+    Y, init = _problem(ms, shape, ranks, seed=5)
+    rng = np.random.default_rng(6)
+    M = (rng.random(shape) > 0.1).astype(np.uint8)
+    M[5, :, :] = 0          # factor 0 row 5: no observed entry
+    M[:, 7, :] = 0          # factor 1 row 7
+    M[:, :, 0] = 0          # factor 2 row 0
+    plan, F, tr = _fit(nef, ms, shape, ranks, Y, M, init, ab, 1)
+    assert plan.describe()["lowerings"][0]["tc"] == (shape[0] > 64)
+    ref, rtr = O.fit(ms, Y, M, init, ab[0], ab[1], 1)
+    for ell, (g, r) in enumerate(zip(F, ref)):
+        assert _rel(g, r) <= FACTOR_RTOL, (ell, _rel(g, r))
+    # R10: multiplier 1 -> bit-identical rows
+    assert np.array_equal(F[0][5], init[0][5])
+    assert np.array_equal(F[1][7], init[1][7])
+    assert np.array_equal(F[2][0], init[2][0])
+    assert _rel(tr, rtr) <= TRACE_RTOL
+
+
+@pytest.mark.parametrize("case", SLAB_CASES, ids=lambda c: "x".join(map(str, c[1])))
+def test_all_missing(nef, case):
+    ms, shape, ranks, ab = case
+    Y, init = _problem(ms, shape, ranks, seed=7)
+    M = np.zeros(shape, dtype=np.uint8)
+    plan, F, tr = _fit(nef, ms, shape, ranks, Y, M, init, ab, 2)
+    assert list(tr) == [0.0, 0.0, 0.0]
+    for g, f in zip(F, init):
+        assert np.array_equal(g, f)
+    s, n = plan.loss(torch.from_numpy(Y).cuda(), torch.from_numpy(M).cuda(), ab[0], ab[1],
+                     [torch.from_numpy(f).cuda() for f in init])
+    assert s == 0.0 and n == 0
+
+
+@pytest.mark.parametrize("ms,shape,ranks,ab,pm", [
+    ("ir,jr,kr->ijk", (160, 64, 96), (1,), (1.0, -0.5), 0.05),    # rank 1
+    ("ir,jr,kr->ijk", (130, 1, 192), (16,), (1.0, 0.0), 0.2),     # unit middle mode
+    ("ir,jr,kr->ijk", (1, 96, 128), (8,), (1.0, 1.0), 0.0),       # unit leading mode
+])
+def test_rank1_and_unit_modes(nef, ms, shape, ranks, ab, pm):
+    Y, init = _problem(ms, shape, ranks, seed=9)
+    M = (np.random.default_rng(10).random(shape) >= pm).astype(np.uint8) if pm > 0 else None
+    _, F, tr = _fit(nef, ms, shape, ranks, Y, M, init, ab, 1)   # the factor bar: after 1 sweep
+    ref, rtr = O.fit(ms, Y, M, init, ab[0], ab[1], 1)
+    for ell, (g, r) in enumerate(zip(F, ref)):
+        assert _rel(g, r) <= FACTOR_RTOL, (ell, _rel(g, r))
+    _, _, tr = _fit(nef, ms, shape, ranks, Y, M, init, ab, 4)
+    _, rtr = O.fit(ms, Y, M, init, ab[0], ab[1], 4)
+    assert _rel(tr, rtr) <= TRACE_RTOL
+
+
+@pytest.mark.parametrize("ab", [(1.0, 0.0), (1.0, -0.5), (0.5, 0.0), (1.0, 1.0)])
+def test_mostly_zero_data(nef, ab):
+    ms, shape, ranks = "ir,jr,kr->ijk", (144, 80, 112), (32,)
+    Y, init = _problem(ms, shape, ranks, seed=11, zero_frac=0.8)
+    M = (np.random.default_rng(12).random(shape) > 0.1).astype(np.uint8)
+    _, F, tr = _fit(nef, ms, shape, ranks, Y, M, init, ab, 1)
+    ref, rtr = O.fit(ms, Y, M, init, ab[0], ab[1], 1)
+    for ell, (g, r) in enumerate(zip(F, ref)):
+        assert _rel(g, r) <= FACTOR_RTOL, (ell, _rel(g, r))
+    assert _rel(tr, rtr) <= TRACE_RTOL
