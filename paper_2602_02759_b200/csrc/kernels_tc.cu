@@ -51,6 +51,10 @@ template <int MM> struct VStages { static constexpr int value = MM == 1 ? 3 : 4;
 #if NEF_WARP_MAP == 0
 constexpr int W_EW0 = 0, W_VG0 = 16, W_DV = 20, W_TMA = 21, W_MMA = 22;
 __device__ __forceinline__ int vg_index(int warp) { return warp >= 16 && warp < 20 ? warp - 16 : -1; }
+#elif NEF_WARP_MAP == 3
+// MMA issuer on sub-partition 3 (the one without a producer besides its V generator); warp 22 idle
+constexpr int W_EW0 = 0, W_VG0 = 16, W_DV = 20, W_TMA = 21, W_MMA = 23;
+__device__ __forceinline__ int vg_index(int warp) { return warp >= 16 && warp < 20 ? warp - 16 : -1; }
 #else
 // the MMA issuer's sub-partition (2) hosts no V generator: V generators on warps 16, 17, 19, 20
 // (sub-partitions 0, 1, 3, 0), TMA producer 21 (1), MMA issuer 22 (2), V-row loads 23 (3)
@@ -61,7 +65,7 @@ __device__ __forceinline__ int vg_index(int warp) {
 #endif
 constexpr int NVG = 4;       // V-generator warps (16 tile columns each)
 constexpr int NEW = 16;      // elementwise warps: 4 TMEM lane quarters x 4 groups of 16 columns
-constexpr int NTHREADS = (NEF_WARP_MAP == 0 ? 23 : 24) * 32;
+constexpr int NTHREADS = (NEF_WARP_MAP == 0 ? 23 : 24) * 32;   // (map 3: warp 22 idle)
 constexpr int Y_STAGE = BM * BN * 4;      // 32 KB
 constexpr int M_STAGE = BM * BN;          // 8 KB
 constexpr int VT_OFF = BN * 64 * 4;       // V^T copy after V inside a stage
@@ -1000,8 +1004,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
         const uint64_t vd = sdesc(sV + vs * V_STAGE_MAX, 16, 1024);
         const uint32_t d = tmem + 128 * b;
         // one asm block, one elect: U_hi and U_lo steps interleaved (tUl = tUh + KB)
-        if (KB == 64) mma_s_block_64(d, tUh, vd, id1, 0u);
-        else mma_s_block_32(d, tUh, vd, id1, 0u);
+        if (KB == 64) mma_s_block_64<id1>(d, tUh, vd, 0u);
+        else mma_s_block_32<id1>(d, tUh, vd, 0u);
         mma_commit_elect(s_full + 8 * b);
       };
       mma_s(0);
@@ -1018,8 +1022,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
           const uint32_t pa = tmem + 128 * b;   // P_a; P_b at pa + 64
           // the accumulators restart at every drain group (see the elementwise loop)
           const uint32_t acc = (u % G) != 0 ? 1u : 0u;
-          if (KB == 64) mma_nd_block_64(tNa, tNb, pa, vtd, id2, acc);
-          else mma_nd_block_32(tNa, tNb, pa, vtd, id2, acc);
+          if (KB == 64) mma_nd_block_64<id2>(tNa, tNb, pa, vtd, acc);
+          else mma_nd_block_32<id2>(tNa, tNb, pa, vtd, acc);
         }
         mma_commit_elect(v_empty + 8 * vs);
         mma_commit_elect(buf_free + 8 * b);
