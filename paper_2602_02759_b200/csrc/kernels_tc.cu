@@ -45,6 +45,9 @@ template <int MM> struct VStages { static constexpr int value = MM == 1 ? 3 : 4;
 // issuer.  The warp schedulers favour higher warp ids, so the producers whose latency is on the
 // critical path sit above the elementwise warps (with the producers below, the V generators
 // and the MMA issuer starved during the elementwise phase of every tile).
+#ifndef NEF_Y_FIRST
+#define NEF_Y_FIRST 0
+#endif
 #ifndef NEF_WARP_MAP
 #define NEF_WARP_MAP 0
 #endif
@@ -1200,17 +1203,29 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
       const int cols_here = (int)(crem < BN ? crem : BN);
       const int st = t % NS;
       const uint32_t tc = tmem + 128 * b + lane_off + 16 * cg;   // S / P_a columns of this warp
-      mbar_wait_ew(s_full + 8 * b, (t >> 1) & 1);
-      if (warp == W_EW0 && lane == 0) trace_ev(a, t, EV_EW_S);
-      tc_fence_after();
       float lsum = 0.f;
       uint32_t sv[16], pb[16];
       float yv[16];
       uint32_t mk[4] = {0u, 0u, 0u, 0u};
+#if NEF_Y_FIRST
+      // Y(t) landed long before S(t) (the TMA runs NS tiles ahead): its shared loads issued
+      // before the wait for S (measured: no gain, default off)
+      mbar_spin(y_full + 8 * st, (t / NS) & 1);
+      if (warp == W_EW0 && lane == 0) trace_ev(a, t, EV_EW_Y);
+      ew_load_y(a, gY + st * Y_STAGE, gM + st * M_STAGE, cg >> 1, cg & 1, m, yoff, yswz, yv, mk);   // (MM == 0: a.has_mask = 0)
+      mbar_wait_ew(s_full + 8 * b, (t >> 1) & 1);
+      if (warp == W_EW0 && lane == 0) trace_ev(a, t, EV_EW_S);
+      tc_fence_after();
+      tmem_ld16(tc, sv);
+#else
+      mbar_wait_ew(s_full + 8 * b, (t >> 1) & 1);
+      if (warp == W_EW0 && lane == 0) trace_ev(a, t, EV_EW_S);
+      tc_fence_after();
       tmem_ld16(tc, sv);
       mbar_spin(y_full + 8 * st, (t / NS) & 1);
       if (warp == W_EW0 && lane == 0) trace_ev(a, t, EV_EW_Y);
       ew_load_y(a, gY + st * Y_STAGE, gM + st * M_STAGE, cg >> 1, cg & 1, m, yoff, yswz, yv, mk);   // (MM == 0: a.has_mask = 0)
+#endif
       tmem_ld_wait(sv);
       __syncwarp();
       if (lane == 0) mbar_arrive(y_empty + 8 * st);  // Y / mask stage read by this warp
