@@ -45,6 +45,9 @@ template <int MM> struct VStages { static constexpr int value = MM == 1 ? 3 : 4;
 // issuer.  The warp schedulers favour higher warp ids, so the producers whose latency is on the
 // critical path sit above the elementwise warps (with the producers below, the V generators
 // and the MMA issuer starved during the elementwise phase of every tile).
+#ifndef NEF_EW_BAR
+#define NEF_EW_BAR 0
+#endif
 #ifndef NEF_Y_FIRST
 #define NEF_Y_FIRST 0
 #endif
@@ -1218,7 +1221,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
       tc_fence_after();
       tmem_ld16(tc, sv);
 #else
+#if NEF_EW_BAR
+      // one elementwise warp polls S(t)'s barrier; the other 15 block on a named barrier (no
+      // polling: their issue slots go to the warps that compute)
+      if (warp == W_EW0 + NEW - 1) mbar_wait_ew(s_full + 8 * b, (t >> 1) & 1);
+      asm volatile("bar.sync 2, %0;" ::"n"(NEW * 32) : "memory");
+#else
       mbar_wait_ew(s_full + 8 * b, (t >> 1) & 1);
+#endif
       if (warp == W_EW0 && lane == 0) trace_ev(a, t, EV_EW_S);
       tc_fence_after();
       tmem_ld16(tc, sv);

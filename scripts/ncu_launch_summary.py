@@ -25,7 +25,9 @@ for r in rows[1:]:
 agg = collections.defaultdict(list)
 for (i, k), m in launch.items():
     agg[k].append(m)
-ours = {k for k in agg if k.startswith(("nef::", "tc::", "void tc::", "void nef::")) or "sentinel" in k or "pad_rows" in k}
+OUR_NAMES = ("sentinel", "pad_rows", "reduce_q_kernel", "update_kernel", "loss_reduce_kernel", "einstep_kernel",
+             "fused_ffma_kernel", "fused_tc_kernel")
+ours = {k for k in agg if k.startswith(("nef::", "tc::", "void tc::", "void nef::")) or any(n in k for n in OUR_NAMES)}
 t = lambda ms: sum(x.get("gpu__time_duration.sum", 0.0) for x in ms)
 tot_ours = sum(t(v) for k, v in agg.items() if k in ours)
 tot_all = sum(t(v) for v in agg.values())
