@@ -17,15 +17,17 @@ ap.add_argument("--config", default="c5")
 ap.add_argument("--ell", type=int, default=0)
 ap.add_argument("--first", type=int, default=200)
 ap.add_argument("--n", type=int, default=8)
+ap.add_argument("--nomask", action="store_true", help="unmasked update (the MM = 0 kernel the fit runs on the sentinel copy)")
 args = ap.parse_args()
 cfg = CONFIGS[args.config]
 d = generate_torch(args.config, torch.device("cuda"))
 plan = nef.Plan(cfg.model, cfg.shape, cfg.ranks)
 F = [f.clone() for f in d["init"]]
-plan.update(args.ell, d["Y"], d["mask"], cfg.alpha, cfg.beta, F)
+M = None if args.nomask else d["mask"]
+plan.update(args.ell, d["Y"], M, cfg.alpha, cfg.beta, F)
 tr = torch.zeros(1024 * 32, dtype=torch.int64, device="cuda")
 nef.nef_debug_trace(tr)
-plan.update(args.ell, d["Y"], d["mask"], cfg.alpha, cfg.beta, F)
+plan.update(args.ell, d["Y"], M, cfg.alpha, cfg.beta, F)
 torch.cuda.synchronize()
 nef.nef_debug_trace(None)
 full = tr.cpu().numpy().reshape(1024, 32).astype(np.int64)
