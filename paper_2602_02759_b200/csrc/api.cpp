@@ -288,7 +288,7 @@ int stream_pass(const Ctx& c, const nef::Lowering& L, const float* Y, const uint
     t.countpart = reinterpret_cast<long long*>(c.ws + L.ws_tc_losspart + o.nparts * 8);
     t.dv = dv;
     t.mode = mode;
-    t.lconst = (sent && c.loff && mode != 0) ? 1 : 0;
+    t.lconst = ((sent || !M) && c.loff && mode != 0) ? 1 : 0;
     t.debug = g_debug;
     t.trace = g_trace;
     {
@@ -546,25 +546,38 @@ int nef_fit(nef_plan_t plan, const float* Y, const uint8_t* mask, double alpha, 
   nef::UpdArgs u = nef::make_upd(alpha, beta, eps);
   // a1 precompute (once per fit): fold the mask into a NaN-sentinel copy of Y for the tcgen05
   // passes (R5: missing values are never used, whatever Y holds there)
+  // R25: for the pairs that split the loss, its data-only part is summed once per fit (with the
+  // sentinel copy when there is a mask, else by a read-only pass) when the loss-carrying
+  // lowering runs on the tcgen05 kernel
+  const int dterm = (g_no_lconst || g_policy != 0) ? 0
+                    : dv.kind == nef::EW_B_M05   ? 1
+                    : dv.kind == nef::EW_KL      ? 2
+                    : dv.kind == nef::EW_A05_B0  ? 3
+                                                 : 0;
+  const double lscale = dterm == 1 ? 2.0 : dterm == 3 ? 4.0 : 1.0;
+  double* dslot = reinterpret_cast<double*>(c.ws + p.ws_dterm);
+  double* dpart = reinterpret_cast<double*>(c.ws + p.ws_dpart);
+  long long* dcpart = reinterpret_cast<long long*>(dpart + nef::kSentParts);
   if (mask && g_policy == 0 && !g_no_sentinel) {
     bool any_tc = false;
     for (const auto& L : p.low) any_tc |= L.tc_ok;
     if (any_tc) {
       float* ys = reinterpret_cast<float*>(c.ws + p.ws_sent);
-      // R25: the data-only part of the loss summed once here for the pairs that split it off
-      const int dterm = g_no_lconst ? 0 : dv.kind == nef::EW_B_M05 ? 1 : dv.kind == nef::EW_KL ? 2 : 0;
-      double* dslot = reinterpret_cast<double*>(c.ws + p.ws_dterm);
-      double* dpart = reinterpret_cast<double*>(c.ws + p.ws_dpart);
-      CK(nef::launch_sentinel(Y, mask, ys, p.n_local, dterm, dpart,
-                              reinterpret_cast<long long*>(dpart + nef::kSentParts), dslot,
+      CK(nef::launch_sentinel(Y, mask, ys, p.n_local, dterm, dpart, dcpart, dslot,
                               reinterpret_cast<long long*>(dslot + 1), c.s));
       g_launches += 3;
       c.ysent = ys;
       if (dterm) {
         c.loff = dslot;
-        c.lscale = dterm == 1 ? 2.0 : 1.0;
+        c.lscale = lscale;
       }
     }
+  } else if (!mask && dterm && p.low[0].tc_ok && iters >= 3) {
+    // (the read-only pass costs about what the split saves on two loss-carrying passes)
+    CK(nef::launch_dterm(Y, p.n_local, dterm, dpart, dcpart, dslot, reinterpret_cast<long long*>(dslot + 1), c.s));
+    g_launches += 3;
+    c.loff = dslot;
+    c.lscale = lscale;
   }
   double* slots = reinterpret_cast<double*>(c.ws + p.ws_trace);
   long long* cslots = reinterpret_cast<long long*>(c.ws + p.ws_trace + 8 * 2048);

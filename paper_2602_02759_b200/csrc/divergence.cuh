@@ -361,6 +361,7 @@ struct Ew<EW_A05_B1> {  // (0.5, 1): a = sqrt(x), b = sqrt(y)
 // is  L(x, y) = scale * rem(x, y) + c(x),  with c depending on the data alone:
 //   (1, -0.5): 2 (sqrt x - sqrt y)^2 / sqrt y = 2 (x + y) / sqrt y - 4 sqrt x
 //   (1, 0)   : x log(x / y) - x + y           = (y - x log y) + (x log x - x)
+//   (0.5, 0) : 2 sqrt x log(x / y) - 4 sqrt x + 4 sqrt y = 4 (sqrt y - sqrt x log(y) / 2) + (2 sqrt x log x - 4 sqrt x)
 // C = sum_observed c(x) is constant over a fit and is summed once by the sentinel pass
 // (launch_sentinel, dterm_c below); the streaming passes then accumulate rem only.  abr2
 // takes the SIGNED sentinel value (a carries its sign; rem of a missing entry is discarded by
@@ -388,6 +389,20 @@ struct LossOff<EW_KL> {
     av = __fmul2_rn(x, make_float2(frcp(yh.x), frcp(yh.y)));
     bv = make_float2(1.f, 1.f);
     rem = __ffma2_rn(make_float2(-x.x, -x.y), make_float2(flog(yh.x), flog(yh.y)), yh);   // y - x log y; scale 1
+  }
+};
+// (0.5, 0): 4 [sqrt x (log(x/y) / 2) - sqrt x + sqrt y] = 4 (sqrt y - sqrt x log(y) / 2) + (2 sqrt x log x - 4 sqrt x)
+template <>
+struct LossOff<EW_A05_B0> {
+  static constexpr bool value = true;
+  static __device__ __forceinline__ void abr2(float2 x, float2 yh, float2& av, float2& bv, float2& rem) {
+    const float2 r = make_float2(frsqrt(yh.x), frsqrt(yh.y));
+    const float2 sx = make_float2(fsqrt(fabsf(x.x)), fsqrt(fabsf(x.y)));
+    bv = r;
+    const float2 a = __fmul2_rn(sx, __fmul2_rn(r, r));   // sqrt(x) / y, signed like x below
+    av = make_float2(copysignf(a.x, x.x), copysignf(a.y, x.y));
+    const float2 sy = __fmul2_rn(yh, r);
+    rem = __ffma2_rn(__fmul2_rn(sx, make_float2(-0.5f, -0.5f)), make_float2(flog(yh.x), flog(yh.y)), sy);   // scale 4
   }
 };
 

@@ -58,9 +58,12 @@ cudaError_t launch_einstep(const EinStep& st, const float* A, const float* B, fl
 
 // out[i] = M[i] ? Y[i] + 0 : -1  (the sentinel copy of Y; M nonzero = observed; observed data >= 0).
 // With dpart (kSentBlocks + 1 partials each of dpart / dcpart): also *dslot = sum over observed
-// entries of the data-only loss term c(x) (dterm 1: (1,-0.5), 2: (1,0), 0: none; R25) and
+// entries of the data-only loss term c(x) (dterm 1: (1,-0.5), 2: (1,0), 3: (0.5,0), 0: none; R25) and
 // *dcslot = the observed count, summed in fixed order.
 constexpr int kSentBlocks = 148 * 16;
+// Unmasked fit (R25): *dslot = sum over all n entries of c(x), *dcslot = n (kSentBlocks partials)
+cudaError_t launch_dterm(const float* Y, int64_t n, int dterm, double* dpart, long long* dcpart, double* dslot,
+                         long long* dcslot, cudaStream_t s);
 cudaError_t launch_sentinel(const float* Y, const uint8_t* M, float* out, int64_t n, int dterm, double* dpart,
                             long long* dcpart, double* dslot, long long* dcslot, cudaStream_t s);
 

@@ -446,6 +446,10 @@ cudaError_t launch_einstep(const EinStep& st, const float* A, const float* B, fl
 __device__ __forceinline__ double dterm_c(int dterm, float x) {
   if (dterm == 1) return -4.0 * (double)sqrtf(x);                    // (1, -0.5)
   if (dterm == 2) return x > 0.f ? (double)x * (double)logf(x) - (double)x : 0.0;   // (1, 0)
+  if (dterm == 3) {                                                                   // (0.5, 0)
+    const double sx = (double)sqrtf(x);
+    return x > 0.f ? 2.0 * sx * (double)logf(x) - 4.0 * sx : 0.0;
+  }
   return 0.0;
 }
 
@@ -468,6 +472,20 @@ __device__ __forceinline__ void sent_block_sum(double acc, long long cnt, double
     dcpart[slot] = c;
   }
 }
+
+// Unmasked fit: data-only loss sum (R25) over every entry, block partials (fixed grid)
+__global__ void dterm_kernel(const float* __restrict__ Y, long long n4, long long n, int dterm, double* dpart,
+                             long long* dcpart) {
+  double acc = 0.0;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4; i += (long long)gridDim.x * blockDim.x) {
+    const float4 y = __ldcs(reinterpret_cast<const float4*>(Y) + i);
+    acc += dterm_c(dterm, y.x) + dterm_c(dterm, y.y) + dterm_c(dterm, y.z) + dterm_c(dterm, y.w);
+  }
+  for (long long i = n4 * 4 + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    acc += dterm_c(dterm, Y[i]);
+  sent_block_sum(acc, 0, dpart, dcpart, blockIdx.x);
+}
+
 
 __global__ void sentinel_kernel(const float* __restrict__ Y, const uint8_t* __restrict__ M, float* __restrict__ out,
                                 long long n4, int dterm, double* dpart, long long* dcpart) {
@@ -504,6 +522,8 @@ __global__ void sentinel_tail_kernel(const float* __restrict__ Y, const uint8_t*
   }
   if (dpart) sent_block_sum(acc, cnt, dpart, dcpart, slot + blockIdx.x);
 }
+
+__global__ void set_count_kernel(long long* c, long long n) { *c = n; }
 
 __global__ void pad_rows_kernel(const float* __restrict__ src, float* __restrict__ dst, long long rows, int K, int Kp) {
   const long long n = rows * Kp;
@@ -584,6 +604,16 @@ cudaError_t launch_pad_rows(const float* src, float* dst, int64_t rows, int64_t 
   const long long n = rows * Kp;
   const int blocks = (int)std::min<long long>((n + 255) / 256, 148 * 8);
   pad_rows_kernel<<<blocks > 0 ? blocks : 1, 256, 0, s>>>(src, dst, rows, (int)K, (int)Kp);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_dterm(const float* Y, int64_t n, int dterm, double* dpart, long long* dcpart, double* dslot,
+                         long long* dcslot, cudaStream_t s) {
+  const bool vec = (reinterpret_cast<uintptr_t>(Y) & 15) == 0;
+  dterm_kernel<<<kSentBlocks, 256, 0, s>>>(Y, vec ? n / 4 : 0, n, dterm, dpart, dcpart);
+  loss_reduce_kernel<<<1, 256, 0, s>>>(dpart, dcpart, kSentBlocks, dslot, dcslot, 1.0, nullptr);
+  // every entry is observed: the count is n
+  set_count_kernel<<<1, 1, 0, s>>>(dcslot, n);
   return cudaGetLastError();
 }
 

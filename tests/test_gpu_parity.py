@@ -111,11 +111,11 @@ def test_n_observed_exact_and_loss(nef, name):
     assert abs(s - rs) <= 1e-4 * abs(rs)
 
 
-@pytest.mark.parametrize("name", ["c3", "c5", "c2"])
+@pytest.mark.parametrize("name", ["c3", "c5", "c4", "c2"])
 def test_fit_loss_of_final_factors(nef, name):
-    """The final loss of a masked fit comes from the loss pass over the sentinel copy; for
-    (1,0) and (1,-0.5) (c3, c5) its data-only part is summed once by the sentinel pass and the
-    streamed part carries the rest (R25).  Pinned tightly against the oracle's loss
+    """The final loss of a fit comes from the loss pass; for (1,0), (1,-0.5) and (0.5,0) (c3, c5
+    masked; c4 unmasked) its data-only part is summed once per fit (by the sentinel pass, or a
+    read-only pass without a mask) and the streamed part carries the rest (R25).  Pinned tightly against the oracle's loss
     of the GPU's own final factors (no trajectory drift in the comparison).  c2 (Euclidean, whole
     divergence per entry) is the control: x - yhat in fp32 of a close fit costs it ~4e-5."""
     tol = 1e-4 if name == "c2" else 1e-5
