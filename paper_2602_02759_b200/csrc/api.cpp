@@ -366,8 +366,13 @@ int num_den(const Ctx& c, int ell, const float* Y, const uint8_t* M, const nef::
   return NEF_OK;
 }
 
+// A plan "communicates" when it is sharded over > 1 ranks, or carries a 1-rank communicator
+// (NEF_NCCL_FORCE=1 at nef_plan_shard with world 1: the multi-GPU code path, NCCL included,
+// exercised on one GPU by the tests)
+bool communicates(const nef::Plan& p) { return p.world > 1 || p.nccl_comm != nullptr; }
+
 int allreduce(const nef::Plan& p, void* buf, size_t count, int dtype, cudaStream_t s) {
-  if (p.world <= 1) return NEF_OK;
+  if (!communicates(p)) return NEF_OK;
   if (!p.nccl_comm)
     return fail(NEF_E_NCCL, "plan sharded without a communicator (nef_plan_shard_host): use nef_num_den, an "
                             "external all-reduce and nef_apply_update");
@@ -383,7 +388,7 @@ int update_one(const Ctx& c, int ell, const float* Y, const uint8_t* M, const ne
   if (st) return st;
   int64_t n = 1;
   for (auto d : c.p->fshape[ell]) n *= d;
-  if (c.p->world > 1 && !c.p->factor_has_shard[ell]) {
+  if (communicates(*c.p) && !c.p->factor_has_shard[ell]) {
     // num and den are adjacent in the workspace (Q_a|Q_b or num|den regions)
     if (den == num + n) {
       st = allreduce(*c.p, num, 2 * (size_t)n, kNcclFloat32, c.s);
@@ -588,7 +593,7 @@ int nef_fit(nef_plan_t plan, const float* Y, const uint8_t* mask, double alpha, 
     // all-reduce the loss slots [0, upto - base) and copy them to the host
     int n = upto - base;
     if (n <= 0) return NEF_OK;
-    if (p.world > 1) {
+    if (communicates(p)) {
       int r = allreduce(p, slots, (size_t)n, kNcclFloat64, c.s);
       if (r) return r;
     }
@@ -675,7 +680,7 @@ int nef_loss(nef_plan_t plan, const float* Y, const uint8_t* mask, double alpha,
   long long* cslot = reinterpret_cast<long long*>(c.ws + p.ws_trace + 8 * 2048);
   st = loss_pass(c, Y, mask, nef::make_div(alpha, beta), slot, cslot);
   if (st) return st;
-  if (p.world > 1) {
+  if (communicates(p)) {
     if ((st = allreduce(p, slot, 1, kNcclFloat64, c.s))) return st;
     if ((st = allreduce(p, cslot, 1, kNcclInt64, c.s))) return st;
   }
@@ -767,7 +772,8 @@ static int shard_impl(nef_plan_t plan, int rank, int world, const void* uid, boo
   int64_t q = n / world, r = n % world;
   int64_t begin = rank * q + std::min<int64_t>(rank, r);
   int64_t len = q + (rank < r ? 1 : 0);
-  if (world > 1 && !host_only) {
+  const bool force = world == 1 && std::getenv("NEF_NCCL_FORCE") && std::getenv("NEF_NCCL_FORCE")[0] == '1';
+  if ((world > 1 || force) && !host_only) {
     if (!uid) return fail(NEF_E_ARG, "null NCCL unique id");
     std::string err;
     if (!load_nccl(err)) return fail(NEF_E_NCCL, err);

@@ -124,3 +124,32 @@ def test_mostly_zero_data(nef, ab):
     for ell, (g, r) in enumerate(zip(F, ref)):
         assert _rel(g, r) <= FACTOR_RTOL, (ell, _rel(g, r))
     assert _rel(tr, rtr) <= TRACE_RTOL
+
+
+def test_nccl_path_on_one_rank(nef, monkeypatch):
+    """The multi-GPU path with its NCCL calls, on a 1-rank communicator (NEF_NCCL_FORCE=1):
+    libnccl loaded, ncclCommInitRank, the all-reduces of the numerator/denominator partials and
+    of the loss slots on the workspace - an identity at one rank, so factors and trace must be
+    bit-identical to the unsharded fit."""
+    from nef_inputs import CONFIGS, generate_numpy
+    d = generate_numpy("c5")
+    cfg = CONFIGS["c5"]
+    Y = torch.from_numpy(d["Y"]).cuda()
+    M = torch.from_numpy(d["mask"]).cuda()
+    runs = []
+    for shard in (False, True):
+        plan = nef.Plan(d["model"], d["shape"], d["ranks"])
+        if shard:
+            monkeypatch.setenv("NEF_NCCL_FORCE", "1")
+            plan.shard(0, 1, nef.nef_nccl_unique_id())
+            monkeypatch.delenv("NEF_NCCL_FORCE")
+            assert plan.info["shard_mode"] == 0
+        F = [torch.from_numpy(f.copy()).cuda() for f in d["init"]]
+        tr = plan.fit(Y, M, cfg.alpha, cfg.beta, F, 2)
+        s, n = plan.loss(Y, M, cfg.alpha, cfg.beta, F)
+        torch.cuda.synchronize()
+        runs.append(([f.cpu() for f in F], list(tr), s, n))
+    (Fa, ta, sa, na), (Fb, tb, sb, nb) = runs
+    for a, b in zip(Fa, Fb):
+        assert torch.equal(a, b)
+    assert ta == tb and sa == sb and na == nb
