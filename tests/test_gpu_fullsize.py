@@ -79,3 +79,57 @@ def test_fullsize_n_observed_exact(nef, name):
     loss, n_obs = plan.loss(d["Y"], d["mask"], cfg.alpha, cfg.beta, d["init"])
     assert n_obs == int(d["mask"].sum(dtype=torch.int64).item())
     assert np.isfinite(loss) and loss > 0
+
+
+# the paper's own multi-index models at their data shapes (synthetic Poisson
+# data from Gamma factors, 10 % missing; ranks as the paper's Tables 1-2 use them), through the
+# planner and the streaming kernels, checked like the configs above on sampled slab rows.
+PAPER_MODELS = [
+    ("uber", "wr,dr,hr,irk,jrk->wdhij", (27, 7, 24, 400, 400), (10, 6), (1.0, 0.0)),
+    ("icews", "ir,jr,ak,kr,tr->ijat", (249, 249, 20, 228), (25, 10), (1.0, 0.0)),
+    ("wits", "er,ir,gr,tk,kr->eigt", (196, 196, 96, 29), (25, 10), (1.0, 0.0)),
+]
+
+
+@pytest.mark.parametrize("case", PAPER_MODELS, ids=lambda c: c[0])
+def test_paper_models_sampled_rows(nef, case):
+    _, ms, shape, ranks, (al, be) = case
+    dev = torch.device("cuda")
+    g = torch.Generator(device=dev).manual_seed(20260219)
+    fs = O.factor_shapes(ms, shape, ranks)
+    truth = [torch._standard_gamma(torch.full(s, 1.0, device=dev), generator=g) * 0.5 for s in fs]
+    lhs = ms.split("->")[0].split(",")
+    rate = torch.einsum(ms, *truth)
+    Y = torch.poisson(rate, generator=g).float()
+    del rate
+    M = (torch.rand(shape, generator=g, device=dev) >= 0.1).to(torch.uint8)
+    init = [torch.rand(s, generator=g, device=dev) * 0.9 + 0.1 for s in fs]
+    F = [f.clone() for f in init]
+    plan = nef.Plan(ms, shape, ranks)
+    assert sum(L["tc"] for L in plan.describe()["lowerings"]) >= 2
+    tr = plan.fit(Y, M, al, be, F, 1)
+    torch.cuda.synchronize()
+    assert np.all(np.isfinite(tr)) and tr[1] <= tr[0] * (1 + 1e-6), tr
+    ops, out = O.parse(ms)
+    rng = np.random.default_rng(3)
+    checked = 0
+    for ell, op in enumerate(ops):
+        obs = [c for c in op if c in out]
+        if not obs:
+            continue
+        letter = obs[0]
+        mode, axis = out.index(letter), op.index(letter)
+        n = shape[mode]
+        rows = sorted(set([0, int(rng.integers(0, n))]))
+        cur = [(F[k] if k < ell else init[k]).cpu().numpy().astype(np.float64) for k in range(len(ops))]
+        got = F[ell].cpu().numpy()
+        for i in rows:
+            Ys = Y.select(mode, i).unsqueeze(mode).cpu().numpy().astype(np.float64)
+            Ms = M.select(mode, i).unsqueeze(mode).cpu().numpy()
+            fsl = list(cur)
+            fsl[ell] = np.take(cur[ell], [i], axis=axis)
+            want = O.update_factor(ms, Ys, Ms, fsl, ell, al, be)
+            gv = np.take(got, [i], axis=axis)
+            assert _rel(gv, want) <= FACTOR_RTOL, (ms, ell, i, _rel(gv, want))
+            checked += 1
+    assert checked >= len(ops)
