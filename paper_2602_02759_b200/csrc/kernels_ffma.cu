@@ -426,6 +426,8 @@ cudaError_t launch_einstep(const EinStep& st, const float* A, const float* B, fl
   span = std::max(std::max(sa, sb), std::max<long long>(st.out_size, st.sum_size));
   d.out_size = st.out_size;
   d.sum_size = st.sum_size;
+  // long sums are split over a warp only for few outputs (a wider split - 65536 outputs x 256
+  // terms of the Tucker core's epilogue - measured 14 % slower over a c2 sweep)
   const bool split = st.out_size < 148 * 256 && st.sum_size >= 128;
   const bool small = span < (1ll << 30);
   const int L = split ? 32 : 1;
@@ -440,8 +442,6 @@ cudaError_t launch_einstep(const EinStep& st, const float* A, const float* B, fl
 }
 
 // --------------------------------------------------------------------------------------
-// 4 entries per thread and iteration: one 4-byte mask load and one 16-byte Y load / store, all
-// fully coalesced across the warp
 // Data-only loss term c(x) of an observed entry (R25, LossOff in divergence.cuh)
 __device__ __forceinline__ double dterm_c(int dterm, float x) {
   if (dterm == 1) return -4.0 * (double)sqrtf(x);                    // (1, -0.5)
@@ -487,6 +487,8 @@ __global__ void dterm_kernel(const float* __restrict__ Y, long long n4, long lon
 }
 
 
+// 4 entries per thread and iteration: one 4-byte mask load and one 16-byte Y load / store, all
+// fully coalesced across the warp
 __global__ void sentinel_kernel(const float* __restrict__ Y, const uint8_t* __restrict__ M, float* __restrict__ out,
                                 long long n4, int dterm, double* dpart, long long* dcpart) {
   double acc = 0.0;
