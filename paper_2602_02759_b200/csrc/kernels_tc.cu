@@ -41,7 +41,10 @@ constexpr int BM = 128, BN = 64;
 // Y (/ mask) pipeline stages: 3 with the uint8 mask stream, else NEF_NS
 template <int MM> struct YStages { static constexpr int value = MM == 1 ? 3 : NEF_NS; };
 // V tile stages: 3 with a uint8 mask stream (its stages take the smem), else 4
-template <int MM> struct VStages { static constexpr int value = MM == 1 ? 3 : 4; };
+#ifndef NEF_NV0
+#define NEF_NV0 4
+#endif
+template <int MM> struct VStages { static constexpr int value = MM == 1 ? 3 : NEF_NV0; };
 // warp roles: 16 elementwise warps, 4 V generators, direct-V row loads, TMA producer, MMA
 // issuer.  The warp schedulers favour higher warp ids, so the producers whose latency is on the
 // critical path sit above the elementwise warps (with the producers below, the V generators
@@ -182,11 +185,11 @@ __device__ __forceinline__ void mbar_wait_mma(uint32_t bar, uint32_t parity) {
   mbar_spin(bar, parity);
 #endif
 }
-// Elementwise warps waiting for S: sixteen of them polling would take the issue slots the V
-// generator and the other elementwise warps need (NEF_EW_WAIT: 0 spin, 1 suspend-hint wait,
-// else nanoseconds of sleep between polls)
+// Elementwise warps waiting for S (NEF_EW_WAIT: 0 spin - the default, measured 1 % faster on
+// c5 than a 32 ns back-off once the MMA issuer also spins - 1 suspend-hint wait, else
+// nanoseconds of sleep between polls)
 #ifndef NEF_EW_WAIT
-#define NEF_EW_WAIT 32
+#define NEF_EW_WAIT 0
 #endif
 __device__ __forceinline__ void mbar_wait_ew(uint32_t bar, uint32_t parity) {
 #if NEF_EW_WAIT == 0
