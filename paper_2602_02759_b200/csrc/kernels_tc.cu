@@ -147,9 +147,10 @@ __device__ __forceinline__ void mbar_spin(uint32_t bar, uint32_t parity) {
   }
 }
 // Producer-side wait (the producer runs ahead of its consumer): poll with a short sleep
-// between tries so the waiting warp leaves the issue slots to the elementwise warps.
+// between tries so the waiting warp leaves the issue slots to the elementwise warps
+// (NEF_PROD_HINT=1: suspend-hint try_wait instead, measured 0.5 % slower on c5).
 #ifndef NEF_PROD_HINT
-#define NEF_PROD_HINT 1
+#define NEF_PROD_HINT 0
 #endif
 __device__ __forceinline__ void mbar_wait_relaxed(uint32_t bar, uint32_t parity, uint32_t ns = 256) {
 #if NEF_PROD_HINT
