@@ -170,7 +170,10 @@ __device__ __forceinline__ void mbar_wait_relaxed(uint32_t bar, uint32_t parity,
         : "r"(bar), "r"(parity)
         : "memory");
     if (done) return;
-    __nanosleep(ns);
+#ifdef NEF_PROD_NS
+    ns = NEF_PROD_NS;   // diagnostics: one sleep length for every producer wait (0: spin)
+#endif
+    if (ns) __nanosleep(ns);
     if (it > (1u << 26)) __trap();
   }
 }
