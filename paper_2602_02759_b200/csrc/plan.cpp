@@ -408,7 +408,9 @@ void tc_geometry(const Plan& p, Lowering& L) {
   L.tc_ok = false;
   bool adjacent = !L.row_modes.empty();
   for (size_t k = 1; k < L.row_modes.size(); ++k) adjacent &= L.row_modes[k] == L.row_modes[k - 1] + 1;
-  if (adjacent && L.K <= 64 && !L.col_modes.empty()) {
+  // bonds below one MMA K step (8) would be mostly zero padding on the tensor core and carry the
+  // least averaging of its TF32 rounding (R26): they stay on the fp32 FFMA path
+  if (adjacent && L.K >= 8 && L.K <= 64 && !L.col_modes.empty()) {
     const int M = (int)p.out.size();
     int r0 = L.row_modes.front(), r1 = L.row_modes.back();
     int64_t R = 1, CI = 1, CO = 1;

@@ -153,3 +153,49 @@ def test_nccl_path_on_one_rank(nef, monkeypatch):
     for a, b in zip(Fa, Fb):
         assert torch.equal(a, b)
     assert ta == tb and sa == sb and na == nb
+
+
+def _random_cases(n, seed):
+    """Seeded random CP / Tucker / 4-way problems that the planner sends to the tcgen05 kernel:
+    random bonds 1..64 (KB 32 and 64, K % 4 != 0 padding), ragged row and column tails, random
+    (alpha, beta) among the specialised pairs and the generic one, with and without a mask."""
+    rng = np.random.default_rng(seed)
+    pairs = [(1.0, 0.0), (1.0, -0.5), (0.5, 0.0), (1.0, 1.0), (0.5, 0.5), (1.0, 0.5), (1.3, -0.2)]
+    out = []
+    while len(out) < n:
+        kind = rng.integers(0, 3)
+        if kind == 0:
+            ms = "ir,jr,kr->ijk"
+            shape = tuple(int(x) for x in rng.integers(64, 200, 3))
+            ranks = (int(rng.integers(1, 65)),)
+        elif kind == 1:
+            ms = "ia,jb,kc,abc->ijk"
+            shape = tuple(int(x) for x in rng.integers(64, 160, 3))
+            ranks = tuple(int(x) for x in rng.integers(2, 17, 3))
+        else:
+            ms = "ik,jk,tl,dl,kl->ijtd"
+            shape = (int(rng.integers(16, 48)), int(rng.integers(16, 48)), int(rng.integers(8, 24)), int(rng.integers(32, 80)))
+            ranks = (int(rng.integers(2, 20)), int(rng.integers(2, 12)))
+        if rng.random() < 0.7:   # TMA-legal strides (multiples of 4 / 16 bytes) -> tcgen05 path
+            shape = tuple(int(x) // 4 * 4 if i > 0 else int(x) for i, x in enumerate(shape))
+        ab = pairs[int(rng.integers(0, len(pairs)))]
+        pm = float(rng.choice([0.0, 0.05, 0.3]))
+        out.append((ms, shape, ranks, ab, pm, int(rng.integers(0, 1 << 30))))
+    return out
+
+
+@pytest.mark.parametrize("case", _random_cases(40, 2026), ids=lambda c: "%s-%s-K%s" % (
+    c[0].split("->")[0].count(",") + 1, "x".join(map(str, c[1])), ",".join(map(str, c[2]))))
+def test_random_problems(nef, case):
+    ms, shape, ranks, ab, pm, seed = case
+    rng = np.random.default_rng(seed)
+    fs = O.factor_shapes(ms, shape, ranks)
+    truth = [rng.gamma(1.0, 1.0, s) for s in fs]
+    Y = (rng.poisson(O.contract(ms, truth)) + rng.gamma(2.0, 0.05, shape)).astype(np.float32)
+    M = (rng.random(shape) >= pm).astype(np.uint8) if pm > 0 else None
+    init = [rng.uniform(0.1, 1, s).astype(np.float32) for s in fs]
+    _, F, tr = _fit(nef, ms, shape, ranks, Y, M, init, ab, 1)
+    ref, rtr = O.fit(ms, Y, M, init, ab[0], ab[1], 1)
+    for ell, (g, r) in enumerate(zip(F, ref)):
+        assert _rel(g, r) <= FACTOR_RTOL, (ell, _rel(g, r))
+    assert _rel(tr, rtr) <= TRACE_RTOL
