@@ -7,6 +7,8 @@ routed to the tcgen05 kernel and to the CUDA-core kernel:
 * rank 1 (K = 1: padded 16-byte table rows) and unit modes;
 * mostly-zero data (x = 0 entries: a = 0, loss terms of the x -> 0 limit).
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -184,7 +186,8 @@ def _random_cases(n, seed):
     return out
 
 
-@pytest.mark.parametrize("case", _random_cases(40, 2026), ids=lambda c: "%s-%s-K%s" % (
+@pytest.mark.parametrize("case", _random_cases(int(os.environ.get("NEF_RANDOM_CASES", "40")),
+                                                int(os.environ.get("NEF_RANDOM_SEED", "2026"))), ids=lambda c: "%s-%s-K%s" % (
     c[0].split("->")[0].count(",") + 1, "x".join(map(str, c[1])), ",".join(map(str, c[2]))))
 def test_random_problems(nef, case):
     ms, shape, ranks, ab, pm, seed = case
