@@ -52,6 +52,9 @@ template <int MM> struct VStages { static constexpr int value = MM == 1 ? 3 : NE
 #ifndef NEF_EW_BAR
 #define NEF_EW_BAR 0
 #endif
+#ifndef NEF_PA_RN
+#define NEF_PA_RN 0   // 1: plain RN for P_a in the Euclidean pair too (diagnostics)
+#endif
 #ifndef NEF_Y_FIRST
 #define NEF_Y_FIRST 0
 #endif
@@ -640,6 +643,19 @@ __device__ __forceinline__ void ew_load_y(const TcArgs& a, const unsigned char* 
   }
 }
 
+// TF32 rounding of P_a (R27).  The tensor core reads the top 19 bits of each operand, so adding
+// d before it truncates rounds with probability set by d: a constant half ulp (0x1000) is
+// round-to-nearest.  For the Euclidean pair a = x is the data itself, and count-like data
+// (integers, or integers plus a small offset) above 2^11 sits on or next to the TF32 grid in a
+// fixed pattern, so RN errs in one direction on average (measured 1e-4 factor bias on Poisson
+// Tucker problems, scripts/emulate_tf32_tucker.py).  There the 16 entries of a half-step take
+// 16 stratified offsets (k + 1/2)/16 ulp, unbiased up to 1/32 ulp, at no extra instruction (the
+// offsets are immediates).  Every other pair scales x by a continuous factor: plain RN.
+template <int KIND>
+__host__ __device__ constexpr uint32_t pa_round(int j) {
+  return (KIND == EW_EUC && !NEF_PA_RN) ? 0x100u + 0x200u * (uint32_t)j : 0x1000u;
+}
+
 // a, b (and, in loss mode, the loss) of 16 entries: sv holds S on entry and P_a on exit, pb
 // receives P_b; zero at missing or out-of-range entries (R5: a select on the observed flag,
 // never a multiply).  cv = valid tile columns from the half-step's first column.
@@ -671,8 +687,8 @@ __device__ __forceinline__ void ew_half(const TcArgs& a, uint32_t (&sv)[16], con
       float2 av, bv, lv;
       Ew<KIND>::abl2(make_float2(o0 ? yv[j] : 1.f, o1 ? yv[j + 1] : 1.f), yh, a.dv, av, bv, lv);
       lsum += (o0 ? lv.x : 0.f) + (o1 ? lv.y : 0.f);
-      sv[j] = o0 ? __float_as_uint(av.x) + 0x1000u : 0u;
-      sv[j + 1] = o1 ? __float_as_uint(av.y) + 0x1000u : 0u;
+      sv[j] = o0 ? __float_as_uint(av.x) + pa_round<KIND>(j) : 0u;
+      sv[j + 1] = o1 ? __float_as_uint(av.y) + pa_round<KIND>(j + 1) : 0u;
       pb[j] = o0 ? __float_as_uint(bv.x) + 0x1000u : 0u;
       pb[j + 1] = o1 ? __float_as_uint(bv.y) + 0x1000u : 0u;
     }
@@ -687,8 +703,8 @@ __device__ __forceinline__ void ew_half(const TcArgs& a, uint32_t (&sv)[16], con
     Ew<KIND>::ab2(make_float2(yv[j], yv[j + 1]), yh, a.dv, av, bv);
     const bool o0 = (ob[j >> 2] & (0xffu << (8 * (j & 3)))) != 0u;
     const bool o1 = (ob[j >> 2] & (0xffu << (8 * ((j + 1) & 3)))) != 0u;
-    sv[j] = o0 ? __float_as_uint(av.x) + 0x1000u : 0u;
-    sv[j + 1] = o1 ? __float_as_uint(av.y) + 0x1000u : 0u;
+    sv[j] = o0 ? __float_as_uint(av.x) + pa_round<KIND>(j) : 0u;
+    sv[j + 1] = o1 ? __float_as_uint(av.y) + pa_round<KIND>(j + 1) : 0u;
     pb[j] = o0 ? __float_as_uint(bv.x) + 0x1000u : 0u;
     pb[j + 1] = o1 ? __float_as_uint(bv.y) + 0x1000u : 0u;
   }
@@ -718,8 +734,8 @@ __device__ __forceinline__ void ew_half_sent(const TcArgs& a, uint32_t (&sv)[16]
         float2 av, bv, rv;
         LossOff<KIND>::abr2(x, yh, av, bv, rv);
         l2 = __fadd2_rn(l2, make_float2(x.x >= 0.f ? rv.x : 0.f, x.y >= 0.f ? rv.y : 0.f));
-        sv[j] = (uint32_t)__viaddmax_s32(__float_as_int(av.x), 0x1000, 0);
-        sv[j + 1] = (uint32_t)__viaddmax_s32(__float_as_int(av.y), 0x1000, 0);
+        sv[j] = (uint32_t)__viaddmax_s32(__float_as_int(av.x), (int)pa_round<KIND>(j), 0);
+        sv[j + 1] = (uint32_t)__viaddmax_s32(__float_as_int(av.y), (int)pa_round<KIND>(j + 1), 0);
         pb[j] = (uint32_t)__viaddmax_s32(__float_as_int(copysignf(bv.x, x.x)), 0x1000, 0);
         pb[j + 1] = (uint32_t)__viaddmax_s32(__float_as_int(copysignf(bv.y, x.y)), 0x1000, 0);
       }
@@ -740,8 +756,8 @@ __device__ __forceinline__ void ew_half_sent(const TcArgs& a, uint32_t (&sv)[16]
       Ew<KIND>::abl2(make_float2(fabsf(x.x), fabsf(x.y)), yh, a.dv, av, bv, lv);
       l2 = __fadd2_rn(l2, make_float2(x.x >= 0.f ? lv.x : 0.f, x.y >= 0.f ? lv.y : 0.f));
       if (a.mode == 2) cnt += (x.x >= 0.f ? 1 : 0) + (x.y >= 0.f ? 1 : 0);
-      sv[j] = (uint32_t)__viaddmax_s32(__float_as_int(copysignf(av.x, x.x)), 0x1000, 0);
-      sv[j + 1] = (uint32_t)__viaddmax_s32(__float_as_int(copysignf(av.y, x.y)), 0x1000, 0);
+      sv[j] = (uint32_t)__viaddmax_s32(__float_as_int(copysignf(av.x, x.x)), (int)pa_round<KIND>(j), 0);
+      sv[j + 1] = (uint32_t)__viaddmax_s32(__float_as_int(copysignf(av.y, x.y)), (int)pa_round<KIND>(j + 1), 0);
       pb[j] = (uint32_t)__viaddmax_s32(__float_as_int(copysignf(bv.x, x.x)), 0x1000, 0);
       pb[j + 1] = (uint32_t)__viaddmax_s32(__float_as_int(copysignf(bv.y, x.y)), 0x1000, 0);
     }
@@ -759,8 +775,8 @@ __device__ __forceinline__ void ew_half_sent(const TcArgs& a, uint32_t (&sv)[16]
       Ew<KIND>::ab2(make_float2(fabsf(x.x), fabsf(x.y)), yh, a.dv, av, bv);
       av = make_float2(copysignf(av.x, x.x), copysignf(av.y, x.y));
     }
-    sv[j] = (uint32_t)__viaddmax_s32(__float_as_int(av.x), 0x1000, 0);
-    sv[j + 1] = (uint32_t)__viaddmax_s32(__float_as_int(av.y), 0x1000, 0);
+    sv[j] = (uint32_t)__viaddmax_s32(__float_as_int(av.x), (int)pa_round<KIND>(j), 0);
+    sv[j + 1] = (uint32_t)__viaddmax_s32(__float_as_int(av.y), (int)pa_round<KIND>(j + 1), 0);
     pb[j] = (uint32_t)__viaddmax_s32(__float_as_int(copysignf(bv.x, x.x)), 0x1000, 0);
     pb[j + 1] = (uint32_t)__viaddmax_s32(__float_as_int(copysignf(bv.y, x.y)), 0x1000, 0);
   }
