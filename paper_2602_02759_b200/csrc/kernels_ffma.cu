@@ -17,6 +17,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 
 #include "divergence.cuh"
 #include "kernels.h"
@@ -86,10 +87,14 @@ UpdArgs make_upd(double alpha, double beta, double eps) {
 // --------------------------------------------------------------------------------------
 // fused streaming pass (CUDA cores)
 // --------------------------------------------------------------------------------------
-constexpr int BM = 64, BN = 64, NT = 256, PADR = BM + 4;
+// Row-block height BM_ (64, or 32 when the lowering has <= 32 rows: factors with few rows over
+// millions of columns, e.g. the paper's ICEWS / WITS time and action factors); 4 x 4 outputs of
+// S per thread, NT = 4 * BM_ threads, 64 columns per tile.
+constexpr int BN = 64;
 
-template <int KP>
+template <int KP, int BM>
 struct __align__(16) FSmem {
+  static constexpr int PADR = BM + 4;
   float Ut[KP][BM];
   float Vt[KP][BN];
   float V[BN][KP];
@@ -106,10 +111,12 @@ struct FusedDev {
   int32_t boff[kMaxTabs][64];
 };
 
-template <int KP, int KIND>
-__global__ void __launch_bounds__(NT) fused_ffma_kernel(const __grid_constant__ FusedDev P) {
+template <int KP, int KIND, int BM>
+__global__ void __launch_bounds__(4 * BM) fused_ffma_kernel(const __grid_constant__ FusedDev P) {
+  constexpr int NT = 4 * BM;     // threads: BM / 4 row groups x 16 column groups
+  constexpr int RG = BM / 4;
   extern __shared__ __align__(16) unsigned char smraw[];
-  FSmem<KP>& sm = *reinterpret_cast<FSmem<KP>*>(smraw);
+  FSmem<KP, BM>& sm = *reinterpret_cast<FSmem<KP, BM>*>(smraw);
   const FusedArgs& a = P.a;
   constexpr int KQ = KP / 16;
   const int t = threadIdx.x;
@@ -143,9 +150,9 @@ __global__ void __launch_bounds__(NT) fused_ffma_kernel(const __grid_constant__ 
     for (int j = 0; j < KQ; ++j) { qa_d[i][j] = 0.0; qb_d[i][j] = 0.0; }
   double loss_acc = 0.0;
   long long cnt = 0;
-  const int rs = (t % 16) * 4;
-  const int cs = (t / 16) * 4;
-  const int kq = (t / 16) * KQ;
+  const int rs = (t % RG) * 4;
+  const int cs = (t / RG) * 4;
+  const int kq = (t / RG) * KQ;
 
   const int64_t total_tiles = (a.n_cols + BN - 1) / BN;
   const int64_t tb = (int64_t)blockIdx.y * a.tiles_per_chunk;
@@ -311,15 +318,21 @@ __global__ void __launch_bounds__(NT) fused_ffma_kernel(const __grid_constant__ 
   }
 }
 
-template <int KP, int KIND>
-static cudaError_t launch_kp(const FusedDev& d, cudaStream_t s) {
-  size_t smem = sizeof(FSmem<KP>);
-  cudaError_t e = cudaFuncSetAttribute(fused_ffma_kernel<KP, KIND>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+template <int KP, int KIND, int BM>
+static cudaError_t launch_kp_bm(const FusedDev& d, cudaStream_t s) {
+  size_t smem = sizeof(FSmem<KP, BM>);
+  cudaError_t e = cudaFuncSetAttribute(fused_ffma_kernel<KP, KIND, BM>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int64_t row_blocks = (d.a.n_rows + BM - 1) / BM;
   dim3 grid((unsigned)row_blocks, (unsigned)d.a.n_chunks);
-  fused_ffma_kernel<KP, KIND><<<grid, NT, smem, s>>>(d);
+  fused_ffma_kernel<KP, KIND, BM><<<grid, 4 * BM, smem, s>>>(d);
   return cudaGetLastError();
+}
+// (<= 32 rows: one row block either way, so the planner's partial layout is unchanged)
+template <int KP, int KIND>
+static cudaError_t launch_kp(const FusedDev& d, cudaStream_t s) {
+  if (d.a.n_rows <= 32 && !std::getenv("NEF_FFMA_BM64")) return launch_kp_bm<KP, KIND, 32>(d, s);
+  return launch_kp_bm<KP, KIND, 64>(d, s);
 }
 
 struct FfmaLauncher {
