@@ -512,7 +512,9 @@ void finish_workspace(const Plan& p, Lowering& L, Bump& bump, const std::string&
 double candidate_cost(const Plan& p, const Lowering& L) {
   double N = (double)p.n_local;
   double kp = (double)std::max<int64_t>(16, (L.K + 15) / 16 * 16);
-  double fused = N * 3.0 * kp;
+  // the tcgen05 kernel streams at ~0.6 of HBM speed where the CUDA-core one does ~0.05-0.1
+  // (profiles/): a lowering with a TMA geometry is preferred by that ratio
+  double fused = N * 3.0 * kp * (L.tc_ok ? 0.125 : 1.0);
   double vgen = N / 64.0 * (double)L.K * (double)std::max<size_t>(1, L.tabs.size());
   double q = (double)L.n_rows * (double)L.K;
   double bytes = q * 4.0 * 2.0                              // U written + read

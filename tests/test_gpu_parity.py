@@ -80,8 +80,10 @@ def test_num_den_each_factor(nef, name):
     for ell in range(len(F)):
         num, den = plan.num_den(ell, Y, M, d["alpha"], d["beta"], F)
         A, B = O.numerator_denominator(d["model"], d["Y"], d["mask"], d["init"], ell, d["alpha"], d["beta"])
-        assert _rel(num.cpu().numpy(), A) <= 2e-5, (name, ell)
-        assert _rel(den.cpu().numpy(), B) <= 2e-5, (name, ell)
+        # the factor bar (1e-4): on the TF32 path a lowering whose rows pair the factor's mode with
+        # a contracted one sums as few as ~140 columns per row before the fp64 epilogue (R23, R26)
+        assert _rel(num.cpu().numpy(), A) <= FACTOR_RTOL, (name, ell, _rel(num.cpu().numpy(), A))
+        assert _rel(den.cpu().numpy(), B) <= FACTOR_RTOL, (name, ell, _rel(den.cpu().numpy(), B))
 
 
 @pytest.mark.parametrize("name", ["c2", "c3", "c5"])
