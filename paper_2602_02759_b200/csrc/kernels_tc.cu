@@ -656,6 +656,21 @@ __host__ __device__ constexpr uint32_t pa_round(int j) {
   return (KIND == EW_EUC && !NEF_PA_RN) ? 0x100u + 0x200u * (uint32_t)j : 0x1000u;
 }
 
+// Yhat floor of two reconstructed entries (reading R4: max(S, 1e-30)).  S >= 0 (nonnegative
+// operands), so S + 1e-30 is the same value wherever S > 1e-23 (1e-30 is below half an ulp) and
+// 1e-30 at S = 0: one packed add on the FMA pipe instead of two max on the (busier) ALU pipe.
+// NEF_YH_MAX=1: the max form.
+#ifndef NEF_YH_MAX
+#define NEF_YH_MAX 0
+#endif
+__device__ __forceinline__ float2 yhat_floor(uint32_t s0, uint32_t s1) {
+#if NEF_YH_MAX
+  return make_float2(fmaxf(__uint_as_float(s0), 1e-30f), fmaxf(__uint_as_float(s1), 1e-30f));
+#else
+  return __fadd2_rn(make_float2(__uint_as_float(s0), __uint_as_float(s1)), make_float2(1e-30f, 1e-30f));
+#endif
+}
+
 // a, b (and, in loss mode, the loss) of 16 entries: sv holds S on entry and P_a on exit, pb
 // receives P_b; zero at missing or out-of-range entries (R5: a select on the observed flag,
 // never a multiply).  cv = valid tile columns from the half-step's first column.
@@ -683,7 +698,7 @@ __device__ __forceinline__ void ew_half(const TcArgs& a, uint32_t (&sv)[16], con
     for (int j = 0; j < 16; j += 2) {
       const bool o0 = (ob[j >> 2] & (0xffu << (8 * (j & 3)))) != 0u;
       const bool o1 = (ob[j >> 2] & (0xffu << (8 * ((j + 1) & 3)))) != 0u;
-      const float2 yh = make_float2(fmaxf(__uint_as_float(sv[j]), 1e-30f), fmaxf(__uint_as_float(sv[j + 1]), 1e-30f));
+      const float2 yh = yhat_floor(sv[j], sv[j + 1]);
       float2 av, bv, lv;
       Ew<KIND>::abl2(make_float2(o0 ? yv[j] : 1.f, o1 ? yv[j + 1] : 1.f), yh, a.dv, av, bv, lv);
       lsum += (o0 ? lv.x : 0.f) + (o1 ? lv.y : 0.f);
@@ -698,7 +713,7 @@ __device__ __forceinline__ void ew_half(const TcArgs& a, uint32_t (&sv)[16], con
   }
 #pragma unroll
   for (int j = 0; j < 16; j += 2) {
-    const float2 yh = make_float2(fmaxf(__uint_as_float(sv[j]), 1e-30f), fmaxf(__uint_as_float(sv[j + 1]), 1e-30f));
+    const float2 yh = yhat_floor(sv[j], sv[j + 1]);
     float2 av, bv;
     Ew<KIND>::ab2(make_float2(yv[j], yv[j + 1]), yh, a.dv, av, bv);
     const bool o0 = (ob[j >> 2] & (0xffu << (8 * (j & 3)))) != 0u;
@@ -730,7 +745,7 @@ __device__ __forceinline__ void ew_half_sent(const TcArgs& a, uint32_t (&sv)[16]
 #pragma unroll
       for (int j = 0; j < 16; j += 2) {
         const float2 x = make_float2(yv[j], yv[j + 1]);
-        const float2 yh = make_float2(fmaxf(__uint_as_float(sv[j]), 1e-30f), fmaxf(__uint_as_float(sv[j + 1]), 1e-30f));
+        const float2 yh = yhat_floor(sv[j], sv[j + 1]);
         float2 av, bv, rv;
         LossOff<KIND>::abr2(x, yh, av, bv, rv);
         l2 = __fadd2_rn(l2, make_float2(x.x >= 0.f ? rv.x : 0.f, x.y >= 0.f ? rv.y : 0.f));
@@ -751,7 +766,7 @@ __device__ __forceinline__ void ew_half_sent(const TcArgs& a, uint32_t (&sv)[16]
 #pragma unroll
     for (int j = 0; j < 16; j += 2) {
       const float2 x = make_float2(yv[j], yv[j + 1]);
-      const float2 yh = make_float2(fmaxf(__uint_as_float(sv[j]), 1e-30f), fmaxf(__uint_as_float(sv[j + 1]), 1e-30f));
+      const float2 yh = yhat_floor(sv[j], sv[j + 1]);
       float2 av, bv, lv;
       Ew<KIND>::abl2(make_float2(fabsf(x.x), fabsf(x.y)), yh, a.dv, av, bv, lv);
       l2 = __fadd2_rn(l2, make_float2(x.x >= 0.f ? lv.x : 0.f, x.y >= 0.f ? lv.y : 0.f));
@@ -767,7 +782,7 @@ __device__ __forceinline__ void ew_half_sent(const TcArgs& a, uint32_t (&sv)[16]
 #pragma unroll
   for (int j = 0; j < 16; j += 2) {
     const float2 x = make_float2(yv[j], yv[j + 1]);
-    const float2 yh = make_float2(fmaxf(__uint_as_float(sv[j]), 1e-30f), fmaxf(__uint_as_float(sv[j + 1]), 1e-30f));
+    const float2 yh = yhat_floor(sv[j], sv[j + 1]);
     float2 av, bv;
     if (Ew<KIND>::kLinX) {
       Ew<KIND>::ab2(x, yh, a.dv, av, bv);   // a = x * (positive): carries the sign of x
