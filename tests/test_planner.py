@@ -174,3 +174,43 @@ def test_cp_lowering_is_direct():
     for L, rows in zip(d["lowerings"], "ijk"):
         assert L["row_idx"] == rows and L["bond"] == "r" and L["epi_identity"]
         assert len(L["tables"]) == 2 and all(len(t["prog"]["steps"]) == 0 for t in L["tables"])
+
+
+def test_kernel_routing_rules():
+    """Which factor updates the planner sends to the tcgen05 kernel (R26, R28): every
+    factor of c2-c5 and of the paper's Uber / ICEWS / WITS shapes; none of c1 (bond 5); never a
+    bond < 8 or a slab < 2048 entries; the lowering of each BASELINE config is pinned so that a
+    cost-model change cannot silently reroute the benchmark."""
+    from nef_inputs import CONFIGS
+
+    def low(ms, shape, ranks):
+        return nef.Plan(ms, shape, ranks).describe()["lowerings"]
+
+    for name in ("c2", "c3", "c4", "c5"):
+        c = CONFIGS[name]
+        assert all(L["tc"] for L in low(c.model, c.shape, c.ranks)), name
+    c = CONFIGS["c1"]
+    assert not any(L["tc"] for L in low(c.model, c.shape, c.ranks))
+    pinned = {
+        "c3": [("i", "jk", "r"), ("j", "ik", "r"), ("k", "ij", "r")],
+        "c5": [("i", "jk", "r"), ("j", "ik", "r"), ("k", "ij", "r")],
+        "c2": [("i", "jk", "a"), ("j", "ik", "b"), ("k", "ij", "c"), ("ij", "k", "c")],
+    }
+    for name, want in pinned.items():
+        c = CONFIGS[name]
+        got = [(L["row_idx"], L["col_idx"], L["bond"]) for L in low(c.model, c.shape, c.ranks)]
+        assert got == want, (name, got)
+    for ms, shape, ranks in [("wr,dr,hr,irk,jrk->wdhij", (27, 7, 24, 400, 400), (10, 6)),
+                             ("ir,jr,ak,kr,tr->ijat", (249, 249, 20, 228), (25, 10)),
+                             ("er,ir,gr,tk,kr->eigt", (196, 196, 96, 29), (25, 10))]:
+        assert all(L["tc"] for L in low(ms, shape, ranks)), ms
+    # bond < 8 -> fp32 path; slab < 2048 -> fp32 path (R26)
+    assert not any(L["tc"] for L in low("ir,jr,kr->ijk", (128, 128, 128), (6,)))
+    for ms, shape, ranks in [("ir,jr,kr->ijk", (130, 1, 192), (16,)), ("ir,jr,kr->ijk", (1, 96, 128), (8,)),
+                             ("ia,jb,kc,abc->ijk", (87, 64, 76), (2, 7, 6))]:
+        ops, out = O.parse(ms)
+        for L in low(ms, shape, ranks):
+            slab = int(np.prod([n for c, n in zip(out, shape) if c not in ops[L["ell"]]]))
+            if L["tc"]:
+                assert slab >= 2048 and L["K"] >= 8, (ms, L["ell"], slab, L["K"])
+    assert [L["tc"] for L in low("ir,jr,kr->ijk", (130, 1, 192), (16,))] == [False, True, False]
