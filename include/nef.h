@@ -92,7 +92,11 @@ int nef_plan_describe(nef_plan_t plan, char* buf, size_t cap, size_t* len);
  * loss_trace: host array of iters+1 doubles, or NULL.  workspace: device scratch of at
  * least nef_plan_info's workspace_bytes.  On a sharded plan the numerator/denominator of
  * every factor that does not contain the shard mode and the loss are all-reduced over
- * NCCL; every rank ends with identical replicated factors. */
+ * NCCL; every rank ends with identical replicated factors.
+ * Once per fit (R22, R25): with a mask, the mask is folded into a copy of Y in the
+ * workspace (missing -> -1) that the streaming passes read instead of Y + mask, and for the
+ * (alpha,beta) pairs (1,0), (1,-0.5), (0.5,0) the data-only part of the loss is summed there
+ * (without a mask, by a read-only pass when iters >= 3); Y and the mask are never written. */
 int nef_fit(nef_plan_t plan, const float* Y, const uint8_t* mask, double alpha, double beta, double eps,
             float* const* factors, int iters, double* loss_trace, void* workspace, size_t ws_bytes,
             void* cuda_stream);
@@ -129,7 +133,9 @@ int nef_fit_host(nef_plan_t plan, const float* Y_host, const uint8_t* mask_host,
 /* Multi-GPU.  Rank 0 calls nef_nccl_unique_id (128 bytes), the caller broadcasts the
  * bytes (e.g. torch.distributed), then every rank calls nef_plan_shard, which splits the
  * largest mode (ties -> outermost) into contiguous near-equal ranges and creates the NCCL
- * communicator on the current CUDA device. */
+ * communicator on the current CUDA device (world == 1 creates none, unless the environment
+ * sets NEF_NCCL_FORCE=1: a 1-rank communicator, so that the sharded path and its all-reduces
+ * run on one GPU for testing). */
 int nef_nccl_unique_id(void* out128);
 int nef_plan_shard(nef_plan_t plan, int rank, int world, const void* nccl_unique_id);
 
