@@ -443,11 +443,15 @@ cudaError_t launch_einstep(const EinStep& st, const float* A, const float* B, fl
   // terms of the Tucker core's epilogue - measured 14 % slower over a c2 sweep)
   const bool split = st.out_size < 148 * 256 && st.sum_size >= 128;
   const bool small = span < (1ll << 30);
-  const int L = split ? 32 : 1;
+  // too few outputs to fill the GPU with short sums: 4 lanes per output (latency-bound steps of
+  // the Tucker side operands, ~20 % occupancy one thread per output)
+  const bool quad = !split && small && st.out_size < 148 * 1024 && st.sum_size >= 8 && !std::getenv("NEF_EINSTEP_NOQUAD");
+  const int L = split ? 32 : quad ? 4 : 1;
   long long blocks = (st.out_size * L + 255) / 256;
   if (blocks > 148 * 32) blocks = 148 * 32;
   if (blocks < 1) blocks = 1;
-  if (split && small) einstep_kernel<int, 32><<<(unsigned)blocks, 256, 0, s>>>(d, A, B, C);
+  if (quad) einstep_kernel<int, 4><<<(unsigned)blocks, 256, 0, s>>>(d, A, B, C);   // (2 or 8 lanes: slower)
+  else if (split && small) einstep_kernel<int, 32><<<(unsigned)blocks, 256, 0, s>>>(d, A, B, C);
   else if (split) einstep_kernel<long long, 32><<<(unsigned)blocks, 256, 0, s>>>(d, A, B, C);
   else if (small) einstep_kernel<int, 1><<<(unsigned)blocks, 256, 0, s>>>(d, A, B, C);
   else einstep_kernel<long long, 1><<<(unsigned)blocks, 256, 0, s>>>(d, A, B, C);
