@@ -562,7 +562,31 @@ __global__ void reduce_q_kernel(const float* __restrict__ part, float* __restric
   }
 }
 
+// Few elements, many partials: warp w of a block sums partials w, w + 8, ... of 32 consecutive
+// elements (coalesced), the 8 warp sums are combined in fixed order (deterministic).
+__global__ void reduce_q8_kernel(const float* __restrict__ part, float* __restrict__ Q, long long n_chunks,
+                                 long long elems) {
+  __shared__ double red[8][32];
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  const long long e = (long long)blockIdx.x * 32 + l;
+  double acc = 0.0;
+  if (e < elems)
+    for (long long c = w; c < n_chunks; c += 8) acc += (double)part[c * elems + e];
+  red[w][l] = acc;
+  __syncthreads();
+  if (w == 0 && e < elems) {
+    double t = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) t += red[k][l];
+    Q[e] = (float)t;
+  }
+}
+
 cudaError_t launch_reduce_q(const float* Qpart, float* Q, int64_t n_chunks, int64_t elems2, cudaStream_t s) {
+  if (elems2 <= 148LL * 2048 && n_chunks >= 16 && !std::getenv("NEF_REDUCE_Q1")) {
+    reduce_q8_kernel<<<(unsigned)((elems2 + 31) / 32), 256, 0, s>>>(Qpart, Q, n_chunks, elems2);
+    return cudaGetLastError();
+  }
   long long blocks = (elems2 + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
   reduce_q_kernel<<<(unsigned)(blocks < 1 ? 1 : blocks), 256, 0, s>>>(Qpart, Q, n_chunks, elems2);
