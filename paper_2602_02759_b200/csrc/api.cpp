@@ -215,6 +215,9 @@ bool use_tc(const nef::Lowering& L, const uint8_t* M, bool sentinel = false) {
 // found a TMA geometry, else the CUDA-core kernel.  U and the column tables must be ready.
 int stream_pass(const Ctx& c, const nef::Lowering& L, const float* Y, const uint8_t* M, int mode,
                 const nef::DivParams& dv, StreamOut& o) {
+  // kernel limits (the planner keeps every lowering inside them; checked again before any launch)
+  if (L.tabs.size() > (size_t)nef::kMaxTabs || L.K > 64)
+    return fail(NEF_E_UNSUPPORTED, "lowering exceeds the kernels' limits (<= 4 column tables, bond <= 64)");
   std::vector<int32_t> boff;
   nef::FusedArgs a = fused_args(c, L, Y, M, mode, dv, boff);
   const double bytes = (double)c.p->n_local * (M ? 5.0 : 4.0);
@@ -289,6 +292,9 @@ int stream_pass(const Ctx& c, const nef::Lowering& L, const float* Y, const uint
     t.dv = dv;
     t.mode = mode;
     t.lconst = ((sent || !M) && c.loff && mode != 0) ? 1 : 0;
+    // unmasked Y streamed as is: every entry is observed, so the kernel must not read "missing"
+    // from a sign bit (an observed -0.0 is a zero); the sentinel copy canonicalises -0 itself
+    t.absy = (!M && !sent) ? 1 : 0;
     t.debug = g_debug;
     t.trace = g_trace;
     {

@@ -734,6 +734,10 @@ __device__ __forceinline__ void ew_half(const TcArgs& a, uint32_t (&sv)[16], con
 template <int KIND>
 __device__ __forceinline__ void ew_half_sent(const TcArgs& a, uint32_t (&sv)[16], float (&yv)[16], int cv, bool row_ok,
                                              uint32_t (&pb)[16], float& lsum, long long& cnt) {
+  if (a.absy) {   // raw unmasked Y (uniform branch): an observed -0.0 must not read as missing
+#pragma unroll
+    for (int j = 0; j < 16; ++j) yv[j] = fabsf(yv[j]);
+  }
   const uint32_t vbits = (!row_ok || cv <= 0) ? 0u : (cv >= 16 ? 0xffffu : ((1u << cv) - 1u));
   if (vbits != 0xffffu) {
 #pragma unroll

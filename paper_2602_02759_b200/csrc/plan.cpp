@@ -333,6 +333,34 @@ void build_tables(const Plan& p, Lowering& L, Bump& bump, bool merge) {
     }
     ++ncomp;
   }
+  // the kernels take at most kMaxTabs column tables: merge the two smallest components (their
+  // outer product becomes one table) until the count fits
+  while (ncomp > kMaxTabs) {
+    std::vector<double> sz(ncomp, 1.0);
+    for (int cidx = 0; cidx < ncomp; ++cidx) {
+      std::string letters;
+      for (size_t i = 0; i < L.col_factors.size(); ++i)
+        if (comp[i] == cidx) letters += p.ops[L.col_factors[i]];
+      std::string seen;
+      for (char c : letters) {
+        if (seen.find(c) != std::string::npos) continue;
+        seen.push_back(c);
+        if (L.col_idx.find(c) != std::string::npos || L.bond.find(c) != std::string::npos) sz[cidx] *= (double)p.dims[(int)c];
+      }
+    }
+    int s0 = 0, s1 = 1;
+    if (sz[s1] < sz[s0]) std::swap(s0, s1);
+    for (int cidx = 2; cidx < ncomp; ++cidx) {
+      if (sz[cidx] < sz[s0]) { s1 = s0; s0 = cidx; }
+      else if (sz[cidx] < sz[s1]) s1 = cidx;
+    }
+    const int keep = std::min(s0, s1), gone = std::max(s0, s1);
+    for (auto& c : comp) {
+      if (c == gone) c = keep;
+      else if (c > gone) --c;
+    }
+    --ncomp;
+  }
   for (int cidx = 0; cidx < ncomp; ++cidx) {
     std::vector<Operand> cin;
     std::string letters;
@@ -548,7 +576,7 @@ int lower_all(Plan& p, std::string& err) {
         Lowering cand;
         std::string why;
         if (!lower_candidate(p, ell, rm, pa, cand, why)) continue;
-        if (cand.K > 128) continue;                       // FFMA kernel bound on the bond
+        if (cand.K > 64) continue;                        // both streaming kernels take bonds <= 64
         Bump tmp;
         finish_lowering(p, cand, tmp);
         double c = candidate_cost(p, cand) + cand.uprog.macs + cand.epi.macs;
@@ -559,7 +587,7 @@ int lower_all(Plan& p, std::string& err) {
       }
     }
     if (!found) {
-      err = "no (row, col, bond) lowering with bond <= 128 for factor " + std::to_string(ell) + " ('" + p.ops[ell] + "')";
+      err = "no (row, col, bond) lowering with bond <= 64 for factor " + std::to_string(ell) + " ('" + p.ops[ell] + "')";
       return NEF_E_UNSUPPORTED;
     }
     // rebuild with a fresh bump so offsets are final

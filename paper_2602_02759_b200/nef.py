@@ -101,6 +101,57 @@ def _stream(stream):
     return ctypes.c_void_p(int(torch.cuda.current_stream().cuda_stream))
 
 
+def _validate(h, Y=None, mask=None, factors=None, host=False):
+    """Check what the C ABI cannot: dtype, contiguity, device and shape of every tensor (the
+    library sees raw pointers only).  Raises NefError(ARG)."""
+    import torch
+
+    def bad(msg):
+        raise NefError(5, msg)
+
+    def where(t, name):
+        if host:
+            if t.is_cuda:
+                bad("%s must be a host tensor" % name)
+        elif not t.is_cuda:
+            bad("%s must be a CUDA tensor" % name)
+        if not t.is_contiguous():
+            bad("%s must be contiguous" % name)
+
+    if Y is not None:
+        where(Y, "Y")
+        if Y.dtype != torch.float32:
+            bad("Y must be float32, got %s" % Y.dtype)
+        if tuple(Y.shape) != nef_local_shape(h):
+            bad("Y shape %s != plan's local shape %s" % (tuple(Y.shape), nef_local_shape(h)))
+    if mask is not None:
+        where(mask, "mask")
+        if mask.dtype not in (torch.uint8, torch.bool):
+            bad("mask must be uint8 or bool, got %s" % mask.dtype)
+        if Y is not None and tuple(mask.shape) != tuple(Y.shape):
+            bad("mask shape %s != Y shape %s" % (tuple(mask.shape), tuple(Y.shape)))
+    if factors is not None:
+        n = nef_plan_info(h)["n_factors"]
+        if len(factors) != n:
+            bad("expected %d factors, got %d" % (n, len(factors)))
+        for l, f in enumerate(factors):
+            where(f, "factor %d" % l)
+            if f.dtype != torch.float32:
+                bad("factor %d must be float32, got %s" % (l, f.dtype))
+            if tuple(f.shape) != nef_factor_shape(h, l):
+                bad("factor %d shape %s != %s" % (l, tuple(f.shape), nef_factor_shape(h, l)))
+            if Y is not None and not host and f.device != Y.device:
+                bad("factor %d on %s, Y on %s" % (l, f.device, Y.device))
+
+
+def _validate_nd(h, ell, num, den):
+    import torch
+    shp = nef_factor_shape(h, ell)
+    for name, t in (("num", num), ("den", den)):
+        if not t.is_cuda or not t.is_contiguous() or t.dtype != torch.float32 or tuple(t.shape) != shp:
+            raise NefError(5, "%s must be a contiguous float32 CUDA tensor of shape %s" % (name, shp))
+
+
 def _fptrs(factors):
     arr = (ctypes.c_void_p * len(factors))(*[int(f.data_ptr()) for f in factors])
     return arr
@@ -151,6 +202,7 @@ def nef_plan_describe(h):
 
 
 def nef_fit(h, Y, mask, alpha, beta, eps, factors, iters, workspace, stream=None, want_trace=True):
+    _validate(h, Y, mask, factors)
     trace = (ctypes.c_double * (iters + 1))() if want_trace else None
     _check(LIB.nef_fit(h, _ptr(Y), _ptr(mask), float(alpha), float(beta), float(eps), _fptrs(factors), int(iters),
                        trace, _ptr(workspace), workspace.numel(), _stream(stream)))
@@ -158,21 +210,27 @@ def nef_fit(h, Y, mask, alpha, beta, eps, factors, iters, workspace, stream=None
 
 
 def nef_update(h, ell, Y, mask, alpha, beta, eps, factors, workspace, stream=None):
+    _validate(h, Y, mask, factors)
     _check(LIB.nef_update(h, int(ell), _ptr(Y), _ptr(mask), float(alpha), float(beta), float(eps), _fptrs(factors),
                           _ptr(workspace), workspace.numel(), _stream(stream)))
 
 
 def nef_num_den(h, ell, Y, mask, alpha, beta, factors, num, den, workspace, stream=None):
+    _validate(h, Y, mask, factors)
+    _validate_nd(h, ell, num, den)
     _check(LIB.nef_num_den(h, int(ell), _ptr(Y), _ptr(mask), float(alpha), float(beta), _fptrs(factors), _ptr(num),
                            _ptr(den), _ptr(workspace), workspace.numel(), _stream(stream)))
 
 
 def nef_apply_update(h, ell, alpha, beta, eps, factors, num, den, stream=None):
+    _validate(h, factors=factors)
+    _validate_nd(h, ell, num, den)
     _check(LIB.nef_apply_update(h, int(ell), float(alpha), float(beta), float(eps), _fptrs(factors), _ptr(num),
                                 _ptr(den), _stream(stream)))
 
 
 def nef_loss(h, Y, mask, alpha, beta, factors, workspace, stream=None):
+    _validate(h, Y, mask, factors)
     s = ctypes.c_double()
     n = ctypes.c_int64()
     _check(LIB.nef_loss(h, _ptr(Y), _ptr(mask), float(alpha), float(beta), _fptrs(factors), ctypes.byref(s),
@@ -186,6 +244,7 @@ def nef_host_scratch_bytes(h, has_mask):
 
 def nef_fit_host(h, Y_host, mask_host, alpha, beta, eps, factors_host, iters, scratch, stream=None):
     """Y_host / mask_host / factors_host: host tensors (ideally pinned), contiguous."""
+    _validate(h, Y_host, mask_host, factors_host, host=True)
     trace = (ctypes.c_double * (iters + 1))()
     fp = (ctypes.c_void_p * len(factors_host))(*[int(f.data_ptr()) for f in factors_host])
     _check(LIB.nef_fit_host(h, _ptr(Y_host), _ptr(mask_host), float(alpha), float(beta), float(eps), fp, int(iters),

@@ -202,3 +202,54 @@ def test_random_problems(nef, case):
     for ell, (g, r) in enumerate(zip(F, ref)):
         assert _rel(g, r) <= FACTOR_RTOL, (ell, _rel(g, r))
     assert _rel(tr, rtr) <= TRACE_RTOL
+
+
+@pytest.mark.parametrize("ab", [(1.0, 0.0), (1.0, 1.0), (0.5, 0.0)])
+def test_negative_zero_in_unmasked_y(nef, ab):
+    """An observed -0.0 is a zero, not a missing entry: unmasked Y is streamed as is
+    by the tcgen05 kernel, which must not read 'missing' from its sign bit.  Same factors as the
+    oracle (and as the fit on +0.0) with a third of the zeros negated."""
+    ms, shape, ranks = "ir,jr,kr->ijk", (144, 80, 112), (32,)
+    Y, init = _problem(ms, shape, ranks, seed=21, zero_frac=0.5)
+    Yn = Y.copy()
+    z = np.argwhere(Yn == 0)
+    sel = z[np.random.default_rng(22).random(len(z)) < 0.33]
+    Yn[tuple(sel.T)] = -0.0
+    assert np.signbit(Yn).sum() > 1000 and not (Yn < 0).any()
+    plan, F, tr = _fit(nef, ms, shape, ranks, Yn, None, init, ab, 1)
+    assert all(L["tc"] for L in plan.describe()["lowerings"])
+    _, F0, tr0 = _fit(nef, ms, shape, ranks, Y, None, init, ab, 1)
+    for a, b in zip(F, F0):
+        assert np.array_equal(a, b)
+    assert np.array_equal(tr, tr0)
+    ref, rtr = O.fit(ms, Yn, None, init, ab[0], ab[1], 1)
+    errs = [_rel(g, r) for g, r in zip(F, ref)]
+    assert max(errs) <= FACTOR_RTOL, errs
+    assert _rel(tr, rtr) <= TRACE_RTOL
+
+
+def test_six_mode_cp_merged_tables(nef):
+    """6-mode CP: five column factors per lowering, merged by the planner to <= 4 tables (the
+    kernels' limit); parity with the oracle after one sweep."""
+    ms, shape, ranks = "ar,br,cr,dr,er,fr->abcdef", (12, 8, 6, 9, 8, 7), (5,)
+    Y, init = _problem(ms, shape, ranks, seed=23)
+    M = (np.random.default_rng(24).random(shape) > 0.1).astype(np.uint8)
+    plan, F, tr = _fit(nef, ms, shape, ranks, Y, M, init, (1.0, 0.0), 1)
+    assert all(len(L["tables"]) <= 4 for L in plan.describe()["lowerings"])
+    ref, rtr = O.fit(ms, Y, M, init, 1.0, 0.0, 1)
+    errs = [_rel(g, r) for g, r in zip(F, ref)]
+    assert max(errs) <= FACTOR_RTOL, errs
+    assert _rel(tr, rtr) <= TRACE_RTOL
+
+
+def test_bond_above_64_last_resort(nef):
+    """A CP of rank 80 exceeds both kernels' bond limit: the planner's last-resort lowering
+    (U = Yhat materialised, K = 1) runs it; parity with the oracle."""
+    ms, shape, ranks = "ir,jr,kr->ijk", (20, 24, 16), (80,)
+    Y, init = _problem(ms, shape, ranks, seed=25)
+    plan, F, tr = _fit(nef, ms, shape, ranks, Y, None, init, (1.0, 0.0), 2)
+    assert all(L["K"] == 1 for L in plan.describe()["lowerings"])
+    ref, rtr = O.fit(ms, Y, None, init, 1.0, 0.0, 2)
+    errs = [_rel(g, r) for g, r in zip(F, ref)]
+    assert max(errs) <= 2e-4, errs     # two sweeps
+    assert _rel(tr, rtr) <= TRACE_RTOL

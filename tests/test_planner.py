@@ -53,25 +53,19 @@ def test_shape_errors():
 
 
 def test_domain_error_before_device_work():
+    """The C ABI's own validation (raw pointers, no tensors: the binding's checks bypassed)."""
+    import ctypes as C
     p = nef.Plan("ir,jr->ij", (3, 4), (2,))
+    ws = p.info["workspace_bytes"]
+    F = (C.c_void_p * 2)(4096, 8192)
 
-    class Fake:
-        def __init__(self, n):
-            self.n = n
+    def raw_fit(alpha, beta, eps):
+        code = nef.LIB.nef_fit(p.h, C.c_void_p(4096), None, alpha, beta, eps, F, 1, None, C.c_void_p(1 << 20), ws,
+                               C.c_void_p(0))
+        return nef.NEF_STATUS[code]
 
-        def data_ptr(self):
-            return 4096
-
-        def numel(self):
-            return self.n
-
-    ws = Fake(p.info["workspace_bytes"])
-    with pytest.raises(nef.NefError) as e:
-        nef.nef_fit(p.h, Fake(12), None, 0.0, 0.5, 1e-12, [Fake(6), Fake(8)], 1, ws, stream=0)
-    assert e.value.status == "DOMAIN"
-    with pytest.raises(nef.NefError) as e:
-        nef.nef_fit(p.h, Fake(12), None, 1.0, 0.0, 0.0, [Fake(6), Fake(8)], 1, ws, stream=0)
-    assert e.value.status == "ARG"
+    assert raw_fit(0.0, 0.5, 1e-12) == "DOMAIN"
+    assert raw_fit(1.0, 0.0, 0.0) == "ARG"
 
 
 def test_swap_strings_from_plan():
@@ -214,3 +208,68 @@ def test_kernel_routing_rules():
             if L["tc"]:
                 assert slab >= 2048 and L["K"] >= 8, (ms, L["ell"], slab, L["K"])
     assert [L["tc"] for L in low("ir,jr,kr->ijk", (130, 1, 192), (16,))] == [False, True, False]
+
+
+def test_many_column_tables_are_merged():
+    """A 6-mode CP puts 5 factors on the column side of every lowering (one Khatri-Rao table per
+    factor); the kernels take at most 4 tables (kMaxTabs), so the planner merges the smallest
+    components (a 5th table overflowed the launch arguments).  The merged lowering
+    must still be the paper's einsum (debug executor vs the oracle)."""
+    ms, shape, ranks = "ar,br,cr,dr,er,fr->abcdef", (4, 3, 2, 3, 2, 3), (3,)
+    plan = nef.Plan(ms, shape, ranks)
+    d = plan.describe()
+    rng = np.random.default_rng(5)
+    f = [rng.uniform(0.2, 1.0, s) for s in O.factor_shapes(ms, shape, ranks)]
+    Y = rng.poisson(2.0, size=shape).astype(float)
+    M = (rng.random(shape) > 0.2).astype(np.uint8)
+    for L in d["lowerings"]:
+        assert len(L["tables"]) <= 4, (L["ell"], len(L["tables"]))
+        _, _, num, den = _execute_lowering(L, ms, Y, M, f, 1.0, 0.0)
+        A, B = O.numerator_denominator(ms, Y, M, f, L["ell"], 1.0, 0.0)
+        np.testing.assert_allclose(num, A, rtol=1e-11)
+        np.testing.assert_allclose(den, B, rtol=1e-11)
+    # the BASELINE-scale 6-mode case of the finding plans within the limit too
+    for L in nef.Plan(ms, (16,) * 6, (5,)).describe()["lowerings"]:
+        assert len(L["tables"]) <= 4
+
+
+@pytest.mark.parametrize("R", [65, 100, 128])
+def test_bond_above_64_never_planned(R):
+    """Both streaming kernels take bonds <= 64 (a CP of rank 65..128 used to plan a
+    bond the kernels reject mid-fit).  Such a model now gets the planner's last-resort lowering
+    (every mode on the row side: U = Yhat materialised, K = 1) - slow but runnable - and no
+    lowering carries a bond above 64."""
+    d = nef.Plan("ir,jr,kr->ijk", (64, 64, 64), (R,)).describe()
+    for L in d["lowerings"]:
+        assert L["K"] <= 64
+        assert L["row_idx"] == "ijk" and L["col_idx"] == "" and not L["tc"]
+    assert all(L["K"] == 64 for L in nef.Plan("ir,jr,kr->ijk", (64, 64, 64), (64,)).describe()["lowerings"])
+
+
+def test_binding_validates_tensors():
+    """The ctypes binding checks dtype, device, contiguity and shape before the C ABI sees raw
+    pointers."""
+    torch = pytest.importorskip("torch")
+    p = nef.Plan("ir,jr->ij", (3, 4), (2,))
+    F = [torch.ones(3, 2), torch.ones(4, 2)]
+    with pytest.raises(nef.NefError) as e:     # CPU tensors
+        nef._validate(p.h, torch.ones(3, 4), None, F)
+    assert e.value.status == "ARG"
+    with pytest.raises(nef.NefError):          # float64 Y (host path checks dtype too)
+        nef._validate(p.h, torch.ones(3, 4, dtype=torch.float64), None, F, host=True)
+    with pytest.raises(nef.NefError):          # non-contiguous
+        nef._validate(p.h, torch.ones(4, 3).t(), None, F, host=True)
+    with pytest.raises(nef.NefError):          # wrong factor shape
+        nef._validate(p.h, torch.ones(3, 4), None, [torch.ones(3, 3), torch.ones(4, 2)], host=True)
+    with pytest.raises(nef.NefError):          # mask dtype
+        nef._validate(p.h, torch.ones(3, 4), torch.ones(3, 4), F, host=True)
+    nef._validate(p.h, torch.ones(3, 4), torch.ones(3, 4, dtype=torch.uint8), F, host=True)
+
+
+def test_uber_parameter_count_from_library(golden):
+    """the Uber model 'wr,dr,hr,irk,jrk->wdhij' at 27x7x24x400x400, R=10, K=6 has 48,580
+    parameters - summed from the library's own nef_factor_shape."""
+    g = golden["uber_param_count"]
+    p = nef.Plan(g["model"], g["shape"], g["ranks"])
+    total = sum(int(np.prod(s)) for s in p.factor_shapes())
+    assert total == g["value"]
