@@ -1,3 +1,3 @@
 """Seeded synthetic input generators (shared by the oracle and the CUDA path; holds
 none of the method's arithmetic)."""
-from .synth import CONFIGS, Config, factor_shapes, generate_numpy, generate_torch  # noqa: F401
+from .synth import CONFIGS, Config, factor_shapes, generate_numpy, generate_torch, split_labels  # noqa: F401

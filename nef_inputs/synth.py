@@ -202,3 +202,23 @@ def _apply_noise_torch(cfg, yhat, g):
         noise = torch._standard_gamma(torch.full_like(yhat, 10.0), generator=g) * 0.1
         return yhat * noise
     raise ValueError(cfg.law)
+
+
+# ------------------------------------------------------------------------------------
+# train / validation / heldout labels: each entry heldout w.p. p_heldout, else
+# validation w.p. p_validation, else train; uint8 codes 0 = excluded (missing data), 1 = train,
+# 2 = validation, 3 = heldout.  A draw only: no arithmetic of the method.
+# ------------------------------------------------------------------------------------
+LABEL_EXCLUDED, LABEL_TRAIN, LABEL_VAL, LABEL_HELDOUT = 0, 1, 2, 3
+
+
+def split_labels(shape, p_heldout=0.1, p_validation=0.05, seed=0, missing=None):
+    if not (0 <= p_heldout < 1 and 0 <= p_validation < 1):
+        raise ValueError("degenerate split probabilities")
+    u = np.random.default_rng(seed).random(tuple(shape))
+    lab = np.full(tuple(shape), LABEL_TRAIN, dtype=np.uint8)
+    lab[u < p_heldout + (1.0 - p_heldout) * p_validation] = LABEL_VAL
+    lab[u < p_heldout] = LABEL_HELDOUT
+    if missing is not None:
+        lab[np.asarray(missing, dtype=bool)] = LABEL_EXCLUDED
+    return lab

@@ -18,6 +18,10 @@ float64 numpy.  Citations ``P:N`` are lines of the paper's LaTeX:
 * g(lambda) 4-case table ......................... P:531-539
 * masking "replace Y, Yhat by M*Y, M*Yhat" ....... P:321 (read as zeroing a and b at
   missing entries, reading R5)
+* other decomposable losses (App. B) ............. P:541-610 (negative binomial, Bernoulli and
+  binomial odds, Jensen-Shannon): a, b, g and the loss as the paper writes them
+* train / validation / heldout protocol .......... P:318-326 (splits, masked training loss,
+  average heldout loss); stopping criteria P:497
 
 Readings where the paper is silent (all listed in DESIGN.md §Readings):
   eps = 1e-12 (R3), Yhat floor eps_y = 1e-30 (R4), mask nonzero = observed (R6),
@@ -244,6 +248,110 @@ def g_inv(t, alpha: float, beta: float):
 
 
 # --------------------------------------------------------------------------------------
+# loss specifications: the (alpha,beta) family and the other decomposable
+# losses of App. B.  A spec is a plain dict; `aux` is an optional per-entry
+# tensor (same shape as Y): the dispersion phi_i (negative binomial) or the number of
+# trials n_i (binomial); without it the scalar in the spec is used for every entry.
+# --------------------------------------------------------------------------------------
+LOSS_KINDS = ("ab", "negbin", "bernoulli", "binomial", "js")
+
+
+def make_loss(kind="ab", alpha=None, beta=None, phi=None, n=None):
+    """Loss spec.  'ab': (alpha, beta) (P:500-539); 'negbin': dispersion phi > 0 (P:541-563);
+    'bernoulli': odds; 'binomial': n trials; 'js'."""
+    if kind not in LOSS_KINDS:
+        raise ValueError("unknown loss kind %r" % kind)
+    if kind == "ab":
+        check_ab(alpha, beta)
+    return {"kind": kind, "alpha": alpha, "beta": beta, "phi": phi, "n": n}
+
+
+def _spec(alpha, beta):
+    """Accept a spec dict (beta None) or a plain (alpha, beta) pair."""
+    if isinstance(alpha, dict):
+        return alpha
+    return make_loss("ab", alpha, beta)
+
+
+def _aux(loss, key, aux, shape):
+    if aux is not None:
+        return np.asarray(aux, dtype=np.float64)
+    return np.full(shape, float(loss[key]))
+
+
+def loss_a(loss, x, y, aux=None):
+    """a(x, y) of the loss (P:529; NB / Bernoulli / binomial a = x / y P:558, P:582, P:589;
+    JS a = log((x + y) / (2y)) P:605)."""
+    x = np.asarray(x, dtype=np.float64)
+    y = np.asarray(y, dtype=np.float64)
+    k = loss["kind"]
+    if k == "ab":
+        return a_fn(x, y, loss["alpha"], loss["beta"])
+    if k in ("negbin", "bernoulli", "binomial"):
+        return x / y
+    return np.log((x + y) / (2.0 * y))
+
+
+def loss_b(loss, x, y, aux=None):
+    """b(x, y): NB (phi + x) / (phi + y); Bernoulli 1 / (1 + y); binomial
+    n / (1 + y) (the update's denominator); JS 1."""
+    x = np.asarray(x, dtype=np.float64)
+    y = np.asarray(y, dtype=np.float64)
+    k = loss["kind"]
+    if k == "ab":
+        return b_fn(x, y, loss["alpha"], loss["beta"])
+    if k == "negbin":
+        phi = _aux(loss, "phi", aux, np.broadcast(x, y).shape)
+        return (phi + x) / (phi + y)
+    if k == "bernoulli":
+        return 1.0 / (1.0 + y) * np.ones_like(x)
+    if k == "binomial":
+        n = _aux(loss, "n", aux, np.broadcast(x, y).shape)
+        return n / (1.0 + y)
+    return np.ones(np.broadcast(x, y).shape)
+
+
+def _xlogy(x, y):
+    """x log y with 0 log(.) = 0 (reading R8)."""
+    with np.errstate(divide="ignore", invalid="ignore"):
+        return np.where(x > 0, x * np.log(np.where(x > 0, y, 1.0)), 0.0)
+
+
+def loss_value(loss, x, y, aux=None):
+    """Per-entry loss: the (alpha,beta)-divergence; NB (phi + x) log(phi + y) - x log y
+    (P:548); Bernoulli log(1 + mu) - x log mu; binomial n log(1 + mu) - x log mu (the
+    binomial NLL in the odds up to terms free of mu, P:587-591 with P:570); JS
+    -(x + y)/2 log((x + y)/2) + (x log x + y log y)/2."""
+    x = np.asarray(x, dtype=np.float64)
+    y = np.asarray(y, dtype=np.float64)
+    k = loss["kind"]
+    if k == "ab":
+        return divergence(x, y, loss["alpha"], loss["beta"])
+    if k == "negbin":
+        phi = _aux(loss, "phi", aux, np.broadcast(x, y).shape)
+        return (phi + x) * np.log(phi + y) - _xlogy(x, y)
+    if k == "bernoulli":
+        return np.log1p(y) - _xlogy(x, y)
+    if k == "binomial":
+        n = _aux(loss, "n", aux, np.broadcast(x, y).shape)
+        return n * np.log1p(y) - _xlogy(x, y)
+    m = (x + y) / 2.0
+    return -m * np.log(m) + 0.5 * (_xlogy(x, x) + y * np.log(y))
+
+
+def loss_ginv(loss, t):
+    """g^{-1}: the (alpha,beta) table (P:531-539); g(lambda) = lambda for NB, Bernoulli and
+    binomial (P:558, P:582); g = log for JS (P:605)."""
+    k = loss["kind"]
+    if k == "ab":
+        return g_inv(t, loss["alpha"], loss["beta"])
+    t = np.asarray(t, dtype=np.float64)
+    if k == "js":
+        return np.exp(t)
+    return t
+
+
+# --------------------------------------------------------------------------------------
 # objective (eq:obj, P:102-106) with mask (P:321)
 # --------------------------------------------------------------------------------------
 def _obs(mask, shape):
@@ -252,29 +360,39 @@ def _obs(mask, shape):
     return np.asarray(mask) != 0          # reading R6: nonzero = observed
 
 
-def loss(model_str, Y, mask, factors, alpha, beta, eps_y=EPS_Y):
-    """Sum over observed entries of L_{alpha,beta}(y_i, max(yhat_i, eps_y)) (eq:obj,
-    P:104; reading R7: sum, not mean).  Returns (sum, n_observed)."""
+def _aux_at(aux, obs):
+    if aux is None:
+        return None
+    return np.where(obs, np.asarray(aux, dtype=np.float64), 1.0)
+
+
+def loss(model_str, Y, mask, factors, alpha, beta=None, eps_y=EPS_Y, aux=None):
+    """Sum over observed entries of L(y_i, max(yhat_i, eps_y)) (eq:obj; reading R7: sum,
+    not mean).  ``alpha`` is either the (alpha, beta) pair's alpha or a loss spec (make_loss).
+    Returns (sum, n_observed)."""
+    spec = _spec(alpha, beta)
     Y = np.asarray(Y, dtype=np.float64)
     obs = _obs(mask, Y.shape)
     yhat = np.maximum(contract(model_str, factors), eps_y)
-    vals = divergence(np.where(obs, Y, 1.0), yhat, alpha, beta)
+    vals = loss_value(spec, np.where(obs, Y, 1.0), yhat, _aux_at(aux, obs))
     return float(np.sum(np.where(obs, vals, 0.0))), int(np.count_nonzero(obs))
 
 
 # --------------------------------------------------------------------------------------
 # one multiplicative update (Theorem 1, P:119-125; Algorithm 1 lines 6-9, P:165-177)
 # --------------------------------------------------------------------------------------
-def numerator_denominator(model_str, Y, mask, factors, ell, alpha, beta, eps_y=EPS_Y):
+def numerator_denominator(model_str, Y, mask, factors, ell, alpha, beta=None, eps_y=EPS_Y, aux=None):
     """(A, B) of Algorithm 1 lines 7-8 for factor ``ell`` (0-based):
     Yhat = einsum(model_str, Theta); A = einsum(einstr_ell, ..., a(Y,Yhat), ...);
     B = einsum(einstr_ell, ..., b(Y,Yhat), ...), with a, b zeroed at missing entries."""
+    spec = _spec(alpha, beta)
     Y = np.asarray(Y, dtype=np.float64)
     obs = _obs(mask, Y.shape)
     yhat = np.maximum(contract(model_str, factors), eps_y)          # Alg. 1 line 6
     xs = np.where(obs, Y, 1.0)                                       # masked values never read
-    a = np.where(obs, a_fn(xs, yhat, alpha, beta), 0.0)              # P:529, P:321
-    b = np.where(obs, b_fn(xs, yhat, alpha, beta), 0.0)
+    ax = _aux_at(aux, obs)
+    a = np.where(obs, loss_a(spec, xs, yhat, ax), 0.0)               # P:529, P:321
+    b = np.where(obs, loss_b(spec, xs, yhat, ax), 0.0)
     einstr = swap(model_str, ell)                                     # P:149
     ops = [np.asarray(f, dtype=np.float64) for f in factors]
     A = contract(einstr, ops[:ell] + [a] + ops[ell + 1:])             # Alg. 1 line 7
@@ -282,39 +400,97 @@ def numerator_denominator(model_str, Y, mask, factors, ell, alpha, beta, eps_y=E
     return A, B
 
 
-def update_factor(model_str, Y, mask, factors, ell, alpha, beta, eps=EPS, eps_y=EPS_Y):
+def update_factor(model_str, Y, mask, factors, ell, alpha, beta=None, eps=EPS, eps_y=EPS_Y, aux=None):
     """Theta^(ell) <- max(eps, Theta^(ell) * g^{-1}(A / B)) (eq:explicit-update P:121;
     Alg. 1 line 9).  B == 0 -> multiplier 1 (reading R10).  Returns the
     new factor (float64); does not modify ``factors``."""
-    A, B = numerator_denominator(model_str, Y, mask, factors, ell, alpha, beta, eps_y)
+    spec = _spec(alpha, beta)
+    A, B = numerator_denominator(model_str, Y, mask, factors, ell, spec, eps_y=eps_y, aux=aux)
     theta = np.asarray(factors[ell], dtype=np.float64)
     pos = B > 0
     ratio = np.where(pos, A / np.where(pos, B, 1.0), 1.0)
-    mult = np.where(pos, g_inv(ratio, alpha, beta), 1.0)
+    mult = np.where(pos, loss_ginv(spec, ratio), 1.0)
     return np.maximum(eps, theta * mult)
 
 
-def fit(model_str, Y, mask, factors, alpha, beta, iters, eps=EPS, eps_y=EPS_Y, check_monotone=False):
+def fit(model_str, Y, mask, factors, alpha, beta, iters, eps=EPS, eps_y=EPS_Y, check_monotone=False, aux=None):
     """Algorithm 1: ``iters`` full sweeps over ell = 1..L in string order,
     Yhat recomputed before every factor update.  Returns (factors, trace) with
-    trace[0] = loss at init and trace[t] = loss after sweep t (reading R9).
+    trace[0] = loss at init and trace[t] = loss after sweep t (reading R9).  ``alpha`` may be
+    a loss spec (then ``beta`` is ignored).
 
     check_monotone asserts Theorem 1 after EVERY factor update (relative slack 1e-12).
     Parity unpinned as a whole trajectory: no closed form exists for it; it is pinned
     through its steps (tests/test_oracle_pins.py) and Theorem 2 monotonicity.
     """
-    check_ab(alpha, beta)
+    spec = _spec(alpha, beta)
     th = [np.array(f, dtype=np.float64) for f in factors]
-    trace = [loss(model_str, Y, mask, th, alpha, beta, eps_y)[0]]
+    trace = [loss(model_str, Y, mask, th, spec, eps_y=eps_y, aux=aux)[0]]
     for _ in range(iters):
         for ell in range(len(th)):
-            before = loss(model_str, Y, mask, th, alpha, beta, eps_y)[0] if check_monotone else None
-            th[ell] = update_factor(model_str, Y, mask, th, ell, alpha, beta, eps, eps_y)
+            before = loss(model_str, Y, mask, th, spec, eps_y=eps_y, aux=aux)[0] if check_monotone else None
+            th[ell] = update_factor(model_str, Y, mask, th, ell, spec, eps=eps, eps_y=eps_y, aux=aux)
             if check_monotone:
-                after = loss(model_str, Y, mask, th, alpha, beta, eps_y)[0]
+                after = loss(model_str, Y, mask, th, spec, eps_y=eps_y, aux=aux)[0]
                 assert after <= before + 1e-12 * abs(before) + 1e-300, (ell, before, after)
-        trace.append(loss(model_str, Y, mask, th, alpha, beta, eps_y)[0])
+        trace.append(loss(model_str, Y, mask, th, spec, eps_y=eps_y, aux=aux)[0])
     return th, trace
+
+
+# --------------------------------------------------------------------------------------
+# train / validation / heldout protocol (P:318-326) and stopping criteria (P:497)
+# labels: 0 = excluded (missing data), 1 = train, 2 = validation (V), 3 = heldout (H)
+# --------------------------------------------------------------------------------------
+ROLE_TRAIN, ROLE_VAL, ROLE_HELDOUT = 1, 2, 3
+
+
+def role_losses(model_str, Y, labels, factors, loss_spec, eps_y=EPS_Y, aux=None):
+    """Loss sums and entry counts of the three roles (train, validation, heldout) at the current
+    factors; the heldout mean sum / count is the paper's evaluation metric."""
+    labels = np.asarray(labels)
+    sums, counts = [], []
+    for r in (ROLE_TRAIN, ROLE_VAL, ROLE_HELDOUT):
+        s_, n_ = loss(model_str, Y, labels == r, factors, loss_spec, eps_y=eps_y, aux=aux)
+        sums.append(s_)
+        counts.append(n_)
+    return sums, counts
+
+
+def stop_decision(train, val, t, rule):
+    """Stopping criteria of P:497 after sweep t (traces hold entries 0..t): validation loss
+    increasing (strictly, vs the previous sweep) for ``val_patience`` consecutive sweeps; a
+    decrease of the training loss of less than ``min_rel_decrease`` relative to its previous
+    value; ``max_iters`` sweeps.  Readings R29-R31.  Returns None or the reason."""
+    p = int(rule["val_patience"])
+    if p > 0 and t >= p and all(val[s] > val[s - 1] for s in range(t - p + 1, t + 1)):
+        return "patience"
+    if t >= 1 and (train[t - 1] - train[t]) < rule["min_rel_decrease"] * abs(train[t - 1]):
+        return "plateau"
+    if t >= rule["max_iters"]:
+        return "max_iters"
+    return None
+
+
+def fit_split(model_str, Y, labels, factors, loss_spec, rule, eps=EPS, eps_y=EPS_Y, aux=None):
+    """Algorithm 1 trained on the train role only (labels == 1), with the train,
+    validation and heldout losses after every sweep and the stopping rules of P:497.  Returns
+    (factors, traces[3], counts[3], sweeps_run, reason): traces[r][t] = loss sum of role r after
+    sweep t, t = 0..sweeps_run; factors = the iterate after sweep ``sweeps_run``."""
+    train_mask = (np.asarray(labels) == ROLE_TRAIN).astype(np.uint8)
+    th = [np.array(f, dtype=np.float64) for f in factors]
+    sums, counts = role_losses(model_str, Y, labels, th, loss_spec, eps_y, aux)
+    traces = [[v] for v in sums]
+    t = 0
+    reason = stop_decision(traces[0], traces[1], 0, rule)
+    while reason is None:
+        for ell in range(len(th)):
+            th[ell] = update_factor(model_str, Y, train_mask, th, ell, loss_spec, eps=eps, eps_y=eps_y, aux=aux)
+        t += 1
+        sums, _ = role_losses(model_str, Y, labels, th, loss_spec, eps_y, aux)
+        for tr, v in zip(traces, sums):
+            tr.append(v)
+        reason = stop_decision(traces[0], traces[1], t, rule)
+    return th, traces, counts, t, reason
 
 
 def param_count(model_str, shape, ranks) -> int:
