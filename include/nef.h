@@ -59,6 +59,39 @@ enum nef_status {
   NEF_E_UNSUPPORTED = 8   /* model string with no lowering in this build                        */
 };
 
+/* Loss specification (the decomposable losses of the paper).
+ *   NEF_LOSS_AB        (alpha, beta)-divergence, P:500-539 (alpha, beta in the paper's convention)
+ *   NEF_LOSS_NEGBIN    negative binomial in its mean, dispersion phi: L = (phi+x) log(phi+y) - x log y,
+ *                      a = x/y, b = (phi+x)/(phi+y), g(lambda) = lambda
+ *   NEF_LOSS_BERNOULLI Bernoulli in the odds mu: L = log(1+mu) - x log mu, a = x/y, b = 1/(1+y),
+ *                      g(lambda) = lambda
+ *   NEF_LOSS_BINOMIAL  binomial with n trials in the odds: L = n log(1+mu) - x log mu, a = x/y,
+ *                      b = n/(1+y)
+ *   NEF_LOSS_JS        Jensen-Shannon: a = log((x+y)/(2y)), b = 1, g = log
+ * param: phi (NEGBIN) or n (BINOMIAL) for every entry, used when aux == NULL (must be > 0).
+ * aux: optional device float tensor with Y's (local) shape and layout holding a per-entry phi_i or
+ * n_i (NEGBIN / BINOMIAL only; else must be NULL).  It is streamed with Y (+4 B per entry) and, in
+ * this build, only by the CUDA-core kernel.  Domain errors: NEF_E_DOMAIN (unknown kind, alpha = 0
+ * with beta != 1, param <= 0 without aux); NEF_E_ARG (aux misaligned / not applicable). */
+enum nef_loss_kind { NEF_LOSS_AB = 0, NEF_LOSS_NEGBIN = 1, NEF_LOSS_BERNOULLI = 2, NEF_LOSS_BINOMIAL = 3, NEF_LOSS_JS = 4 };
+typedef struct nef_loss_spec {
+  int kind;              /* nef_loss_kind */
+  double alpha, beta;    /* NEF_LOSS_AB */
+  double param;          /* NEF_LOSS_NEGBIN: phi; NEF_LOSS_BINOMIAL: n (when aux == NULL) */
+  const float* aux;      /* device, per-entry phi / n, or NULL */
+} nef_loss_spec;
+
+/* Stopping rules of P:497 for nef_fit_split (readings R30, R31): stop after the sweep at which
+ * the validation loss rose (strictly, vs the previous sweep) for val_patience consecutive sweeps
+ * (0 disables), or the training loss fell by less than min_rel_decrease relative to its previous
+ * value (a rise counts), or max_iters sweeps ran; priority in that order.  Paper: 5, 1e-6, 5000. */
+typedef struct nef_stop_rule {
+  int max_iters;
+  double min_rel_decrease;
+  int val_patience;
+} nef_stop_rule;
+enum nef_stop_reason { NEF_STOP_PATIENCE = 1, NEF_STOP_PLATEAU = 2, NEF_STOP_MAX_ITERS = 3 };
+
 /* Build a plan for `einsum` over a GLOBAL tensor of `n_modes` dims `shape` (output order)
  * with `n_ranks` contracted-index sizes `ranks` (first-appearance order).  Host only:
  * parses, builds einstr_l = swap(model_str, l) for every l (Alg. 1
@@ -71,7 +104,11 @@ int nef_plan(const char* einsum, int n_modes, const int64_t* shape, int n_ranks,
  * [local_begin, local_begin + local_len) = this rank's index range of that mode (whole
  * range if unsharded); workspace_bytes = device scratch nef_fit / nef_loss / nef_update
  * need for a problem WITH a mask (a maskless problem needs no more).  Any out-pointer may
- * be NULL. */
+ * be NULL.
+ * Memory: workspace_bytes includes a 4-byte-per-local-entry copy of Y (the mask folded in as a
+ * sign sentinel, R22) that masked fits stream instead of Y + mask - e.g. +17.2 GB for
+ * the 2048x2048x1024 tensor, on top of Y (17.2 GB) and the mask (4.3 GB); plus small per-factor
+ * scratch (side operands, split partials, < 1 % of Y). */
 int nef_plan_info(nef_plan_t plan, int* n_factors, int* shard_mode, int64_t* local_begin, int64_t* local_len,
                   size_t* workspace_bytes);
 
@@ -101,9 +138,33 @@ int nef_fit(nef_plan_t plan, const float* Y, const uint8_t* mask, double alpha, 
             float* const* factors, int iters, double* loss_trace, void* workspace, size_t ws_bytes,
             void* cuda_stream);
 
+/* nef_fit for any loss of an nef_loss_spec: the (alpha,beta) entry point above is this with
+ * NEF_LOSS_AB.  Same arguments, ownership and errors; aux (if any) is this rank's local slice. */
+int nef_fit_ex(nef_plan_t plan, const float* Y, const uint8_t* mask, const nef_loss_spec* loss, double eps,
+               float* const* factors, int iters, double* loss_trace, void* workspace, size_t ws_bytes,
+               void* cuda_stream);
+
+/* Train / validation / heldout protocol with the stopping rules of P:497.
+ * labels: device uint8, Y's local shape: 0 = excluded (missing data), 1 = train, 2 = validation,
+ * 3 = heldout (reading R29).  Algorithm 1 runs on the train entries only; once per sweep the
+ * same streamed pass that updates the first factor also sums the loss of each role.
+ * traces: host, 3 x (rule->max_iters + 1) doubles, role-major ([train][t], [validation][t],
+ * [heldout][t]); entries 0..*sweeps are written (trace[r][t] = loss sum of role r after sweep t;
+ * the paper's heldout metric is trace[2][t] / counts[2]).  counts: host int64[3], entries per
+ * role.  On return the factors are the iterate after sweep *sweeps, the sweep at which a rule
+ * fired (reading R32); *reason is an nef_stop_reason.  The host reads the three sums once per
+ * sweep (pinned memory + an event, while the sweep continues on the stream).  Sharded plans
+ * all-reduce the sums over NCCL.  Errors as nef_fit; NEF_E_ARG for a null labels / rule. */
+int nef_fit_split(nef_plan_t plan, const float* Y, const uint8_t* labels, const nef_loss_spec* loss, double eps,
+                  float* const* factors, const nef_stop_rule* rule, double* traces, int64_t* counts, int* sweeps,
+                  int* reason, void* workspace, size_t ws_bytes, void* cuda_stream);
+
 /* One factor update (Algorithm 1 lines 6-9 for a single ell), the step-level API. */
 int nef_update(nef_plan_t plan, int ell, const float* Y, const uint8_t* mask, double alpha, double beta,
                double eps, float* const* factors, void* workspace, size_t ws_bytes, void* cuda_stream);
+
+int nef_update_ex(nef_plan_t plan, int ell, const float* Y, const uint8_t* mask, const nef_loss_spec* loss,
+                  double eps, float* const* factors, void* workspace, size_t ws_bytes, void* cuda_stream);
 
 /* Numerator A and denominator B of the update of factor `ell` (Alg. 1 lines 7-8, before
  * any all-reduce), written to num/den (device, size of factor ell).  For tests and for
@@ -112,15 +173,25 @@ int nef_num_den(nef_plan_t plan, int ell, const float* Y, const uint8_t* mask, d
                 float* const* factors, float* num, float* den, void* workspace, size_t ws_bytes,
                 void* cuda_stream);
 
-/* Theta_ell <- max(eps, Theta_ell * g^{-1}(num/den)) with den == 0 -> multiplier 1. */
+int nef_num_den_ex(nef_plan_t plan, int ell, const float* Y, const uint8_t* mask, const nef_loss_spec* loss,
+                   float* const* factors, float* num, float* den, void* workspace, size_t ws_bytes,
+                   void* cuda_stream);
+
+/* Theta_ell <- max(eps, Theta_ell * g^{-1}(num/den)) with den == 0 -> multiplier 1
+ * (eq:explicit-update P:121; g per P:531-539, identity for NB / odds losses, exp for JS). */
 int nef_apply_update(nef_plan_t plan, int ell, double alpha, double beta, double eps, float* const* factors,
                      const float* num, const float* den, void* cuda_stream);
+int nef_apply_update_ex(nef_plan_t plan, int ell, const nef_loss_spec* loss, double eps, float* const* factors,
+                        const float* num, const float* den, void* cuda_stream);
 
-/* Loss sum over observed entries (fp64) and the number of observed entries, for the
- * current factors (all-reduced over ranks on a sharded plan). */
+/* Loss sum over observed entries (fp64; eq:obj P:102-106, divergence P:500-525) and the number
+ * of observed entries, for the current factors (all-reduced over ranks on a sharded plan). */
 int nef_loss(nef_plan_t plan, const float* Y, const uint8_t* mask, double alpha, double beta,
              float* const* factors, double* loss_sum, int64_t* n_observed, void* workspace, size_t ws_bytes,
              void* cuda_stream);
+int nef_loss_ex(nef_plan_t plan, const float* Y, const uint8_t* mask, const nef_loss_spec* loss,
+                float* const* factors, double* loss_sum, int64_t* n_observed, void* workspace, size_t ws_bytes,
+                void* cuda_stream);
 
 /* End-to-end variant taking HOST buffers: copies Y (and mask) host->device into
  * `device_scratch`, the factors host->device, runs nef_fit, copies the factors back
@@ -142,8 +213,9 @@ int nef_plan_shard(nef_plan_t plan, int rank, int world, const void* nccl_unique
 /* The same split without a communicator (host planning only): the plan describes this rank's
  * local tensor (nef_plan_info: local_begin / local_len; nef_plan_describe: "factor_has_shard",
  * false = the factor's A|B must be summed over ranks).  nef_num_den then returns this rank's
- * partial A|B, which the caller all-reduces (e.g. torch.distributed) before nef_apply_update;
- * nef_fit / nef_update / nef_loss on such a plan with world > 1 return NEF_E_NCCL.
+ * partial A|B, which the caller all-reduces (e.g. torch.distributed) before nef_apply_update, and
+ * nef_loss returns this rank's partial loss sum and observed count; nef_fit / nef_update on such
+ * a plan with world > 1 return NEF_E_NCCL.
  * Errors: NEF_E_ARG (bad rank / world, already sharded), NEF_E_SHAPE (largest mode < world). */
 int nef_plan_shard_host(nef_plan_t plan, int rank, int world);
 

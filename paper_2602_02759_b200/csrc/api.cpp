@@ -124,6 +124,13 @@ struct Ctx {
   const float* ysent = nullptr;   // NaN-sentinel copy of Y (mask folded in), when prepared
   const double* loff = nullptr;   // R25: [data-only loss sum][observed count] of the sentinel pass
   double lscale = 1.0;            //      loss = lscale * (streamed part) + loff[0]
+  const float* aux = nullptr;     // per-entry phi / n (App. B losses), Y's layout; CUDA-core kernel only
+  int split = 0;                  // the mask holds labels 0..3 (R29); loss slots are [3] per pass
+  // split fits: after the loss-carrying pass, copy the loss slots to pinned host memory and
+  // record an event, so the host can take the stopping decision while the sweep continues
+  void* pin = nullptr;
+  cudaEvent_t pin_ev = nullptr;
+  bool pin_counts = false;
 };
 
 float* resolve(const Ctx& c, const nef::BufRef& b) {
@@ -181,9 +188,11 @@ nef::FusedArgs fused_args(const Ctx& c, const nef::Lowering& L, const float* Y, 
   a.Qpart = reinterpret_cast<float*>(c.ws + L.ws_Qpart);
   a.losspart = reinterpret_cast<double*>(c.ws + L.ws_losspart);
   int64_t nparts = ((L.n_rows + 63) / 64) * L.n_chunks;
-  a.countpart = reinterpret_cast<long long*>(c.ws + L.ws_losspart + nparts * 8);
+  a.countpart = reinterpret_cast<long long*>(c.ws + L.ws_losspart + 3 * nparts * 8);
   a.dv = dv;
   a.mode = mode;
+  a.aux = c.aux;
+  a.split = (c.split && M) ? 1 : 0;
   return a;
 }
 
@@ -207,8 +216,9 @@ struct StreamOut {
   bool lconst = false;            // loss partials hold only the factor-dependent part (R25)
 };
 
-bool use_tc(const nef::Lowering& L, const uint8_t* M, bool sentinel = false) {
-  return g_policy == 0 && L.tc_ok && (!M || sentinel || (L.tc_mask_ok && (reinterpret_cast<uintptr_t>(M) & 15) == 0));
+bool use_tc(const nef::Lowering& L, const uint8_t* M, bool sentinel = false, const float* aux = nullptr) {
+  return g_policy == 0 && L.tc_ok && !aux &&
+         (!M || sentinel || (L.tc_mask_ok && (reinterpret_cast<uintptr_t>(M) & 15) == 0));
 }
 
 // One streaming pass over Y (+mask) for lowering L: the tcgen05 kernel where the planner
@@ -220,9 +230,11 @@ int stream_pass(const Ctx& c, const nef::Lowering& L, const float* Y, const uint
     return fail(NEF_E_UNSUPPORTED, "lowering exceeds the kernels' limits (<= 4 column tables, bond <= 64)");
   std::vector<int32_t> boff;
   nef::FusedArgs a = fused_args(c, L, Y, M, mode, dv, boff);
-  const double bytes = (double)c.p->n_local * (M ? 5.0 : 4.0);
-  const bool sent = M && c.ysent;
-  if (use_tc(L, M, sent)) {
+  const double bytes = (double)c.p->n_local * ((M ? 5.0 : 4.0) + (c.aux ? 4.0 : 0.0));
+  // split fits: the loss-carrying passes stream Y with the labels (train / validation / heldout
+  // losses of one pass); update-only passes stream the train-folded sentinel copy
+  const bool sent = M && c.ysent && !(c.split && mode != 0);
+  if (use_tc(L, M, sent, c.aux)) {
     if (sent) {   // stream the NaN-sentinel copy: no mask stream (4 B / entry)
       Y = c.ysent;
       M = nullptr;
@@ -288,9 +300,10 @@ int stream_pass(const Ctx& c, const nef::Lowering& L, const float* Y, const uint
     t.Qpart = reinterpret_cast<float*>(c.ws + L.ws_tc_Qpart);
     t.losspart = reinterpret_cast<double*>(c.ws + L.ws_tc_losspart);
     o.nparts = L.tc_row_blocks * chunks;
-    t.countpart = reinterpret_cast<long long*>(c.ws + L.ws_tc_losspart + o.nparts * 8);
+    t.countpart = reinterpret_cast<long long*>(c.ws + L.ws_tc_losspart + 3 * o.nparts * 8);
     t.dv = dv;
     t.mode = mode;
+    t.split = (c.split && M && !sent) ? 1 : 0;
     t.lconst = ((sent || !M) && c.loff && mode != 0) ? 1 : 0;
     // unmasked Y streamed as is: every entry is observed, so the kernel must not read "missing"
     // from a sign bit (an observed -0.0 is a zero); the sentinel copy canonicalises -0 itself
@@ -328,6 +341,31 @@ int stream_pass(const Ctx& c, const nef::Lowering& L, const float* Y, const uint
   return NEF_OK;
 }
 
+bool communicates(const nef::Plan& p);
+int allreduce(const nef::Plan& p, void* buf, size_t count, int dtype, cudaStream_t s);
+
+// Loss partials of one pass -> slot[r] (double) + cslot[r] (long long), one role (three on a split
+// fit); then, for split fits, the slots go to pinned host memory behind an event (Ctx::pin)
+int reduce_loss(const Ctx& c, const StreamOut& o, const uint8_t* M, double* slot, long long* cslot) {
+  const int nrole = (c.split && M) ? 3 : 1;
+  for (int q = 0; q < nrole; ++q) {
+    CK(nef::launch_loss_reduce(o.losspart + q * o.nparts, o.countpart + q * o.nparts, o.nparts, slot + q, cslot + q,
+                               c.s, o.lconst ? c.lscale : 1.0, o.lconst ? c.loff : nullptr));
+    ++g_launches;
+  }
+  if (c.pin) {
+    if (communicates(*c.p)) {
+      if (int r = allreduce(*c.p, slot, 3, kNcclFloat64, c.s)) return r;
+      if (c.pin_counts)
+        if (int r = allreduce(*c.p, cslot, 3, kNcclInt64, c.s)) return r;
+    }
+    CK(cudaMemcpyAsync(c.pin, slot, 3 * sizeof(double), cudaMemcpyDeviceToHost, c.s));
+    if (c.pin_counts) CK(cudaMemcpyAsync(static_cast<char*>(c.pin) + 32, cslot, 3 * sizeof(long long), cudaMemcpyDeviceToHost, c.s));
+    CK(cudaEventRecord(c.pin_ev, c.s));
+  }
+  return NEF_OK;
+}
+
 // Loss-only pass with lowering 0 -> slot (double) + count slot (long long)
 int loss_pass(const Ctx& c, const float* Y, const uint8_t* M, const nef::DivParams& dv, double* slot, long long* cslot) {
   const nef::Lowering& L = c.p->low[0];
@@ -335,10 +373,7 @@ int loss_pass(const Ctx& c, const float* Y, const uint8_t* M, const nef::DivPara
   if (st) return st;
   StreamOut o;
   if ((st = stream_pass(c, L, Y, M, 2, dv, o))) return st;
-  CK(nef::launch_loss_reduce(o.losspart, o.countpart, o.nparts, slot, cslot, c.s, o.lconst ? c.lscale : 1.0,
-                             o.lconst ? c.loff : nullptr));
-  ++g_launches;
-  return NEF_OK;
+  return reduce_loss(c, o, M, slot, cslot);
 }
 
 // Steps 1-4 of one factor update: leaves A in *num, B in *den (device pointers into ws).
@@ -349,11 +384,7 @@ int num_den(const Ctx& c, int ell, const float* Y, const uint8_t* M, const nef::
   if (st) return st;
   StreamOut o;
   if ((st = stream_pass(c, L, Y, M, mode, dv, o))) return st;
-  if (mode == 1) {
-    CK(nef::launch_loss_reduce(o.losspart, o.countpart, o.nparts, slot, cslot, c.s, o.lconst ? c.lscale : 1.0,
-                               o.lconst ? c.loff : nullptr));
-    ++g_launches;
-  }
+  if (mode == 1 && (st = reduce_loss(c, o, M, slot, cslot))) return st;
   const int64_t qe = L.n_rows * L.K;
   float* Q = reinterpret_cast<float*>(c.ws + L.ws_Q);
   CK(nef::launch_reduce_q(o.Qpart, Q, o.n_chunks, 2 * qe, c.s));
@@ -425,6 +456,45 @@ int validate_common(nef_plan_t plan, const float* Y, float* const* factors, void
   if (!ws || ws_bytes < plan->p.ws_bytes)
     return fail(NEF_E_ARG, "workspace too small: need " + std::to_string(plan->p.ws_bytes) + " bytes");
   if (reinterpret_cast<uintptr_t>(ws) & 255) return fail(NEF_E_ARG, "workspace must be 256-byte aligned");
+  return NEF_OK;
+}
+
+// loss specification (include/nef.h nef_loss_spec), validated
+struct Spec {
+  int fam = nef::FAM_AB;
+  double alpha = 1.0, beta = 0.0, prm = 0.0;
+  const float* aux = nullptr;
+};
+
+nef_loss_spec ab_spec(double alpha, double beta) {
+  nef_loss_spec l{};
+  l.kind = NEF_LOSS_AB;
+  l.alpha = alpha;
+  l.beta = beta;
+  return l;
+}
+
+int validate_spec(const nef_loss_spec* l, Spec& sp) {
+  if (!l) return fail(NEF_E_ARG, "null loss spec");
+  if (l->kind < NEF_LOSS_AB || l->kind > NEF_LOSS_JS) return fail(NEF_E_DOMAIN, "unknown loss kind");
+  sp.fam = l->kind;
+  if (l->kind == NEF_LOSS_AB) {
+    if (int st = validate_ab(l->alpha, l->beta)) return st;
+    sp.alpha = l->alpha;
+    sp.beta = l->beta;
+  }
+  if (l->kind == NEF_LOSS_NEGBIN || l->kind == NEF_LOSS_BINOMIAL) {
+    if (l->aux) {
+      if (reinterpret_cast<uintptr_t>(l->aux) & 3) return fail(NEF_E_ARG, "misaligned aux tensor");
+      sp.aux = l->aux;
+    } else if (!(l->param > 0.0) || !std::isfinite(l->param)) {
+      return fail(NEF_E_DOMAIN, l->kind == NEF_LOSS_NEGBIN ? "negative binomial needs phi > 0 (P:543)"
+                                                           : "binomial needs n > 0 trials (P:587)");
+    }
+    sp.prm = l->param;
+  } else if (l->aux) {
+    return fail(NEF_E_ARG, "aux tensor given for a loss without per-entry parameters");
+  }
   return NEF_OK;
 }
 
@@ -542,25 +612,27 @@ int nef_plan_describe(nef_plan_t plan, char* buf, size_t cap, size_t* len) {
   return NEF_OK;
 }
 
-int nef_fit(nef_plan_t plan, const float* Y, const uint8_t* mask, double alpha, double beta, double eps,
-            float* const* factors, int iters, double* loss_trace, void* workspace, size_t ws_bytes, void* stream) {
+int nef_fit_ex(nef_plan_t plan, const float* Y, const uint8_t* mask, const nef_loss_spec* loss, double eps,
+               float* const* factors, int iters, double* loss_trace, void* workspace, size_t ws_bytes, void* stream) {
   int st = validate_common(plan, Y, factors, workspace, ws_bytes);
   if (st) return st;
-  if ((st = validate_ab(alpha, beta))) return st;
+  Spec sp;
+  if ((st = validate_spec(loss, sp))) return st;
   if (!(eps > 0.0) || !std::isfinite(eps)) return fail(NEF_E_ARG, "eps must be > 0");
   if (iters < 0) return fail(NEF_E_ARG, "iters must be >= 0");
   if (int dst = check_device()) return dst;
   g_launches = 0;
   const nef::Plan& p = plan->p;
   Ctx c{&p, factors, static_cast<char*>(workspace), ws_bytes, static_cast<cudaStream_t>(stream)};
-  nef::DivParams dv = nef::make_div(alpha, beta);
-  nef::UpdArgs u = nef::make_upd(alpha, beta, eps);
+  c.aux = sp.aux;
+  nef::DivParams dv = nef::make_div_fam(sp.fam, sp.alpha, sp.beta, sp.prm);
+  nef::UpdArgs u = nef::make_upd_fam(sp.fam, sp.alpha, sp.beta, eps);
   // a1 precompute (once per fit): fold the mask into a NaN-sentinel copy of Y for the tcgen05
   // passes (R5: missing values are never used, whatever Y holds there)
   // R25: for the pairs that split the loss, its data-only part is summed once per fit (with the
   // sentinel copy when there is a mask, else by a read-only pass) when the loss-carrying
   // lowering runs on the tcgen05 kernel
-  const int dterm = (g_no_lconst || g_policy != 0) ? 0
+  const int dterm = (g_no_lconst || g_policy != 0 || sp.fam != nef::FAM_AB) ? 0
                     : dv.kind == nef::EW_B_M05   ? 1
                     : dv.kind == nef::EW_KL      ? 2
                     : dv.kind == nef::EW_A05_B0  ? 3
@@ -569,9 +641,9 @@ int nef_fit(nef_plan_t plan, const float* Y, const uint8_t* mask, double alpha, 
   double* dslot = reinterpret_cast<double*>(c.ws + p.ws_dterm);
   double* dpart = reinterpret_cast<double*>(c.ws + p.ws_dpart);
   long long* dcpart = reinterpret_cast<long long*>(dpart + nef::kSentParts);
-  if (mask && g_policy == 0 && !g_no_sentinel) {
-    bool any_tc = false;
-    for (const auto& L : p.low) any_tc |= L.tc_ok;
+  bool any_tc = false;
+  for (const auto& L : p.low) any_tc |= L.tc_ok;
+  if (mask && g_policy == 0 && !g_no_sentinel && !sp.aux) {
     if (any_tc) {
       float* ys = reinterpret_cast<float*>(c.ws + p.ws_sent);
       CK(nef::launch_sentinel(Y, mask, ys, p.n_local, dterm, dpart, dcpart, dslot,
@@ -583,7 +655,7 @@ int nef_fit(nef_plan_t plan, const float* Y, const uint8_t* mask, double alpha, 
         c.lscale = lscale;
       }
     }
-  } else if (!mask && dterm && p.low[0].tc_ok && iters >= 3) {
+  } else if (!mask && dterm && p.low[0].tc_ok && iters >= 3 && !sp.aux) {
     // (the read-only pass costs about what the split saves on two loss-carrying passes)
     CK(nef::launch_dterm(Y, p.n_local, dterm, dpart, dcpart, dslot, reinterpret_cast<long long*>(dslot + 1), c.s));
     g_launches += 3;
@@ -624,31 +696,152 @@ int nef_fit(nef_plan_t plan, const float* Y, const uint8_t* mask, double alpha, 
   return NEF_OK;
 }
 
-int nef_update(nef_plan_t plan, int ell, const float* Y, const uint8_t* mask, double alpha, double beta, double eps,
-               float* const* factors, void* workspace, size_t ws_bytes, void* stream) {
+int nef_fit(nef_plan_t plan, const float* Y, const uint8_t* mask, double alpha, double beta, double eps,
+            float* const* factors, int iters, double* loss_trace, void* workspace, size_t ws_bytes, void* stream) {
+  const nef_loss_spec ls = ab_spec(alpha, beta);
+  return nef_fit_ex(plan, Y, mask, &ls, eps, factors, iters, loss_trace, workspace, ws_bytes, stream);
+}
+
+// Train / validation / heldout fit with the stopping rules of P:497 (readings R29-R32).  Per
+// sweep t + 1, the first factor's pass also yields the three loss sums of the iterate t that
+// enters it; they reach pinned host memory behind an event while the rest of the sweep runs, the
+// host applies the rules, and on a stop the factors saved before sweep t + 1 (iterate t) are
+// restored.
+int nef_fit_split(nef_plan_t plan, const float* Y, const uint8_t* labels, const nef_loss_spec* loss, double eps,
+                  float* const* factors, const nef_stop_rule* rule, double* traces, int64_t* counts, int* sweeps,
+                  int* reason, void* workspace, size_t ws_bytes, void* stream) {
   int st = validate_common(plan, Y, factors, workspace, ws_bytes);
   if (st) return st;
-  if ((st = validate_ab(alpha, beta))) return st;
+  Spec sp;
+  if ((st = validate_spec(loss, sp))) return st;
+  if (!labels) return fail(NEF_E_ARG, "null labels");
+  if (!rule || rule->max_iters < 0 || rule->val_patience < 0 || !(rule->min_rel_decrease == rule->min_rel_decrease))
+    return fail(NEF_E_ARG, "bad stop rule");
+  if (!(eps > 0.0) || !std::isfinite(eps)) return fail(NEF_E_ARG, "eps must be > 0");
+  if (int dst = check_device()) return dst;
+  g_launches = 0;
+  const nef::Plan& p = plan->p;
+  Ctx c{&p, factors, static_cast<char*>(workspace), ws_bytes, static_cast<cudaStream_t>(stream)};
+  c.aux = sp.aux;
+  c.split = 1;
+  const nef::DivParams dv = nef::make_div_fam(sp.fam, sp.alpha, sp.beta, sp.prm);
+  const nef::UpdArgs u = nef::make_upd_fam(sp.fam, sp.alpha, sp.beta, eps);
+  bool any_tc = false;
+  for (const auto& L : p.low) any_tc |= L.tc_ok;
+  if (any_tc && g_policy == 0 && !g_no_sentinel && !sp.aux) {   // train entries folded into a sentinel copy
+    double* dslot = reinterpret_cast<double*>(c.ws + p.ws_dterm);
+    double* dpart = reinterpret_cast<double*>(c.ws + p.ws_dpart);
+    float* ys = reinterpret_cast<float*>(c.ws + p.ws_sent);
+    CK(nef::launch_sentinel(Y, labels, ys, p.n_local, 0, dpart, reinterpret_cast<long long*>(dpart + nef::kSentParts),
+                            dslot, reinterpret_cast<long long*>(dslot + 1), c.s, 1));
+    g_launches += 3;
+    c.ysent = ys;
+  }
+  const int L = (int)p.ops.size();
+  std::vector<float*> fsave(L);
+  std::vector<size_t> fbytes(L);
+  {
+    char* q = c.ws + p.ws_fsave;
+    for (int l = 0; l < L; ++l) {
+      size_t n = 1;
+      for (auto d : p.fshape[l]) n *= (size_t)d;
+      fbytes[l] = n * 4;
+      fsave[l] = reinterpret_cast<float*>(q);
+      q += (n * 4 + 255) / 256 * 256;
+    }
+  }
+  void* pin = nullptr;
+  CK(cudaHostAlloc(&pin, 64, cudaHostAllocDefault));
+  cudaEvent_t ev = nullptr;
+  if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) {
+    cudaFreeHost(pin);
+    return fail(NEF_E_CUDA, "cudaEventCreate failed");
+  }
+  c.pin = pin;
+  c.pin_ev = ev;
+  double* slots = reinterpret_cast<double*>(c.ws + p.ws_trace);
+  long long* cslots = reinterpret_cast<long long*>(c.ws + p.ws_trace + 8 * 2048);
+  const int T = rule->max_iters;
+  std::vector<double> tr[3];
+  int why = 0, t = 0;
+  auto run = [&]() -> int {
+    for (t = 0;; ++t) {
+      c.pin_counts = (t == 0);
+      if (t < T) {   // sweep t + 1; its first pass carries the losses of iterate t
+        for (int l = 0; l < L; ++l) CK(cudaMemcpyAsync(fsave[l], factors[l], fbytes[l], cudaMemcpyDeviceToDevice, c.s));
+        for (int ell = 0; ell < L; ++ell)
+          if (int r = update_one(c, ell, Y, labels, dv, u, ell == 0 ? 1 : 0, slots, cslots)) return r;
+      } else if (int r = loss_pass(c, Y, labels, dv, slots, cslots)) {
+        return r;
+      }
+      CK(cudaEventSynchronize(ev));
+      const double* h = static_cast<const double*>(pin);
+      for (int q = 0; q < 3; ++q) tr[q].push_back(h[q]);
+      if (t == 0 && counts)
+        for (int q = 0; q < 3; ++q) counts[q] = static_cast<const long long*>(pin)[4 + q];
+      // P:497 stopping rules (R30, R31): patience > plateau > max_iters
+      const int pt = rule->val_patience;
+      bool inc = pt > 0 && t >= pt;
+      for (int k = t - pt + 1; inc && k <= t; ++k) inc = tr[1][k] > tr[1][k - 1];
+      if (inc) why = NEF_STOP_PATIENCE;
+      else if (t >= 1 && (tr[0][t - 1] - tr[0][t]) < rule->min_rel_decrease * std::fabs(tr[0][t - 1])) why = NEF_STOP_PLATEAU;
+      else if (t >= T) why = NEF_STOP_MAX_ITERS;
+      if (why) {
+        if (t < T)   // sweep t + 1 already ran: back to iterate t
+          for (int l = 0; l < L; ++l) CK(cudaMemcpyAsync(factors[l], fsave[l], fbytes[l], cudaMemcpyDeviceToDevice, c.s));
+        CK(cudaStreamSynchronize(c.s));
+        return NEF_OK;
+      }
+    }
+  };
+  st = run();
+  cudaEventDestroy(ev);
+  cudaFreeHost(pin);
+  if (st) return st;
+  if (traces)
+    for (int q = 0; q < 3; ++q)
+      for (int k = 0; k <= t; ++k) traces[(size_t)q * (T + 1) + k] = tr[q][k];
+  if (sweeps) *sweeps = t;
+  if (reason) *reason = why;
+  return NEF_OK;
+}
+
+int nef_update_ex(nef_plan_t plan, int ell, const float* Y, const uint8_t* mask, const nef_loss_spec* loss, double eps,
+                  float* const* factors, void* workspace, size_t ws_bytes, void* stream) {
+  int st = validate_common(plan, Y, factors, workspace, ws_bytes);
+  if (st) return st;
+  Spec sp;
+  if ((st = validate_spec(loss, sp))) return st;
   if (!(eps > 0.0)) return fail(NEF_E_ARG, "eps must be > 0");
   if (ell < 0 || ell >= (int)plan->p.ops.size()) return fail(NEF_E_ARG, "ell out of range");
   if (int dst = check_device()) return dst;
   g_launches = 0;
   Ctx c{&plan->p, factors, static_cast<char*>(workspace), ws_bytes, static_cast<cudaStream_t>(stream)};
-  return update_one(c, ell, Y, mask, nef::make_div(alpha, beta), nef::make_upd(alpha, beta, eps), 0, nullptr, nullptr);
+  c.aux = sp.aux;
+  return update_one(c, ell, Y, mask, nef::make_div_fam(sp.fam, sp.alpha, sp.beta, sp.prm),
+                    nef::make_upd_fam(sp.fam, sp.alpha, sp.beta, eps), 0, nullptr, nullptr);
 }
 
-int nef_num_den(nef_plan_t plan, int ell, const float* Y, const uint8_t* mask, double alpha, double beta,
-                float* const* factors, float* num, float* den, void* workspace, size_t ws_bytes, void* stream) {
+int nef_update(nef_plan_t plan, int ell, const float* Y, const uint8_t* mask, double alpha, double beta, double eps,
+               float* const* factors, void* workspace, size_t ws_bytes, void* stream) {
+  const nef_loss_spec ls = ab_spec(alpha, beta);
+  return nef_update_ex(plan, ell, Y, mask, &ls, eps, factors, workspace, ws_bytes, stream);
+}
+
+int nef_num_den_ex(nef_plan_t plan, int ell, const float* Y, const uint8_t* mask, const nef_loss_spec* loss,
+                   float* const* factors, float* num, float* den, void* workspace, size_t ws_bytes, void* stream) {
   int st = validate_common(plan, Y, factors, workspace, ws_bytes);
   if (st) return st;
-  if ((st = validate_ab(alpha, beta))) return st;
+  Spec sp;
+  if ((st = validate_spec(loss, sp))) return st;
   if (ell < 0 || ell >= (int)plan->p.ops.size()) return fail(NEF_E_ARG, "ell out of range");
   if (!num || !den) return fail(NEF_E_ARG, "null num/den");
   if (int dst = check_device()) return dst;
   g_launches = 0;
   Ctx c{&plan->p, factors, static_cast<char*>(workspace), ws_bytes, static_cast<cudaStream_t>(stream)};
+  c.aux = sp.aux;
   float *n0 = nullptr, *d0 = nullptr;
-  st = num_den(c, ell, Y, mask, nef::make_div(alpha, beta), 0, nullptr, nullptr, &n0, &d0);
+  st = num_den(c, ell, Y, mask, nef::make_div_fam(sp.fam, sp.alpha, sp.beta, sp.prm), 0, nullptr, nullptr, &n0, &d0);
   if (st) return st;
   int64_t n = 1;
   for (auto d : plan->p.fshape[ell]) n *= d;
@@ -657,10 +850,17 @@ int nef_num_den(nef_plan_t plan, int ell, const float* Y, const uint8_t* mask, d
   return NEF_OK;
 }
 
-int nef_apply_update(nef_plan_t plan, int ell, double alpha, double beta, double eps, float* const* factors,
-                     const float* num, const float* den, void* stream) {
+int nef_num_den(nef_plan_t plan, int ell, const float* Y, const uint8_t* mask, double alpha, double beta,
+                float* const* factors, float* num, float* den, void* workspace, size_t ws_bytes, void* stream) {
+  const nef_loss_spec ls = ab_spec(alpha, beta);
+  return nef_num_den_ex(plan, ell, Y, mask, &ls, factors, num, den, workspace, ws_bytes, stream);
+}
+
+int nef_apply_update_ex(nef_plan_t plan, int ell, const nef_loss_spec* loss, double eps, float* const* factors,
+                        const float* num, const float* den, void* stream) {
   if (!plan || !factors || !num || !den) return fail(NEF_E_ARG, "null argument");
-  int st = validate_ab(alpha, beta);
+  Spec sp;
+  int st = validate_spec(loss, sp);
   if (st) return st;
   if (ell < 0 || ell >= (int)plan->p.ops.size()) return fail(NEF_E_ARG, "ell out of range");
   if (!(eps > 0.0)) return fail(NEF_E_ARG, "eps must be > 0");
@@ -668,25 +868,34 @@ int nef_apply_update(nef_plan_t plan, int ell, double alpha, double beta, double
   for (auto d : plan->p.fshape[ell]) n *= d;
   if (int dst = check_device()) return dst;
   g_launches = 0;
-  CK(nef::launch_update(factors[ell], num, den, n, nef::make_upd(alpha, beta, eps), static_cast<cudaStream_t>(stream)));
+  CK(nef::launch_update(factors[ell], num, den, n, nef::make_upd_fam(sp.fam, sp.alpha, sp.beta, eps),
+                        static_cast<cudaStream_t>(stream)));
   ++g_launches;
   return NEF_OK;
 }
 
-int nef_loss(nef_plan_t plan, const float* Y, const uint8_t* mask, double alpha, double beta, float* const* factors,
-             double* loss_sum, int64_t* n_observed, void* workspace, size_t ws_bytes, void* stream) {
+int nef_apply_update(nef_plan_t plan, int ell, double alpha, double beta, double eps, float* const* factors,
+                     const float* num, const float* den, void* stream) {
+  const nef_loss_spec ls = ab_spec(alpha, beta);
+  return nef_apply_update_ex(plan, ell, &ls, eps, factors, num, den, stream);
+}
+
+int nef_loss_ex(nef_plan_t plan, const float* Y, const uint8_t* mask, const nef_loss_spec* loss, float* const* factors,
+                double* loss_sum, int64_t* n_observed, void* workspace, size_t ws_bytes, void* stream) {
   int st = validate_common(plan, Y, factors, workspace, ws_bytes);
   if (st) return st;
-  if ((st = validate_ab(alpha, beta))) return st;
+  Spec sp;
+  if ((st = validate_spec(loss, sp))) return st;
   if (int dst = check_device()) return dst;
   g_launches = 0;
   const nef::Plan& p = plan->p;
   Ctx c{&p, factors, static_cast<char*>(workspace), ws_bytes, static_cast<cudaStream_t>(stream)};
+  c.aux = sp.aux;
   double* slot = reinterpret_cast<double*>(c.ws + p.ws_trace);
   long long* cslot = reinterpret_cast<long long*>(c.ws + p.ws_trace + 8 * 2048);
-  st = loss_pass(c, Y, mask, nef::make_div(alpha, beta), slot, cslot);
+  st = loss_pass(c, Y, mask, nef::make_div_fam(sp.fam, sp.alpha, sp.beta, sp.prm), slot, cslot);
   if (st) return st;
-  if (communicates(p)) {
+  if (communicates(p) && p.nccl_comm) {   // (host-only split: this rank's partial sums)
     if ((st = allreduce(p, slot, 1, kNcclFloat64, c.s))) return st;
     if ((st = allreduce(p, cslot, 1, kNcclInt64, c.s))) return st;
   }
@@ -698,6 +907,12 @@ int nef_loss(nef_plan_t plan, const float* Y, const uint8_t* mask, double alpha,
   if (loss_sum) *loss_sum = h;
   if (n_observed) *n_observed = hc;
   return NEF_OK;
+}
+
+int nef_loss(nef_plan_t plan, const float* Y, const uint8_t* mask, double alpha, double beta, float* const* factors,
+             double* loss_sum, int64_t* n_observed, void* workspace, size_t ws_bytes, void* stream) {
+  const nef_loss_spec ls = ab_spec(alpha, beta);
+  return nef_loss_ex(plan, Y, mask, &ls, factors, loss_sum, n_observed, workspace, ws_bytes, stream);
 }
 
 size_t nef_host_scratch_bytes(nef_plan_t plan, int has_mask) {

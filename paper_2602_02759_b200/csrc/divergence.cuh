@@ -164,9 +164,13 @@ __device__ __forceinline__ float kl_loss(float x, float y) {
 // (paper convention; EW_* in kernels.h).  Ew<EW_GENERIC> defers to the runtime codes.
 // ab2 evaluates two entries at once; the specialisations use the packed fp32x2 multiplies of
 // sm_100 (FMUL2: one issue slot for two products).
+// Traits: kLinX - a = x * (positive factor), so a carries the sign of x (the sentinel's "missing");
+// kSignedA - a may be negative at an observed entry (log forms: the (0,1) pair, Jensen-Shannon),
+// so the sentinel path selects on x instead of clamping a at zero.
 template <int KIND>
 struct Ew {
   static constexpr bool kLinX = false;   // a = x * (positive factor)
+  static constexpr bool kSignedA = true;  // generic pairs include the (0, 1) log case
   static __device__ __forceinline__ void ab(float x, float yh, const DivParams& d, float& av, float& bv) {
     const float2 r = ab_entry_ool(x, yh, d);
     av = r.x;
@@ -187,6 +191,7 @@ struct Ew {
 template <>
 struct Ew<EW_KL> {  // (1, 0): a = x / y, b = 1
   static constexpr bool kLinX = true;   // a = x * (positive factor)
+  static constexpr bool kSignedA = false;
   static __device__ __forceinline__ void ab(float x, float yh, const DivParams&, float& av, float& bv) {
     av = x * frcp(yh);
     bv = 1.f;
@@ -212,6 +217,7 @@ struct Ew<EW_KL> {  // (1, 0): a = x / y, b = 1
 template <>
 struct Ew<EW_EUC> {  // (1, 1): a = x, b = y
   static constexpr bool kLinX = true;   // a = x * (positive factor)
+  static constexpr bool kSignedA = false;
   static __device__ __forceinline__ void ab(float x, float yh, const DivParams&, float& av, float& bv) {
     av = x;
     bv = yh;
@@ -234,6 +240,7 @@ struct Ew<EW_EUC> {  // (1, 1): a = x, b = y
 template <>
 struct Ew<EW_B_M05> {  // (1, -0.5): a = x y^-3/2, b = y^-1/2; L = 2 (sqrt x - sqrt y)^2 / sqrt y
   static constexpr bool kLinX = true;   // a = x * (positive factor)
+  static constexpr bool kSignedA = false;
   static __device__ __forceinline__ void ab(float x, float yh, const DivParams&, float& av, float& bv) {
     const float r = frsqrt(yh);
     bv = r;
@@ -264,6 +271,7 @@ struct Ew<EW_B_M05> {  // (1, -0.5): a = x y^-3/2, b = y^-1/2; L = 2 (sqrt x - s
 template <>
 struct Ew<EW_A05_B0> {  // (0.5, 0): a = sqrt(x) / y, b = y^-1/2; L = 4 y^1/2 f(log(x/y)/2)
   static constexpr bool kLinX = false;   // a = x * (positive factor)
+  static constexpr bool kSignedA = false;
   static __device__ __forceinline__ void ab(float x, float yh, const DivParams&, float& av, float& bv) {
     const float r = frsqrt(yh);
     bv = r;
@@ -302,6 +310,7 @@ struct Ew<EW_A05_B0> {  // (0.5, 0): a = sqrt(x) / y, b = y^-1/2; L = 4 y^1/2 f(
 template <>
 struct Ew<EW_B05> {  // (1, 0.5): a = x y^-1/2, b = y^1/2
   static constexpr bool kLinX = true;   // a = x * (positive factor)
+  static constexpr bool kSignedA = false;
   static __device__ __forceinline__ void ab(float x, float yh, const DivParams&, float& av, float& bv) {
     const float r = frsqrt(yh);
     av = x * r;
@@ -322,6 +331,7 @@ struct Ew<EW_B05> {  // (1, 0.5): a = x y^-1/2, b = y^1/2
 template <>
 struct Ew<EW_B2> {  // (1, 2): a = x y, b = y^2
   static constexpr bool kLinX = true;   // a = x * (positive factor)
+  static constexpr bool kSignedA = false;
   static __device__ __forceinline__ void ab(float x, float yh, const DivParams&, float& av, float& bv) {
     av = x * yh;
     bv = yh * yh;
@@ -341,6 +351,7 @@ struct Ew<EW_B2> {  // (1, 2): a = x y, b = y^2
 template <>
 struct Ew<EW_A05_B1> {  // (0.5, 1): a = sqrt(x), b = sqrt(y)
   static constexpr bool kLinX = false;   // a = x * (positive factor)
+  static constexpr bool kSignedA = false;
   static __device__ __forceinline__ void ab(float x, float yh, const DivParams&, float& av, float& bv) {
     av = fsqrt(x);
     bv = fsqrt(yh);
@@ -354,6 +365,128 @@ struct Ew<EW_A05_B1> {  // (0.5, 1): a = sqrt(x), b = sqrt(y)
                                               float2& l) {
     ab2(x, yh, d, av, bv);
     l = make_float2(loss(x.x, yh.x, d), loss(x.y, yh.y, d));
+  }
+};
+
+// ---- App. B losses; y = max(yhat, 1e-30) is the model (odds for Bernoulli / binomial)
+__device__ __forceinline__ float xlogy0(float x, float ly) { return x > 0.f ? x * ly : 0.f; }   // 0 log y = 0 (R8)
+
+template <>
+struct Ew<EW_NB> {  // a = x / y, b = (phi + x) / (phi + y); L = (phi + x) log(phi + y) - x log y
+  static constexpr bool kLinX = true;
+  static constexpr bool kSignedA = false;
+  static __device__ __forceinline__ void ab(float x, float yh, const DivParams& d, float& av, float& bv) {
+    av = x * frcp(yh);
+    bv = (d.prm + x) * frcp(d.prm + yh);
+  }
+  static __device__ __forceinline__ void ab2(float2 x, float2 yh, const DivParams& d, float2& av, float2& bv) {
+    ab(x.x, yh.x, d, av.x, bv.x);
+    ab(x.y, yh.y, d, av.y, bv.y);
+  }
+  static __device__ __forceinline__ float loss(float x, float yh, const DivParams& d) {
+    return (d.prm + x) * logf(d.prm + yh) - xlogy0(x, logf(yh));
+  }
+  static __device__ __forceinline__ void abl2(float2 x, float2 yh, const DivParams& d, float2& av, float2& bv,
+                                              float2& l) {
+    ab2(x, yh, d, av, bv);
+    l = make_float2(loss(x.x, yh.x, d), loss(x.y, yh.y, d));
+  }
+  // per-entry phi (aux): the same forms with phi_i in place of the scalar
+  static __device__ __forceinline__ void ab_aux(float x, float yh, float phi, float& av, float& bv) {
+    av = x * frcp(yh);
+    bv = (phi + x) * frcp(phi + yh);
+  }
+  static __device__ __forceinline__ float loss_aux(float x, float yh, float phi) {
+    return (phi + x) * logf(phi + yh) - xlogy0(x, logf(yh));
+  }
+};
+
+template <>
+struct Ew<EW_BERN> {  // odds: a = x / y, b = 1 / (1 + y); L = log(1 + y) - x log y
+  static constexpr bool kLinX = true;
+  static constexpr bool kSignedA = false;
+  static __device__ __forceinline__ void ab(float x, float yh, const DivParams&, float& av, float& bv) {
+    av = x * frcp(yh);
+    bv = frcp(1.f + yh);
+  }
+  static __device__ __forceinline__ void ab2(float2 x, float2 yh, const DivParams& d, float2& av, float2& bv) {
+    ab(x.x, yh.x, d, av.x, bv.x);
+    ab(x.y, yh.y, d, av.y, bv.y);
+  }
+  static __device__ __forceinline__ float loss(float x, float yh, const DivParams&) {
+    return log1pf(yh) - xlogy0(x, logf(yh));
+  }
+  static __device__ __forceinline__ void abl2(float2 x, float2 yh, const DivParams& d, float2& av, float2& bv,
+                                              float2& l) {
+    ab2(x, yh, d, av, bv);
+    l = make_float2(loss(x.x, yh.x, d), loss(x.y, yh.y, d));
+  }
+};
+
+template <>
+struct Ew<EW_BINOM> {  // odds with n trials: a = x / y, b = n / (1 + y); L = n log(1 + y) - x log y
+  static constexpr bool kLinX = true;
+  static constexpr bool kSignedA = false;
+  static __device__ __forceinline__ void ab(float x, float yh, const DivParams& d, float& av, float& bv) {
+    av = x * frcp(yh);
+    bv = d.prm * frcp(1.f + yh);
+  }
+  static __device__ __forceinline__ void ab2(float2 x, float2 yh, const DivParams& d, float2& av, float2& bv) {
+    ab(x.x, yh.x, d, av.x, bv.x);
+    ab(x.y, yh.y, d, av.y, bv.y);
+  }
+  static __device__ __forceinline__ float loss(float x, float yh, const DivParams& d) {
+    return d.prm * log1pf(yh) - xlogy0(x, logf(yh));
+  }
+  static __device__ __forceinline__ void abl2(float2 x, float2 yh, const DivParams& d, float2& av, float2& bv,
+                                              float2& l) {
+    ab2(x, yh, d, av, bv);
+    l = make_float2(loss(x.x, yh.x, d), loss(x.y, yh.y, d));
+  }
+  static __device__ __forceinline__ void ab_aux(float x, float yh, float n, float& av, float& bv) {
+    av = x * frcp(yh);
+    bv = n * frcp(1.f + yh);
+  }
+  static __device__ __forceinline__ float loss_aux(float x, float yh, float n) {
+    return n * log1pf(yh) - xlogy0(x, logf(yh));
+  }
+};
+
+// Jensen-Shannon: a = log((x + y) / (2y)), b = 1, g = log.  With u = (x - y) / (x + y) the
+// loss is m / 2 [(1 + u) log(1 + u) + (1 - u) log(1 - u)], m = (x + y) / 2: the series
+// sum_k u^2k / (k (2k - 1)) for |u| < 0.3 (no cancellation near x = y), the direct form elsewhere,
+// m log 2 at x = 0.
+__device__ __forceinline__ float js_loss(float x, float y) {
+  const float m = 0.5f * (x + y);
+  const float u = (x - y) / (x + y);
+  const float u2 = u * u;
+  float s = 1.f / 45.f;                        // k = 5
+  s = fmaf(s, u2, 1.f / 28.f);                 // k = 4
+  s = fmaf(s, u2, 1.f / 15.f);                 // k = 3
+  s = fmaf(s, u2, 1.f / 6.f);                  // k = 2
+  s = fmaf(s, u2, 1.f);                        // k = 1
+  const float ser = u2 * s;
+  const float dir = (1.f + u) * log1pf(u) + (1.f - u) * log1pf(-u);
+  const float f = fabsf(u) < 0.3f ? ser : dir;
+  return x > 0.f ? 0.5f * m * f : m * 0.69314718055994531f;
+}
+template <>
+struct Ew<EW_JS> {
+  static constexpr bool kLinX = false;
+  static constexpr bool kSignedA = true;   // a < 0 where x < y
+  static __device__ __forceinline__ void ab(float x, float yh, const DivParams&, float& av, float& bv) {
+    av = flog(fmaf(x, frcp(yh), 1.f) * 0.5f);   // log((x / y + 1) / 2)
+    bv = 1.f;
+  }
+  static __device__ __forceinline__ void ab2(float2 x, float2 yh, const DivParams& d, float2& av, float2& bv) {
+    ab(x.x, yh.x, d, av.x, bv.x);
+    ab(x.y, yh.y, d, av.y, bv.y);
+  }
+  static __device__ __forceinline__ float loss(float x, float yh, const DivParams&) { return js_loss(x, yh); }
+  static __device__ __forceinline__ void abl2(float2 x, float2 yh, const DivParams& d, float2& av, float2& bv,
+                                              float2& l) {
+    ab2(x, yh, d, av, bv);
+    l = make_float2(js_loss(x.x, yh.x), js_loss(x.y, yh.y));
   }
 };
 
@@ -417,6 +550,10 @@ inline cudaError_t dispatch_ew(int kind, F&& f) {
     case EW_B05: return f.template operator()<EW_B05>();
     case EW_B2: return f.template operator()<EW_B2>();
     case EW_A05_B1: return f.template operator()<EW_A05_B1>();
+    case EW_NB: return f.template operator()<EW_NB>();
+    case EW_BERN: return f.template operator()<EW_BERN>();
+    case EW_BINOM: return f.template operator()<EW_BINOM>();
+    case EW_JS: return f.template operator()<EW_JS>();
     default: return f.template operator()<EW_GENERIC>();
   }
 }

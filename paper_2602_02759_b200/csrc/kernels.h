@@ -14,8 +14,14 @@ enum PowCode : int { POW_0 = 0, POW_1, POW_M1, POW_H, POW_MH, POW_M15, POW_15, P
 int pow_code(double p);
 
 // compile-time specialisations of the elementwise stage (divergence.cuh)
-enum EwKind : int { EW_GENERIC = 0, EW_KL, EW_EUC, EW_B_M05, EW_A05_B0, EW_B05, EW_B2, EW_A05_B1 };
+enum EwKind : int { EW_GENERIC = 0, EW_KL, EW_EUC, EW_B_M05, EW_A05_B0, EW_B05, EW_B2, EW_A05_B1,
+                    // App. B losses: negative binomial (scalar phi, or per-entry phi streamed
+                    // as aux), Bernoulli odds, binomial odds (scalar n, or per-entry n as aux), Jensen-Shannon
+                    EW_NB, EW_BERN, EW_BINOM, EW_JS };
 int ew_kind(double alpha, double beta);
+
+// loss families (include/nef.h nef_loss_kind)
+enum LossFam : int { FAM_AB = 0, FAM_NEGBIN = 1, FAM_BERNOULLI = 2, FAM_BINOMIAL = 3, FAM_JS = 4 };
 
 // Elementwise constants of the (alpha,beta)-divergence
 struct DivParams {
@@ -25,8 +31,10 @@ struct DivParams {
   int log_case;                 // (alpha, beta) = (0, 1): a = log(x/yhat), b = 1
   int loss_case;                // 0 generic, 1 beta=0, 2 alpha=-beta, 3 alpha=0, 4 alpha=beta=0, 5 (1,1)
   int kind;                     // EwKind
+  float prm;                    // NB dispersion phi / binomial trials n (scalar; per-entry values via aux)
 };
 DivParams make_div(double alpha, double beta);
+DivParams make_div_fam(int fam, double alpha, double beta, double prm);
 
 // Fused streaming pass over Y (and mask) for one lowering.
 struct FusedArgs {
@@ -49,6 +57,9 @@ struct FusedArgs {
   long long* countpart;         // [row_blocks * n_chunks] observed counts
   DivParams dv;
   int mode;                     // 0: update only, 1: update + loss, 2: loss only
+  const float* aux;             // per-entry phi (NB) / n (binomial), Y's layout, or null (scalar dv.prm)
+  int split;                    // M holds labels 0..3 (R29): train = 1; the loss partials are per role
+                                //   (losspart / countpart: [3][row_blocks * n_chunks])
 };
 
 cudaError_t launch_fused_ffma(const FusedArgs& a, cudaStream_t s);
@@ -65,7 +76,7 @@ constexpr int kSentBlocks = 148 * 16;
 cudaError_t launch_dterm(const float* Y, int64_t n, int dterm, double* dpart, long long* dcpart, double* dslot,
                          long long* dcslot, cudaStream_t s);
 cudaError_t launch_sentinel(const float* Y, const uint8_t* M, float* out, int64_t n, int dterm, double* dpart,
-                            long long* dcpart, double* dslot, long long* dcslot, cudaStream_t s);
+                            long long* dcpart, double* dslot, long long* dcslot, cudaStream_t s, int split = 0);
 
 // dst[r][0..Kp) = src[r][0..K) padded with zeros (16-byte row pitch for TMA)
 cudaError_t launch_pad_rows(const float* src, float* dst, int64_t rows, int64_t K, int64_t Kp, cudaStream_t s);
@@ -80,6 +91,7 @@ struct UpdArgs {
   double eps;
 };
 UpdArgs make_upd(double alpha, double beta, double eps);
+UpdArgs make_upd_fam(int fam, double alpha, double beta, double eps);
 cudaError_t launch_update(float* theta, const float* num, const float* den, int64_t n, UpdArgs u, cudaStream_t s);
 
 // Sum CTA loss partials (fixed order) into slot[0] (double) and count into cslot[0].  With off

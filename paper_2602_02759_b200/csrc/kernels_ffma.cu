@@ -69,6 +69,26 @@ DivParams make_div(double alpha, double beta) {
   return d;
 }
 
+DivParams make_div_fam(int fam, double alpha, double beta, double prm) {
+  if (fam == FAM_AB) return make_div(alpha, beta);
+  DivParams d{};
+  d.alpha = 1.f;
+  d.beta = 0.f;
+  d.prm = (float)prm;
+  d.kind = fam == FAM_NEGBIN ? EW_NB : fam == FAM_BERNOULLI ? EW_BERN : fam == FAM_BINOMIAL ? EW_BINOM : EW_JS;
+  return d;
+}
+
+UpdArgs make_upd_fam(int fam, double alpha, double beta, double eps) {
+  if (fam == FAM_AB) return make_upd(alpha, beta, eps);
+  // g(lambda) = lambda for NB / Bernoulli / binomial, log for JS
+  UpdArgs u{};
+  u.eps = eps;
+  u.g_case = fam == FAM_JS ? 1 : 0;
+  u.inv_expo = 1.0;
+  return u;
+}
+
 UpdArgs make_upd(double alpha, double beta, double eps) {
   // g(lambda) table
   UpdArgs u{};
@@ -101,6 +121,7 @@ struct __align__(16) FSmem {
   float Pa[BN][PADR];
   float Pb[BN][PADR];
   uint8_t Mk[BN][PADR];
+  float Ax[BN][PADR];          // per-entry phi / n (aux losses only)
   long long coff[BN];
   long long roff[BM];
   int toff[kMaxTabs][BN];
@@ -148,8 +169,8 @@ __global__ void __launch_bounds__(4 * BM) fused_ffma_kernel(const __grid_constan
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int j = 0; j < KQ; ++j) { qa_d[i][j] = 0.0; qb_d[i][j] = 0.0; }
-  double loss_acc = 0.0;
-  long long cnt = 0;
+  double loss_acc[3] = {0.0, 0.0, 0.0};   // [role]: split fits keep train / validation / heldout apart
+  long long cnt[3] = {0, 0, 0};
   const int rs = (t % RG) * 4;
   const int cs = (t / RG) * 4;
   const int kq = (t / RG) * KQ;
@@ -184,15 +205,20 @@ __global__ void __launch_bounds__(4 * BM) fused_ffma_kernel(const __grid_constan
       int r, c;
       if (a.row_fast) { r = e % BM; c = e / BM; } else { r = e / BN; c = e % BN; }
       long long ro = sm.roff[r], co = sm.coff[c];
-      float y = 0.f;
+      float y = 0.f, ax = 1.f;
       uint8_t m = 0;
       if (ro >= 0 && co >= 0) {
         long long off = ro + co;
-        m = a.M ? (uint8_t)(__ldg(a.M + off) != 0) : (uint8_t)1;
-        if (m) y = __ldg(a.Y + off);
+        // mask: observed flag (R6); split fit: the label itself (R29)
+        m = a.M ? (a.split ? __ldg(a.M + off) : (uint8_t)(__ldg(a.M + off) != 0)) : (uint8_t)1;
+        if (m) {
+          y = __ldg(a.Y + off);
+          if (a.aux) ax = __ldg(a.aux + off);
+        }
       }
       sm.Pa[c][r] = y;
       sm.Mk[c][r] = m;
+      if (a.aux) sm.Ax[c][r] = ax;
     }
     // V tile = prod of column tables (Khatri-Rao / side operands), both layouts
     for (int e = t; e < BN * KP; e += NT) {
@@ -223,7 +249,7 @@ __global__ void __launch_bounds__(4 * BM) fused_ffma_kernel(const __grid_constan
         for (int j = 0; j < 4; ++j) s[i][j] = fmaf(uu[i], vv[j], s[i][j]);
     }
     // divergence weights a, b (+ loss) in registers
-    float lsum = 0.f;
+    float lsum[3] = {0.f, 0.f, 0.f};
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const int c = cs + j;
@@ -233,16 +259,31 @@ __global__ void __launch_bounds__(4 * BM) fused_ffma_kernel(const __grid_constan
       float pa[4], pb[4];
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
-        const bool obs = (m4 >> (8 * i)) & 0xffu;
+        const uint32_t role = (m4 >> (8 * i)) & 0xffu;   // 0 unobserved; 1 train (and any observed entry)
+        const bool obs = a.split ? role == 1u : role != 0u;
         const float yh = fmaxf(s[i][j], 1e-30f);       // Yhat floor (reading R4)
-        const float x = yy[i];
-        float av, bv;
-        Ew<KIND>::ab(x, yh, a.dv, av, bv);
+        const float x = role ? yy[i] : 1.f;
+        float av, bv, lv = 0.f;
+        if constexpr (KIND == EW_NB || KIND == EW_BINOM) {
+          if (a.aux) {                                   // per-entry phi / n
+            const float ax = role ? sm.Ax[c][rs + i] : 1.f;
+            Ew<KIND>::ab_aux(x, yh, ax, av, bv);
+            if (a.mode != 0 && role) lv = Ew<KIND>::loss_aux(x, yh, ax);
+          } else {
+            Ew<KIND>::ab(x, yh, a.dv, av, bv);
+            if (a.mode != 0 && role) lv = Ew<KIND>::loss(x, yh, a.dv);
+          }
+        } else {
+          Ew<KIND>::ab(x, yh, a.dv, av, bv);
+          if (a.mode != 0 && role) lv = Ew<KIND>::loss(x, yh, a.dv);
+        }
         pa[i] = obs ? av : 0.f;                          // select, never multiply (R5)
         pb[i] = obs ? bv : 0.f;
-        if (a.mode != 0 && obs) {
-          lsum += Ew<KIND>::loss(x, yh, a.dv);
-          cnt += 1;
+        if (a.mode != 0 && role) {
+          const int q = a.split ? (int)role - 1 : 0;
+          if (q == 0) { lsum[0] += lv; cnt[0] += 1; }
+          else if (q == 1) { lsum[1] += lv; cnt[1] += 1; }
+          else if (q == 2) { lsum[2] += lv; cnt[2] += 1; }
         }
       }
       if (a.mode != 2) {
@@ -250,7 +291,9 @@ __global__ void __launch_bounds__(4 * BM) fused_ffma_kernel(const __grid_constan
         *reinterpret_cast<float4*>(&sm.Pb[c][rs]) = make_float4(pb[0], pb[1], pb[2], pb[3]);
       }
     }
-    loss_acc += (double)lsum;
+    loss_acc[0] += (double)lsum[0];
+    loss_acc[1] += (double)lsum[1];
+    loss_acc[2] += (double)lsum[2];
     __syncthreads();
     if (a.mode != 2) {
       float qa[4][KQ], qb[4][KQ];
@@ -300,20 +343,24 @@ __global__ void __launch_bounds__(4 * BM) fused_ffma_kernel(const __grid_constan
     }
   }
   if (a.mode != 0) {
-    // fixed-order block reduction of the loss (deterministic)
+    // fixed-order block reduction of the loss (deterministic), one per role on split fits
     __shared__ double red[NT];
     __shared__ long long redc[NT];
-    red[t] = loss_acc;
-    redc[t] = cnt;
-    __syncthreads();
-    for (int w = NT / 2; w > 0; w >>= 1) {
-      if (t < w) { red[t] += red[t + w]; redc[t] += redc[t + w]; }
+    const int64_t parts = (int64_t)gridDim.x * gridDim.y;
+    const int64_t id = (int64_t)blockIdx.y * gridDim.x + blockIdx.x;
+    for (int q = 0; q < (a.split ? 3 : 1); ++q) {
+      red[t] = loss_acc[q];
+      redc[t] = cnt[q];
       __syncthreads();
-    }
-    if (t == 0) {
-      int64_t id = (int64_t)blockIdx.y * gridDim.x + blockIdx.x;
-      a.losspart[id] = red[0];
-      a.countpart[id] = redc[0];
+      for (int w = NT / 2; w > 0; w >>= 1) {
+        if (t < w) { red[t] += red[t + w]; redc[t] += redc[t + w]; }
+        __syncthreads();
+      }
+      if (t == 0) {
+        a.losspart[q * parts + id] = red[0];
+        a.countpart[q * parts + id] = redc[0];
+      }
+      __syncthreads();
     }
   }
 }
@@ -506,12 +553,14 @@ __global__ void dterm_kernel(const float* __restrict__ Y, long long n4, long lon
 
 // 4 entries per thread and iteration: one 4-byte mask load and one 16-byte Y load / store, all
 // fully coalesced across the warp
+// split (R29): M holds labels and only train entries (label 1) count as observed
 __global__ void sentinel_kernel(const float* __restrict__ Y, const uint8_t* __restrict__ M, float* __restrict__ out,
-                                long long n4, int dterm, double* dpart, long long* dcpart) {
+                                long long n4, int dterm, double* dpart, long long* dcpart, int split) {
   double acc = 0.0;
   long long cnt = 0;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4; i += (long long)gridDim.x * blockDim.x) {
-    const uint32_t w = __ldcs(reinterpret_cast<const unsigned int*>(M) + i);
+    const uint32_t w0 = __ldcs(reinterpret_cast<const unsigned int*>(M) + i);
+    const uint32_t w = split ? __vcmpeq4(w0, 0x01010101u) : w0;
     float4 y = __ldcs(reinterpret_cast<const float4*>(Y) + i);
     if (dpart) {
       cnt += __popc(__vcmpne4(w, 0u)) >> 3;
@@ -532,12 +581,14 @@ __global__ void sentinel_kernel(const float* __restrict__ Y, const uint8_t* __re
   if (dpart) sent_block_sum(acc, cnt, dpart, dcpart, blockIdx.x);
 }
 __global__ void sentinel_tail_kernel(const float* __restrict__ Y, const uint8_t* __restrict__ M, float* __restrict__ out,
-                                     long long from, long long n, int dterm, double* dpart, long long* dcpart, int slot) {
+                                     long long from, long long n, int dterm, double* dpart, long long* dcpart, int slot,
+                                     int split) {
   double acc = 0.0;
   long long cnt = 0;
   for (long long i = from + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-    if (M[i]) { ++cnt; acc += dterm_c(dterm, Y[i]); }
-    out[i] = M[i] ? Y[i] + 0.f : -1.f;
+    const bool o = split ? M[i] == 1 : M[i] != 0;
+    if (o) { ++cnt; acc += dterm_c(dterm, Y[i]); }
+    out[i] = o ? Y[i] + 0.f : -1.f;
   }
   if (dpart) sent_block_sum(acc, cnt, dpart, dcpart, slot + blockIdx.x);
 }
@@ -661,16 +712,16 @@ cudaError_t launch_dterm(const float* Y, int64_t n, int dterm, double* dpart, lo
 }
 
 cudaError_t launch_sentinel(const float* Y, const uint8_t* M, float* out, int64_t n, int dterm, double* dpart,
-                            long long* dcpart, double* dslot, long long* dcslot, cudaStream_t s) {
+                            long long* dcpart, double* dslot, long long* dcslot, cudaStream_t s, int split) {
   const bool vec = (((reinterpret_cast<uintptr_t>(Y) | reinterpret_cast<uintptr_t>(out)) & 15) | (reinterpret_cast<uintptr_t>(M) & 3)) == 0;
   const long long n4 = vec ? n / 4 : 0;
   // every one of the kSentBlocks + 1 partials is written (fixed grids), then summed in fixed order
   if (vec) {
-    sentinel_kernel<<<kSentBlocks, 256, 0, s>>>(Y, M, out, n4, dterm, dpart, dcpart);
-    sentinel_tail_kernel<<<1, 256, 0, s>>>(Y, M, out, n4 * 4, n, dterm, dpart, dcpart, kSentBlocks);
+    sentinel_kernel<<<kSentBlocks, 256, 0, s>>>(Y, M, out, n4, dterm, dpart, dcpart, split);
+    sentinel_tail_kernel<<<1, 256, 0, s>>>(Y, M, out, n4 * 4, n, dterm, dpart, dcpart, kSentBlocks, split);
   } else {
-    sentinel_tail_kernel<<<kSentBlocks, 256, 0, s>>>(Y, M, out, 0, n, dterm, dpart, dcpart, 0);
-    sentinel_tail_kernel<<<1, 256, 0, s>>>(Y, M, out, n, n, dterm, dpart, dcpart, kSentBlocks);
+    sentinel_tail_kernel<<<kSentBlocks, 256, 0, s>>>(Y, M, out, 0, n, dterm, dpart, dcpart, 0, split);
+    sentinel_tail_kernel<<<1, 256, 0, s>>>(Y, M, out, n, n, dterm, dpart, dcpart, kSentBlocks, split);
   }
   if (dpart) loss_reduce_kernel<<<1, 256, 0, s>>>(dpart, dcpart, kSentBlocks + 1, dslot, dcslot, 1.0, nullptr);
   return cudaGetLastError();

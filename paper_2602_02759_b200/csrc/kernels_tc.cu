@@ -677,21 +677,61 @@ __device__ __forceinline__ float2 yhat_floor(uint32_t s0, uint32_t s1) {
 // TF32 operands: the tensor core reads only the top 19 bits of each 32-bit container, so
 // adding half a TF32 ulp (0x1000) to the bit pattern is round-to-nearest (ties away) of the
 // value the MMA consumes; the low 13 bits need not be cleared.
-template <int KIND>
+// P_a of one entry in the MM = 1 path (o: training-observed).  SPA (Euclidean pair, bond <= 32):
+// P_a = hi + lo, both TF32 - hi the RN of a, lo = a - hi (its own RN error ~2^-22 relative) -
+// so the numerator N = P_a_hi V + P_a_lo V carries no TF32 rounding of a (the data itself for
+// this pair, R27, R34); lo goes to TMEM columns 384 + 64 b.
+template <int KIND, bool SPA>
+__device__ __forceinline__ void put_pa(uint32_t (&sv)[16], uint32_t (&pl)[16], int j, bool o, float av) {
+  if constexpr (SPA) {
+    const uint32_t hi = (__float_as_uint(av) + 0x1000u) & 0xffffe000u;
+    sv[j] = o ? hi : 0u;
+    pl[j] = o ? __float_as_uint(av - __uint_as_float(hi)) + 0x1000u : 0u;
+  } else {
+    sv[j] = o ? __float_as_uint(av) + pa_round<KIND>(j) : 0u;
+  }
+}
+
+template <int KIND, bool SPA>
 __device__ __forceinline__ void ew_half(const TcArgs& a, uint32_t (&sv)[16], const float (&yv)[16],
                                         const uint32_t (&mk)[4], int cv, bool row_ok, uint32_t (&pb)[16],
-                                        float& lsum, long long& cnt) {
-  // observed bytes: mask byte nonzero (R6) and row / column in range
-  uint32_t ob[4];
-#pragma unroll
-  for (int j4 = 0; j4 < 4; ++j4) ob[j4] = a.has_mask ? mk[j4] : 0x01010101u;
+                                        uint32_t (&pl)[16], float (&ls)[3], long long (&cn)[3]) {
+  // per-byte valid flags of the tile (row / column in range) as 0x00 / 0xff bytes
   const uint32_t vbits = (!row_ok || cv <= 0) ? 0u : (cv >= 16 ? 0xffffu : ((1u << cv) - 1u));
-  if (vbits != 0xffffu) {
+  uint32_t vb[4];
 #pragma unroll
-    for (int j4 = 0; j4 < 4; ++j4) {
-      const uint32_t b = (vbits >> (4 * j4)) & 0xfu;
-      ob[j4] &= ((b * 0x00204081u) & 0x01010101u) * 0xffu;   // 4 bits -> 4 bytes of 0x00 / 0xff
+  for (int j4 = 0; j4 < 4; ++j4) {
+    const uint32_t b = (vbits >> (4 * j4)) & 0xfu;
+    vb[j4] = ((b * 0x00204081u) & 0x01010101u) * 0xffu;   // 4 bits -> 4 bytes of 0x00 / 0xff
+  }
+  // training-observed bytes: mask byte nonzero (R6), or label == 1 (train) for a split fit (R29)
+  uint32_t ob[4], rl[4];
+#pragma unroll
+  for (int j4 = 0; j4 < 4; ++j4) {
+    const uint32_t m = a.has_mask ? mk[j4] : 0x01010101u;
+    rl[j4] = m & vb[j4];                                   // labels of in-range entries (split fits)
+    ob[j4] = (a.split ? __vcmpeq4(m, 0x01010101u) : m) & vb[j4];
+  }
+  if (a.mode != 0 && a.split) {   // split fit: train / validation / heldout losses of every labelled entry
+#pragma unroll
+    for (int j = 0; j < 16; j += 2) {
+      const uint32_t r0 = (rl[j >> 2] >> (8 * (j & 3))) & 0xffu;
+      const uint32_t r1 = (rl[j >> 2] >> (8 * ((j + 1) & 3))) & 0xffu;
+      const float2 yh = yhat_floor(sv[j], sv[j + 1]);
+      float2 av, bv, lv;
+      Ew<KIND>::abl2(make_float2(r0 ? yv[j] : 1.f, r1 ? yv[j + 1] : 1.f), yh, a.dv, av, bv, lv);
+#pragma unroll
+      for (int q = 0; q < 3; ++q) ls[q] += (r0 == (uint32_t)(q + 1) ? lv.x : 0.f) + (r1 == (uint32_t)(q + 1) ? lv.y : 0.f);
+      put_pa<KIND, SPA>(sv, pl, j, r0 == 1u, av.x);
+      put_pa<KIND, SPA>(sv, pl, j + 1, r1 == 1u, av.y);
+      pb[j] = r0 == 1u ? __float_as_uint(bv.x) + 0x1000u : 0u;
+      pb[j + 1] = r1 == 1u ? __float_as_uint(bv.y) + 0x1000u : 0u;
     }
+#pragma unroll
+    for (int q = 0; q < 3; ++q)
+#pragma unroll
+      for (int j4 = 0; j4 < 4; ++j4) cn[q] += __popc(__vcmpeq4(rl[j4], (uint32_t)(q + 1) * 0x01010101u)) >> 3;
+    return;
   }
   if (a.mode != 0) {   // loss of the iterate entering the sweep (uniform branch)
 #pragma unroll
@@ -701,27 +741,47 @@ __device__ __forceinline__ void ew_half(const TcArgs& a, uint32_t (&sv)[16], con
       const float2 yh = yhat_floor(sv[j], sv[j + 1]);
       float2 av, bv, lv;
       Ew<KIND>::abl2(make_float2(o0 ? yv[j] : 1.f, o1 ? yv[j + 1] : 1.f), yh, a.dv, av, bv, lv);
-      lsum += (o0 ? lv.x : 0.f) + (o1 ? lv.y : 0.f);
-      sv[j] = o0 ? __float_as_uint(av.x) + pa_round<KIND>(j) : 0u;
-      sv[j + 1] = o1 ? __float_as_uint(av.y) + pa_round<KIND>(j + 1) : 0u;
+      ls[0] += (o0 ? lv.x : 0.f) + (o1 ? lv.y : 0.f);
+      put_pa<KIND, SPA>(sv, pl, j, o0, av.x);
+      put_pa<KIND, SPA>(sv, pl, j + 1, o1, av.y);
       pb[j] = o0 ? __float_as_uint(bv.x) + 0x1000u : 0u;
       pb[j + 1] = o1 ? __float_as_uint(bv.y) + 0x1000u : 0u;
     }
 #pragma unroll
-    for (int j4 = 0; j4 < 4; ++j4) cnt += __popc(__vcmpne4(ob[j4], 0u)) >> 3;
+    for (int j4 = 0; j4 < 4; ++j4) cn[0] += __popc(__vcmpne4(ob[j4], 0u)) >> 3;
     return;
   }
 #pragma unroll
   for (int j = 0; j < 16; j += 2) {
     const float2 yh = yhat_floor(sv[j], sv[j + 1]);
-    float2 av, bv;
-    Ew<KIND>::ab2(make_float2(yv[j], yv[j + 1]), yh, a.dv, av, bv);
     const bool o0 = (ob[j >> 2] & (0xffu << (8 * (j & 3)))) != 0u;
     const bool o1 = (ob[j >> 2] & (0xffu << (8 * ((j + 1) & 3)))) != 0u;
-    sv[j] = o0 ? __float_as_uint(av.x) + pa_round<KIND>(j) : 0u;
-    sv[j + 1] = o1 ? __float_as_uint(av.y) + pa_round<KIND>(j + 1) : 0u;
+    float2 av, bv;
+    Ew<KIND>::ab2(make_float2(o0 ? yv[j] : 1.f, o1 ? yv[j + 1] : 1.f), yh, a.dv, av, bv);
+    put_pa<KIND, SPA>(sv, pl, j, o0, av.x);
+    put_pa<KIND, SPA>(sv, pl, j + 1, o1, av.y);
     pb[j] = o0 ? __float_as_uint(bv.x) + 0x1000u : 0u;
     pb[j + 1] = o1 ? __float_as_uint(bv.y) + 0x1000u : 0u;
+  }
+}
+
+// P_a bits of one entry in the sentinel path: a >= 0 kinds clamp (a carries the sign of x, so the
+// add-then-max both rounds and zeroes a missing entry); signed-a kinds (log forms) select on x.
+template <int KIND>
+__device__ __forceinline__ uint32_t pa_sent(float av, float x, int j) {
+  if constexpr (Ew<KIND>::kSignedA) return x >= 0.f ? __float_as_uint(av) + pa_round<KIND>(j) : 0u;
+  else return (uint32_t)__viaddmax_s32(__float_as_int(Ew<KIND>::kLinX ? av : copysignf(av, x)), (int)pa_round<KIND>(j), 0);
+}
+
+// The same for the sentinel path (a >= 0 kinds; x < 0 = missing): hi = max(RN(a), 0), lo = a - hi
+template <int KIND, bool SPA>
+__device__ __forceinline__ void put_pa_sent(uint32_t (&sv)[16], uint32_t (&pl)[16], int j, float av, float x) {
+  if constexpr (SPA) {
+    const uint32_t hi = (uint32_t)__viaddmax_s32(__float_as_int(av), 0x1000, 0) & 0xffffe000u;
+    sv[j] = hi;
+    pl[j] = x >= 0.f ? __float_as_uint(av - __uint_as_float(hi)) + 0x1000u : 0u;
+  } else {
+    sv[j] = pa_sent<KIND>(av, x, j);
   }
 }
 
@@ -731,9 +791,9 @@ __device__ __forceinline__ void ew_half(const TcArgs& a, uint32_t (&sv)[16], con
 // max(bits + 0x1000, 0), both rounds (TF32 RN of the value the tensor core truncates) and zeroes
 // the missing entries.  Entries outside the tile's valid rows / columns (TMA zero fill) are
 // turned into -1 first.
-template <int KIND>
+template <int KIND, bool SPA>
 __device__ __forceinline__ void ew_half_sent(const TcArgs& a, uint32_t (&sv)[16], float (&yv)[16], int cv, bool row_ok,
-                                             uint32_t (&pb)[16], float& lsum, long long& cnt) {
+                                             uint32_t (&pb)[16], uint32_t (&pl)[16], float& lsum, long long& cnt) {
   if (a.absy) {   // raw unmasked Y (uniform branch): an observed -0.0 must not read as missing
 #pragma unroll
     for (int j = 0; j < 16; ++j) yv[j] = fabsf(yv[j]);
@@ -775,8 +835,16 @@ __device__ __forceinline__ void ew_half_sent(const TcArgs& a, uint32_t (&sv)[16]
       Ew<KIND>::abl2(make_float2(fabsf(x.x), fabsf(x.y)), yh, a.dv, av, bv, lv);
       l2 = __fadd2_rn(l2, make_float2(x.x >= 0.f ? lv.x : 0.f, x.y >= 0.f ? lv.y : 0.f));
       if (a.mode == 2) cnt += (x.x >= 0.f ? 1 : 0) + (x.y >= 0.f ? 1 : 0);
-      sv[j] = (uint32_t)__viaddmax_s32(__float_as_int(copysignf(av.x, x.x)), (int)pa_round<KIND>(j), 0);
-      sv[j + 1] = (uint32_t)__viaddmax_s32(__float_as_int(copysignf(av.y, x.y)), (int)pa_round<KIND>(j + 1), 0);
+      if constexpr (Ew<KIND>::kSignedA) {
+        sv[j] = pa_sent<KIND>(av.x, x.x, j);
+        sv[j + 1] = pa_sent<KIND>(av.y, x.y, j + 1);
+      } else if constexpr (SPA) {
+        put_pa_sent<KIND, SPA>(sv, pl, j, copysignf(av.x, x.x), x.x);
+        put_pa_sent<KIND, SPA>(sv, pl, j + 1, copysignf(av.y, x.y), x.y);
+      } else {
+        sv[j] = (uint32_t)__viaddmax_s32(__float_as_int(copysignf(av.x, x.x)), (int)pa_round<KIND>(j), 0);
+        sv[j + 1] = (uint32_t)__viaddmax_s32(__float_as_int(copysignf(av.y, x.y)), (int)pa_round<KIND>(j + 1), 0);
+      }
       pb[j] = (uint32_t)__viaddmax_s32(__float_as_int(copysignf(bv.x, x.x)), 0x1000, 0);
       pb[j + 1] = (uint32_t)__viaddmax_s32(__float_as_int(copysignf(bv.y, x.y)), 0x1000, 0);
     }
@@ -792,10 +860,9 @@ __device__ __forceinline__ void ew_half_sent(const TcArgs& a, uint32_t (&sv)[16]
       Ew<KIND>::ab2(x, yh, a.dv, av, bv);   // a = x * (positive): carries the sign of x
     } else {
       Ew<KIND>::ab2(make_float2(fabsf(x.x), fabsf(x.y)), yh, a.dv, av, bv);
-      av = make_float2(copysignf(av.x, x.x), copysignf(av.y, x.y));
     }
-    sv[j] = (uint32_t)__viaddmax_s32(__float_as_int(av.x), (int)pa_round<KIND>(j), 0);
-    sv[j + 1] = (uint32_t)__viaddmax_s32(__float_as_int(av.y), (int)pa_round<KIND>(j + 1), 0);
+    put_pa_sent<KIND, SPA>(sv, pl, j, av.x, x.x);
+    put_pa_sent<KIND, SPA>(sv, pl, j + 1, av.y, x.y);
     pb[j] = (uint32_t)__viaddmax_s32(__float_as_int(copysignf(bv.x, x.x)), 0x1000, 0);
     pb[j + 1] = (uint32_t)__viaddmax_s32(__float_as_int(copysignf(bv.y, x.y)), 0x1000, 0);
   }
@@ -925,6 +992,8 @@ template <int KB, int KIND, int MM>
 __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_constant__ Params P) {
   constexpr int NV = VStages<MM>::value;
   constexpr int NS = YStages<MM>::value;
+  // Euclidean pair with bond <= 32: numerator operand split hi + lo (put_pa), TMEM 384..511 free
+  constexpr bool SPA = (KIND == EW_EUC && KB == 32 && !NEF_PA_RN);
   extern __shared__ unsigned char smraw[];
   const TcArgs& a = P.a;
   const int tid = threadIdx.x;
@@ -1072,8 +1141,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
           const uint32_t pa = tmem + 128 * b;   // P_a; P_b at pa + 64
           // the accumulators restart at every drain group (see the elementwise loop)
           const uint32_t acc = (u % G) != 0 ? 1u : 0u;
-          if (KB == 64) mma_nd_block_64<id2>(tNa, tNb, pa, vtd, acc);
-          else mma_nd_block_32<id2>(tNa, tNb, pa, vtd, acc);
+          if constexpr (SPA) {
+            if (b == 0) mma_nd3_block_32_b0<id2>(tNa, tNb, pa, vtd, acc);
+            else mma_nd3_block_32_b1<id2>(tNa, tNb, pa, vtd, acc);
+          } else if constexpr (KB == 64) {
+            mma_nd_block_64<id2>(tNa, tNb, pa, vtd, acc);
+          } else {
+            mma_nd_block_32<id2>(tNa, tNb, pa, vtd, acc);
+          }
         }
         mma_commit_elect(v_empty + 8 * vs);
         mma_commit_elect(buf_free + 8 * b);
@@ -1236,8 +1311,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
         }
       }
     };
-    double loss_acc = 0.0;
-    long long cnt = 0;
+    double loss_acc[3] = {0.0, 0.0, 0.0};   // [role] (split fits: train / validation / heldout)
+    long long cnt[3] = {0, 0, 0};
     // valid columns of a tile: the tile's offset inside its column block, advanced per tile
     // (no 64-bit division in the loop)
     const int64_t cext = a.layout == 0 ? a.CO : a.CI;
@@ -1250,8 +1325,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
       const int cols_here = (int)(crem < BN ? crem : BN);
       const int st = t % NS;
       const uint32_t tc = tmem + 128 * b + lane_off + 16 * cg;   // S / P_a columns of this warp
-      float lsum = 0.f;
-      uint32_t sv[16], pb[16];
+      float lsum[3] = {0.f, 0.f, 0.f};
+      uint32_t sv[16], pb[16], pl[16];
       float yv[16];
       uint32_t mk[4] = {0u, 0u, 0u, 0u};
 #if NEF_Y_FIRST
@@ -1284,8 +1359,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
       __syncwarp();
       if (lane == 0) mbar_arrive(y_empty + 8 * st);  // Y / mask stage read by this warp
       if (!(a.dbg & 256)) {
-        if (MM == 1) ew_half<KIND>(a, sv, yv, mk, cols_here - 16 * cg, row_ok, pb, lsum, cnt);
-        else ew_half_sent<KIND>(a, sv, yv, cols_here - 16 * cg, row_ok, pb, lsum, cnt);
+        if (MM == 1) ew_half<KIND, SPA>(a, sv, yv, mk, cols_here - 16 * cg, row_ok, pb, pl, lsum, cnt);
+        else ew_half_sent<KIND, SPA>(a, sv, yv, cols_here - 16 * cg, row_ok, pb, pl, lsum[0], cnt[0]);
       } else {   // dbg 256: timing experiment without the elementwise math (P_b = S + Y)
 #pragma unroll
         for (int j = 0; j < 16; ++j) pb[j] = sv[j] + __float_as_uint(yv[j]) + mk[j >> 2];
@@ -1293,6 +1368,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
       if (a.mode != 2) {
         tmem_st16(tc, sv);
         tmem_st16(tc + 64, pb);
+        if constexpr (SPA) tmem_st16(tmem + 384 + 64 * b + lane_off + 16 * cg, pl);
       }
       if (a.debug && blockIdx.x == 0 && blockIdx.y == 0 && t == 0) {
 #pragma unroll
@@ -1300,7 +1376,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
       }
       if (warp == W_EW0 && lane == 0) trace_ev(a, t, EV_EW_HALF);
       if (a.mode != 2) tmem_st_wait();
-      if (a.mode != 0) loss_acc += (double)lsum;
+      if (a.mode != 0) {
+        loss_acc[0] += (double)lsum[0];
+        if (MM == 1 && a.split) { loss_acc[1] += (double)lsum[1]; loss_acc[2] += (double)lsum[2]; }
+      }
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(p_full + 8 * b);      // P(t) in TMEM (or, loss only: S(t) consumed)
@@ -1328,17 +1407,23 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
       mbar_spin(nd_full, 0);
     }
     if (a.mode != 0) {
-      gRed[ew] = loss_acc;
-      gRedC[ew] = cnt;
-      asm volatile("bar.sync 1, %0;" ::"n"(NEW * 32) : "memory");
-      for (int w = NEW * 16; w > 0; w >>= 1) {
-        if (ew < w) { gRed[ew] += gRed[ew + w]; gRedC[ew] += gRedC[ew + w]; }
+      // fixed-order block sums, one per role (split fits: losspart / countpart are [3][parts])
+      const int nrole = (MM == 1 && a.split) ? 3 : 1;
+      const int64_t parts = (int64_t)gridDim.x * gridDim.y;
+      const int64_t id = (int64_t)blockIdx.y * gridDim.x + blockIdx.x;
+      for (int q = 0; q < nrole; ++q) {
+        gRed[ew] = loss_acc[q];
+        gRedC[ew] = cnt[q];
         asm volatile("bar.sync 1, %0;" ::"n"(NEW * 32) : "memory");
-      }
-      if (ew == 0) {
-        const int64_t id = (int64_t)blockIdx.y * gridDim.x + blockIdx.x;
-        a.losspart[id] = gRed[0];
-        a.countpart[id] = gRedC[0];
+        for (int w = NEW * 16; w > 0; w >>= 1) {
+          if (ew < w) { gRed[ew] += gRed[ew + w]; gRedC[ew] += gRedC[ew + w]; }
+          asm volatile("bar.sync 1, %0;" ::"n"(NEW * 32) : "memory");
+        }
+        if (ew == 0) {
+          a.losspart[q * parts + id] = gRed[0];
+          a.countpart[q * parts + id] = gRedC[0];
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(NEW * 32) : "memory");
       }
     }
   }

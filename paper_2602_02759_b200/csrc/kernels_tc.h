@@ -53,6 +53,7 @@ struct TcArgs {
                               //   LossOff<KIND>, the data-only sum comes from the sentinel pass
   int absy;                   // MM = 0 on raw unmasked Y: every entry observed, sign bits ignored
                               //   (an observed -0.0 is zero, not the sentinel's "missing")
+  int split;                  // MM = 1 with labels 0..3 (R29): train = 1; loss partials per role [3][parts]
   int drain_tiles;            // N / D drained into a separate split partial every this many tiles
   int64_t n_groups;           // drain groups per chunk: Qpart is [chunks][n_groups][2][n_rows][K]
   int dbg;                    // diagnostics: 1 prefill N/D with 1 and always accumulate,

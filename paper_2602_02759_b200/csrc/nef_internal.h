@@ -126,6 +126,7 @@ struct Plan {
   int64_t ws_trace = 0;              // fp64 trace accumulators
   int64_t ws_dterm = 0;              // [double][long long]: data-only loss sum, observed count (R25)
   int64_t ws_dpart = 0;              // their kSentParts block partials (doubles, then counts)
+  int64_t ws_fsave = 0;              // factor copies of nef_fit_split (iterate entering a sweep)
   int64_t ws_sent = 0;               // NaN-sentinel copy of Y (nef_fit with a mask)
   // sharding
   int shard_mode = -1, rank = 0, world = 1;

@@ -507,7 +507,7 @@ void finish_workspace(const Plan& p, Lowering& L, Bump& bump, const std::string&
   int64_t felems = prod_idx(p, p.ops[L.ell]);
   L.ws_num = bump.take(2 * felems * 4);   // num | den adjacent (one all-reduce)
   L.ws_den = L.ws_num + felems * 4;
-  L.ws_losspart = bump.take(row_blocks * chunks * 16);
+  L.ws_losspart = bump.take(row_blocks * chunks * 48);   // [3 roles] loss sums + counts (split fits)
   // epilogue: Num (ell's layout) = einsum(Q[row_idx + bond], row factors except ell)
   std::string qidx = uidx;
   if (L.row_factors.size() == 1 && p.ops[L.ell] == qidx) {
@@ -530,7 +530,7 @@ void finish_workspace(const Plan& p, Lowering& L, Bump& bump, const std::string&
   if (L.tc_ok) {
     L.ws_tc_Qpart = bump.take(L.tc_chunks * L.tc_groups * L.tc_row_blocks * 128 * L.K * 2 * 4);
     int64_t nparts = L.tc_row_blocks * L.tc_chunks;
-    L.ws_tc_losspart = bump.take(nparts * 16);
+    L.ws_tc_losspart = bump.take(nparts * 48);   // [3 roles] loss sums + counts (split fits)
   }
   L.ws_end = bump.off;
 }
@@ -604,8 +604,16 @@ int lower_all(Plan& p, std::string& err) {
   // sentinel pass sums (R25): [data-only loss sum][observed count], then its block partials
   p.ws_dterm = p.ws_trace + (int64_t)8 * 4096;
   p.ws_dpart = p.ws_dterm + 256;
+  // nef_fit_split: a copy of the factors entering each sweep (a stopped fit returns that iterate)
+  p.ws_fsave = (p.ws_dpart + (int64_t)16 * (kSentParts) + 255) / 256 * 256;
+  int64_t fbytes = 0;
+  for (auto& sh : p.fshape) {
+    int64_t n = 1;
+    for (auto d : sh) n *= d;
+    fbytes += (n * 4 + 255) / 256 * 256;
+  }
   // NaN-sentinel copy of the local Y (nef_fit with a mask, R5): 4 B per local entry
-  p.ws_sent = (p.ws_dpart + (int64_t)16 * (kSentParts) + 255) / 256 * 256;
+  p.ws_sent = (p.ws_fsave + fbytes + 255) / 256 * 256;
   p.ws_bytes = (size_t)(p.ws_sent + p.n_local * 4 + 256);
   return NEF_OK;
 }

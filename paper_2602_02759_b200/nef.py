@@ -58,6 +58,13 @@ def _load():
         "nef_debug_dump": (ctypes.c_int, [vp]),
         "nef_debug_trace": (ctypes.c_int, [vp]),
         "nef_profile_read": (ctypes.c_int, [ctypes.POINTER(d), i64p, ctypes.POINTER(d)]),
+        "nef_fit_ex": (ctypes.c_int, [vp, vp, vp, vp, d, vp, ctypes.c_int, ctypes.POINTER(d), vp, ctypes.c_size_t, vp]),
+        "nef_fit_split": (ctypes.c_int, [vp, vp, vp, vp, d, vp, vp, ctypes.POINTER(d), i64p, ctypes.POINTER(ctypes.c_int),
+                                         ctypes.POINTER(ctypes.c_int), vp, ctypes.c_size_t, vp]),
+        "nef_update_ex": (ctypes.c_int, [vp, ctypes.c_int, vp, vp, vp, d, vp, vp, ctypes.c_size_t, vp]),
+        "nef_num_den_ex": (ctypes.c_int, [vp, ctypes.c_int, vp, vp, vp, vp, vp, vp, vp, ctypes.c_size_t, vp]),
+        "nef_apply_update_ex": (ctypes.c_int, [vp, ctypes.c_int, vp, d, vp, vp, vp, vp]),
+        "nef_loss_ex": (ctypes.c_int, [vp, vp, vp, vp, vp, ctypes.POINTER(d), i64p, vp, ctypes.c_size_t, vp]),
         "nef_plan_destroy": (None, [vp]),
         "nef_last_error": (ctypes.c_char_p, []),
         "nef_version": (ctypes.c_char_p, []),
@@ -75,7 +82,27 @@ EXPORTED = ("nef_plan", "nef_plan_info", "nef_factor_shape", "nef_local_shape", 
             "nef_nccl_unique_id", "nef_plan_shard", "nef_plan_shard_host", "nef_last_launch_count",
             "nef_set_kernel_policy",
             "nef_profile_enable", "nef_profile_read", "nef_debug_dump", "nef_debug_trace",
+            "nef_fit_ex", "nef_fit_split", "nef_update_ex", "nef_num_den_ex", "nef_apply_update_ex", "nef_loss_ex",
             "nef_plan_destroy", "nef_last_error", "nef_version")
+
+LOSS_KINDS = {"ab": 0, "negbin": 1, "bernoulli": 2, "binomial": 3, "js": 4}
+STOP_REASONS = {1: "patience", 2: "plateau", 3: "max_iters"}
+
+
+class nef_loss_spec(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int), ("alpha", ctypes.c_double), ("beta", ctypes.c_double),
+                ("param", ctypes.c_double), ("aux", ctypes.c_void_p)]
+
+
+class nef_stop_rule(ctypes.Structure):
+    _fields_ = [("max_iters", ctypes.c_int), ("min_rel_decrease", ctypes.c_double), ("val_patience", ctypes.c_int)]
+
+
+def loss_spec(kind="ab", alpha=1.0, beta=0.0, param=0.0, aux=None):
+    """Build an nef_loss_spec: kind in ab / negbin / bernoulli / binomial / js; param = phi (negbin)
+    or n (binomial); aux = optional per-entry phi / n CUDA tensor (float32, Y's shape)."""
+    return nef_loss_spec(LOSS_KINDS[kind], float(alpha), float(beta), float(param),
+                         ctypes.c_void_p(int(aux.data_ptr())) if aux is not None else None)
 
 
 def _check(code):
@@ -252,6 +279,70 @@ def nef_fit_host(h, Y_host, mask_host, alpha, beta, eps, factors_host, iters, sc
     return np.array(trace[:], dtype=np.float64)
 
 
+def _check_aux(h, spec, aux):
+    if aux is not None:
+        import torch
+        if not aux.is_cuda or not aux.is_contiguous() or aux.dtype != torch.float32 or tuple(aux.shape) != nef_local_shape(h):
+            raise NefError(5, "aux must be a contiguous float32 CUDA tensor of Y's local shape")
+
+
+def nef_fit_ex(h, Y, mask, spec, eps, factors, iters, workspace, stream=None, aux=None):
+    _validate(h, Y, mask, factors)
+    _check_aux(h, spec, aux)
+    trace = (ctypes.c_double * (iters + 1))()
+    _check(LIB.nef_fit_ex(h, _ptr(Y), _ptr(mask), ctypes.byref(spec), float(eps), _fptrs(factors), int(iters), trace,
+                          _ptr(workspace), workspace.numel(), _stream(stream)))
+    return np.array(trace[:], dtype=np.float64)
+
+
+def nef_fit_split(h, Y, labels, spec, eps, factors, max_iters, min_rel_decrease, val_patience, workspace, stream=None,
+                  aux=None):
+    """Returns dict(traces=[train, validation, heldout] arrays of sweeps + 1 loss sums, counts, sweeps, reason)."""
+    _validate(h, Y, labels, factors)
+    _check_aux(h, spec, aux)
+    rule = nef_stop_rule(int(max_iters), float(min_rel_decrease), int(val_patience))
+    tr = (ctypes.c_double * (3 * (max_iters + 1)))()
+    counts = (ctypes.c_int64 * 3)()
+    sweeps = ctypes.c_int()
+    reason = ctypes.c_int()
+    _check(LIB.nef_fit_split(h, _ptr(Y), _ptr(labels), ctypes.byref(spec), float(eps), _fptrs(factors),
+                             ctypes.byref(rule), tr, counts, ctypes.byref(sweeps), ctypes.byref(reason),
+                             _ptr(workspace), workspace.numel(), _stream(stream)))
+    n = sweeps.value
+    T = max_iters + 1
+    traces = [np.array(tr[q * T:q * T + n + 1], dtype=np.float64) for q in range(3)]
+    return dict(traces=traces, counts=[int(c) for c in counts], sweeps=n, reason=STOP_REASONS.get(reason.value, "?"))
+
+
+def nef_update_ex(h, ell, Y, mask, spec, eps, factors, workspace, stream=None):
+    _validate(h, Y, mask, factors)
+    _check(LIB.nef_update_ex(h, int(ell), _ptr(Y), _ptr(mask), ctypes.byref(spec), float(eps), _fptrs(factors),
+                             _ptr(workspace), workspace.numel(), _stream(stream)))
+
+
+def nef_num_den_ex(h, ell, Y, mask, spec, factors, num, den, workspace, stream=None):
+    _validate(h, Y, mask, factors)
+    _validate_nd(h, ell, num, den)
+    _check(LIB.nef_num_den_ex(h, int(ell), _ptr(Y), _ptr(mask), ctypes.byref(spec), _fptrs(factors), _ptr(num),
+                              _ptr(den), _ptr(workspace), workspace.numel(), _stream(stream)))
+
+
+def nef_apply_update_ex(h, ell, spec, eps, factors, num, den, stream=None):
+    _validate(h, factors=factors)
+    _validate_nd(h, ell, num, den)
+    _check(LIB.nef_apply_update_ex(h, int(ell), ctypes.byref(spec), float(eps), _fptrs(factors), _ptr(num), _ptr(den),
+                                   _stream(stream)))
+
+
+def nef_loss_ex(h, Y, mask, spec, factors, workspace, stream=None):
+    _validate(h, Y, mask, factors)
+    s = ctypes.c_double()
+    n = ctypes.c_int64()
+    _check(LIB.nef_loss_ex(h, _ptr(Y), _ptr(mask), ctypes.byref(spec), _fptrs(factors), ctypes.byref(s),
+                           ctypes.byref(n), _ptr(workspace), workspace.numel(), _stream(stream)))
+    return s.value, n.value
+
+
 def nef_nccl_unique_id() -> bytes:
     buf = ctypes.create_string_buffer(128)
     _check(LIB.nef_nccl_unique_id(buf))
@@ -375,3 +466,23 @@ class Plan:
 
     def loss(self, Y, mask, alpha, beta, factors, stream=None):
         return nef_loss(self.h, Y, mask, alpha, beta, factors, self.workspace(Y.device), stream)
+
+    # any loss of nef_loss_spec: spec = loss_spec("negbin", param=2.0) etc.
+    def fit_ex(self, Y, mask, spec, factors, iters, eps=1e-12, stream=None, aux=None):
+        return nef_fit_ex(self.h, Y, mask, spec, eps, factors, iters, self.workspace(Y.device), stream, aux)
+
+    def fit_split(self, Y, labels, spec, factors, max_iters=5000, min_rel_decrease=1e-6, val_patience=5, eps=1e-12,
+                  stream=None, aux=None):
+        return nef_fit_split(self.h, Y, labels, spec, eps, factors, max_iters, min_rel_decrease, val_patience,
+                             self.workspace(Y.device), stream, aux)
+
+    def num_den_ex(self, ell, Y, mask, spec, factors, stream=None):
+        import torch
+        shp = self.factor_shape(ell)
+        num = torch.empty(shp, dtype=torch.float32, device=Y.device)
+        den = torch.empty(shp, dtype=torch.float32, device=Y.device)
+        nef_num_den_ex(self.h, ell, Y, mask, spec, factors, num, den, self.workspace(Y.device), stream)
+        return num, den
+
+    def loss_ex(self, Y, mask, spec, factors, stream=None):
+        return nef_loss_ex(self.h, Y, mask, spec, factors, self.workspace(Y.device), stream)
