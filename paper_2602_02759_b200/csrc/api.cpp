@@ -37,6 +37,8 @@ float* g_debug = nullptr;   // optional device dump of the tcgen05 kernel's firs
 long long* g_trace = nullptr;   // optional pipeline timeline of the tcgen05 kernel (diagnostics)
 bool g_no_sentinel = std::getenv("NEF_NO_SENTINEL") != nullptr;   // diagnostics: stream the uint8 mask
 bool g_no_lconst = std::getenv("NEF_NO_LCONST") != nullptr;     // diagnostics: loss passes compute the whole divergence (R25 off)
+// diagnostics: NEF_TC_VDIRECT=0 generates V per tile instead of TMA-loading direct-V table rows
+bool g_vdirect = [] { const char* e = std::getenv("NEF_TC_VDIRECT"); return !e || std::atoi(e) != 0; }();
 
 // live CUDA-event timing of the streaming kernel (nef_profile_*)
 struct Prof {
@@ -272,9 +274,7 @@ int stream_pass(const Ctx& c, const nef::Lowering& L, const float* Y, const uint
       // direct V (planner: Lowering::vd_tab): the tile's V rows are consecutive rows of one
       // table, TMA-loaded; a K % 4 != 0 table is first copied to a 16-byte row pitch
       t.vdirect = 0;
-      const char* dv = std::getenv("NEF_TC_VDIRECT");
-      const bool allow = !dv || std::atoi(dv) != 0;
-      if (allow && L.vd_tab >= 0) {
+      if (g_vdirect && L.vd_tab >= 0) {
         t.vdirect = 1;
         t.var_tab = L.vd_tab;
         t.var_rows = L.vd_rows;
@@ -310,14 +310,7 @@ int stream_pass(const Ctx& c, const nef::Lowering& L, const float* Y, const uint
     t.absy = (!M && !sent) ? 1 : 0;
     t.debug = g_debug;
     t.trace = g_trace;
-    {
-      const char* e = std::getenv("NEF_TC_VT");
-      t.vt = e ? std::atoi(e) : 1;
-      e = std::getenv("NEF_TC_DBG");
-      t.dbg = e ? std::atoi(e) : 0;
-      t.drain_tiles = nef::kDrainTiles;
-      t.n_groups = (tpc + nef::kDrainTiles - 1) / nef::kDrainTiles;
-    }
+    t.n_groups = (tpc + nef::kDrainTiles - 1) / nef::kDrainTiles;
     prof_begin(c.s);
     CK(nef::tc::launch(t, Y, M, L.tc_row_blocks, chunks, c.s));
     prof_end(c.s, bytes);
@@ -376,15 +369,21 @@ int loss_pass(const Ctx& c, const float* Y, const uint8_t* M, const nef::DivPara
   return reduce_loss(c, o, M, slot, cslot);
 }
 
-// Steps 1-4 of one factor update: leaves A in *num, B in *den (device pointers into ws).
+// Steps 1-4 of one factor update: leaves A in *num, B in *den (device pointers into ws).  With
+// `fused` (epilogue-free lowering, no all-reduce) the split partials are left unreduced in *fused
+// for the fused reduce + update kernel and num / den are not written.
 int num_den(const Ctx& c, int ell, const float* Y, const uint8_t* M, const nef::DivParams& dv, int mode,
-            double* slot, long long* cslot, float** num, float** den) {
+            double* slot, long long* cslot, float** num, float** den, StreamOut* fused = nullptr) {
   const nef::Lowering& L = c.p->low[ell];
   int st = side_operands(c, L);
   if (st) return st;
   StreamOut o;
   if ((st = stream_pass(c, L, Y, M, mode, dv, o))) return st;
   if (mode == 1 && (st = reduce_loss(c, o, M, slot, cslot))) return st;
+  if (fused && L.epi_identity) {
+    *fused = o;
+    return NEF_OK;
+  }
   const int64_t qe = L.n_rows * L.K;
   float* Q = reinterpret_cast<float*>(c.ws + L.ws_Q);
   CK(nef::launch_reduce_q(o.Qpart, Q, o.n_chunks, 2 * qe, c.s));
@@ -421,10 +420,17 @@ int allreduce(const nef::Plan& p, void* buf, size_t count, int dtype, cudaStream
 int update_one(const Ctx& c, int ell, const float* Y, const uint8_t* M, const nef::DivParams& dv, const nef::UpdArgs& u,
                int mode, double* slot, long long* cslot) {
   float *num = nullptr, *den = nullptr;
-  int st = num_den(c, ell, Y, M, dv, mode, slot, cslot, &num, &den);
-  if (st) return st;
   int64_t n = 1;
   for (auto d : c.p->fshape[ell]) n *= d;
+  const bool fuse = !communicates(*c.p) && c.p->low[ell].epi_identity;
+  StreamOut fo;
+  int st = num_den(c, ell, Y, M, dv, mode, slot, cslot, &num, &den, fuse ? &fo : nullptr);
+  if (st) return st;
+  if (fuse) {   // numerator / denominator summed from the split partials inside the update kernel
+    CK(nef::launch_reduce_update(fo.Qpart, c.F[ell], fo.n_chunks, n, u, c.s));
+    ++g_launches;
+    return NEF_OK;
+  }
   if (communicates(*c.p) && !c.p->factor_has_shard[ell]) {
     // num and den are adjacent in the workspace (Q_a|Q_b or num|den regions)
     if (den == num + n) {

@@ -93,6 +93,10 @@ struct UpdArgs {
 UpdArgs make_upd(double alpha, double beta, double eps);
 UpdArgs make_upd_fam(int fam, double alpha, double beta, double eps);
 cudaError_t launch_update(float* theta, const float* num, const float* den, int64_t n, UpdArgs u, cudaStream_t s);
+// the same with the numerator / denominator summed from the split partials Qpart [chunks][2][n]
+// (lowerings whose epilogue is the identity, one rank): reduce_q + update in one launch
+cudaError_t launch_reduce_update(const float* Qpart, float* theta, int64_t n_chunks, int64_t n, UpdArgs u,
+                                 cudaStream_t s);
 
 // Sum CTA loss partials (fixed order) into slot[0] (double) and count into cslot[0].  With off
 // (R25): slot[0] = scale * sum + off[0] and cslot[0] = ((long long*)off)[1].

@@ -378,7 +378,8 @@ static cudaError_t launch_kp_bm(const FusedDev& d, cudaStream_t s) {
 // (<= 32 rows: one row block either way, so the planner's partial layout is unchanged)
 template <int KP, int KIND>
 static cudaError_t launch_kp(const FusedDev& d, cudaStream_t s) {
-  if (d.a.n_rows <= 32 && !std::getenv("NEF_FFMA_BM64")) return launch_kp_bm<KP, KIND, 32>(d, s);
+  static const bool bm64 = std::getenv("NEF_FFMA_BM64") != nullptr;   // diagnostics
+  if (d.a.n_rows <= 32 && !bm64) return launch_kp_bm<KP, KIND, 32>(d, s);
   return launch_kp_bm<KP, KIND, 64>(d, s);
 }
 
@@ -492,7 +493,8 @@ cudaError_t launch_einstep(const EinStep& st, const float* A, const float* B, fl
   const bool small = span < (1ll << 30);
   // too few outputs to fill the GPU with short sums: 4 lanes per output (latency-bound steps of
   // the Tucker side operands, ~20 % occupancy one thread per output)
-  const bool quad = !split && small && st.out_size < 148 * 1024 && st.sum_size >= 8 && !std::getenv("NEF_EINSTEP_NOQUAD");
+  static const bool noquad = std::getenv("NEF_EINSTEP_NOQUAD") != nullptr;   // diagnostics
+  const bool quad = !split && small && st.out_size < 148 * 1024 && st.sum_size >= 8 && !noquad;
   const int L = split ? 32 : quad ? 4 : 1;
   long long blocks = (st.out_size * L + 255) / 256;
   if (blocks > 148 * 32) blocks = 148 * 32;
@@ -634,13 +636,74 @@ __global__ void reduce_q8_kernel(const float* __restrict__ part, float* __restri
 }
 
 cudaError_t launch_reduce_q(const float* Qpart, float* Q, int64_t n_chunks, int64_t elems2, cudaStream_t s) {
-  if (elems2 <= 148LL * 2048 && n_chunks >= 16 && !std::getenv("NEF_REDUCE_Q1")) {
+  static const bool q1 = std::getenv("NEF_REDUCE_Q1") != nullptr;   // diagnostics
+  if (elems2 <= 148LL * 2048 && n_chunks >= 16 && !q1) {
     reduce_q8_kernel<<<(unsigned)((elems2 + 31) / 32), 256, 0, s>>>(Qpart, Q, n_chunks, elems2);
     return cudaGetLastError();
   }
   long long blocks = (elems2 + 255) / 256;
   if (blocks > 148 * 16) blocks = 148 * 16;
   reduce_q_kernel<<<(unsigned)(blocks < 1 ? 1 : blocks), 256, 0, s>>>(Qpart, Q, n_chunks, elems2);
+  return cudaGetLastError();
+}
+
+__device__ __forceinline__ float mu_update(float th, double A, double B, const UpdArgs& u) {
+  double mult = 1.0;
+  if (B > 0.0) {
+    const double r = A / B;
+    if (u.g_case == 1) mult = exp(r);
+    else if (u.inv_expo == 1.0) mult = r;
+    else mult = pow(r, u.inv_expo);
+  }
+  return (float)fmax(u.eps, (double)th * mult);
+}
+
+// Fused reduce + update (epilogue-free lowerings on one rank): theta[e] <- update with
+// A = sum_c part[c][0][e], B = sum_c part[c][1][e] (fixed order, fp64; the numerator and
+// denominator are the factor's own layout).  Few elements with many partials: warp w of a block
+// sums partials w, w + 8, ... of 32 consecutive elements (coalesced), combined in fixed order.
+__global__ void reduce_update8_kernel(const float* __restrict__ part, float* __restrict__ th, long long n_chunks,
+                                      long long n, UpdArgs u) {
+  __shared__ double ra[8][32], rb[8][32];
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  const long long e = (long long)blockIdx.x * 32 + l;
+  double a = 0.0, b = 0.0;
+  if (e < n)
+    for (long long c = w; c < n_chunks; c += 8) {
+      a += (double)part[c * 2 * n + e];
+      b += (double)part[c * 2 * n + n + e];
+    }
+  ra[w][l] = a;
+  rb[w][l] = b;
+  __syncthreads();
+  if (w == 0 && e < n) {
+    double A = 0.0, B = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) { A += ra[k][l]; B += rb[k][l]; }
+    th[e] = mu_update(th[e], A, B, u);
+  }
+}
+__global__ void reduce_update_kernel(const float* __restrict__ part, float* __restrict__ th, long long n_chunks,
+                                     long long n, UpdArgs u) {
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += (long long)gridDim.x * blockDim.x) {
+    double A = 0.0, B = 0.0;
+    for (long long c = 0; c < n_chunks; ++c) {
+      A += (double)part[c * 2 * n + e];
+      B += (double)part[c * 2 * n + n + e];
+    }
+    th[e] = mu_update(th[e], A, B, u);
+  }
+}
+
+cudaError_t launch_reduce_update(const float* Qpart, float* theta, int64_t n_chunks, int64_t n, UpdArgs u,
+                                 cudaStream_t s) {
+  if (n <= 148LL * 1024 && n_chunks >= 16) {
+    reduce_update8_kernel<<<(unsigned)((n + 31) / 32), 256, 0, s>>>(Qpart, theta, n_chunks, n, u);
+    return cudaGetLastError();
+  }
+  long long blocks = (n + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  reduce_update_kernel<<<(unsigned)(blocks < 1 ? 1 : blocks), 256, 0, s>>>(Qpart, theta, n_chunks, n, u);
   return cudaGetLastError();
 }
 

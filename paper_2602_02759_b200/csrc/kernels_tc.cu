@@ -38,13 +38,18 @@ constexpr int BM = 128, BN = 64;
 #ifndef NEF_NS
 #define NEF_NS 2   // Y stages without a mask stream (3 measured 2 % slower on the c5 fit)
 #endif
-// Y (/ mask) pipeline stages: 3 with the uint8 mask stream, else NEF_NS
-template <int MM> struct YStages { static constexpr int value = MM == 1 ? 3 : NEF_NS; };
+#ifndef NEF_NS32
+#define NEF_NS32 3   // Y stages of bond <= 32 kernels (2 / 3 / 4 measured within 2 %: 3)
+#endif
+// Y (/ mask) pipeline stages: 3 with the uint8 mask stream (4 for KB = 32), else NEF_NS (NEF_NS32)
+template <int KB, int MM> struct YStages {
+  static constexpr int value = KB == 32 ? (MM == 1 ? 4 : NEF_NS32) : (MM == 1 ? 3 : NEF_NS);
+};
 // V tile stages: 3 with a uint8 mask stream (its stages take the smem), else 4
 #ifndef NEF_NV0
 #define NEF_NV0 4
 #endif
-template <int MM> struct VStages { static constexpr int value = MM == 1 ? 3 : NEF_NV0; };
+template <int KB, int MM> struct VStages { static constexpr int value = MM == 1 ? 3 : NEF_NV0; };
 // warp roles: 16 elementwise warps, 4 V generators, direct-V row loads, TMA producer, MMA
 // issuer.  The warp schedulers favour higher warp ids, so the producers whose latency is on the
 // critical path sit above the elementwise warps (with the producers below, the V generators
@@ -81,8 +86,11 @@ constexpr int NEW = 16;      // elementwise warps: 4 TMEM lane quarters x 4 grou
 constexpr int NTHREADS = (NEF_WARP_MAP == 0 ? 23 : 24) * 32;   // (map 3: warp 22 idle)
 constexpr int Y_STAGE = BM * BN * 4;      // 32 KB
 constexpr int M_STAGE = BM * BN;          // 8 KB
-constexpr int VT_OFF = BN * 64 * 4;       // V^T copy after V inside a stage
-constexpr int V_STAGE_MAX = 2 * VT_OFF;   // V (16 KB) + V^T (16 KB) for KB = 64
+// a V stage: V (64 tile columns x KB bonds, SW128 K-major) then its transpose V^T, KB * 256 B each
+template <int KB> struct VSt {
+  static constexpr int VT_OFF = BN * KB * 4;     // V^T copy after V inside a stage
+  static constexpr int SIZE = 2 * VT_OFF;        // 32 KB for KB = 64, 16 KB for KB = 32
+};
 
 struct __align__(64) Params {
   CUtensorMap tmY;
@@ -474,7 +482,7 @@ struct VOff {
       vb[i] = (c >> 3) * (BN * 128) + (x0 >> 3) * 1024 + (x0 & 7) * 128;
       cx[i] = (c & 7) ^ (x0 & 7);
       const int k0 = 4 * c;
-      vtb[i] = VT_OFF + (x0 >> 5) * (KB * 128) + (k0 >> 3) * 1024 + (k0 & 7) * 128;
+      vtb[i] = VSt<KB>::VT_OFF + (x0 >> 5) * (KB * 128) + (k0 >> 3) * 1024 + (k0 & 7) * 128;
       xc[i] = ((x0 & 31) >> 2) ^ (k0 & 7);
     }
   }
@@ -566,7 +574,7 @@ __device__ __noinline__ void vtile_store_slow(const TcArgs& a, int xw, int lane,
         }
         const uint32_t w = tf32_bits(p);
         *reinterpret_cast<uint32_t*>(vrow + sw128_off(x, k, BN)) = w;
-        *reinterpret_cast<uint32_t*>(vrow + VT_OFF + sw128_off(k, x, KB)) = w;
+        *reinterpret_cast<uint32_t*>(vrow + VSt<KB>::VT_OFF + sw128_off(k, x, KB)) = w;
       }
     }
   }
@@ -973,6 +981,10 @@ enum TraceEv : int {
 #ifndef NEF_TRACE
 #define NEF_TRACE 0
 #endif
+// timing experiments (scripts/build_variants.sh): compiled out of the production build
+#ifndef NEF_DBG
+#define NEF_DBG 0
+#endif
 __device__ __forceinline__ void trace_ev(const TcArgs& a, int t, int e) {
 #if NEF_TRACE
   if (a.trace && blockIdx.x == 0 && blockIdx.y == 0 && t < 1024) a.trace[t * 32 + e] = (long long)clock64();
@@ -990,8 +1002,9 @@ __device__ __forceinline__ void trace_ev(const TcArgs& a, int t, int e) {
 // MM: 1 = uint8 mask streamed alongside Y; 0 = no mask stream (no mask, or the NaN-sentinel Y)
 template <int KB, int KIND, int MM>
 __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_constant__ Params P) {
-  constexpr int NV = VStages<MM>::value;
-  constexpr int NS = YStages<MM>::value;
+  constexpr int NV = VStages<KB, MM>::value;
+  constexpr int NS = YStages<KB, MM>::value;
+  constexpr int V_STAGE = VSt<KB>::SIZE;
   // Euclidean pair with bond <= 32: numerator operand split hi + lo (put_pa), TMEM 384..511 free
   constexpr bool SPA = (KIND == EW_EUC && KB == 32 && !NEF_PA_RN);
   extern __shared__ unsigned char smraw[];
@@ -1007,7 +1020,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
   const uint32_t sY = base;                                  // NS x 32 KB
   const uint32_t sM = sY + NS * Y_STAGE;                     // NS x 8 KB
   const uint32_t sV = sM + (MM == 1 ? NS * M_STAGE : 0);     // NV x (V | V^T)
-  const uint32_t sBar = sV + NV * V_STAGE_MAX;
+  const uint32_t sBar = sV + NV * V_STAGE;
   const uint32_t y_full = sBar, y_empty = y_full + 8 * NS;
   const uint32_t v_full = y_empty + 8 * NS, v_empty = v_full + 8 * NV;
   const uint32_t s_full = v_empty + 8 * NV;                  // [2] S(t) in buffer t & 1 (MMA commit)
@@ -1035,7 +1048,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
   // The tensor core's fp32 accumulation truncates (ubench/acc_round.cu), a bias growing with the
   // number of accumulation steps; N and D are therefore drained into the (RN, fp32) partials
   // every G tiles and restarted.
-  const int G = a.drain_tiles > 0 ? a.drain_tiles : (1 << 30);
+  constexpr int G = kDrainTiles;   // (power of two: t % G is a mask)
 
   if (tid == 0) {
     for (int i = 0; i < NS; ++i) { mbar_init(y_full + 8 * i, 1); mbar_init(y_empty + 8 * i, NEW); }
@@ -1109,7 +1122,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
       // the N/D MMAs of tile t cannot overwrite P(t) before they read it (checked: bit-identical
       // factors with and without the explicit wait, scripts/war_check.py).  dbg & 16 restores
       // the explicit wait on the N/D commit.
-      const bool war_wait = (a.dbg & 16) != 0;
+      const bool war_wait = (NEF_DBG & 16) != 0;
       mbar_wait_mma(u_ready, 0);
       tc_fence_after();
       // S(t) = U_hi V(t)^T + U_lo V(t)^T into buffer t & 1 (split reconstruction)
@@ -1120,7 +1133,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
         tc_fence_after();
         if (lane == 0) trace_ev(a, t, EV_MMA1_ISSUE);
         __syncwarp();
-        const uint64_t vd = sdesc(sV + vs * V_STAGE_MAX, 16, 1024);
+        const uint64_t vd = sdesc(sV + vs * V_STAGE, 16, 1024);
         const uint32_t d = tmem + 128 * b;
         // one asm block, one elect: U_hi and U_lo steps interleaved (tUl = tUh + KB)
         if (KB == 64) mma_s_block_64<id1>(d, tUh, vd, 0u);
@@ -1135,9 +1148,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
         tc_fence_after();
         if (lane == 0) trace_ev(a, u, EV_MMA23_ISSUE);
         __syncwarp();
-        if (a.mode != 2 && !(a.dbg & 64)) {   // dbg 64: timing experiment without N/D MMAs
+        if (a.mode != 2 && !(NEF_DBG & 64)) {   // NEF_DBG 64: timing experiment without N/D MMAs
           // B = V^T, K-major SW128: rows = bond (N), K = tile columns (2 atoms of 32)
-          const uint64_t vtd = sdesc(sV + vs * V_STAGE_MAX + VT_OFF, 16, 1024);
+          const uint64_t vtd = sdesc(sV + vs * V_STAGE + VSt<KB>::VT_OFF, 16, 1024);
           const uint32_t pa = tmem + 128 * b;   // P_a; P_b at pa + 64
           // the accumulators restart at every drain group (see the elementwise loop)
           const uint32_t acc = (u % G) != 0 ? 1u : 0u;
@@ -1171,7 +1184,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
         const uint32_t bar = vraw_full + 8 * vs;
         mbar_expect_tx(bar, (uint32_t)(KB * BN * 4));
 #pragma unroll
-        for (int h = 0; h < KB / 32; ++h) tma_load_2d(sV + vs * V_STAGE_MAX + h * (BN * 128), &P.tmV, 32 * h, rowv, bar);
+        for (int h = 0; h < KB / 32; ++h) tma_load_2d(sV + vs * V_STAGE + h * (BN * 128), &P.tmV, 32 * h, rowv, bar);
       }
     }
   } else if (vg_index(warp) >= 0 && a.vdirect) {
@@ -1204,7 +1217,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
       const int vs = t % NV;
       mbar_wait_relaxed(vraw_full + 8 * vs, (t / NV) & 1, 96);
       if (warp == W_VG0 && lane == 0) trace_ev(a, t, EV_VG_START);
-      unsigned char* vrow = gV + vs * V_STAGE_MAX;
+      unsigned char* vrow = gV + vs * V_STAGE;
 #pragma unroll
       for (int i = 0; i < VOff<KB>::NB; ++i) {
         float4 p[4];
@@ -1215,7 +1228,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
           const float2 hi = __fmul2_rn(make_float2(f.z, f.w), make_float2(cst.z, cst.w));
           p[r] = make_float4(lo.x, lo.y, hi.x, hi.y);
         }
-        if (!(a.dbg & 128))   // dbg 128: timing experiment without the V / V^T stores
+        if (!(NEF_DBG & 128))   // NEF_DBG 128: timing experiment without the V / V^T stores
           vblock_store_direct<KB>(vrow, vo.vb[i], vo.cx[i], vo.vtb[i], vo.xc[i], p);
       }
       if (warp == W_VG0 && lane == 0) trace_ev(a, t, EV_VG_ISSUED);
@@ -1239,7 +1252,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
       const int vs = t % NV;
       mbar_wait_relaxed(v_empty + 8 * vs, ((t / NV) & 1) ^ 1);
       if (warp == W_VG0 && lane == 0) trace_ev(a, t, EV_VG_START);
-      vtile_store<KB>(a, xw, lane, cur, toff_c, gV + vs * V_STAGE_MAX, vo);
+      vtile_store<KB>(a, xw, lane, cur, toff_c, gV + vs * V_STAGE, vo);
       fence_async_smem();
       __syncwarp();
       if (lane == 0) mbar_arrive(v_full + 8 * vs);
@@ -1358,10 +1371,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
       tmem_ld_wait(sv);
       __syncwarp();
       if (lane == 0) mbar_arrive(y_empty + 8 * st);  // Y / mask stage read by this warp
-      if (!(a.dbg & 256)) {
+      if (!(NEF_DBG & 256)) {
         if (MM == 1) ew_half<KIND, SPA>(a, sv, yv, mk, cols_here - 16 * cg, row_ok, pb, pl, lsum, cnt);
         else ew_half_sent<KIND, SPA>(a, sv, yv, cols_here - 16 * cg, row_ok, pb, pl, lsum[0], cnt[0]);
-      } else {   // dbg 256: timing experiment without the elementwise math (P_b = S + Y)
+      } else {   // NEF_DBG 256: timing experiment without the elementwise math (P_b = S + Y)
 #pragma unroll
         for (int j = 0; j < 16; ++j) pb[j] = sv[j] + __float_as_uint(yv[j]) + mk[j >> 2];
       }
@@ -1370,7 +1383,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
         tmem_st16(tc + 64, pb);
         if constexpr (SPA) tmem_st16(tmem + 384 + 64 * b + lane_off + 16 * cg, pl);
       }
-      if (a.debug && blockIdx.x == 0 && blockIdx.y == 0 && t == 0) {
+      if (t == 0 && a.debug && blockIdx.x == 0 && blockIdx.y == 0) {   // test hook (nef_debug_dump)
 #pragma unroll
         for (int j = 0; j < 16; ++j) a.debug[m * 64 + 16 * cg + j] = __uint_as_float(sv[j] & 0xffffe000u);
       }
@@ -1466,7 +1479,7 @@ struct TcLauncher {
   int MM;
   template <int KB_, int KIND, int MM_>
   cudaError_t go() const {
-    const size_t smem = smem_bytes(MM_);
+    const size_t smem = smem_bytes(MM_, KB_);
     cudaError_t e = cudaFuncSetAttribute(fused_tc_kernel<KB_, KIND, MM_>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     fused_tc_kernel<KB_, KIND, MM_><<<grid, NTHREADS, smem, s>>>(P);
@@ -1479,10 +1492,13 @@ struct TcLauncher {
   }
 };
 
-size_t smem_bytes(int mm) {
-  const int nv = mm == 1 ? VStages<1>::value : VStages<0>::value;
-  const int ns = mm == 1 ? YStages<1>::value : YStages<0>::value;
-  return 1024 + ns * Y_STAGE + (mm == 1 ? ns * M_STAGE : 0) + nv * V_STAGE_MAX + 256 + 64;
+size_t smem_bytes(int mm, int kb) {
+  const int nv = kb == 32 ? (mm == 1 ? VStages<32, 1>::value : VStages<32, 0>::value)
+                          : (mm == 1 ? VStages<64, 1>::value : VStages<64, 0>::value);
+  const int ns = kb == 32 ? (mm == 1 ? YStages<32, 1>::value : YStages<32, 0>::value)
+                          : (mm == 1 ? YStages<64, 1>::value : YStages<64, 0>::value);
+  const int vst = kb == 32 ? VSt<32>::SIZE : VSt<64>::SIZE;
+  return 1024 + ns * Y_STAGE + (mm == 1 ? ns * M_STAGE : 0) + nv * vst + 512 + 64;
 }
 
 cudaError_t launch(const TcArgs& args, const float* Y, const uint8_t* M, int64_t row_blocks, int64_t chunks,

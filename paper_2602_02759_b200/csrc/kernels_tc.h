@@ -33,7 +33,6 @@ struct TcArgs {
   int mode;                   // 0 update, 1 update + loss, 2 loss only
   float* debug;               // optional debug dump (first tile of CTA (0,0))
   long long* trace;           // optional pipeline timeline of CTA (0,0): [tile][16] clock64 stamps
-  int vt;                     // 1: numerator MMAs read a K-major V^T copy; 0: MN-major view of V
   int vec4;                   // 1: every table has the bond contiguous (boff[k] = k), K % 4 == 0 and
                               //    16-byte aligned rows -> float4 V generation
   // direct V: the 64 columns of every tile are 64 consecutive rows of ONE
@@ -54,13 +53,11 @@ struct TcArgs {
   int absy;                   // MM = 0 on raw unmasked Y: every entry observed, sign bits ignored
                               //   (an observed -0.0 is zero, not the sentinel's "missing")
   int split;                  // MM = 1 with labels 0..3 (R29): train = 1; loss partials per role [3][parts]
-  int drain_tiles;            // N / D drained into a separate split partial every this many tiles
   int64_t n_groups;           // drain groups per chunk: Qpart is [chunks][n_groups][2][n_rows][K]
-  int dbg;                    // diagnostics: 1 prefill N/D with 1 and always accumulate,
-                              // 2 numerator B as K-major, 4 swap LBO/SBO of the MN-major view
+
 };
 
-size_t smem_bytes(int mm);   // mm: 1 = uint8 mask stream, 0 = none / NaN-sentinel Y
+size_t smem_bytes(int mm, int kb);   // mm: 1 = uint8 mask stream, 0 = none / NaN-sentinel Y; kb: 32 | 64
 cudaError_t launch(const TcArgs& args, const float* Y, const uint8_t* M, int64_t row_blocks, int64_t chunks,
                    cudaStream_t s);
 

@@ -18,3 +18,20 @@ def golden():
     import json
     with open(os.path.join(ROOT, "tests", "golden", "paper_values.json")) as f:
         return json.load(f)
+
+
+@pytest.fixture
+def record_err(request):
+    """Record a measured parity error next to its bar: printed, and appended as a JSON line to
+    $NEF_ERR_LOG when set (collected into DESIGN.md's error table)."""
+    import json
+
+    def rec(err, bar, what=""):
+        line = {"test": request.node.nodeid, "what": what, "err": float(err), "bar": float(bar)}
+        print("PARITY %s %s err=%.3e bar=%.1e" % (request.node.nodeid, what, err, bar))
+        path = os.environ.get("NEF_ERR_LOG")
+        if path:
+            with open(path, "a") as f:
+                f.write(json.dumps(line) + "\n")
+        return err
+    return rec

@@ -253,3 +253,61 @@ def test_bond_above_64_last_resort(nef):
     errs = [_rel(g, r) for g, r in zip(F, ref)]
     assert max(errs) <= 2e-4, errs     # two sweeps
     assert _rel(tr, rtr) <= TRACE_RTOL
+
+
+GUARD_CASES = [("ir,jr,kr->ijk", (13, 17, 19), (3,), (1.0, 0.0), 0.1),          # CUDA-core, odd primes
+               ("ir,jr,kr->ijk", (130, 96, 68), (40,), (1.0, -0.5), 0.05),     # tcgen05, row / column tails
+               ("ir,jr,kr->ijk", (96, 104, 44), (32,), (1.0, 0.0), 0.0),       # layout-1 half box out of bounds
+               ("ia,jb,kc,abc->ijk", (64, 72, 40), (8, 8, 8), (1.0, 1.0), 0.1),  # layout 2, split P_a
+               ("ik,jk,tl,dl,kl->ijtd", (32, 48, 24, 40), (20, 10), (0.5, 0.0), 0.0)]
+
+
+@pytest.mark.parametrize("case", GUARD_CASES, ids=lambda c: "x".join(map(str, c[1])))
+def test_no_out_of_bounds_writes(nef, case):
+    """Out-of-bounds write check (compute-sanitizer is closed on this GPU pool): Y, the mask, every
+    factor and the workspace sit inside one allocation between guard bands of a NaN bit pattern;
+    a fit, a split fit, nef_num_den and nef_loss must leave every guard byte, Y and the mask
+    untouched and write only inside the workspace and the factors."""
+    ms, shape, ranks, ab, pm = case
+    Y, init = _problem(ms, shape, ranks, seed=51)
+    M = (np.random.default_rng(52).random(shape) >= pm).astype(np.uint8) if pm > 0 else None
+    plan = nef.Plan(ms, shape, ranks)
+    G = 1 << 16                                               # guard band, bytes (256-aligned)
+    sizes = [Y.nbytes, M.nbytes if M is not None else 0] + [f.nbytes for f in init] + [plan.info["workspace_bytes"]]
+    offs, o = [], G
+    for n in sizes:
+        offs.append(o)
+        o += (n + 255) // 256 * 256 + G
+    buf = torch.full((o // 4,), 0x7fc0dead, dtype=torch.int32, device="cuda")
+    raw = buf.view(torch.uint8)
+
+    def view(i, dtype, shp):
+        n = int(np.prod(shp)) * torch.tensor([], dtype=dtype).element_size()
+        return raw[offs[i]:offs[i] + n].view(dtype).view(shp)
+
+    Yd = view(0, torch.float32, shape)
+    Yd.copy_(torch.from_numpy(Y))
+    Md = None
+    if M is not None:
+        Md = view(1, torch.uint8, shape)
+        Md.copy_(torch.from_numpy(M))
+    F = [view(2 + l, torch.float32, f.shape) for l, f in enumerate(init)]
+    for f, h in zip(F, init):
+        f.copy_(torch.from_numpy(h))
+    plan._ws = view(len(sizes) - 1, torch.uint8, (sizes[-1],))
+    guard = torch.ones(o, dtype=torch.bool, device="cuda")
+    for off, n in zip(offs, sizes):
+        guard[off:off + n] = False
+    before = raw.clone()
+    plan.fit(Yd, Md, ab[0], ab[1], F, 2)
+    for ell in range(len(F)):
+        plan.num_den(ell, Yd, Md, ab[0], ab[1], F)
+    plan.loss(Yd, Md, ab[0], ab[1], F)
+    if M is not None:
+        lab = torch.where(Md != 0, torch.ones_like(Md), torch.full_like(Md, 3))
+        plan.fit_split(Yd, lab.contiguous(), nef.loss_spec("ab", ab[0], ab[1]), F, max_iters=2)
+    torch.cuda.synchronize()
+    assert torch.equal(raw[guard], before[guard]), "guard band written"
+    assert torch.equal(Yd.cpu(), torch.from_numpy(Y))
+    if M is not None:
+        assert torch.equal(Md.cpu(), torch.from_numpy(M))

@@ -46,7 +46,7 @@ def _ab(d, reading):
 
 @pytest.mark.parametrize("reading", ["paper", "literal"])
 @pytest.mark.parametrize("name", sorted(CONFIGS))
-def test_one_sweep_factors(nef, name, reading):
+def test_one_sweep_factors(nef, name, reading, record_err):
     d = generate_numpy(name)
     alpha, beta = _ab(d, reading)
     Y, M, F = _dev(d)
@@ -54,36 +54,46 @@ def test_one_sweep_factors(nef, name, reading):
     tr = plan.fit(Y, M, alpha, beta, F, 1)
     torch.cuda.synchronize()
     ref, rtr = O.fit(d["model"], d["Y"], d["mask"], d["init"], alpha, beta, 1)
-    for ell, (g, r) in enumerate(zip(F, ref)):
-        assert _rel(g.cpu().numpy(), r) <= FACTOR_RTOL, (name, reading, ell, _rel(g.cpu().numpy(), r))
-    assert _rel(tr, rtr) <= TRACE_RTOL
+    errs = [_rel(g.cpu().numpy(), r) for g, r in zip(F, ref)]
+    record_err(max(errs), FACTOR_RTOL, "factors after 1 sweep")
+    assert max(errs) <= FACTOR_RTOL, (name, reading, errs)
+    record_err(_rel(tr, rtr), TRACE_RTOL, "trace")
+    assert _rel(tr, rtr) <= TRACE_RTOL, _rel(tr, rtr)
 
 
 @pytest.mark.parametrize("name,iters", [("c1", 100), ("c2", 12), ("c3", 10), ("c4", 10), ("c5", 10)])
-def test_loss_trajectory(nef, name, iters):
+def test_loss_trajectory(nef, name, iters, record_err):
     d = generate_numpy(name)
     Y, M, F = _dev(d)
     plan = nef.Plan(d["model"], d["shape"], d["ranks"])
     tr = plan.fit(Y, M, d["alpha"], d["beta"], F, iters)
     _, rtr = O.fit(d["model"], d["Y"], d["mask"], d["init"], d["alpha"], d["beta"], iters)
     assert len(tr) == iters + 1
+    record_err(_rel(tr, rtr), TRACE_RTOL, "trajectory %d sweeps" % iters)
     assert _rel(tr, rtr) <= TRACE_RTOL, (name, _rel(tr, rtr))
     # Theorem 2 on the GPU trace, with fp32 slack
     assert all(b <= a * (1 + 1e-5) for a, b in zip(tr, tr[1:]))
 
 
+# A and B at the factor bar (error table): both contract the same TF32-rounded V and
+# S, so their rounding errors are correlated and largely cancel in A / B - measured worst A error
+# 5.6e-5 (c5 small shape, factor j: 9 380-entry slabs) against a worst factor error of 2.2e-5
+NUMDEN_RTOL = 1e-4
+
+
 @pytest.mark.parametrize("name", sorted(CONFIGS))
-def test_num_den_each_factor(nef, name):
+def test_num_den_each_factor(nef, name, record_err):
     d = generate_numpy(name)
     Y, M, F = _dev(d)
     plan = nef.Plan(d["model"], d["shape"], d["ranks"])
+    worst = 0.0
     for ell in range(len(F)):
         num, den = plan.num_den(ell, Y, M, d["alpha"], d["beta"], F)
         A, B = O.numerator_denominator(d["model"], d["Y"], d["mask"], d["init"], ell, d["alpha"], d["beta"])
-        # the factor bar (1e-4): on the TF32 path a lowering whose rows pair the factor's mode with
-        # a contracted one sums as few as ~140 columns per row before the fp64 epilogue (R23, R26)
-        assert _rel(num.cpu().numpy(), A) <= FACTOR_RTOL, (name, ell, _rel(num.cpu().numpy(), A))
-        assert _rel(den.cpu().numpy(), B) <= FACTOR_RTOL, (name, ell, _rel(den.cpu().numpy(), B))
+        ea, eb = _rel(num.cpu().numpy(), A), _rel(den.cpu().numpy(), B)
+        worst = max(worst, ea, eb)
+        assert ea <= NUMDEN_RTOL and eb <= NUMDEN_RTOL, (name, ell, ea, eb)
+    record_err(worst, NUMDEN_RTOL, "numerator / denominator")
 
 
 @pytest.mark.parametrize("name", ["c2", "c3", "c5"])
@@ -154,8 +164,18 @@ def test_deterministic(nef):
     ("iab,jbc,kca->ijk", (9, 10, 11), (2, 3, 2), (0.0, 1.0)),
     ("ir,jr->ij", (300, 257), (33,), (2.0, -1.0)),
     ("i,jr,kr->ijk", (7, 8, 9), (5,), (1.0, 2.0)),
+    # the paper's other families, small and at tcgen05-routable sizes
+    ("ij,jk,ik->ijk", (40, 36, 44), (), (1.0, 0.0)),                       # many-body
+    ("ij,jk,ik->ijk", (96, 80, 64), (), (1.0, -0.5)),
+    ("ia,jb,kc,ar,br,cr->ijk", (30, 28, 26), (4, 5, 3, 6), (1.0, 0.0)),    # LR-Tucker
+    ("ia,jb,kc,ar,br,cr->ijk", (96, 80, 64), (12, 10, 8, 6), (1.0, 1.0)),
+    ("ia,jab,kb->ijk", (33, 30, 28), (4, 5), (1.0, 0.0)),                  # tensor train
+    ("ia,jab,kbc,lc->ijkl", (24, 20, 16, 28), (3, 4, 5), (0.5, 0.0)),
+    ("ia,jab,kb->ijk", (96, 80, 64), (8, 8), (1.0, -0.5)),
+    ("ir,jkr->ijk", (40, 32, 36), (6,), (1.0, 0.0)),                       # custom
+    ("ia,jb,kb,ab->ijk", (30, 26, 22), (3, 4), (1.0, 0.0)),
 ])
-def test_other_models(nef, ms, shape, ranks, ab):
+def test_other_models(nef, ms, shape, ranks, ab, record_err):
     rng = np.random.default_rng(3)
     truth = [rng.gamma(1.0, 1.0, s) for s in O.factor_shapes(ms, shape, ranks)]
     Y = rng.poisson(O.contract(ms, truth)).astype(np.float32) + 0.25
@@ -165,9 +185,11 @@ def test_other_models(nef, ms, shape, ranks, ab):
     F = [torch.from_numpy(f).cuda() for f in init]
     tr = plan.fit(torch.from_numpy(Y).cuda(), torch.from_numpy(M).cuda(), ab[0], ab[1], F, 1)
     ref, rtr = O.fit(ms, Y, M, init, ab[0], ab[1], 1)
-    for g, r in zip(F, ref):
-        assert _rel(g.cpu().numpy(), r) <= FACTOR_RTOL
-    assert _rel(tr, rtr) <= TRACE_RTOL
+    errs = [_rel(g.cpu().numpy(), r) for g, r in zip(F, ref)]
+    record_err(max(errs), FACTOR_RTOL, "%s factors after 1 sweep (tc %s)" % (
+        ms, [L["tc"] for L in plan.describe()["lowerings"]]))
+    assert max(errs) <= FACTOR_RTOL, errs
+    assert _rel(tr, rtr) <= TRACE_RTOL, _rel(tr, rtr)
 
 
 def test_iters_zero_and_errors(nef):
@@ -198,3 +220,22 @@ def test_host_entry_point(nef):
     assert _rel(tr, rtr) <= TRACE_RTOL
     for g, r in zip(Fh, ref):
         assert _rel(g.numpy(), r) <= 5e-4
+
+
+# BASELINE.json iteration counts on shapes the planner routes entirely to the tcgen05 kernel
+# (every factor update, incl. the Tucker core and c4's kl): c2 50 sweeps, c3 / c4 20, c5 10
+TC_TRAJ = [("c2", (80, 72, 64), 50), ("c3", (160, 144, 96), 20), ("c4", (32, 48, 24, 40), 20),
+           ("c5", (144, 96, 80), 10)]
+
+
+@pytest.mark.parametrize("name,shape,iters", TC_TRAJ, ids=[c[0] for c in TC_TRAJ])
+def test_loss_trajectory_tcgen05(nef, name, shape, iters, record_err):
+    d = generate_numpy(name, shape=shape)
+    Y, M, F = _dev(d)
+    plan = nef.Plan(d["model"], d["shape"], d["ranks"])
+    assert all(L["tc"] for L in plan.describe()["lowerings"]), name
+    tr = plan.fit(Y, M, d["alpha"], d["beta"], F, iters)
+    ref, rtr = O.fit(d["model"], d["Y"], d["mask"], d["init"], d["alpha"], d["beta"], iters)
+    record_err(_rel(tr, rtr), TRACE_RTOL, "tcgen05 trajectory %d sweeps" % iters)
+    assert _rel(tr, rtr) <= TRACE_RTOL, (name, _rel(tr, rtr))
+    assert all(b <= a * (1 + 1e-5) for a, b in zip(tr, tr[1:]))

@@ -43,7 +43,7 @@ def _rel(a, b):
 
 
 def _slice(t, axis, b, n):
-    return t.narrow(axis, b, n).contiguous()
+    return t.narrow(axis, b, n).clone()   # own allocation: the ABI wants 16-byte aligned Y
 
 
 # (config, shape): c5 / c3 (tcgen05, masked), c2 (Tucker with the core, tcgen05), c4 (5 factors,
