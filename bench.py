@@ -104,30 +104,54 @@ def oracle_sample(name, target_s=12.0):
     cfg = CONFIGS[name]
     row = math.prod(cfg.shape[1:])
 
-    def run(s):
+    def run(s, reps=1):
         d = generate_numpy(name, shape=(s,) + tuple(cfg.shape[1:]))
         th = [f.astype(np.float64) for f in d["init"]]
-        t0 = time.perf_counter()
-        for ell in range(len(th)):
-            th[ell] = O.update_factor(d["model"], d["Y"], d["mask"], th, ell, d["alpha"], d["beta"])
-        O.loss(d["model"], d["Y"], d["mask"], th, d["alpha"], d["beta"])
-        return time.perf_counter() - t0
+        c0, t0 = os.times(), time.perf_counter()
+        for _ in range(reps):
+            for ell in range(len(th)):
+                th[ell] = O.update_factor(d["model"], d["Y"], d["mask"], th, ell, d["alpha"], d["beta"])
+            O.loss(d["model"], d["Y"], d["mask"], th, d["alpha"], d["beta"])
+        t, c1 = time.perf_counter() - t0, os.times()
+        return t / reps, (c1.user - c0.user) + (c1.system - c0.system), t
 
     s = 1 if row > 200000 else max(1, min(cfg.shape[0], 200000 // row))
-    t = run(s)
+    t, cpu, t_total = run(s)
+    # grow the sample to ~target_s: more mode-0 rows, then (whole tensor) repeated sweeps
     s2 = int(max(1, min(cfg.shape[0], s * target_s / max(t, 1e-3))))
-    if s2 > s:
-        s, t = s2, run(s2)
-    try:
-        from threadpoolctl import threadpool_info
-        cores = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
-    except Exception:
-        cores = 1
+    reps = max(1, int(target_s / max(t * s2 / s, 1e-3))) if s2 == cfg.shape[0] else 1
+    if s2 > s or reps > 1:
+        s = s2
+        t, cpu, t_total = run(s, reps)
+    # threads actually used: process CPU time over wall time of the timed run (numpy's elementwise
+    # work is single-threaded; its einsum contractions may use the BLAS pool)
     n = s * row
-    return {"value": n / t, "unit": UNIT, "cores": int(cores), "kind": "oracle",
-            "sample": "%s first %d of %d mode-0 rows (%d entries, %s), 1 sweep + 1 loss, %.2f s" % (
-                name, s, cfg.shape[0], n, "x".join(map(str, (s,) + tuple(cfg.shape[1:]))), t),
+    return {"value": n / t, "unit": UNIT, "cores": round(cpu / max(t_total, 1e-9), 2), "kind": "oracle",
+            "cores_available": len(os.sched_getaffinity(0)),
+            "sample": "%s first %d of %d mode-0 rows (%d entries, %s), %d x (1 sweep + 1 loss), %.2f s" % (
+                name, s, cfg.shape[0], n, "x".join(map(str, (s,) + tuple(cfg.shape[1:]))), reps, t_total),
             "seconds": t, "entries": n}, s
+
+
+def host_info():
+    info = {"cores_available": len(os.sched_getaffinity(0))}
+    try:
+        for line in open("/proc/meminfo"):
+            if line.startswith("MemTotal"):
+                info["ram_gb"] = round(int(line.split()[1]) / 1048576, 1)
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                info["cpu"] = line.split(":", 1)[1].strip()
+                break
+    except OSError:
+        pass
+    return info
+
+
+PRECISION = ("f32 data and factors; tcgen05 kind::tf32 MMAs (reconstruction with the updated factor's side "
+             "split hi + lo, numerator / denominator operands TF32 round-to-nearest, Euclidean bond <= 32: "
+             "numerator operand split hi + lo); fp32 tensor-core accumulation drained every 256 tiles; fp64 "
+             "split-partial, loss and update arithmetic")
 
 
 def run_reference(args):
@@ -159,7 +183,7 @@ def run_reference(args):
     out = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": args.gpus,
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t, "higher_is_better": True,
            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-           "config": dict(_workload(cfg), sample_rows=s),
+           "config": dict(_workload(cfg), sample_rows=s), "host": host_info(),
            "cpu_baseline": {"value": v, "unit": UNIT, "cores": base["cores"], "kind": "oracle",
                             "sample": base["sample"].split(", 1 sweep")[0] + ", each step 1 sweep + 1 loss"},
            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -288,7 +312,8 @@ def main():
     if rank == 0:
         out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
-               "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+               "scaling": "strong", "vs_baseline": None, "dtype": "f32/tf32", "precision": PRECISION,
+               "data": "synthetic", "host": host_info(),
                "config": dict(_workload(cfg), parallelism=("shard mode %d over %d ranks, NCCL all-reduce of partials"
                                                            % (sm, world)) if world > 1 else "single GPU",
                               l2="inputs (%.1f GB) larger than L2 (126 MB); no flush needed" % (

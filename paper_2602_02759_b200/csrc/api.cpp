@@ -37,6 +37,7 @@ float* g_debug = nullptr;   // optional device dump of the tcgen05 kernel's firs
 long long* g_trace = nullptr;   // optional pipeline timeline of the tcgen05 kernel (diagnostics)
 bool g_no_sentinel = std::getenv("NEF_NO_SENTINEL") != nullptr;   // diagnostics: stream the uint8 mask
 bool g_no_lconst = std::getenv("NEF_NO_LCONST") != nullptr;     // diagnostics: loss passes compute the whole divergence (R25 off)
+bool g_no_sqy = std::getenv("NEF_NO_SQY") != nullptr;           // diagnostics: (0.5, 0) streams y, not sqrt(y)
 // diagnostics: NEF_TC_VDIRECT=0 generates V per tile instead of TMA-loading direct-V table rows
 bool g_vdirect = [] { const char* e = std::getenv("NEF_TC_VDIRECT"); return !e || std::atoi(e) != 0; }();
 
@@ -127,6 +128,7 @@ struct Ctx {
   const double* loff = nullptr;   // R25: [data-only loss sum][observed count] of the sentinel pass
   double lscale = 1.0;            //      loss = lscale * (streamed part) + loff[0]
   const float* aux = nullptr;     // per-entry phi / n (App. B losses), Y's layout; CUDA-core kernel only
+  bool sqy = false;               // ysent holds sqrt(y) for the (0.5, 0) pair (R35), masked or not
   int split = 0;                  // the mask holds labels 0..3 (R29); loss slots are [3] per pass
   // split fits: after the loss-carrying pass, copy the loss slots to pinned host memory and
   // record an event, so the host can take the stopping decision while the sweep continues
@@ -235,11 +237,13 @@ int stream_pass(const Ctx& c, const nef::Lowering& L, const float* Y, const uint
   const double bytes = (double)c.p->n_local * ((M ? 5.0 : 4.0) + (c.aux ? 4.0 : 0.0));
   // split fits: the loss-carrying passes stream Y with the labels (train / validation / heldout
   // losses of one pass); update-only passes stream the train-folded sentinel copy
-  const bool sent = M && c.ysent && !(c.split && mode != 0);
+  const bool sent = c.ysent && (M || c.sqy) && !(c.split && mode != 0);
+  nef::DivParams dvk = dv;
   if (use_tc(L, M, sent, c.aux)) {
     if (sent) {   // stream the NaN-sentinel copy: no mask stream (4 B / entry)
       Y = c.ysent;
       M = nullptr;
+      if (c.sqy) dvk.kind = nef::EW_A05_B0_SQ;   // the copy holds sqrt(y) (R35)
     }
     nef::tc::TcArgs t{};
     t.layout = L.tc_layout;
@@ -301,7 +305,7 @@ int stream_pass(const Ctx& c, const nef::Lowering& L, const float* Y, const uint
     t.losspart = reinterpret_cast<double*>(c.ws + L.ws_tc_losspart);
     o.nparts = L.tc_row_blocks * chunks;
     t.countpart = reinterpret_cast<long long*>(c.ws + L.ws_tc_losspart + 3 * o.nparts * 8);
-    t.dv = dv;
+    t.dv = dvk;
     t.mode = mode;
     t.split = (c.split && M && !sent) ? 1 : 0;
     t.lconst = ((sent || !M) && c.loff && mode != 0) ? 1 : 0;
@@ -649,11 +653,14 @@ int nef_fit_ex(nef_plan_t plan, const float* Y, const uint8_t* mask, const nef_l
   long long* dcpart = reinterpret_cast<long long*>(dpart + nef::kSentParts);
   bool any_tc = false;
   for (const auto& L : p.low) any_tc |= L.tc_ok;
-  if (mask && g_policy == 0 && !g_no_sentinel && !sp.aux) {
+  // R35: the (0.5, 0) pair needs the data only as sqrt(y) (a = y^(1/2) yhat^-1, the loss split of
+  // R25): the once-per-fit copy holds sqrt(y), masked or not, and the passes save one MUFU per entry
+  c.sqy = dv.kind == nef::EW_A05_B0 && any_tc && g_policy == 0 && !g_no_sentinel && !sp.aux && !g_no_sqy;
+  if ((mask || c.sqy) && g_policy == 0 && !g_no_sentinel && !sp.aux) {
     if (any_tc) {
       float* ys = reinterpret_cast<float*>(c.ws + p.ws_sent);
       CK(nef::launch_sentinel(Y, mask, ys, p.n_local, dterm, dpart, dcpart, dslot,
-                              reinterpret_cast<long long*>(dslot + 1), c.s));
+                              reinterpret_cast<long long*>(dslot + 1), c.s, 0, c.sqy ? 1 : 0));
       g_launches += 3;
       c.ysent = ys;
       if (dterm) {

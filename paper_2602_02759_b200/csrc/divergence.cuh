@@ -368,6 +368,32 @@ struct Ew<EW_A05_B1> {  // (0.5, 1): a = sqrt(x), b = sqrt(y)
   }
 };
 
+// (0.5, 0) with s = sqrt(x) streamed instead of x (R35: a = x^alpha y^(beta-1) needs x only through
+// x^alpha): a = s / y, b = y^-1/2, one MUFU per entry instead of two
+template <>
+struct Ew<EW_A05_B0_SQ> {
+  static constexpr bool kLinX = true;    // a = s * (positive): carries the sentinel's sign
+  static constexpr bool kSignedA = false;
+  static __device__ __forceinline__ void ab(float s, float yh, const DivParams&, float& av, float& bv) {
+    const float r = frsqrt(yh);
+    bv = r;
+    av = s * r * r;
+  }
+  static __device__ __forceinline__ void ab2(float2 s, float2 yh, const DivParams&, float2& av, float2& bv) {
+    const float2 r = make_float2(frsqrt(yh.x), frsqrt(yh.y));
+    bv = r;
+    av = __fmul2_rn(s, __fmul2_rn(r, r));
+  }
+  static __device__ __forceinline__ float loss(float s, float yh, const DivParams& d) {
+    return Ew<EW_A05_B0>::loss(s * s, yh, d);
+  }
+  static __device__ __forceinline__ void abl2(float2 s, float2 yh, const DivParams& d, float2& av, float2& bv,
+                                              float2& l) {
+    ab2(s, yh, d, av, bv);
+    l = make_float2(loss(s.x, yh.x, d), loss(s.y, yh.y, d));
+  }
+};
+
 // ---- App. B losses; y = max(yhat, 1e-30) is the model (odds for Bernoulli / binomial)
 __device__ __forceinline__ float xlogy0(float x, float ly) { return x > 0.f ? x * ly : 0.f; }   // 0 log y = 0 (R8)
 
@@ -539,6 +565,19 @@ struct LossOff<EW_A05_B0> {
   }
 };
 
+template <>
+struct LossOff<EW_A05_B0_SQ> {   // the (0.5, 0) split with s = sqrt(x) streamed
+  static constexpr bool value = true;
+  static __device__ __forceinline__ void abr2(float2 s, float2 yh, float2& av, float2& bv, float2& rem) {
+    const float2 r = make_float2(frsqrt(yh.x), frsqrt(yh.y));
+    bv = r;
+    av = __fmul2_rn(s, __fmul2_rn(r, r));   // signed like s (the sentinel's -1 at missing entries)
+    const float2 sy = __fmul2_rn(yh, r);
+    const float2 sa = make_float2(fabsf(s.x), fabsf(s.y));
+    rem = __ffma2_rn(__fmul2_rn(sa, make_float2(-0.5f, -0.5f)), make_float2(flog(yh.x), flog(yh.y)), sy);   // scale 4
+  }
+};
+
 // dispatch helper: calls f.template operator()<KIND>() for the pair's kind
 template <typename F>
 inline cudaError_t dispatch_ew(int kind, F&& f) {
@@ -554,6 +593,7 @@ inline cudaError_t dispatch_ew(int kind, F&& f) {
     case EW_BERN: return f.template operator()<EW_BERN>();
     case EW_BINOM: return f.template operator()<EW_BINOM>();
     case EW_JS: return f.template operator()<EW_JS>();
+    case EW_A05_B0_SQ: return f.template operator()<EW_A05_B0_SQ>();
     default: return f.template operator()<EW_GENERIC>();
   }
 }

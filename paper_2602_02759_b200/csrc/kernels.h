@@ -17,7 +17,9 @@ int pow_code(double p);
 enum EwKind : int { EW_GENERIC = 0, EW_KL, EW_EUC, EW_B_M05, EW_A05_B0, EW_B05, EW_B2, EW_A05_B1,
                     // App. B losses: negative binomial (scalar phi, or per-entry phi streamed
                     // as aux), Bernoulli odds, binomial odds (scalar n, or per-entry n as aux), Jensen-Shannon
-                    EW_NB, EW_BERN, EW_BINOM, EW_JS };
+                    EW_NB, EW_BERN, EW_BINOM, EW_JS,
+                    // (0.5, 0) streaming sqrt(Y) (nef_fit's once-per-fit copy, R35): Y^alpha precomputed
+                    EW_A05_B0_SQ };
 int ew_kind(double alpha, double beta);
 
 // loss families (include/nef.h nef_loss_kind)
@@ -76,7 +78,10 @@ constexpr int kSentBlocks = 148 * 16;
 cudaError_t launch_dterm(const float* Y, int64_t n, int dterm, double* dpart, long long* dcpart, double* dslot,
                          long long* dcslot, cudaStream_t s);
 cudaError_t launch_sentinel(const float* Y, const uint8_t* M, float* out, int64_t n, int dterm, double* dpart,
-                            long long* dcpart, double* dslot, long long* dcslot, cudaStream_t s, int split = 0);
+                            long long* dcpart, double* dslot, long long* dcslot, cudaStream_t s, int split = 0,
+                            int sqrt_y = 0);
+// sqrt_y (R35): the copy holds sqrt(y) at observed entries (-1 at missing ones); M may be null (all
+// observed).  The data-only loss sum and the observed count still come from y itself.
 
 // dst[r][0..Kp) = src[r][0..K) padded with zeros (16-byte row pitch for TMA)
 cudaError_t launch_pad_rows(const float* src, float* dst, int64_t rows, int64_t K, int64_t Kp, cudaStream_t s);

@@ -472,7 +472,82 @@ __global__ void einstep_kernel(const __grid_constant__ EinStepDev st, const floa
   }
 }
 
+// Fast path for the common step shape: ONE summed index of at most 64 terms and at most three
+// output indices (the side operands and epilogues of CP / Tucker / the paper's custom models,
+// e.g. T[j,k,a] = sum_c C[k,c] T1[j,a,c]): one thread per output, the output index decomposed
+// with two 32-bit divisions, the sum unrolled into four independent fp32 partial sums (<= 64
+// terms: relative error ~ 1e-7, the result feeds TF32 MMAs or an fp32 factor), combined in fp64.
+// The generic kernel above issued ~300 instructions per output of 16 terms (odometer per term,
+// fp64 conversions): ~3x this path's count (ncu: 33 us at IPC 3.2 for 1 M outputs on c2).
+struct EinStep1Dev {
+  int nout;
+  int odim[3], as_o[3], bs_o[3];
+  int S, as, bs;
+  int out_size;
+};
+template <bool HASB>
+__global__ void einstep1_kernel(const __grid_constant__ EinStep1Dev st, const float* __restrict__ A,
+                                const float* __restrict__ B, float* __restrict__ C) {
+  for (int o = blockIdx.x * blockDim.x + threadIdx.x; o < st.out_size; o += gridDim.x * blockDim.x) {
+    int ao = 0, bo = 0, rem = o;
+#pragma unroll
+    for (int d = 2; d >= 0; --d) {
+      if (d >= st.nout) continue;
+      const int n = st.odim[d];
+      const int q = d > 0 ? rem / n : 0;
+      const int i = rem - q * n;
+      rem = q;
+      ao += i * st.as_o[d];
+      bo += i * st.bs_o[d];
+    }
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    int s = 0;
+    for (; s + 4 <= st.S; s += 4) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const float a = __ldg(A + ao + (s + u) * st.as);
+        acc[u] = HASB ? fmaf(a, __ldg(B + bo + (s + u) * st.bs), acc[u]) : acc[u] + a;
+      }
+    }
+    for (; s < st.S; ++s) {
+      const float a = __ldg(A + ao + s * st.as);
+      acc[0] = HASB ? fmaf(a, __ldg(B + bo + s * st.bs), acc[0]) : acc[0] + a;
+    }
+    C[o] = (float)(((double)acc[0] + (double)acc[1]) + ((double)acc[2] + (double)acc[3]));
+  }
+}
+
 cudaError_t launch_einstep(const EinStep& st, const float* A, const float* B, float* C, cudaStream_t s) {
+  static const bool no_fast = std::getenv("NEF_EINSTEP_GENERIC") != nullptr;   // diagnostics
+  {
+    // fast path eligibility: one summed index (<= 64 terms), <= 3 output indices, 32-bit offsets
+    bool ok = !no_fast && st.nsum == 1 && st.sum_size <= 64 && st.nout <= 3 && st.out_size < (1ll << 30);
+    long long span_a = (st.sdim[0] - 1) * st.as_s[0], span_b = (st.sdim[0] - 1) * st.bs_s[0];
+    for (int k = 0; k < st.nout; ++k) {
+      span_a += (st.odim[k] - 1) * st.as_o[k];
+      span_b += (st.odim[k] - 1) * st.bs_o[k];
+    }
+    ok = ok && span_a < (1ll << 30) && span_b < (1ll << 30);
+    if (ok) {
+      EinStep1Dev d{};
+      d.nout = st.nout;
+      for (int k = 0; k < st.nout; ++k) {
+        d.odim[k] = (int)st.odim[k];
+        d.as_o[k] = (int)st.as_o[k];
+        d.bs_o[k] = (int)st.bs_o[k];
+      }
+      d.S = (int)st.sdim[0];
+      d.as = (int)st.as_s[0];
+      d.bs = (int)st.bs_s[0];
+      d.out_size = (int)st.out_size;
+      long long blocks = (st.out_size + 255) / 256;
+      if (blocks > 148 * 32) blocks = 148 * 32;
+      if (blocks < 1) blocks = 1;
+      if (B) einstep1_kernel<true><<<(unsigned)blocks, 256, 0, s>>>(d, A, B, C);
+      else einstep1_kernel<false><<<(unsigned)blocks, 256, 0, s>>>(d, A, B, C);
+      return cudaGetLastError();
+    }
+  }
   EinStepDev d{};
   d.nout = st.nout;
   d.nsum = st.nsum;
@@ -557,11 +632,11 @@ __global__ void dterm_kernel(const float* __restrict__ Y, long long n4, long lon
 // fully coalesced across the warp
 // split (R29): M holds labels and only train entries (label 1) count as observed
 __global__ void sentinel_kernel(const float* __restrict__ Y, const uint8_t* __restrict__ M, float* __restrict__ out,
-                                long long n4, int dterm, double* dpart, long long* dcpart, int split) {
+                                long long n4, int dterm, double* dpart, long long* dcpart, int split, int sqy) {
   double acc = 0.0;
   long long cnt = 0;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4; i += (long long)gridDim.x * blockDim.x) {
-    const uint32_t w0 = __ldcs(reinterpret_cast<const unsigned int*>(M) + i);
+    const uint32_t w0 = M ? __ldcs(reinterpret_cast<const unsigned int*>(M) + i) : 0x01010101u;
     const uint32_t w = split ? __vcmpeq4(w0, 0x01010101u) : w0;
     float4 y = __ldcs(reinterpret_cast<const float4*>(Y) + i);
     if (dpart) {
@@ -572,6 +647,9 @@ __global__ void sentinel_kernel(const float* __restrict__ Y, const uint8_t* __re
         if (w & 0xff0000u) acc += dterm_c(dterm, y.z);
         if (w & 0xff000000u) acc += dterm_c(dterm, y.w);
       }
+    }
+    if (sqy) {   // R35: sqrt(y) streamed for (0.5, 0); |y| so that an observed -0 is +0
+      y.x = sqrtf(fabsf(y.x)); y.y = sqrtf(fabsf(y.y)); y.z = sqrtf(fabsf(y.z)); y.w = sqrtf(fabsf(y.w));
     }
     // observed: + 0 turns -0 into +0 (the kernel reads the sign); missing: -1
     y.x = (w & 0xffu) ? y.x + 0.f : -1.f;
@@ -584,13 +662,13 @@ __global__ void sentinel_kernel(const float* __restrict__ Y, const uint8_t* __re
 }
 __global__ void sentinel_tail_kernel(const float* __restrict__ Y, const uint8_t* __restrict__ M, float* __restrict__ out,
                                      long long from, long long n, int dterm, double* dpart, long long* dcpart, int slot,
-                                     int split) {
+                                     int split, int sqy) {
   double acc = 0.0;
   long long cnt = 0;
   for (long long i = from + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-    const bool o = split ? M[i] == 1 : M[i] != 0;
+    const bool o = !M || (split ? M[i] == 1 : M[i] != 0);
     if (o) { ++cnt; acc += dterm_c(dterm, Y[i]); }
-    out[i] = o ? Y[i] + 0.f : -1.f;
+    out[i] = o ? (sqy ? sqrtf(fabsf(Y[i])) : Y[i] + 0.f) : -1.f;
   }
   if (dpart) sent_block_sum(acc, cnt, dpart, dcpart, slot + blockIdx.x);
 }
@@ -680,7 +758,8 @@ __global__ void reduce_update8_kernel(const float* __restrict__ part, float* __r
     double A = 0.0, B = 0.0;
 #pragma unroll
     for (int k = 0; k < 8; ++k) { A += ra[k][l]; B += rb[k][l]; }
-    th[e] = mu_update(th[e], A, B, u);
+    // A and B rounded to fp32 as reduce_q stores them: bit-identical to reduce_q + update
+    th[e] = mu_update(th[e], (double)(float)A, (double)(float)B, u);
   }
 }
 __global__ void reduce_update_kernel(const float* __restrict__ part, float* __restrict__ th, long long n_chunks,
@@ -691,7 +770,7 @@ __global__ void reduce_update_kernel(const float* __restrict__ part, float* __re
       A += (double)part[c * 2 * n + e];
       B += (double)part[c * 2 * n + n + e];
     }
-    th[e] = mu_update(th[e], A, B, u);
+    th[e] = mu_update(th[e], (double)(float)A, (double)(float)B, u);
   }
 }
 
@@ -775,16 +854,17 @@ cudaError_t launch_dterm(const float* Y, int64_t n, int dterm, double* dpart, lo
 }
 
 cudaError_t launch_sentinel(const float* Y, const uint8_t* M, float* out, int64_t n, int dterm, double* dpart,
-                            long long* dcpart, double* dslot, long long* dcslot, cudaStream_t s, int split) {
+                            long long* dcpart, double* dslot, long long* dcslot, cudaStream_t s, int split,
+                            int sqy) {
   const bool vec = (((reinterpret_cast<uintptr_t>(Y) | reinterpret_cast<uintptr_t>(out)) & 15) | (reinterpret_cast<uintptr_t>(M) & 3)) == 0;
   const long long n4 = vec ? n / 4 : 0;
   // every one of the kSentBlocks + 1 partials is written (fixed grids), then summed in fixed order
   if (vec) {
-    sentinel_kernel<<<kSentBlocks, 256, 0, s>>>(Y, M, out, n4, dterm, dpart, dcpart, split);
-    sentinel_tail_kernel<<<1, 256, 0, s>>>(Y, M, out, n4 * 4, n, dterm, dpart, dcpart, kSentBlocks, split);
+    sentinel_kernel<<<kSentBlocks, 256, 0, s>>>(Y, M, out, n4, dterm, dpart, dcpart, split, sqy);
+    sentinel_tail_kernel<<<1, 256, 0, s>>>(Y, M, out, n4 * 4, n, dterm, dpart, dcpart, kSentBlocks, split, sqy);
   } else {
-    sentinel_tail_kernel<<<kSentBlocks, 256, 0, s>>>(Y, M, out, 0, n, dterm, dpart, dcpart, 0, split);
-    sentinel_tail_kernel<<<1, 256, 0, s>>>(Y, M, out, n, n, dterm, dpart, dcpart, kSentBlocks, split);
+    sentinel_tail_kernel<<<kSentBlocks, 256, 0, s>>>(Y, M, out, 0, n, dterm, dpart, dcpart, 0, split, sqy);
+    sentinel_tail_kernel<<<1, 256, 0, s>>>(Y, M, out, n, n, dterm, dpart, dcpart, kSentBlocks, split, sqy);
   }
   if (dpart) loss_reduce_kernel<<<1, 256, 0, s>>>(dpart, dcpart, kSentBlocks + 1, dslot, dcslot, 1.0, nullptr);
   return cudaGetLastError();

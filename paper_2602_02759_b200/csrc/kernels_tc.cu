@@ -773,6 +773,15 @@ __device__ __forceinline__ void ew_half(const TcArgs& a, uint32_t (&sv)[16], con
   }
 }
 
+// P_b bits of one entry in the sentinel path: b > 0 at an observed entry takes the sign of x by a
+// copysign, and the add-then-max rounds it (TF32 RN) and zeroes a missing entry; b == 1 kinds
+// (KL, Jensen-Shannon: exact in TF32) are one compare-and-set
+template <int KIND>
+__device__ __forceinline__ uint32_t pb_sent(float bv, float x) {
+  if constexpr (KIND == EW_KL || KIND == EW_JS) return x >= 0.f ? 0x3f800000u : 0u;
+  else return (uint32_t)__viaddmax_s32(__float_as_int(copysignf(bv, x)), 0x1000, 0);
+}
+
 // P_a bits of one entry in the sentinel path: a >= 0 kinds clamp (a carries the sign of x, so the
 // add-then-max both rounds and zeroes a missing entry); signed-a kinds (log forms) select on x.
 template <int KIND>
@@ -801,7 +810,7 @@ __device__ __forceinline__ void put_pa_sent(uint32_t (&sv)[16], uint32_t (&pl)[1
 // turned into -1 first.
 template <int KIND, bool SPA>
 __device__ __forceinline__ void ew_half_sent(const TcArgs& a, uint32_t (&sv)[16], float (&yv)[16], int cv, bool row_ok,
-                                             uint32_t (&pb)[16], uint32_t (&pl)[16], float& lsum, long long& cnt) {
+                                             uint32_t (&pb)[16], uint32_t (&pl)[16], double& lacc, long long& cnt) {
   if (a.absy) {   // raw unmasked Y (uniform branch): an observed -0.0 must not read as missing
 #pragma unroll
     for (int j = 0; j < 16; ++j) yv[j] = fabsf(yv[j]);
@@ -823,10 +832,10 @@ __device__ __forceinline__ void ew_half_sent(const TcArgs& a, uint32_t (&sv)[16]
         l2 = __fadd2_rn(l2, make_float2(x.x >= 0.f ? rv.x : 0.f, x.y >= 0.f ? rv.y : 0.f));
         sv[j] = (uint32_t)__viaddmax_s32(__float_as_int(av.x), (int)pa_round<KIND>(j), 0);
         sv[j + 1] = (uint32_t)__viaddmax_s32(__float_as_int(av.y), (int)pa_round<KIND>(j + 1), 0);
-        pb[j] = (uint32_t)__viaddmax_s32(__float_as_int(copysignf(bv.x, x.x)), 0x1000, 0);
-        pb[j + 1] = (uint32_t)__viaddmax_s32(__float_as_int(copysignf(bv.y, x.y)), 0x1000, 0);
+        pb[j] = pb_sent<KIND>(bv.x, x.x);
+        pb[j + 1] = pb_sent<KIND>(bv.y, x.y);
       }
-      lsum += l2.x + l2.y;
+      lacc += (double)(l2.x + l2.y);   // (inside the uniform loss branch: nothing in update passes)
       return;
     }
   }
@@ -853,10 +862,10 @@ __device__ __forceinline__ void ew_half_sent(const TcArgs& a, uint32_t (&sv)[16]
         sv[j] = (uint32_t)__viaddmax_s32(__float_as_int(copysignf(av.x, x.x)), (int)pa_round<KIND>(j), 0);
         sv[j + 1] = (uint32_t)__viaddmax_s32(__float_as_int(copysignf(av.y, x.y)), (int)pa_round<KIND>(j + 1), 0);
       }
-      pb[j] = (uint32_t)__viaddmax_s32(__float_as_int(copysignf(bv.x, x.x)), 0x1000, 0);
-      pb[j + 1] = (uint32_t)__viaddmax_s32(__float_as_int(copysignf(bv.y, x.y)), 0x1000, 0);
+      pb[j] = pb_sent<KIND>(bv.x, x.x);
+      pb[j + 1] = pb_sent<KIND>(bv.y, x.y);
     }
-    lsum += l2.x + l2.y;
+    lacc += (double)(l2.x + l2.y);
     return;
   }
 #pragma unroll
@@ -871,8 +880,8 @@ __device__ __forceinline__ void ew_half_sent(const TcArgs& a, uint32_t (&sv)[16]
     }
     put_pa_sent<KIND, SPA>(sv, pl, j, av.x, x.x);
     put_pa_sent<KIND, SPA>(sv, pl, j + 1, av.y, x.y);
-    pb[j] = (uint32_t)__viaddmax_s32(__float_as_int(copysignf(bv.x, x.x)), 0x1000, 0);
-    pb[j + 1] = (uint32_t)__viaddmax_s32(__float_as_int(copysignf(bv.y, x.y)), 0x1000, 0);
+    pb[j] = pb_sent<KIND>(bv.x, x.x);
+    pb[j + 1] = pb_sent<KIND>(bv.y, x.y);
   }
 }
 
@@ -991,6 +1000,12 @@ __device__ __forceinline__ void trace_ev(const TcArgs& a, int t, int e) {
 #endif
 }
 
+#ifndef NEF_NBUF3
+#define NEF_NBUF3 1   // bond <= 32: three TMEM tile buffers (0: two, as for bond 64)
+#endif
+// TMEM column of tile buffer b: 0 and 128, the third (bond <= 32 only) at 384
+__device__ __forceinline__ uint32_t buf_col(int b) { return b == 2 ? 384u : 128u * (uint32_t)b; }
+
 // ------------------------------------------------------------------ the kernel
 // TMEM (512 columns x 128 lanes): two tile buffers of 128 columns, each holding S in its first
 // 64 columns; the elementwise warps overwrite S in place with P_a and put P_b in the other 64
@@ -1007,6 +1022,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
   constexpr int V_STAGE = VSt<KB>::SIZE;
   // Euclidean pair with bond <= 32: numerator operand split hi + lo (put_pa), TMEM 384..511 free
   constexpr bool SPA = (KIND == EW_EUC && KB == 32 && !NEF_PA_RN);
+  // TMEM tile buffers: bond <= 32 leaves columns 384..511 free - a third buffer (S(t+3) queued
+  // behind the N/D MMAs of tile t, so the elementwise stage of t+1 and t+2 overlap them) unless
+  // the split P_a uses them
+  constexpr int NBUF = (KB == 32 && MM == 0 && !SPA && NEF_NBUF3) ? 3 : 2;
   extern __shared__ unsigned char smraw[];
   const TcArgs& a = P.a;
   const int tid = threadIdx.x;
@@ -1023,10 +1042,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
   const uint32_t sBar = sV + NV * V_STAGE;
   const uint32_t y_full = sBar, y_empty = y_full + 8 * NS;
   const uint32_t v_full = y_empty + 8 * NS, v_empty = v_full + 8 * NV;
-  const uint32_t s_full = v_empty + 8 * NV;                  // [2] S(t) in buffer t & 1 (MMA commit)
-  const uint32_t p_full = s_full + 16;                       // [2] P(t) written (8 elementwise warps)
-  const uint32_t buf_free = p_full + 16;                     // [2] N,D MMAs of tile t retired (commit)
-  const uint32_t nd_full = buf_free + 16, u_ready = nd_full + 8;
+  const uint32_t s_full = v_empty + 8 * NV;                  // [NBUF] S(t) in buffer t % NBUF (MMA commit)
+  const uint32_t p_full = s_full + 8 * NBUF;                 // [NBUF] P(t) written (16 elementwise warps)
+  const uint32_t buf_free = p_full + 8 * NBUF;               // [NBUF] N,D MMAs of tile t retired (commit)
+  const uint32_t nd_full = buf_free + 8 * NBUF, u_ready = nd_full + 8;
   const uint32_t vraw_full = u_ready + 8;                    // NV barriers: direct-V rows landed (TMA)
   const uint32_t drain_ready = vraw_full + 8 * NV;           // N/D of a drain group retired (commit)
   const uint32_t sTmem = drain_ready + 8;
@@ -1053,7 +1072,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
   if (tid == 0) {
     for (int i = 0; i < NS; ++i) { mbar_init(y_full + 8 * i, 1); mbar_init(y_empty + 8 * i, NEW); }
     for (int i = 0; i < NV; ++i) { mbar_init(v_full + 8 * i, NVG); mbar_init(v_empty + 8 * i, 1); }
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < NBUF; ++i) {
       mbar_init(s_full + 8 * i, 1);
       mbar_init(p_full + 8 * i, NEW);
       mbar_init(buf_free + 8 * i, 1);
@@ -1126,32 +1145,33 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
       mbar_wait_mma(u_ready, 0);
       tc_fence_after();
       // S(t) = U_hi V(t)^T + U_lo V(t)^T into buffer t & 1 (split reconstruction)
-      auto mma_s = [&](int t) {
-        const int vs = t % NV, b = t & 1;
+      auto mma_s = [&](int t, int b, uint32_t ph) {   // b = t % NBUF, ph = (t / NBUF) & 1
+        const int vs = t % NV;
         mbar_wait_mma(v_full + 8 * vs, (t / NV) & 1);
-        if (t >= 2 && war_wait) mbar_wait_mma(buf_free + 8 * b, ((t >> 1) - 1) & 1);
+        if (t >= NBUF && war_wait) mbar_wait_mma(buf_free + 8 * b, ph ^ 1);
         tc_fence_after();
         if (lane == 0) trace_ev(a, t, EV_MMA1_ISSUE);
         __syncwarp();
         const uint64_t vd = sdesc(sV + vs * V_STAGE, 16, 1024);
-        const uint32_t d = tmem + 128 * b;
+        const uint32_t d = tmem + buf_col(b);
         // one asm block, one elect: U_hi and U_lo steps interleaved (tUl = tUh + KB)
         if (KB == 64) mma_s_block_64<id1>(d, tUh, vd, 0u);
         else mma_s_block_32<id1>(d, tUh, vd, 0u);
         mma_commit_elect(s_full + 8 * b);
       };
-      mma_s(0);
-      if (T > 1) mma_s(1);
+      for (int i = 0; i < NBUF && i < T; ++i) mma_s(i, i, 0);
+      int b = 0;                  // buffer of tile u (and of tile u + NBUF's S)
+      uint32_t ph = 0;            // (u / NBUF) & 1
       for (int u = 0; u < T; ++u) {
-        const int vs = u % NV, b = u & 1;
-        mbar_wait_mma(p_full + 8 * b, (u >> 1) & 1);
+        const int vs = u % NV;
+        mbar_wait_mma(p_full + 8 * b, ph);
         tc_fence_after();
         if (lane == 0) trace_ev(a, u, EV_MMA23_ISSUE);
         __syncwarp();
         if (a.mode != 2 && !(NEF_DBG & 64)) {   // NEF_DBG 64: timing experiment without N/D MMAs
           // B = V^T, K-major SW128: rows = bond (N), K = tile columns (2 atoms of 32)
           const uint64_t vtd = sdesc(sV + vs * V_STAGE + VSt<KB>::VT_OFF, 16, 1024);
-          const uint32_t pa = tmem + 128 * b;   // P_a; P_b at pa + 64
+          const uint32_t pa = tmem + buf_col(b);   // P_a; P_b at pa + 64
           // the accumulators restart at every drain group (see the elementwise loop)
           const uint32_t acc = (u % G) != 0 ? 1u : 0u;
           if constexpr (SPA) {
@@ -1166,7 +1186,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
         mma_commit_elect(v_empty + 8 * vs);
         mma_commit_elect(buf_free + 8 * b);
         if (u % G == G - 1 && u != T - 1) mma_commit_elect(drain_ready);
-        if (u + 2 < T) mma_s(u + 2);
+        if (u + NBUF < T) mma_s(u + NBUF, b, ph ^ 1);
+        if (++b == NBUF) { b = 0; ph ^= 1; }
       }
       mma_commit_elect(nd_full);
     }
@@ -1331,13 +1352,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
     const int64_t cext = a.layout == 0 ? a.CO : a.CI;
     const int tiles_blk = (int)(a.layout == 0 ? a.tiles : a.tiles_inner);
     int tin = (int)(a.layout == 0 ? t_begin : t_begin % a.tiles_inner);
+    int b = 0;           // tile buffer t % NBUF
+    uint32_t bph = 0;    // (t / NBUF) & 1
     for (int t = 0; t < T; ++t, ++tin) {
-      const int b = t & 1;
       if (tin >= tiles_blk) tin = 0;
       const int64_t crem = cext - (int64_t)tin * BN;
       const int cols_here = (int)(crem < BN ? crem : BN);
       const int st = t % NS;
-      const uint32_t tc = tmem + 128 * b + lane_off + 16 * cg;   // S / P_a columns of this warp
+      const uint32_t tc = tmem + buf_col(b) + lane_off + 16 * cg;   // S / P_a columns of this warp
       float lsum[3] = {0.f, 0.f, 0.f};
       uint32_t sv[16], pb[16], pl[16];
       float yv[16];
@@ -1348,7 +1370,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
       mbar_spin(y_full + 8 * st, (t / NS) & 1);
       if (warp == W_EW0 && lane == 0) trace_ev(a, t, EV_EW_Y);
       ew_load_y(a, gY + st * Y_STAGE, gM + st * M_STAGE, cg >> 1, cg & 1, m, yoff, yswz, yv, mk);   // (MM == 0: a.has_mask = 0)
-      mbar_wait_ew(s_full + 8 * b, (t >> 1) & 1);
+      mbar_wait_ew(s_full + 8 * b, bph);
       if (warp == W_EW0 && lane == 0) trace_ev(a, t, EV_EW_S);
       tc_fence_after();
       tmem_ld16(tc, sv);
@@ -1356,10 +1378,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
 #if NEF_EW_BAR
       // one elementwise warp polls S(t)'s barrier; the other 15 block on a named barrier (no
       // polling: their issue slots go to the warps that compute)
-      if (warp == W_EW0 + NEW - 1) mbar_wait_ew(s_full + 8 * b, (t >> 1) & 1);
+      if (warp == W_EW0 + NEW - 1) mbar_wait_ew(s_full + 8 * b, bph);
       asm volatile("bar.sync 2, %0;" ::"n"(NEW * 32) : "memory");
 #else
-      mbar_wait_ew(s_full + 8 * b, (t >> 1) & 1);
+      mbar_wait_ew(s_full + 8 * b, bph);
 #endif
       if (warp == W_EW0 && lane == 0) trace_ev(a, t, EV_EW_S);
       tc_fence_after();
@@ -1373,7 +1395,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
       if (lane == 0) mbar_arrive(y_empty + 8 * st);  // Y / mask stage read by this warp
       if (!(NEF_DBG & 256)) {
         if (MM == 1) ew_half<KIND, SPA>(a, sv, yv, mk, cols_here - 16 * cg, row_ok, pb, pl, lsum, cnt);
-        else ew_half_sent<KIND, SPA>(a, sv, yv, cols_here - 16 * cg, row_ok, pb, pl, lsum[0], cnt[0]);
+        else ew_half_sent<KIND, SPA>(a, sv, yv, cols_here - 16 * cg, row_ok, pb, pl, loss_acc[0], cnt[0]);
       } else {   // NEF_DBG 256: timing experiment without the elementwise math (P_b = S + Y)
 #pragma unroll
         for (int j = 0; j < 16; ++j) pb[j] = sv[j] + __float_as_uint(yv[j]) + mk[j >> 2];
@@ -1389,9 +1411,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
       }
       if (warp == W_EW0 && lane == 0) trace_ev(a, t, EV_EW_HALF);
       if (a.mode != 2) tmem_st_wait();
-      if (a.mode != 0) {
+      if (MM == 1 && a.mode != 0) {
         loss_acc[0] += (double)lsum[0];
-        if (MM == 1 && a.split) { loss_acc[1] += (double)lsum[1]; loss_acc[2] += (double)lsum[2]; }
+        if (a.split) { loss_acc[1] += (double)lsum[1]; loss_acc[2] += (double)lsum[2]; }
       }
       tc_fence_before();
       __syncwarp();
@@ -1405,6 +1427,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
         tc_fence_after();
         drain_nd(t / G, false);
       }
+      if (++b == NBUF) { b = 0; bph ^= 1; }
     }
     // epilogue: the last group's N | D -> split partials (added to the earlier groups' drains)
     if (a.mode != 2) {
