@@ -159,6 +159,21 @@ int nef_fit_split(nef_plan_t plan, const float* Y, const uint8_t* labels, const 
                   float* const* factors, const nef_stop_rule* rule, double* traces, int64_t* counts, int* sweeps,
                   int* reason, void* workspace, size_t ws_bytes, void* cuda_stream);
 
+/* Batched random restarts (N4; the paper notes restarts help).  `restarts` independent
+ * fits of the same Y / mask / loss from different initial factors: factors holds restarts x L
+ * device pointers, restart-major (restart r's factor ell at factors[r * L + ell]), each updated in
+ * place.  Every factor update's streamed pass is ONE launch for all restarts (launch index z =
+ * restart) on the tcgen05 kernel, so the restarts' CTAs stream the same Y tiles together - Y is
+ * read from HBM about once per update for all restarts (the others hit L2) - and their side
+ * operands, reductions and updates are separate.  (Lowerings on the CUDA-core kernel run one
+ * launch per restart.)  loss_traces: host, restarts x (iters + 1) doubles, restart-major, or NULL.
+ * workspace: nef_restarts_workspace_bytes(plan, restarts) bytes (one plan workspace per restart,
+ * sharing one sentinel copy of Y).  iters < 2048.  Errors as nef_fit. */
+size_t nef_restarts_workspace_bytes(nef_plan_t plan, int restarts);
+int nef_fit_restarts(nef_plan_t plan, const float* Y, const uint8_t* mask, const nef_loss_spec* loss, double eps,
+                     float* const* factors, int restarts, int iters, double* loss_traces, void* workspace,
+                     size_t ws_bytes, void* cuda_stream);
+
 /* One factor update (Algorithm 1 lines 6-9 for a single ell), the step-level API. */
 int nef_update(nef_plan_t plan, int ell, const float* Y, const uint8_t* mask, double alpha, double beta,
                double eps, float* const* factors, void* workspace, size_t ws_bytes, void* cuda_stream);

@@ -227,115 +227,164 @@ bool use_tc(const nef::Lowering& L, const uint8_t* M, bool sentinel = false, con
 
 // One streaming pass over Y (+mask) for lowering L: the tcgen05 kernel where the planner
 // found a TMA geometry, else the CUDA-core kernel.  U and the column tables must be ready.
-int stream_pass(const Ctx& c, const nef::Lowering& L, const float* Y, const uint8_t* M, int mode,
-                const nef::DivParams& dv, StreamOut& o) {
+// TcArgs of one restart's pass; chunks_b > 0 forces the chunk count (batched restarts)
+int fill_tc(const Ctx& c, const nef::Lowering& L, const nef::FusedArgs& a, const std::vector<int32_t>& boff, int mode,
+            const nef::DivParams& dvk, bool sent, const uint8_t* M, int64_t chunks_b, nef::tc::TcArgs& t,
+            int64_t& chunks, StreamOut& o) {
+  t = nef::tc::TcArgs{};
+  t.layout = L.tc_layout;
+  t.R = L.tc_R;
+  t.CI = L.tc_CI;
+  t.CO = L.tc_CO;
+  t.tiles_inner = (L.tc_CI + 63) / 64;
+  t.tiles = L.tc_tiles;
+  const int64_t want = chunks_b > 0 ? chunks_b : L.tc_chunks;
+  int64_t tpc = (L.tc_tiles + want - 1) / want;
+  chunks = (L.tc_tiles + tpc - 1) / tpc;   // no empty chunk
+  t.tiles_per_chunk = tpc;
+  t.K = (int)L.K;
+  t.KB = L.tc_KB;
+  t.n_rows = L.n_rows;
+  t.U = a.U;
+  t.nc = a.nc;
+  for (int k = 0; k < a.nc; ++k) t.cdim[k] = a.cdim[k];
+  t.ntab = a.ntab;
+  for (int q = 0; q < a.ntab; ++q) {
+    t.tab[q] = a.tab[q];
+    for (int k = 0; k < a.nc; ++k) t.tcs[q][k] = a.tcs[q][k];
+    for (int k = 0; k < L.K; ++k) t.boff[q][k] = boff[(size_t)q * L.K + k];
+  }
+  bool v4 = (L.K % 4 == 0);
+  for (int q = 0; q < a.ntab && v4; ++q) {
+    v4 = (reinterpret_cast<uintptr_t>(a.tab[q]) & 15) == 0;
+    for (int k = 0; k < a.nc; ++k) v4 = v4 && (a.tcs[q][k] % 4 == 0);
+    for (int k = 0; k < L.K; ++k) v4 = v4 && (boff[(size_t)q * L.K + k] == k);
+  }
+  t.vec4 = v4 && a.ntab > 0 ? 1 : 0;
+  // direct V (planner: Lowering::vd_tab): the tile's V rows are consecutive rows of one
+  // table, TMA-loaded; a K % 4 != 0 table is first copied to a 16-byte row pitch
+  t.vdirect = 0;
+  if (g_vdirect && L.vd_tab >= 0) {
+    t.vdirect = 1;
+    t.var_tab = L.vd_tab;
+    t.var_rows = L.vd_rows;
+    t.vd_E = L.vd_E;
+    // tiles per run: runs are whole column blocks (E a multiple of the block extent, or
+    // E == block) or E / 64 aligned tiles
+    const int64_t blk = L.tc_layout == 0 ? L.tc_CO : L.tc_CI;
+    const int64_t tiles_blk = (blk + 63) / 64;
+    if (L.vd_E % blk == 0) t.vd_tpr = (L.vd_E / blk) * tiles_blk;
+    else t.vd_tpr = L.vd_E / 64;
+    t.vd_pitch = L.vd_Kp;
+    t.vd_rows_ptr = a.tab[L.vd_tab];
+    if (L.ws_vpad >= 0) {
+      float* pad = reinterpret_cast<float*>(c.ws + L.ws_vpad);
+      CK(nef::launch_pad_rows(a.tab[L.vd_tab], pad, L.vd_rows, L.K, L.vd_Kp, c.s));
+      ++g_launches;
+      t.vd_rows_ptr = pad;
+    }
+  }
+  t.Qpart = reinterpret_cast<float*>(c.ws + L.ws_tc_Qpart);
+  t.losspart = reinterpret_cast<double*>(c.ws + L.ws_tc_losspart);
+  o.nparts = L.tc_row_blocks * chunks;
+  t.countpart = reinterpret_cast<long long*>(c.ws + L.ws_tc_losspart + 3 * o.nparts * 8);
+  t.dv = dvk;
+  t.mode = mode;
+  t.split = (c.split && M && !sent) ? 1 : 0;
+  t.lconst = ((sent || !M) && c.loff && mode != 0) ? 1 : 0;
+  // unmasked Y streamed as is: every entry is observed, so the kernel must not read "missing"
+  // from a sign bit (an observed -0.0 is a zero); the sentinel copy canonicalises -0 itself
+  t.absy = (!M && !sent) ? 1 : 0;
+  t.debug = g_debug;
+  t.trace = g_trace;
+  t.n_groups = (tpc + nef::kDrainTiles - 1) / nef::kDrainTiles;
+  o.Qpart = t.Qpart;
+  o.n_chunks = chunks * t.n_groups;
+  o.losspart = t.losspart;
+  o.countpart = t.countpart;
+  o.lconst = t.lconst != 0;
+  return NEF_OK;
+}
+
+// One streaming pass over Y (+mask) for lowering L, for S restarts (contexts cs[0..S-1], N4): the
+// tcgen05 kernel where the planner found a TMA geometry - ONE launch whose z index is the
+// restart, so every restart's CTAs stream the same Y tiles (the other restarts' reads hit L2) -
+// else the CUDA-core kernel per restart.  U and the column tables must be ready.
+int stream_pass_multi(const Ctx* cs, int S, const nef::Lowering& L, const float* Y, const uint8_t* M, int mode,
+                      const nef::DivParams& dv, StreamOut* os) {
+  const Ctx& c = cs[0];
   // kernel limits (the planner keeps every lowering inside them; checked again before any launch)
   if (L.tabs.size() > (size_t)nef::kMaxTabs || L.K > 64)
     return fail(NEF_E_UNSUPPORTED, "lowering exceeds the kernels' limits (<= 4 column tables, bond <= 64)");
   std::vector<int32_t> boff;
-  nef::FusedArgs a = fused_args(c, L, Y, M, mode, dv, boff);
   const double bytes = (double)c.p->n_local * ((M ? 5.0 : 4.0) + (c.aux ? 4.0 : 0.0));
   // split fits: the loss-carrying passes stream Y with the labels (train / validation / heldout
   // losses of one pass); update-only passes stream the train-folded sentinel copy
   const bool sent = c.ysent && (M || c.sqy) && !(c.split && mode != 0);
   nef::DivParams dvk = dv;
-  if (use_tc(L, M, sent, c.aux)) {
+  if (use_tc(L, M, sent, c.aux) && (S == 1 || (g_vdirect && L.vd_tab >= 0))) {
+    const float* Yk = Y;
+    const uint8_t* Mk = M;
     if (sent) {   // stream the NaN-sentinel copy: no mask stream (4 B / entry)
-      Y = c.ysent;
-      M = nullptr;
+      Yk = c.ysent;
+      Mk = nullptr;
       if (c.sqy) dvk.kind = nef::EW_A05_B0_SQ;   // the copy holds sqrt(y) (R35)
     }
-    nef::tc::TcArgs t{};
-    t.layout = L.tc_layout;
-    t.R = L.tc_R;
-    t.CI = L.tc_CI;
-    t.CO = L.tc_CO;
-    t.tiles_inner = (L.tc_CI + 63) / 64;
-    t.tiles = L.tc_tiles;
-    int64_t tpc = (L.tc_tiles + L.tc_chunks - 1) / L.tc_chunks;
-    int64_t chunks = (L.tc_tiles + tpc - 1) / tpc;   // no empty chunk
-    t.tiles_per_chunk = tpc;
-    t.K = (int)L.K;
-    t.KB = L.tc_KB;
-    t.n_rows = L.n_rows;
-    t.U = a.U;
-    t.nc = a.nc;
-    for (int k = 0; k < a.nc; ++k) t.cdim[k] = a.cdim[k];
-    t.ntab = a.ntab;
-    for (int q = 0; q < a.ntab; ++q) {
-      t.tab[q] = a.tab[q];
-      for (int k = 0; k < a.nc; ++k) t.tcs[q][k] = a.tcs[q][k];
-      for (int k = 0; k < L.K; ++k) t.boff[q][k] = boff[(size_t)q * L.K + k];
-    }
-    {
-      bool v4 = (L.K % 4 == 0);
-      for (int q = 0; q < a.ntab && v4; ++q) {
-        v4 = (reinterpret_cast<uintptr_t>(a.tab[q]) & 15) == 0;
-        for (int k = 0; k < a.nc; ++k) v4 = v4 && (a.tcs[q][k] % 4 == 0);
-        for (int k = 0; k < L.K; ++k) v4 = v4 && (boff[(size_t)q * L.K + k] == k);
-      }
-      t.vec4 = v4 && a.ntab > 0 ? 1 : 0;
-      // direct V (planner: Lowering::vd_tab): the tile's V rows are consecutive rows of one
-      // table, TMA-loaded; a K % 4 != 0 table is first copied to a 16-byte row pitch
-      t.vdirect = 0;
-      if (g_vdirect && L.vd_tab >= 0) {
-        t.vdirect = 1;
-        t.var_tab = L.vd_tab;
-        t.var_rows = L.vd_rows;
-        t.vd_E = L.vd_E;
-        // tiles per run: runs are whole column blocks (E a multiple of the block extent, or
-        // E == block) or E / 64 aligned tiles
-        {
-          const int64_t blk = L.tc_layout == 0 ? L.tc_CO : L.tc_CI;
-          const int64_t tiles_blk = (blk + 63) / 64;
-          if (L.vd_E % blk == 0) t.vd_tpr = (L.vd_E / blk) * tiles_blk;
-          else t.vd_tpr = L.vd_E / 64;
-        }
-        t.vd_pitch = L.vd_Kp;
-        t.vd_rows_ptr = a.tab[L.vd_tab];
-        if (L.ws_vpad >= 0) {
-          float* pad = reinterpret_cast<float*>(c.ws + L.ws_vpad);
-          CK(nef::launch_pad_rows(a.tab[L.vd_tab], pad, L.vd_rows, L.K, L.vd_Kp, c.s));
-          ++g_launches;
-          t.vd_rows_ptr = pad;
-        }
+    // batched restarts: one wave of row blocks x chunks x restarts; the restarts' partials must
+    // fit the single-restart workspace layout (else one launch per restart)
+    int64_t chunks_b = 0;
+    if (S > 1) {
+      chunks_b = std::max<int64_t>(1, c.p->num_sms / (L.tc_row_blocks * S));
+      const int64_t tpc = (L.tc_tiles + chunks_b - 1) / chunks_b;
+      const int64_t groups = (tpc + nef::kDrainTiles - 1) / nef::kDrainTiles;
+      if (chunks_b * groups > L.tc_chunks * L.tc_groups) {
+        for (int r = 0; r < S; ++r)
+          if (int st = stream_pass_multi(cs + r, 1, L, Y, M, mode, dv, os + r)) return st;
+        return NEF_OK;
       }
     }
-    t.Qpart = reinterpret_cast<float*>(c.ws + L.ws_tc_Qpart);
-    t.losspart = reinterpret_cast<double*>(c.ws + L.ws_tc_losspart);
-    o.nparts = L.tc_row_blocks * chunks;
-    t.countpart = reinterpret_cast<long long*>(c.ws + L.ws_tc_losspart + 3 * o.nparts * 8);
-    t.dv = dvk;
-    t.mode = mode;
-    t.split = (c.split && M && !sent) ? 1 : 0;
-    t.lconst = ((sent || !M) && c.loff && mode != 0) ? 1 : 0;
-    // unmasked Y streamed as is: every entry is observed, so the kernel must not read "missing"
-    // from a sign bit (an observed -0.0 is a zero); the sentinel copy canonicalises -0 itself
-    t.absy = (!M && !sent) ? 1 : 0;
-    t.debug = g_debug;
-    t.trace = g_trace;
-    t.n_groups = (tpc + nef::kDrainTiles - 1) / nef::kDrainTiles;
+    nef::tc::TcArgs t0{};
+    int64_t chunks = 0;
+    for (int r = 0; r < S; ++r) {
+      nef::FusedArgs a = fused_args(cs[r], L, Yk, Mk, mode, dv, boff);
+      nef::tc::TcArgs t;
+      if (int st = fill_tc(cs[r], L, a, boff, mode, dvk, sent, M, chunks_b, t, chunks, os[r])) return st;
+      if (r == 0) t0 = t;
+      if (S > 1) {
+        t0.Ur[r] = t.U;
+        for (int q = 0; q < nef::kMaxTabs; ++q) t0.tabr[r][q] = t.tab[q];
+        t0.Qpartr[r] = t.Qpart;
+        t0.losspartr[r] = t.losspart;
+        t0.countpartr[r] = t.countpart;
+        t0.vdr[r] = t.vd_rows_ptr;
+      }
+    }
+    t0.nrs = S > 1 ? S : 0;
     prof_begin(c.s);
-    CK(nef::tc::launch(t, Y, M, L.tc_row_blocks, chunks, c.s));
+    CK(nef::tc::launch(t0, Yk, Mk, L.tc_row_blocks, chunks, c.s));
     prof_end(c.s, bytes);
     ++g_launches;
-    o.Qpart = t.Qpart;
-    o.n_chunks = chunks * t.n_groups;
-    o.losspart = t.losspart;
-    o.countpart = t.countpart;
-    o.lconst = t.lconst != 0;
     return NEF_OK;
   }
-  prof_begin(c.s);
-  CK(nef::launch_fused_ffma(a, c.s));
-  prof_end(c.s, bytes);
-  ++g_launches;
-  o.Qpart = a.Qpart;
-  o.n_chunks = L.n_chunks;
-  o.losspart = a.losspart;
-  o.countpart = a.countpart;
-  o.nparts = ((L.n_rows + 63) / 64) * L.n_chunks;
+  for (int r = 0; r < S; ++r) {
+    nef::FusedArgs a = fused_args(cs[r], L, Y, M, mode, dv, boff);
+    prof_begin(c.s);
+    CK(nef::launch_fused_ffma(a, c.s));
+    prof_end(c.s, bytes);
+    ++g_launches;
+    StreamOut& o = os[r];
+    o.Qpart = a.Qpart;
+    o.n_chunks = L.n_chunks;
+    o.losspart = a.losspart;
+    o.countpart = a.countpart;
+    o.nparts = ((L.n_rows + 63) / 64) * L.n_chunks;
+  }
   return NEF_OK;
+}
+
+int stream_pass(const Ctx& c, const nef::Lowering& L, const float* Y, const uint8_t* M, int mode,
+                const nef::DivParams& dv, StreamOut& o) {
+  return stream_pass_multi(&c, 1, L, Y, M, mode, dv, &o);
 }
 
 bool communicates(const nef::Plan& p);
@@ -376,18 +425,16 @@ int loss_pass(const Ctx& c, const float* Y, const uint8_t* M, const nef::DivPara
 // Steps 1-4 of one factor update: leaves A in *num, B in *den (device pointers into ws).  With
 // `fused` (epilogue-free lowering, no all-reduce) the split partials are left unreduced in *fused
 // for the fused reduce + update kernel and num / den are not written.
-int num_den(const Ctx& c, int ell, const float* Y, const uint8_t* M, const nef::DivParams& dv, int mode,
-            double* slot, long long* cslot, float** num, float** den, StreamOut* fused = nullptr) {
+// After the streamed pass of factor ell: the loss slots (mode 1), then A | B - the split
+// partials reduced in fixed order and the epilogue einsum (einstr_ell on the row side) - left in
+// *num / *den.  With `fused` (epilogue-free lowering, no all-reduce) the partials stay unreduced
+// for the fused reduce + update kernel and num / den are not written.
+int finish_num_den(const Ctx& c, int ell, const uint8_t* M, int mode, double* slot, long long* cslot,
+                   const StreamOut& o, float** num, float** den, bool fused) {
   const nef::Lowering& L = c.p->low[ell];
-  int st = side_operands(c, L);
-  if (st) return st;
-  StreamOut o;
-  if ((st = stream_pass(c, L, Y, M, mode, dv, o))) return st;
+  int st;
   if (mode == 1 && (st = reduce_loss(c, o, M, slot, cslot))) return st;
-  if (fused && L.epi_identity) {
-    *fused = o;
-    return NEF_OK;
-  }
+  if (fused && L.epi_identity) return NEF_OK;
   const int64_t qe = L.n_rows * L.K;
   float* Q = reinterpret_cast<float*>(c.ws + L.ws_Q);
   CK(nef::launch_reduce_q(o.Qpart, Q, o.n_chunks, 2 * qe, c.s));
@@ -406,6 +453,17 @@ int num_den(const Ctx& c, int ell, const float* Y, const uint8_t* M, const nef::
   return NEF_OK;
 }
 
+// Steps 1-4 of one factor update: leaves A in *num, B in *den (device pointers into ws).
+int num_den(const Ctx& c, int ell, const float* Y, const uint8_t* M, const nef::DivParams& dv, int mode,
+            double* slot, long long* cslot, float** num, float** den) {
+  const nef::Lowering& L = c.p->low[ell];
+  int st = side_operands(c, L);
+  if (st) return st;
+  StreamOut o;
+  if ((st = stream_pass(c, L, Y, M, mode, dv, o))) return st;
+  return finish_num_den(c, ell, M, mode, slot, cslot, o, num, den, false);
+}
+
 // A plan "communicates" when it is sharded over > 1 ranks, or carries a 1-rank communicator
 // (NEF_NCCL_FORCE=1 at nef_plan_shard with world 1: the multi-GPU code path, NCCL included,
 // exercised on one GPU by the tests)
@@ -421,17 +479,18 @@ int allreduce(const nef::Plan& p, void* buf, size_t count, int dtype, cudaStream
   return NEF_OK;
 }
 
-int update_one(const Ctx& c, int ell, const float* Y, const uint8_t* M, const nef::DivParams& dv, const nef::UpdArgs& u,
-               int mode, double* slot, long long* cslot) {
-  float *num = nullptr, *den = nullptr;
+// Steps 5-6 after the streamed pass: finish A | B, all-reduce (sharded plans, factors without the
+// shard mode), update.  Epilogue-free lowerings on one rank reduce and update in one launch.
+int finish_update(const Ctx& c, int ell, const uint8_t* M, const nef::UpdArgs& u, int mode, double* slot,
+                  long long* cslot, const StreamOut& o) {
   int64_t n = 1;
   for (auto d : c.p->fshape[ell]) n *= d;
   const bool fuse = !communicates(*c.p) && c.p->low[ell].epi_identity;
-  StreamOut fo;
-  int st = num_den(c, ell, Y, M, dv, mode, slot, cslot, &num, &den, fuse ? &fo : nullptr);
+  float *num = nullptr, *den = nullptr;
+  int st = finish_num_den(c, ell, M, mode, slot, cslot, o, &num, &den, fuse);
   if (st) return st;
   if (fuse) {   // numerator / denominator summed from the split partials inside the update kernel
-    CK(nef::launch_reduce_update(fo.Qpart, c.F[ell], fo.n_chunks, n, u, c.s));
+    CK(nef::launch_reduce_update(o.Qpart, c.F[ell], o.n_chunks, n, u, c.s));
     ++g_launches;
     return NEF_OK;
   }
@@ -448,6 +507,16 @@ int update_one(const Ctx& c, int ell, const float* Y, const uint8_t* M, const ne
   CK(nef::launch_update(c.F[ell], num, den, n, u, c.s));
   ++g_launches;
   return NEF_OK;
+}
+
+int update_one(const Ctx& c, int ell, const float* Y, const uint8_t* M, const nef::DivParams& dv, const nef::UpdArgs& u,
+               int mode, double* slot, long long* cslot) {
+  const nef::Lowering& L = c.p->low[ell];
+  int st = side_operands(c, L);
+  if (st) return st;
+  StreamOut o;
+  if ((st = stream_pass(c, L, Y, M, mode, dv, o))) return st;
+  return finish_update(c, ell, M, u, mode, slot, cslot, o);
 }
 
 int validate_ab(double alpha, double beta) {
@@ -713,6 +782,103 @@ int nef_fit(nef_plan_t plan, const float* Y, const uint8_t* mask, double alpha, 
             float* const* factors, int iters, double* loss_trace, void* workspace, size_t ws_bytes, void* stream) {
   const nef_loss_spec ls = ab_spec(alpha, beta);
   return nef_fit_ex(plan, Y, mask, &ls, eps, factors, iters, loss_trace, workspace, ws_bytes, stream);
+}
+
+// Batched random restarts (N4): S independent fits of the same data, each factor
+// update's streamed pass launched ONCE for all restarts (grid z = restart) so that the restarts'
+// CTAs read the same Y tiles together - one HBM stream, the other restarts served by L2.
+size_t nef_restarts_workspace_bytes(nef_plan_t plan, int restarts) {
+  if (!plan || restarts < 1) return 0;
+  const nef::Plan& p = plan->p;
+  const size_t per = ((size_t)p.ws_sent + 255) / 256 * 256;   // everything but the sentinel copy
+  return per * (size_t)restarts + (size_t)p.n_local * 4 + 256;
+}
+
+int nef_fit_restarts(nef_plan_t plan, const float* Y, const uint8_t* mask, const nef_loss_spec* loss, double eps,
+                     float* const* factors, int restarts, int iters, double* loss_traces, void* workspace,
+                     size_t ws_bytes, void* stream) {
+  if (!plan) return fail(NEF_E_ARG, "null plan");
+  const nef::Plan& p = plan->p;
+  const int S = restarts;
+  if (S < 1) return fail(NEF_E_ARG, "restarts must be >= 1");
+  if (iters < 0 || iters >= 2048) return fail(NEF_E_ARG, "iters must be in [0, 2048) for batched restarts");
+  if (!Y || (reinterpret_cast<uintptr_t>(Y) & 15)) return fail(NEF_E_ARG, "Y must be a non-null 16-byte aligned device pointer");
+  if (!factors) return fail(NEF_E_ARG, "null factor array");
+  const int L = (int)p.ops.size();
+  for (int i = 0; i < S * L; ++i)
+    if (!factors[i] || (reinterpret_cast<uintptr_t>(factors[i]) & 3)) return fail(NEF_E_ARG, "null or misaligned factor pointer");
+  if (!workspace || ws_bytes < nef_restarts_workspace_bytes(plan, S))
+    return fail(NEF_E_ARG, "workspace too small: need " + std::to_string(nef_restarts_workspace_bytes(plan, S)) + " bytes");
+  if (reinterpret_cast<uintptr_t>(workspace) & 255) return fail(NEF_E_ARG, "workspace must be 256-byte aligned");
+  Spec sp;
+  int st = validate_spec(loss, sp);
+  if (st) return st;
+  if (!(eps > 0.0) || !std::isfinite(eps)) return fail(NEF_E_ARG, "eps must be > 0");
+  if (int dst = check_device()) return dst;
+  g_launches = 0;
+  const size_t per = ((size_t)p.ws_sent + 255) / 256 * 256;
+  char* ws = static_cast<char*>(workspace);
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  std::vector<Ctx> cs(S);
+  for (int r = 0; r < S; ++r) {
+    cs[r] = Ctx{&p, factors + (size_t)r * L, ws + r * per, per, s};
+    cs[r].aux = sp.aux;
+  }
+  const nef::DivParams dv = nef::make_div_fam(sp.fam, sp.alpha, sp.beta, sp.prm);
+  const nef::UpdArgs u = nef::make_upd_fam(sp.fam, sp.alpha, sp.beta, eps);
+  // once per fit, shared by the restarts: the sentinel copy (and its data-only loss sum, R25)
+  const int dterm = (g_no_lconst || g_policy != 0 || sp.fam != nef::FAM_AB) ? 0
+                    : dv.kind == nef::EW_B_M05   ? 1
+                    : dv.kind == nef::EW_KL      ? 2
+                    : dv.kind == nef::EW_A05_B0  ? 3
+                                                 : 0;
+  bool any_tc = false;
+  for (const auto& Lw : p.low) any_tc |= Lw.tc_ok;
+  const bool sqy = dv.kind == nef::EW_A05_B0 && any_tc && g_policy == 0 && !g_no_sentinel && !sp.aux && !g_no_sqy;
+  if ((mask || sqy) && any_tc && g_policy == 0 && !g_no_sentinel && !sp.aux) {
+    double* dslot = reinterpret_cast<double*>(ws + p.ws_dterm);
+    double* dpart = reinterpret_cast<double*>(ws + p.ws_dpart);
+    float* ys = reinterpret_cast<float*>(ws + per * S);
+    CK(nef::launch_sentinel(Y, mask, ys, p.n_local, dterm, dpart, reinterpret_cast<long long*>(dpart + nef::kSentParts),
+                            dslot, reinterpret_cast<long long*>(dslot + 1), s, 0, sqy ? 1 : 0));
+    g_launches += 3;
+    for (auto& c : cs) {
+      c.ysent = ys;
+      c.sqy = sqy;
+      if (dterm) {
+        c.loff = dslot;
+        c.lscale = dterm == 1 ? 2.0 : dterm == 3 ? 4.0 : 1.0;
+      }
+    }
+  }
+  std::vector<StreamOut> os(S);
+  auto slot = [&](int r) { return reinterpret_cast<double*>(cs[r].ws + p.ws_trace); };
+  auto cslot = [&](int r) { return reinterpret_cast<long long*>(cs[r].ws + p.ws_trace + 8 * 2048); };
+  for (int t = 0; t <= iters; ++t) {
+    const bool last = t == iters;   // the final loss-only pass
+    for (int ell = 0; ell < (last ? 1 : L); ++ell) {
+      const nef::Lowering& Lw = p.low[ell];
+      const int mode = last ? 2 : (ell == 0 ? 1 : 0);
+      for (int r = 0; r < S; ++r)
+        if ((st = side_operands(cs[r], Lw))) return st;
+      if ((st = stream_pass_multi(cs.data(), S, Lw, Y, mask, mode, dv, os.data()))) return st;
+      for (int r = 0; r < S; ++r) {
+        if (last) st = reduce_loss(cs[r], os[r], mask, slot(r) + t, cslot(r) + t);
+        else st = finish_update(cs[r], ell, mask, u, mode, slot(r) + t, cslot(r) + t, os[r]);
+        if (st) return st;
+      }
+    }
+  }
+  std::vector<double> host((size_t)S * (iters + 1));
+  for (int r = 0; r < S; ++r) {
+    if (communicates(p))
+      if ((st = allreduce(p, slot(r), (size_t)iters + 1, kNcclFloat64, s))) return st;
+    CK(cudaMemcpyAsync(host.data() + (size_t)r * (iters + 1), slot(r), sizeof(double) * (iters + 1),
+                       cudaMemcpyDeviceToHost, s));
+  }
+  CK(cudaStreamSynchronize(s));
+  if (loss_traces) std::memcpy(loss_traces, host.data(), sizeof(double) * host.size());
+  return NEF_OK;
 }
 
 // Train / validation / heldout fit with the stopping rules of P:497 (readings R29-R32).  Per

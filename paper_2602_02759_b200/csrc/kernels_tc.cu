@@ -50,40 +50,27 @@ template <int KB, int MM> struct YStages {
 #define NEF_NV0 4
 #endif
 template <int KB, int MM> struct VStages { static constexpr int value = MM == 1 ? 3 : NEF_NV0; };
-// warp roles: 16 elementwise warps, 4 V generators, direct-V row loads, TMA producer, MMA
-// issuer.  The warp schedulers favour higher warp ids, so the producers whose latency is on the
-// critical path sit above the elementwise warps (with the producers below, the V generators
-// and the MMA issuer starved during the elementwise phase of every tile).
-#ifndef NEF_EW_BAR
-#define NEF_EW_BAR 0
-#endif
 #ifndef NEF_PA_RN
 #define NEF_PA_RN 0   // 1: plain RN for P_a in the Euclidean pair too (diagnostics)
 #endif
-#ifndef NEF_Y_FIRST
-#define NEF_Y_FIRST 0
+// elementwise warp width: 16 warps of 32 rows x 16 tile columns (default), or (NEF_EW_COLS = 32)
+// 8 warps of 32 rows x 32 columns - half the per-tile overhead per entry and 136 registers per
+// thread instead of 80, but half the warps to hide the TMEM / shared-memory latencies: measured
+// 2-3 % slower on c5 and c3, 3 % faster on c4 (the issue-bound (0.5, 0) pair)
+#ifndef NEF_EW_COLS
+#define NEF_EW_COLS 16
 #endif
-#ifndef NEF_WARP_MAP
-#define NEF_WARP_MAP 0
-#endif
-#if NEF_WARP_MAP == 0
-constexpr int W_EW0 = 0, W_VG0 = 16, W_DV = 20, W_TMA = 21, W_MMA = 22;
-__device__ __forceinline__ int vg_index(int warp) { return warp >= 16 && warp < 20 ? warp - 16 : -1; }
-#elif NEF_WARP_MAP == 3
-// MMA issuer on sub-partition 3 (the one without a producer besides its V generator); warp 22 idle
-constexpr int W_EW0 = 0, W_VG0 = 16, W_DV = 20, W_TMA = 21, W_MMA = 23;
-__device__ __forceinline__ int vg_index(int warp) { return warp >= 16 && warp < 20 ? warp - 16 : -1; }
-#else
-// the MMA issuer's sub-partition (2) hosts no V generator: V generators on warps 16, 17, 19, 20
-// (sub-partitions 0, 1, 3, 0), TMA producer 21 (1), MMA issuer 22 (2), V-row loads 23 (3)
-constexpr int W_EW0 = 0, W_VG0 = 16, W_DV = 23, W_TMA = 21, W_MMA = 22;
-__device__ __forceinline__ int vg_index(int warp) {
-  return warp == 16 ? 0 : warp == 17 ? 1 : warp == 19 ? 2 : warp == 20 ? 3 : -1;
-}
-#endif
-constexpr int NVG = 4;       // V-generator warps (16 tile columns each)
-constexpr int NEW = 16;      // elementwise warps: 4 TMEM lane quarters x 4 groups of 16 columns
-constexpr int NTHREADS = (NEF_WARP_MAP == 0 ? 23 : 24) * 32;   // (map 3: warp 22 idle)
+constexpr int EWC = NEF_EW_COLS;           // tile columns per elementwise warp
+constexpr int EWH = EWC / 16;              // 16-column half-steps per elementwise warp and tile
+constexpr int NEW = 4 * (BN / EWC);        // elementwise warps: 4 TMEM lane quarters x BN / EWC column groups
+constexpr int NVG = 4;                     // V-generator warps (16 tile columns each)
+// warp roles: elementwise warps, 4 V generators, direct-V row loads, TMA producer, MMA issuer.
+// The warp schedulers favour higher warp ids, so the producers whose latency is on the critical
+// path sit above the elementwise warps (with the producers below, the V generators and the MMA
+// issuer starved during the elementwise phase of every tile).
+constexpr int W_EW0 = 0, W_VG0 = NEW, W_DV = NEW + 4, W_TMA = NEW + 5, W_MMA = NEW + 6;
+__device__ __forceinline__ int vg_index(int warp) { return warp >= W_VG0 && warp < W_VG0 + NVG ? warp - W_VG0 : -1; }
+constexpr int NTHREADS = (NEW + 7) * 32;
 constexpr int Y_STAGE = BM * BN * 4;      // 32 KB
 constexpr int M_STAGE = BM * BN;          // 8 KB
 // a V stage: V (64 tile columns x KB bonds, SW128 K-major) then its transpose V^T, KB * 256 B each
@@ -95,7 +82,7 @@ template <int KB> struct VSt {
 struct __align__(64) Params {
   CUtensorMap tmY;
   CUtensorMap tmM;
-  CUtensorMap tmV;   // direct-V table rows (2-D {K, var_rows}, box {32, 64}, SW128)
+  CUtensorMap tmV[kMaxRestarts];   // direct-V table rows per restart (2-D {K, var_rows}, box {32, 64}, SW128)
   TcArgs a;
 };
 
@@ -194,7 +181,9 @@ __device__ __forceinline__ void mbar_wait_relaxed(uint32_t bar, uint32_t parity,
 #define NEF_MMA_WAIT 0
 #endif
 __device__ __forceinline__ void mbar_wait_mma(uint32_t bar, uint32_t parity) {
-#if NEF_MMA_WAIT
+#if NEF_MMA_WAIT == -1
+  mbar_wait(bar, parity);   // suspend-time hint: descheduled until the phase completes
+#elif NEF_MMA_WAIT
   mbar_wait_relaxed(bar, parity, NEF_MMA_WAIT);
 #else
   mbar_spin(bar, parity);
@@ -921,7 +910,7 @@ __device__ __noinline__ TabOffs direct_offs(const TcArgs& a, int64_t col) {
 // Tile-constant rows of a run, bond chunk c (4 values) of this lane: loads issued here (all in
 // flight together), product formed by cst_product when needed (software-pipelined by the caller).
 struct CstLoad { float v[kMaxTabs][4]; };
-__device__ __forceinline__ void cst_issue(const TcArgs& a, int64_t col, int c, CstLoad& L) {
+__device__ __forceinline__ void cst_issue(const TcArgs& a, const float* const* tabs, int64_t col, int c, CstLoad& L) {
   const TabOffs off = direct_offs(a, col);
 #pragma unroll
   for (int q = 0; q < kMaxTabs; ++q)
@@ -929,7 +918,7 @@ __device__ __forceinline__ void cst_issue(const TcArgs& a, int64_t col, int c, C
     for (int e = 0; e < 4; ++e) {
       const int k = 4 * c + e;
       const bool use = q < a.ntab && q != a.var_tab && k < a.K;
-      L.v[q][e] = use ? __ldg(a.tab[q] + off.o[q] + k) : 1.f;   // bond stride 1 (planner)
+      L.v[q][e] = use ? __ldg(tabs[q] + off.o[q] + k) : 1.f;   // bond stride 1 (planner)
     }
 }
 __device__ __forceinline__ float4 cst_product(const TcArgs& a, int c, const CstLoad& L) {
@@ -1059,6 +1048,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
 
   const int64_t rb = blockIdx.x;
   const int64_t ch = blockIdx.y;
+  const int rs = blockIdx.z;   // restart (N4; 0 unless batched)
   const int64_t t_begin = ch * a.tiles_per_chunk;
   const int64_t t_end = (t_begin + a.tiles_per_chunk < a.tiles) ? t_begin + a.tiles_per_chunk : a.tiles;
   const int T = (int)(t_end > t_begin ? t_end - t_begin : 0);
@@ -1205,7 +1195,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
         const uint32_t bar = vraw_full + 8 * vs;
         mbar_expect_tx(bar, (uint32_t)(KB * BN * 4));
 #pragma unroll
-        for (int h = 0; h < KB / 32; ++h) tma_load_2d(sV + vs * V_STAGE + h * (BN * 128), &P.tmV, 32 * h, rowv, bar);
+        for (int h = 0; h < KB / 32; ++h) tma_load_2d(sV + vs * V_STAGE + h * (BN * 128), &P.tmV[rs], 32 * h, rowv, bar);
       }
     }
   } else if (vg_index(warp) >= 0 && a.vdirect) {
@@ -1223,7 +1213,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
     bool pend = false;
     if (T > 0) {
       rn.init(a, t_begin);
-      cst_issue(a, tile_col0(a, t_begin), c, ld);
+      cst_issue(a, a.tabr[rs], tile_col0(a, t_begin), c, ld);
       cst = cst_product(a, c, ld);
     }
     for (int t = 0; t < T; ++t) {
@@ -1232,7 +1222,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
         pend = false;
       }
       if (t + 1 < T && rn.next()) {
-        cst_issue(a, tile_col0(a, rn.tile), c, ld);
+        cst_issue(a, a.tabr[rs], tile_col0(a, rn.tile), c, ld);
         pend = true;
       }
       const int vs = t % NV;
@@ -1284,27 +1274,30 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
     }
   } else if (warp >= W_EW0 && warp < W_EW0 + NEW) {
     // ------------------------------------------------------------ elementwise + epilogue
-    const int ew = tid - W_EW0 * 32;       // 0..511
-    const int cg = (warp - W_EW0) >> 2;    // column group: tile columns [16 cg, 16 cg + 16)
+    const int ew = tid - W_EW0 * 32;       // 0 .. NEW * 32 - 1
+    const int gw = (warp - W_EW0) >> 2;    // column group of this warp: tile columns [EWC gw, EWC gw + EWC)
+    const int cg0 = gw * EWH;              // its first 16-column group
     const int qd = warp & 3;               // TMEM lane quarter
     const int m = qd * 32 + lane;          // row within the block (= TMEM lane)
     const uint32_t lane_off = (uint32_t)(qd * 32) << 16;
-    int yoff, yswz;
-    ew_y_line(a, cg >> 1, m, yoff, yswz);
+    int yoff[EWH], yswz[EWH];
+#pragma unroll
+    for (int h = 0; h < EWH; ++h) ew_y_line(a, (cg0 + h) >> 1, m, yoff[h], yswz[h]);
     const int64_t row = row0 + m;
     const bool row_ok = m < rows_here;
     constexpr int NCH = KB / 16;           // 16-column chunks of U_hi (and of U_lo, N, D)
-    // U -> TMEM, split hi / lo: the 2 NCH chunks are shared out among the 4 column groups
+    constexpr int NGW = NEW / 4;           // column groups of elementwise warps
+    // U -> TMEM, split hi / lo: the 2 NCH chunks are shared out among the column groups
     {
 #pragma unroll 1
-      for (int c = cg * (2 * NCH / 4); c < (cg + 1) * (2 * NCH / 4); ++c) {
+      for (int c = gw * (2 * NCH / NGW); c < (gw + 1) * (2 * NCH / NGW); ++c) {
         const bool lo = c >= NCH;
         const int h = lo ? c - NCH : c;
         uint32_t r[16];
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
           const int k = h * 16 + j;
-          const float u = (row_ok && k < a.K) ? __ldg(a.U + row * a.K + k) : 0.f;
+          const float u = (row_ok && k < a.K) ? __ldg(a.Ur[rs] + row * a.K + k) : 0.f;
           const uint32_t hi = tf32_bits(u);
           r[j] = lo ? tf32_bits(u - __uint_as_float(hi)) : hi;
         }
@@ -1320,10 +1313,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
     auto drain_nd = [&](int64_t grp, bool zero) {
       const int64_t elems = a.n_rows * (int64_t)a.K;
 #pragma unroll 1
-      for (int c = cg * (2 * NCH / 4); c < (cg + 1) * (2 * NCH / 4); ++c) {
+      for (int c = gw * (2 * NCH / NGW); c < (gw + 1) * (2 * NCH / NGW); ++c) {
         const int which = c >= NCH ? 1 : 0;
         const int h = which ? c - NCH : c;
-        float* out = a.Qpart + ((ch * a.n_groups + grp) * 2 + which) * elems + row * a.K + h * 16;
+        float* out = a.Qpartr[rs] + ((ch * a.n_groups + grp) * 2 + which) * elems + row * a.K + h * 16;
         uint32_t r[16];
         if (!zero) {
           tmem_ld16((which ? tNb : tNa) + lane_off + h * 16, r);
@@ -1354,60 +1347,59 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
     int tin = (int)(a.layout == 0 ? t_begin : t_begin % a.tiles_inner);
     int b = 0;           // tile buffer t % NBUF
     uint32_t bph = 0;    // (t / NBUF) & 1
+    int st = 0;          // Y stage t % NS
+    uint32_t sph = 0;    // (t / NS) & 1
+    const uint32_t tlane = tmem + lane_off + 16 * cg0;   // this warp's columns in a tile buffer
     for (int t = 0; t < T; ++t, ++tin) {
       if (tin >= tiles_blk) tin = 0;
       const int64_t crem = cext - (int64_t)tin * BN;
       const int cols_here = (int)(crem < BN ? crem : BN);
-      const int st = t % NS;
-      const uint32_t tc = tmem + buf_col(b) + lane_off + 16 * cg;   // S / P_a columns of this warp
+      const uint32_t tc = tlane + buf_col(b);   // S / P_a columns of this warp
       float lsum[3] = {0.f, 0.f, 0.f};
-      uint32_t sv[16], pb[16], pl[16];
-      float yv[16];
-      uint32_t mk[4] = {0u, 0u, 0u, 0u};
-#if NEF_Y_FIRST
-      // Y(t) landed long before S(t) (the TMA runs NS tiles ahead): its shared loads issued
-      // before the wait for S (measured: no gain, default off)
-      mbar_spin(y_full + 8 * st, (t / NS) & 1);
-      if (warp == W_EW0 && lane == 0) trace_ev(a, t, EV_EW_Y);
-      ew_load_y(a, gY + st * Y_STAGE, gM + st * M_STAGE, cg >> 1, cg & 1, m, yoff, yswz, yv, mk);   // (MM == 0: a.has_mask = 0)
+      uint32_t sv[EWH][16], pb[EWH][16], pl[EWH][16];
+      float yv[EWH][16];
+      uint32_t mk[EWH][4];
       mbar_wait_ew(s_full + 8 * b, bph);
       if (warp == W_EW0 && lane == 0) trace_ev(a, t, EV_EW_S);
       tc_fence_after();
-      tmem_ld16(tc, sv);
-#else
-#if NEF_EW_BAR
-      // one elementwise warp polls S(t)'s barrier; the other 15 block on a named barrier (no
-      // polling: their issue slots go to the warps that compute)
-      if (warp == W_EW0 + NEW - 1) mbar_wait_ew(s_full + 8 * b, bph);
-      asm volatile("bar.sync 2, %0;" ::"n"(NEW * 32) : "memory");
-#else
-      mbar_wait_ew(s_full + 8 * b, bph);
-#endif
-      if (warp == W_EW0 && lane == 0) trace_ev(a, t, EV_EW_S);
-      tc_fence_after();
-      tmem_ld16(tc, sv);
-      mbar_spin(y_full + 8 * st, (t / NS) & 1);
+#pragma unroll
+      for (int h = 0; h < EWH; ++h) tmem_ld16(tc + 16 * h, sv[h]);
+      mbar_spin(y_full + 8 * st, sph);
       if (warp == W_EW0 && lane == 0) trace_ev(a, t, EV_EW_Y);
-      ew_load_y(a, gY + st * Y_STAGE, gM + st * M_STAGE, cg >> 1, cg & 1, m, yoff, yswz, yv, mk);   // (MM == 0: a.has_mask = 0)
-#endif
-      tmem_ld_wait(sv);
+#pragma unroll
+      for (int h = 0; h < EWH; ++h) {
+        mk[h][0] = mk[h][1] = mk[h][2] = mk[h][3] = 0u;
+        ew_load_y(a, gY + st * Y_STAGE, gM + st * M_STAGE, (cg0 + h) >> 1, (cg0 + h) & 1, m, yoff[h], yswz[h], yv[h],
+                  mk[h]);   // (MM == 0: a.has_mask = 0)
+      }
+#pragma unroll
+      for (int h = 0; h < EWH; ++h) tmem_ld_wait(sv[h]);
       __syncwarp();
       if (lane == 0) mbar_arrive(y_empty + 8 * st);  // Y / mask stage read by this warp
-      if (!(NEF_DBG & 256)) {
-        if (MM == 1) ew_half<KIND, SPA>(a, sv, yv, mk, cols_here - 16 * cg, row_ok, pb, pl, lsum, cnt);
-        else ew_half_sent<KIND, SPA>(a, sv, yv, cols_here - 16 * cg, row_ok, pb, pl, loss_acc[0], cnt[0]);
-      } else {   // NEF_DBG 256: timing experiment without the elementwise math (P_b = S + Y)
 #pragma unroll
-        for (int j = 0; j < 16; ++j) pb[j] = sv[j] + __float_as_uint(yv[j]) + mk[j >> 2];
+      for (int h = 0; h < EWH; ++h) {
+        const int cv = cols_here - 16 * (cg0 + h);
+        if (!(NEF_DBG & 256)) {
+          if (MM == 1) ew_half<KIND, SPA>(a, sv[h], yv[h], mk[h], cv, row_ok, pb[h], pl[h], lsum, cnt);
+          else ew_half_sent<KIND, SPA>(a, sv[h], yv[h], cv, row_ok, pb[h], pl[h], loss_acc[0], cnt[0]);
+        } else {   // NEF_DBG 256: timing experiment without the elementwise math (P_b = S + Y)
+#pragma unroll
+          for (int j = 0; j < 16; ++j) pb[h][j] = sv[h][j] + __float_as_uint(yv[h][j]) + mk[h][j >> 2];
+        }
       }
       if (a.mode != 2) {
-        tmem_st16(tc, sv);
-        tmem_st16(tc + 64, pb);
-        if constexpr (SPA) tmem_st16(tmem + 384 + 64 * b + lane_off + 16 * cg, pl);
-      }
-      if (t == 0 && a.debug && blockIdx.x == 0 && blockIdx.y == 0) {   // test hook (nef_debug_dump)
 #pragma unroll
-        for (int j = 0; j < 16; ++j) a.debug[m * 64 + 16 * cg + j] = __uint_as_float(sv[j] & 0xffffe000u);
+        for (int h = 0; h < EWH; ++h) {
+          tmem_st16(tc + 16 * h, sv[h]);
+          tmem_st16(tc + 16 * h + 64, pb[h]);
+          if constexpr (SPA) tmem_st16(tmem + 384 + 64 * b + lane_off + 16 * (cg0 + h), pl[h]);
+        }
+      }
+      if (t == 0 && a.debug && blockIdx.x == 0 && blockIdx.y == 0 && rs == 0) {   // test hook (nef_debug_dump)
+#pragma unroll
+        for (int h = 0; h < EWH; ++h)
+#pragma unroll
+          for (int j = 0; j < 16; ++j) a.debug[m * 64 + 16 * (cg0 + h) + j] = __uint_as_float(sv[h][j] & 0xffffe000u);
       }
       if (warp == W_EW0 && lane == 0) trace_ev(a, t, EV_EW_HALF);
       if (a.mode != 2) tmem_st_wait();
@@ -1428,6 +1420,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
         drain_nd(t / G, false);
       }
       if (++b == NBUF) { b = 0; bph ^= 1; }
+      if (++st == NS) { st = 0; sph ^= 1; }
     }
     // epilogue: the last group's N | D -> split partials (added to the earlier groups' drains)
     if (a.mode != 2) {
@@ -1456,8 +1449,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
           asm volatile("bar.sync 1, %0;" ::"n"(NEW * 32) : "memory");
         }
         if (ew == 0) {
-          a.losspart[q * parts + id] = gRed[0];
-          a.countpart[q * parts + id] = gRedC[0];
+          a.losspartr[rs][q * parts + id] = gRed[0];
+          a.countpartr[rs][q * parts + id] = gRedC[0];
         }
         asm volatile("bar.sync 1, %0;" ::"n"(NEW * 32) : "memory");
       }
@@ -1573,17 +1566,27 @@ cudaError_t launch(const TcArgs& args, const float* Y, const uint8_t* M, int64_t
       ok = encode(&P.tmM, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, M, d, sm, bm, CU_TENSOR_MAP_SWIZZLE_64B);
     }
   }
-  if (ok && args.vdirect) {
+  // restart arrays: a single launch is restart 0 = the plain fields
+  if (P.a.nrs < 1) {
+    P.a.nrs = 1;
+    P.a.Ur[0] = args.U;
+    for (int q = 0; q < kMaxTabs; ++q) P.a.tabr[0][q] = args.tab[q];
+    P.a.Qpartr[0] = args.Qpart;
+    P.a.losspartr[0] = args.losspart;
+    P.a.countpartr[0] = args.countpart;
+    P.a.vdr[0] = args.vd_rows_ptr;
+  }
+  if (P.a.nrs > 1 && !args.vdirect) return cudaErrorInvalidValue;
+  for (int r = 0; ok && args.vdirect && r < P.a.nrs; ++r) {
     // table rows [var_rows][K] -> V stage, two 32-float SW128 boxes (K beyond the row: zeros)
     uint64_t d[2] = {(uint64_t)args.K, (uint64_t)args.var_rows};
     uint64_t sv[1] = {(uint64_t)args.vd_pitch * 4};
     uint32_t bv[2] = {32, 64};
-    ok = encode(&P.tmV, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, args.vd_rows_ptr, d, sv, bv,
-                CU_TENSOR_MAP_SWIZZLE_128B);
+    ok = encode(&P.tmV[r], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, P.a.vdr[r], d, sv, bv, CU_TENSOR_MAP_SWIZZLE_128B);
   }
   if (!ok) return cudaErrorInvalidValue;
   P.a.has_mask = M ? 1 : 0;
-  dim3 grid((unsigned)row_blocks, (unsigned)chunks);
+  dim3 grid((unsigned)row_blocks, (unsigned)chunks, (unsigned)P.a.nrs);
   return dispatch_ew(args.dv.kind, TcLauncher{P, grid, s, args.KB, M ? 1 : 0});
 }
 

@@ -29,6 +29,16 @@ struct TcArgs {
   float* Qpart;               // [chunks][n_groups][2][n_rows][K]
   double* losspart;           // [row_blocks * chunks]
   long long* countpart;
+  // batched restarts (N4): launch z index rs runs restart rs on the same Y tiles (its CTAs
+  // stream the tiles the rs = 0 CTAs of the same (row block, chunk) fetch, from L2).  Index 0 is
+  // the fields above; direct-V launches only.
+  int nrs;
+  const float* Ur[kMaxRestarts];
+  const float* tabr[kMaxRestarts][kMaxTabs];
+  float* Qpartr[kMaxRestarts];
+  double* losspartr[kMaxRestarts];
+  long long* countpartr[kMaxRestarts];
+  const float* vdr[kMaxRestarts];   // direct-V table rows per restart (tensor map source)
   DivParams dv;
   int mode;                   // 0 update, 1 update + loss, 2 loss only
   float* debug;               // optional debug dump (first tile of CTA (0,0))

@@ -12,6 +12,7 @@ namespace nef {
 constexpr int kMaxDims = 8;      // max indices per operand / per einsum step side
 constexpr int kMaxTabs = 4;      // max KR tables on the column side of a lowering
 constexpr int kMaxModes = 8;     // max observed modes
+constexpr int kMaxRestarts = 4;  // restarts sharing one streamed pass (N4)
 constexpr int kSentParts = 148 * 16 + 1;   // sentinel pass block partials (kernels.h kSentBlocks + 1)
 // tcgen05 path: the tensor core's fp32 accumulation truncates, so the numerator / denominator
 // accumulators are drained to separate split partials every kDrainTiles tiles (<= 2048

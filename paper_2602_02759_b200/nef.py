@@ -65,6 +65,9 @@ def _load():
         "nef_num_den_ex": (ctypes.c_int, [vp, ctypes.c_int, vp, vp, vp, vp, vp, vp, vp, ctypes.c_size_t, vp]),
         "nef_apply_update_ex": (ctypes.c_int, [vp, ctypes.c_int, vp, d, vp, vp, vp, vp]),
         "nef_loss_ex": (ctypes.c_int, [vp, vp, vp, vp, vp, ctypes.POINTER(d), i64p, vp, ctypes.c_size_t, vp]),
+        "nef_restarts_workspace_bytes": (ctypes.c_size_t, [vp, ctypes.c_int]),
+        "nef_fit_restarts": (ctypes.c_int, [vp, vp, vp, vp, d, vp, ctypes.c_int, ctypes.c_int, ctypes.POINTER(d), vp,
+                                            ctypes.c_size_t, vp]),
         "nef_plan_destroy": (None, [vp]),
         "nef_last_error": (ctypes.c_char_p, []),
         "nef_version": (ctypes.c_char_p, []),
@@ -82,7 +85,7 @@ EXPORTED = ("nef_plan", "nef_plan_info", "nef_factor_shape", "nef_local_shape", 
             "nef_nccl_unique_id", "nef_plan_shard", "nef_plan_shard_host", "nef_last_launch_count",
             "nef_set_kernel_policy",
             "nef_profile_enable", "nef_profile_read", "nef_debug_dump", "nef_debug_trace",
-            "nef_fit_ex", "nef_fit_split", "nef_update_ex", "nef_num_den_ex", "nef_apply_update_ex", "nef_loss_ex",
+            "nef_fit_ex", "nef_fit_split", "nef_restarts_workspace_bytes", "nef_fit_restarts", "nef_update_ex", "nef_num_den_ex", "nef_apply_update_ex", "nef_loss_ex",
             "nef_plan_destroy", "nef_last_error", "nef_version")
 
 LOSS_KINDS = {"ab": 0, "negbin": 1, "bernoulli": 2, "binomial": 3, "js": 4}
@@ -314,6 +317,22 @@ def nef_fit_split(h, Y, labels, spec, eps, factors, max_iters, min_rel_decrease,
     return dict(traces=traces, counts=[int(c) for c in counts], sweeps=n, reason=STOP_REASONS.get(reason.value, "?"))
 
 
+def nef_restarts_workspace_bytes(h, restarts):
+    return int(LIB.nef_restarts_workspace_bytes(h, int(restarts)))
+
+
+def nef_fit_restarts(h, Y, mask, spec, eps, restart_factors, iters, workspace, stream=None):
+    """restart_factors: list (restarts) of factor lists; returns the loss traces, restarts x (iters + 1)."""
+    S = len(restart_factors)
+    for F in restart_factors:
+        _validate(h, Y, mask, F)
+    flat = [f for F in restart_factors for f in F]
+    tr = (ctypes.c_double * (S * (iters + 1)))()
+    _check(LIB.nef_fit_restarts(h, _ptr(Y), _ptr(mask), ctypes.byref(spec), float(eps), _fptrs(flat), S, int(iters), tr,
+                                _ptr(workspace), workspace.numel(), _stream(stream)))
+    return np.array(tr[:], dtype=np.float64).reshape(S, iters + 1)
+
+
 def nef_update_ex(h, ell, Y, mask, spec, eps, factors, workspace, stream=None):
     _validate(h, Y, mask, factors)
     _check(LIB.nef_update_ex(h, int(ell), _ptr(Y), _ptr(mask), ctypes.byref(spec), float(eps), _fptrs(factors),
@@ -475,6 +494,12 @@ class Plan:
                   stream=None, aux=None):
         return nef_fit_split(self.h, Y, labels, spec, eps, factors, max_iters, min_rel_decrease, val_patience,
                              self.workspace(Y.device), stream, aux)
+
+    def fit_restarts(self, Y, mask, spec, restart_factors, iters, eps=1e-12, stream=None):
+        import torch
+        need = nef_restarts_workspace_bytes(self.h, len(restart_factors))
+        ws = torch.empty(need, dtype=torch.uint8, device=Y.device)
+        return nef_fit_restarts(self.h, Y, mask, spec, eps, restart_factors, iters, ws, stream)
 
     def num_den_ex(self, ell, Y, mask, spec, factors, stream=None):
         import torch
