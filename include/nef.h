@@ -245,8 +245,10 @@ int64_t nef_last_launch_count(void);
 int nef_profile_enable(int enable);
 int nef_profile_read(double* kernel_ms, int64_t* launches, double* algorithmic_bytes);
 
-/* Select the streaming kernel: 0 = automatic (tcgen05 where supported), 1 = CUDA-core FFMA
- * kernel only.  Process-wide; for tests and A/B measurement. */
+/* Select the streaming kernel: bit 0 clear = automatic (tcgen05 where supported), set = CUDA-core
+ * FFMA kernel only; bit 1 set = no sweep graphs (nef_fit then launches every kernel of every sweep
+ * itself instead of replaying its cached one-sweep CUDA graph).  Process-wide; for tests and A/B
+ * measurement. */
 int nef_set_kernel_policy(int policy);
 
 /* Test hook: when device_buffer != NULL the tcgen05 streaming kernel writes the P_a tile

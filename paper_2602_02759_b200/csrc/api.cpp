@@ -24,8 +24,26 @@
 #include "nef_internal.h"
 #include "../../include/nef.h"
 
+// A captured sweep of nef_fit (CUDA graph, replayed once per sweep; see sweep_graph below)
+struct SweepGraph {
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t exec = nullptr;
+  std::string key;                         // the inputs it was captured for (pointers, loss, flags)
+  std::vector<cudaGraphNode_t> ev_nodes;   // event-record nodes of the streaming launches, in order
+  std::vector<cudaEvent_t> own;            // the events they record when profiling is off
+  std::vector<double> bytes;               // algorithmic bytes of each streaming launch
+  bool on_prof = false;                    // nodes currently point at profiling events
+  ~SweepGraph() {
+    if (exec) cudaGraphExecDestroy(exec);
+    if (graph) cudaGraphDestroy(graph);
+    for (auto e : own) cudaEventDestroy(e);
+  }
+};
+
 struct nef_plan_s {
   nef::Plan p;
+  SweepGraph* g = nullptr;   // cached sweep graph (one entry: the last input set)
+  ~nef_plan_s() { delete g; }
 };
 
 namespace {
@@ -41,28 +59,50 @@ bool g_no_sqy = std::getenv("NEF_NO_SQY") != nullptr;           // diagnostics: 
 // diagnostics: NEF_TC_VDIRECT=0 generates V per tile instead of TMA-loading direct-V table rows
 bool g_vdirect = [] { const char* e = std::getenv("NEF_TC_VDIRECT"); return !e || std::atoi(e) != 0; }();
 
+bool g_graphs = [] { const char* e = std::getenv("NEF_NO_GRAPH"); return !e || e[0] != '1'; }();   // diagnostics
+
 // live CUDA-event timing of the streaming kernel (nef_profile_*)
 struct Prof {
   bool on = false;
   std::vector<cudaEvent_t> ev;   // pairs (start, end)
   size_t used = 0;               // number of pairs recorded since enable
   double bytes = 0;
+  SweepGraph* cap = nullptr;     // a sweep graph being captured: its own events, as graph nodes
 };
 Prof g_prof;
 
-void prof_begin(cudaStream_t s) {
-  if (!g_prof.on) return;
+bool prof_reserve() {
   if (2 * g_prof.used + 2 > g_prof.ev.size()) {
     for (int k = 0; k < 64; ++k) {
       cudaEvent_t e;
-      if (cudaEventCreate(&e) != cudaSuccess) { g_prof.on = false; return; }
+      if (cudaEventCreate(&e) != cudaSuccess) { g_prof.on = false; return false; }
       g_prof.ev.push_back(e);
     }
   }
+  return true;
+}
+
+void prof_begin(cudaStream_t s) {
+  if (g_prof.cap) {   // capture: an external event-record node (re-pointed at every replay)
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    g_prof.cap->own.push_back(e);
+    cudaEventRecordWithFlags(e, s, cudaEventRecordExternal);
+    return;
+  }
+  if (!g_prof.on || !prof_reserve()) return;
   cudaEventRecord(g_prof.ev[2 * g_prof.used], s);
 }
 
 void prof_end(cudaStream_t s, double bytes) {
+  if (g_prof.cap) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    g_prof.cap->own.push_back(e);
+    g_prof.cap->bytes.push_back(bytes);
+    cudaEventRecordWithFlags(e, s, cudaEventRecordExternal);
+    return;
+  }
   if (!g_prof.on) return;
   cudaEventRecord(g_prof.ev[2 * g_prof.used + 1], s);
   g_prof.used++;
@@ -577,6 +617,106 @@ int validate_spec(const nef_loss_spec* l, Spec& sp) {
   return NEF_OK;
 }
 
+// ------------------------------------------------------------------ sweep graphs
+// One sweep of nef_fit captured as a CUDA graph (cached per plan for one input set): the loss of
+// the iterate entering the sweep goes to a fixed slot and a one-thread kernel appends it to the
+// trace at a device-side counter, so the graph is identical for every sweep.  The streaming
+// launches keep their CUDA-event timing as external event-record nodes, re-pointed at fresh
+// profiling events before each replay when nef_profile is on.
+std::string sweep_key(const Ctx& c, const float* Y, const uint8_t* M, const nef::DivParams& dv, const nef::UpdArgs& u) {
+  std::string k;
+  char buf[64];
+  auto add = [&](const void* q) { std::snprintf(buf, sizeof buf, "%p,", q); k += buf; };
+  add(Y); add(M); add(c.ws); add(c.ysent); add(c.loff); add(c.aux);
+  for (size_t l = 0; l < c.p->ops.size(); ++l) add(c.F[l]);
+  std::snprintf(buf, sizeof buf, "%zu,%d,%d,%d,%.17g,", c.ws_bytes, g_policy, (int)g_vdirect, (int)c.sqy, c.lscale);
+  k += buf;
+  k.append(reinterpret_cast<const char*>(&dv), sizeof dv);
+  k.append(reinterpret_cast<const char*>(&u), sizeof u);
+  return k;
+}
+
+int update_one(const Ctx& c, int ell, const float* Y, const uint8_t* M, const nef::DivParams& dv, const nef::UpdArgs& u,
+               int mode, double* slot, long long* cslot);
+
+SweepGraph* sweep_graph(nef_plan_t plan, const Ctx& c, const float* Y, const uint8_t* M, const nef::DivParams& dv,
+                        const nef::UpdArgs& u, double* slots, long long* cslots) {
+  const std::string key = sweep_key(c, Y, M, dv, u);
+  if (plan->g && plan->g->key == key) return plan->g;
+  delete plan->g;
+  plan->g = nullptr;
+  auto* sg = new SweepGraph();
+  sg->key = key;
+  const int kSlots = 2048;
+  double* fixed = slots + kSlots - 2;
+  long long* cfixed = cslots + kSlots - 2;
+  long long* ctr = cslots + kSlots - 1;
+  const int64_t launches0 = g_launches;
+  if (cudaStreamBeginCapture(c.s, cudaStreamCaptureModeThreadLocal) != cudaSuccess) { delete sg; return nullptr; }
+  g_prof.cap = sg;
+  int st = NEF_OK;
+  for (int ell = 0; ell < (int)c.p->ops.size() && !st; ++ell)
+    st = update_one(c, ell, Y, M, dv, u, ell == 0 ? 1 : 0, fixed, cfixed);
+  if (!st && nef::launch_slot_push(fixed, cfixed, slots, cslots, ctr, c.s) != cudaSuccess) st = NEF_E_CUDA;
+  g_prof.cap = nullptr;
+  cudaGraph_t graph = nullptr;
+  const cudaError_t ec = cudaStreamEndCapture(c.s, &graph);
+  g_launches = launches0;
+  if (st || ec != cudaSuccess || !graph) {
+    if (graph) cudaGraphDestroy(graph);
+    cudaGetLastError();
+    delete sg;
+    return nullptr;
+  }
+  sg->graph = graph;
+  if (cudaGraphInstantiate(&sg->exec, graph, 0) != cudaSuccess) {
+    cudaGetLastError();
+    delete sg;
+    return nullptr;
+  }
+  // event-record nodes in capture order (matched through their events)
+  size_t nn = 0;
+  cudaGraphGetNodes(graph, nullptr, &nn);
+  std::vector<cudaGraphNode_t> nodes(nn);
+  cudaGraphGetNodes(graph, nodes.data(), &nn);
+  sg->ev_nodes.assign(sg->own.size(), nullptr);
+  for (auto nd : nodes) {
+    cudaGraphNodeType ty;
+    cudaGraphNodeGetType(nd, &ty);
+    if (ty != cudaGraphNodeTypeEventRecord) continue;
+    cudaEvent_t e;
+    cudaGraphEventRecordNodeGetEvent(nd, &e);
+    for (size_t i = 0; i < sg->own.size(); ++i)
+      if (sg->own[i] == e) sg->ev_nodes[i] = nd;
+  }
+  for (auto nd : sg->ev_nodes)
+    if (!nd) { delete sg; return nullptr; }
+  plan->g = sg;
+  return sg;
+}
+
+int replay_sweep(SweepGraph* sg, cudaStream_t s) {
+  const size_t nl = sg->bytes.size();   // streaming launches per sweep
+  if (g_prof.on) {
+    for (size_t i = 0; i < nl; ++i) {
+      if (!prof_reserve()) break;
+      cudaGraphExecEventRecordNodeSetEvent(sg->exec, sg->ev_nodes[2 * i], g_prof.ev[2 * g_prof.used]);
+      cudaGraphExecEventRecordNodeSetEvent(sg->exec, sg->ev_nodes[2 * i + 1], g_prof.ev[2 * g_prof.used + 1]);
+      g_prof.used++;
+      g_prof.bytes += sg->bytes[i];
+    }
+    sg->on_prof = true;
+  } else if (sg->on_prof) {
+    for (size_t i = 0; i < sg->own.size(); ++i) cudaGraphExecEventRecordNodeSetEvent(sg->exec, sg->ev_nodes[i], sg->own[i]);
+    sg->on_prof = false;
+  }
+  CK(cudaGraphLaunch(sg->exec, s));
+  size_t n = 0;
+  cudaGraphGetNodes(sg->graph, nullptr, &n);
+  g_launches += (int64_t)(n - sg->own.size());   // kernel (and push) nodes of the sweep
+  return NEF_OK;
+}
+
 int check_device() {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
@@ -627,8 +767,9 @@ int nef_debug_trace(int64_t* device_buffer) {
 }
 
 int nef_set_kernel_policy(int policy) {
-  if (policy < 0 || policy > 1) return fail(NEF_E_ARG, "policy must be 0 or 1");
-  g_policy = policy;
+  if (policy < 0 || policy > 3) return fail(NEF_E_ARG, "policy must be 0..3");
+  g_policy = policy & 1;
+  g_graphs = (policy & 2) == 0 && [] { const char* e = std::getenv("NEF_NO_GRAPH"); return !e || e[0] != '1'; }();
   return NEF_OK;
 }
 
@@ -762,7 +903,20 @@ int nef_fit_ex(nef_plan_t plan, const float* Y, const uint8_t* mask, const nef_l
     base = upto;
     return NEF_OK;
   };
-  for (int t = 0; t < iters; ++t) {
+  // Sweeps: replay a captured one-sweep CUDA graph (launch-bound small problems: one submission
+  // per sweep instead of ~25) when the plan runs on one rank and the trace fits the slots; else
+  // launch the sweep's kernels one by one.
+  int t0 = 0;
+  if (g_graphs && !communicates(p) && iters >= 2 && iters + 1 <= kSlots - 2) {
+    SweepGraph* sg = sweep_graph(plan, c, Y, mask, dv, u, slots, cslots);
+    if (sg) {
+      CK(cudaMemsetAsync(cslots + kSlots - 1, 0, sizeof(long long), c.s));   // slot counter
+      for (int t = 0; t < iters; ++t)
+        if ((st = replay_sweep(sg, c.s))) return st;
+      t0 = iters;
+    }
+  }
+  for (int t = t0; t < iters; ++t) {
     if (t - base >= kSlots) { if ((st = flush(t))) return st; }
     for (int ell = 0; ell < (int)p.ops.size(); ++ell) {
       int mode = (ell == 0) ? 1 : 0;

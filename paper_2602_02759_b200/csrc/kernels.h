@@ -108,5 +108,7 @@ cudaError_t launch_reduce_update(const float* Qpart, float* theta, int64_t n_chu
 cudaError_t launch_loss_reduce(const double* part, const long long* cpart, int64_t n, double* slot,
                                long long* cslot, cudaStream_t s, double scale = 1.0, const double* off = nullptr);
 
-// Loss sum via the planner's lowering 0 (no update)
+// Captured sweeps (nef_fit's CUDA graph): slots[*ctr] = *v, cslots[*ctr] = *c, ++*ctr
+cudaError_t launch_slot_push(const double* v, const long long* c, double* slots, long long* cslots, long long* ctr,
+                             cudaStream_t s);
 }  // namespace nef

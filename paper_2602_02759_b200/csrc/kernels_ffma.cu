@@ -675,6 +675,19 @@ __global__ void sentinel_tail_kernel(const float* __restrict__ Y, const uint8_t*
 
 __global__ void set_count_kernel(long long* c, long long n) { *c = n; }
 
+// sweep-graph loss slot: slots[*ctr] = *v, cslots[*ctr] = *c, ++*ctr (one thread)
+__global__ void slot_push_kernel(const double* v, const long long* c, double* slots, long long* cslots, long long* ctr) {
+  const long long i = *ctr;
+  slots[i] = *v;
+  cslots[i] = *c;
+  *ctr = i + 1;
+}
+cudaError_t launch_slot_push(const double* v, const long long* c, double* slots, long long* cslots, long long* ctr,
+                             cudaStream_t s) {
+  slot_push_kernel<<<1, 1, 0, s>>>(v, c, slots, cslots, ctr);
+  return cudaGetLastError();
+}
+
 __global__ void pad_rows_kernel(const float* __restrict__ src, float* __restrict__ dst, long long rows, int K, int Kp) {
   const long long n = rows * Kp;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {

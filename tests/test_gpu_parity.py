@@ -239,3 +239,26 @@ def test_loss_trajectory_tcgen05(nef, name, shape, iters, record_err):
     record_err(_rel(tr, rtr), TRACE_RTOL, "tcgen05 trajectory %d sweeps" % iters)
     assert _rel(tr, rtr) <= TRACE_RTOL, (name, _rel(tr, rtr))
     assert all(b <= a * (1 + 1e-5) for a, b in zip(tr, tr[1:]))
+
+
+@pytest.mark.parametrize("name", ["c2", "c4", "c1"])
+def test_sweep_graph_bit_identical(nef, name):
+    """nef_fit replays a captured one-sweep CUDA graph (cached per plan and input set); the
+    factors and the trace are bit-identical to launching every kernel of every sweep, on the
+    first (capturing) call and on a second call that reuses the cached graph."""
+    d = generate_numpy(name)
+    Y, M, F0 = _dev(d)
+    plan = nef.Plan(d["model"], d["shape"], d["ranks"])
+    runs = []
+    F = [f.clone() for f in F0]
+    for policy in (2, 0, 0):   # plain launches; graph captured; the same inputs: cached graph replayed
+        nef.nef_set_kernel_policy(policy)
+        for f, f0 in zip(F, F0):
+            f.copy_(f0)
+        tr = plan.fit(Y, M, d["alpha"], d["beta"], F, 4)
+        runs.append(([f.cpu() for f in F], tr))
+    nef.nef_set_kernel_policy(0)
+    for Fa, ta in runs[1:]:
+        for a, b in zip(runs[0][0], Fa):
+            assert torch.equal(a, b)
+        assert np.array_equal(runs[0][1], ta)
