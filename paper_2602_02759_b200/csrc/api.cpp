@@ -42,8 +42,14 @@ struct SweepGraph {
 
 struct nef_plan_s {
   nef::Plan p;
-  SweepGraph* g = nullptr;   // cached sweep graph (one entry: the last input set)
-  ~nef_plan_s() { delete g; }
+  SweepGraph* g = nullptr;            // cached sweep graph (one entry: the last input set)
+  cudaStream_t cap_stream = nullptr;  // private stream the sweep is captured on (the caller's may be
+                                      // the legacy default stream, which cannot be captured)
+  bool graph_failed = false;          // a capture failed: this plan launches kernel by kernel
+  ~nef_plan_s() {
+    delete g;
+    if (cap_stream) cudaStreamDestroy(cap_stream);
+  }
 };
 
 namespace {
@@ -643,8 +649,16 @@ SweepGraph* sweep_graph(nef_plan_t plan, const Ctx& c, const float* Y, const uin
                         const nef::UpdArgs& u, double* slots, long long* cslots) {
   const std::string key = sweep_key(c, Y, M, dv, u);
   if (plan->g && plan->g->key == key) return plan->g;
+  if (plan->graph_failed) return nullptr;
   delete plan->g;
   plan->g = nullptr;
+  if (!plan->cap_stream && cudaStreamCreateWithFlags(&plan->cap_stream, cudaStreamNonBlocking) != cudaSuccess) {
+    cudaGetLastError();
+    plan->graph_failed = true;
+    return nullptr;
+  }
+  Ctx cc = c;                 // captured on the private stream; replayed on the caller's
+  cc.s = plan->cap_stream;
   auto* sg = new SweepGraph();
   sg->key = key;
   const int kSlots = 2048;
@@ -652,25 +666,34 @@ SweepGraph* sweep_graph(nef_plan_t plan, const Ctx& c, const float* Y, const uin
   long long* cfixed = cslots + kSlots - 2;
   long long* ctr = cslots + kSlots - 1;
   const int64_t launches0 = g_launches;
-  if (cudaStreamBeginCapture(c.s, cudaStreamCaptureModeThreadLocal) != cudaSuccess) { delete sg; return nullptr; }
+  const std::string err0 = g_err;
+  if (cudaStreamBeginCapture(cc.s, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+    cudaGetLastError();
+    plan->graph_failed = true;
+    delete sg;
+    return nullptr;
+  }
   g_prof.cap = sg;
   int st = NEF_OK;
   for (int ell = 0; ell < (int)c.p->ops.size() && !st; ++ell)
-    st = update_one(c, ell, Y, M, dv, u, ell == 0 ? 1 : 0, fixed, cfixed);
-  if (!st && nef::launch_slot_push(fixed, cfixed, slots, cslots, ctr, c.s) != cudaSuccess) st = NEF_E_CUDA;
+    st = update_one(cc, ell, Y, M, dv, u, ell == 0 ? 1 : 0, fixed, cfixed);
+  if (!st && nef::launch_slot_push(fixed, cfixed, slots, cslots, ctr, cc.s) != cudaSuccess) st = NEF_E_CUDA;
   g_prof.cap = nullptr;
   cudaGraph_t graph = nullptr;
-  const cudaError_t ec = cudaStreamEndCapture(c.s, &graph);
+  const cudaError_t ec = cudaStreamEndCapture(cc.s, &graph);
   g_launches = launches0;
-  if (st || ec != cudaSuccess || !graph) {
+  if (st || ec != cudaSuccess || !graph) {   // fall back to plain launches for this plan
     if (graph) cudaGraphDestroy(graph);
     cudaGetLastError();
+    g_err = err0;
+    plan->graph_failed = true;
     delete sg;
     return nullptr;
   }
   sg->graph = graph;
   if (cudaGraphInstantiate(&sg->exec, graph, 0) != cudaSuccess) {
     cudaGetLastError();
+    plan->graph_failed = true;
     delete sg;
     return nullptr;
   }

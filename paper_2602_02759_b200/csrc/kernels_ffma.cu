@@ -429,9 +429,11 @@ __global__ void einstep_kernel(const __grid_constant__ EinStepDev st, const floa
   const I chunk = (I)((st.sum_size + L - 1) / L);
   const I s0 = (I)lane * chunk;
   const I s1 = (I)((long long)s0 + chunk < st.sum_size ? (long long)s0 + chunk : st.sum_size);
-  // the loop bound is uniform across the L lanes of an output (L divides the block size)
-  for (long long o = gt / L; o < st.out_size; o += stride) {
-    I rem = (I)o, ao = 0, bo = 0;
+  // warp-uniform trip count: the L lanes of an output combine with whole-warp shuffles
+  for (long long o = gt / L;; o += stride) {
+    const bool valid = o < st.out_size;
+    if (L > 1 ? __all_sync(0xffffffffu, !valid) : !valid) break;
+    I rem = (I)(valid ? o : 0), ao = 0, bo = 0;
     for (int d = st.nout - 1; d >= 0; --d) {
       const I od = (I)st.odim[d];
       const I i = rem % od;
@@ -451,7 +453,7 @@ __global__ void einstep_kernel(const __grid_constant__ EinStepDev st, const floa
       }
     }
     double acc = 0.0;
-    for (I s = s0; s < s1; ++s) {
+    for (I s = s0; valid && s < s1; ++s) {
       double v = (double)__ldg(A + ao);
       if (B) v *= (double)__ldg(B + bo);
       acc += v;
@@ -468,28 +470,36 @@ __global__ void einstep_kernel(const __grid_constant__ EinStepDev st, const floa
 #pragma unroll
       for (int w = L / 2; w > 0; w >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, w);
     }
-    if (lane == 0) C[o] = (float)acc;
+    if (valid && lane == 0) C[o] = (float)acc;
   }
 }
 
-// Fast path for the common step shape: ONE summed index of at most 64 terms and at most three
-// output indices (the side operands and epilogues of CP / Tucker / the paper's custom models,
-// e.g. T[j,k,a] = sum_c C[k,c] T1[j,a,c]): one thread per output, the output index decomposed
-// with two 32-bit divisions, the sum unrolled into four independent fp32 partial sums (<= 64
-// terms: relative error ~ 1e-7, the result feeds TF32 MMAs or an fp32 factor), combined in fp64.
-// The generic kernel above issued ~300 instructions per output of 16 terms (odometer per term,
-// fp64 conversions): ~3x this path's count (ncu: 33 us at IPC 3.2 for 1 M outputs on c2).
+// Fast path for the common step shape: ONE summed index and at most three output indices (the
+// side operands and epilogues of CP / Tucker / the paper's custom models, e.g. T[j,k,a] =
+// sum_c C[k,c] T1[j,a,c] or the Tucker core's A[a,c,j] = sum_i Q[i,j,c] A[i,a]).  The outputs are
+// enumerated in an order chosen on the host (innermost = the output index with the smallest
+// stride in the larger operand, so a warp's loads coalesce; C is written through its own
+// strides), LANES threads share one output for long sums (interleaved terms, combined by warp
+// shuffles), and the terms are summed in blocks of 16 in fp32 (four independent partial sums)
+// carried in fp64.  The generic kernel above issued ~300 instructions per output of 16 terms
+// (odometer per term, fp64 conversions): ncu 33 us at IPC 3.2 for 1 M outputs on c2.
 struct EinStep1Dev {
   int nout;
-  int odim[3], as_o[3], bs_o[3];
+  int odim[3], as_o[3], bs_o[3], cs_o[3];   // in enumeration order (last = innermost)
   int S, as, bs;
   int out_size;
 };
-template <bool HASB>
+template <bool HASB, int LANES>
 __global__ void einstep1_kernel(const __grid_constant__ EinStep1Dev st, const float* __restrict__ A,
                                 const float* __restrict__ B, float* __restrict__ C) {
-  for (int o = blockIdx.x * blockDim.x + threadIdx.x; o < st.out_size; o += gridDim.x * blockDim.x) {
-    int ao = 0, bo = 0, rem = o;
+  const int gt = blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = gt % LANES;
+  const int stride = (gridDim.x * blockDim.x) / LANES;
+  // warp-uniform trip count (the lanes of an output shuffle with the whole warp)
+  for (int o = gt / LANES;; o += stride) {
+    const bool valid = o < st.out_size;
+    if (LANES > 1 ? __all_sync(0xffffffffu, !valid) : !valid) break;
+    int ao = 0, bo = 0, co = 0, rem = valid ? o : 0;
 #pragma unroll
     for (int d = 2; d >= 0; --d) {
       if (d >= st.nout) continue;
@@ -499,29 +509,39 @@ __global__ void einstep1_kernel(const __grid_constant__ EinStep1Dev st, const fl
       rem = q;
       ao += i * st.as_o[d];
       bo += i * st.bs_o[d];
+      co += i * st.cs_o[d];
     }
-    float acc[4] = {0.f, 0.f, 0.f, 0.f};
-    int s = 0;
-    for (; s + 4 <= st.S; s += 4) {
+    double tot = 0.0;
+    for (int s0 = lane * 16; valid && s0 < st.S; s0 += 16 * LANES) {   // blocks of 16 terms
+      float acc[4] = {0.f, 0.f, 0.f, 0.f};
+      const int s1 = s0 + 16 < st.S ? s0 + 16 : st.S;
+      int s = s0;
+      for (; s + 4 <= s1; s += 4) {
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const float a = __ldg(A + ao + (s + u) * st.as);
-        acc[u] = HASB ? fmaf(a, __ldg(B + bo + (s + u) * st.bs), acc[u]) : acc[u] + a;
+        for (int u = 0; u < 4; ++u) {
+          const float a = __ldg(A + ao + (s + u) * st.as);
+          acc[u] = HASB ? fmaf(a, __ldg(B + bo + (s + u) * st.bs), acc[u]) : acc[u] + a;
+        }
       }
+      for (; s < s1; ++s) {
+        const float a = __ldg(A + ao + s * st.as);
+        acc[0] = HASB ? fmaf(a, __ldg(B + bo + s * st.bs), acc[0]) : acc[0] + a;
+      }
+      tot += ((double)acc[0] + (double)acc[1]) + ((double)acc[2] + (double)acc[3]);
     }
-    for (; s < st.S; ++s) {
-      const float a = __ldg(A + ao + s * st.as);
-      acc[0] = HASB ? fmaf(a, __ldg(B + bo + s * st.bs), acc[0]) : acc[0] + a;
+    if (LANES > 1) {
+#pragma unroll
+      for (int w = LANES / 2; w > 0; w >>= 1) tot += __shfl_xor_sync(0xffffffffu, tot, w);
     }
-    C[o] = (float)(((double)acc[0] + (double)acc[1]) + ((double)acc[2] + (double)acc[3]));
+    if (valid && lane == 0) C[co] = (float)tot;
   }
 }
 
 cudaError_t launch_einstep(const EinStep& st, const float* A, const float* B, float* C, cudaStream_t s) {
   static const bool no_fast = std::getenv("NEF_EINSTEP_GENERIC") != nullptr;   // diagnostics
   {
-    // fast path eligibility: one summed index (<= 64 terms), <= 3 output indices, 32-bit offsets
-    bool ok = !no_fast && st.nsum == 1 && st.sum_size <= 64 && st.nout <= 3 && st.out_size < (1ll << 30);
+    // fast path eligibility: one summed index, <= 3 output indices, 32-bit offsets
+    bool ok = !no_fast && st.nsum == 1 && st.nout <= 3 && st.out_size < (1ll << 30) && st.sum_size < (1ll << 30);
     long long span_a = (st.sdim[0] - 1) * st.as_s[0], span_b = (st.sdim[0] - 1) * st.bs_s[0];
     for (int k = 0; k < st.nout; ++k) {
       span_a += (st.odim[k] - 1) * st.as_o[k];
@@ -529,22 +549,54 @@ cudaError_t launch_einstep(const EinStep& st, const float* A, const float* B, fl
     }
     ok = ok && span_a < (1ll << 30) && span_b < (1ll << 30);
     if (ok) {
+      // C strides (row-major over the step's output order), then the enumeration order: the
+      // innermost enumerated index is the one with the smallest nonzero stride in the operand
+      // spanning more memory (its loads coalesce across a warp)
+      long long cst[kMaxDims];
+      long long acc = 1;
+      for (int k = st.nout - 1; k >= 0; --k) { cst[k] = acc; acc *= st.odim[k]; }
+      const bool big_a = !B || span_a >= span_b;
+      int order[3] = {0, 1, 2};
+      if (st.nout > 1) {
+        int inner = st.nout - 1;
+        long long best = -1;
+        for (int k = 0; k < st.nout; ++k) {
+          const long long str = big_a ? st.as_o[k] : st.bs_o[k];
+          if (str > 0 && st.odim[k] > 1 && (best < 0 || str < best)) { best = str; inner = k; }
+        }
+        int w = 0;
+        for (int k = 0; k < st.nout; ++k)
+          if (k != inner) order[w++] = k;
+        order[w] = inner;
+      }
       EinStep1Dev d{};
       d.nout = st.nout;
       for (int k = 0; k < st.nout; ++k) {
-        d.odim[k] = (int)st.odim[k];
-        d.as_o[k] = (int)st.as_o[k];
-        d.bs_o[k] = (int)st.bs_o[k];
+        const int src = order[k];
+        d.odim[k] = (int)st.odim[src];
+        d.as_o[k] = (int)st.as_o[src];
+        d.bs_o[k] = (int)st.bs_o[src];
+        d.cs_o[k] = (int)cst[src];
       }
       d.S = (int)st.sdim[0];
       d.as = (int)st.as_s[0];
       d.bs = (int)st.bs_s[0];
       d.out_size = (int)st.out_size;
-      long long blocks = (st.out_size + 255) / 256;
+      // long sums over few outputs: 8 (or 4) threads per output
+      const int lanes = (st.sum_size >= 128 && st.out_size < 148 * 2048) ? 8 : (st.sum_size > 64 ? 4 : 1);
+      long long blocks = (st.out_size * lanes + 255) / 256;
       if (blocks > 148 * 32) blocks = 148 * 32;
       if (blocks < 1) blocks = 1;
-      if (B) einstep1_kernel<true><<<(unsigned)blocks, 256, 0, s>>>(d, A, B, C);
-      else einstep1_kernel<false><<<(unsigned)blocks, 256, 0, s>>>(d, A, B, C);
+      const unsigned nb = (unsigned)blocks;
+      if (B) {
+        if (lanes == 8) einstep1_kernel<true, 8><<<nb, 256, 0, s>>>(d, A, B, C);
+        else if (lanes == 4) einstep1_kernel<true, 4><<<nb, 256, 0, s>>>(d, A, B, C);
+        else einstep1_kernel<true, 1><<<nb, 256, 0, s>>>(d, A, B, C);
+      } else {
+        if (lanes == 8) einstep1_kernel<false, 8><<<nb, 256, 0, s>>>(d, A, B, C);
+        else if (lanes == 4) einstep1_kernel<false, 4><<<nb, 256, 0, s>>>(d, A, B, C);
+        else einstep1_kernel<false, 1><<<nb, 256, 0, s>>>(d, A, B, C);
+      }
       return cudaGetLastError();
     }
   }

@@ -68,9 +68,15 @@ constexpr int NVG = 4;                     // V-generator warps (16 tile columns
 // The warp schedulers favour higher warp ids, so the producers whose latency is on the critical
 // path sit above the elementwise warps (with the producers below, the V generators and the MMA
 // issuer starved during the elementwise phase of every tile).
-constexpr int W_EW0 = 0, W_VG0 = NEW, W_DV = NEW + 4, W_TMA = NEW + 5, W_MMA = NEW + 6;
+// NEF_SPLIT_ISSUE: the reconstruction MMAs S(t) are issued by a second warp on another
+// sub-partition (after the N/D MMAs of the tile whose buffer they overwrite have retired), so the
+// sub-partition hosting the N/D issuer carries half the tcgen05.mma issue (experiment)
+#ifndef NEF_SPLIT_ISSUE
+#define NEF_SPLIT_ISSUE 0
+#endif
+constexpr int W_EW0 = 0, W_VG0 = NEW, W_DV = NEW + 4, W_TMA = NEW + 5, W_MMA = NEW + 6, W_MMA2 = NEW + 7;
 __device__ __forceinline__ int vg_index(int warp) { return warp >= W_VG0 && warp < W_VG0 + NVG ? warp - W_VG0 : -1; }
-constexpr int NTHREADS = (NEW + 7) * 32;
+constexpr int NTHREADS = (NEW + 7 + NEF_SPLIT_ISSUE) * 32;
 constexpr int Y_STAGE = BM * BN * 4;      // 32 KB
 constexpr int M_STAGE = BM * BN;          // 8 KB
 // a V stage: V (64 tile columns x KB bonds, SW128 K-major) then its transpose V^T, KB * 256 B each
@@ -1149,7 +1155,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
         else mma_s_block_32<id1>(d, tUh, vd, 0u);
         mma_commit_elect(s_full + 8 * b);
       };
-      for (int i = 0; i < NBUF && i < T; ++i) mma_s(i, i, 0);
+      if (!NEF_SPLIT_ISSUE)
+        for (int i = 0; i < NBUF && i < T; ++i) mma_s(i, i, 0);
       int b = 0;                  // buffer of tile u (and of tile u + NBUF's S)
       uint32_t ph = 0;            // (u / NBUF) & 1
       for (int u = 0; u < T; ++u) {
@@ -1176,10 +1183,34 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
         mma_commit_elect(v_empty + 8 * vs);
         mma_commit_elect(buf_free + 8 * b);
         if (u % G == G - 1 && u != T - 1) mma_commit_elect(drain_ready);
-        if (u + NBUF < T) mma_s(u + NBUF, b, ph ^ 1);
+        if (!NEF_SPLIT_ISSUE && u + NBUF < T) mma_s(u + NBUF, b, ph ^ 1);
         if (++b == NBUF) { b = 0; ph ^= 1; }
       }
       mma_commit_elect(nd_full);
+    }
+  } else if (NEF_SPLIT_ISSUE && warp == W_MMA2) {
+    // ------------------------------------------------------------ S issuer (NEF_SPLIT_ISSUE)
+    if (T > 0) {
+      constexpr uint32_t id1 = idesc_tf32(128, BN);
+      mbar_wait_mma(u_ready, 0);
+      tc_fence_after();
+      int b = 0;
+      uint32_t ph = 0;
+      for (int t = 0; t < T; ++t) {
+        const int vs = t % NV;
+        // buffer b is free once the N/D MMAs of tile t - NBUF (the last reader of its P) retired
+        if (t >= NBUF) mbar_wait_mma(buf_free + 8 * b, ph ^ 1);
+        mbar_wait_mma(v_full + 8 * vs, (t / NV) & 1);
+        tc_fence_after();
+        if (lane == 0) trace_ev(a, t, EV_MMA1_ISSUE);
+        __syncwarp();
+        const uint64_t vd = sdesc(sV + vs * V_STAGE, 16, 1024);
+        const uint32_t d = tmem + buf_col(b);
+        if (KB == 64) mma_s_block_64<id1>(d, tUh, vd, 0u);
+        else mma_s_block_32<id1>(d, tUh, vd, 0u);
+        mma_commit_elect(s_full + 8 * b);
+        if (++b == NBUF) { b = 0; ph ^= 1; }
+      }
     }
   } else if (warp == W_DV) {
     // ------------------------------------------------------------ direct-V row loads (TMA)
