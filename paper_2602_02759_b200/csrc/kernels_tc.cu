@@ -74,9 +74,21 @@ constexpr int NVG = 4;                     // V-generator warps (16 tile columns
 #ifndef NEF_SPLIT_ISSUE
 #define NEF_SPLIT_ISSUE 0
 #endif
+// NEF_ND_BAR: the N/D issuer waits for P(t) on a named barrier (bar.sync, no polling) that the
+// elementwise warps bar.arrive on (experiment)
+#ifndef NEF_ND_BAR
+#define NEF_ND_BAR 1   // measured: the polling issuer made its sub-partition's elementwise warps lag
+                       // ~1 400 cycles per tile (c5 trace); with the barrier ~300
+#endif
+// NEF_S_WATCH: a watcher warp polls S(t)'s mbarrier and releases the elementwise warps through a
+// named barrier, so elementwise warps that finish a tile early sleep instead of polling (experiment)
+#ifndef NEF_S_WATCH
+#define NEF_S_WATCH 0
+#endif
 constexpr int W_EW0 = 0, W_VG0 = NEW, W_DV = NEW + 4, W_TMA = NEW + 5, W_MMA = NEW + 6, W_MMA2 = NEW + 7;
+constexpr int W_SW = NEW + 7 + NEF_SPLIT_ISSUE;   // S watcher (NEF_S_WATCH)
 __device__ __forceinline__ int vg_index(int warp) { return warp >= W_VG0 && warp < W_VG0 + NVG ? warp - W_VG0 : -1; }
-constexpr int NTHREADS = (NEW + 7 + NEF_SPLIT_ISSUE) * 32;
+constexpr int NTHREADS = (NEW + 7 + NEF_SPLIT_ISSUE + NEF_S_WATCH) * 32;
 constexpr int Y_STAGE = BM * BN * 4;      // 32 KB
 constexpr int M_STAGE = BM * BN;          // 8 KB
 // a V stage: V (64 tile columns x KB bonds, SW128 K-major) then its transpose V^T, KB * 256 B each
@@ -1161,7 +1173,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
       uint32_t ph = 0;            // (u / NBUF) & 1
       for (int u = 0; u < T; ++u) {
         const int vs = u % NV;
+#if NEF_ND_BAR
+        // P(u) written by every elementwise warp: a hardware named barrier per tile buffer (the
+        // issuer sleeps instead of polling an mbarrier)
+        asm volatile("bar.sync %0, %1;" ::"r"(3 + b), "n"((NEW + 1) * 32) : "memory");
+#else
         mbar_wait_mma(p_full + 8 * b, ph);
+#endif
         tc_fence_after();
         if (lane == 0) trace_ev(a, u, EV_MMA23_ISSUE);
         __syncwarp();
@@ -1211,6 +1229,15 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
         mma_commit_elect(s_full + 8 * b);
         if (++b == NBUF) { b = 0; ph ^= 1; }
       }
+    }
+  } else if (NEF_S_WATCH && warp == W_SW) {
+    // ------------------------------------------------------------ S watcher (NEF_S_WATCH)
+    int b = 0;
+    uint32_t ph = 0;
+    for (int t = 0; t < T; ++t) {
+      mbar_spin(s_full + 8 * b, ph);
+      asm volatile("bar.arrive %0, %1;" ::"r"(6 + b), "n"((NEW + 1) * 32) : "memory");
+      if (++b == NBUF) { b = 0; ph ^= 1; }
     }
   } else if (warp == W_DV) {
     // ------------------------------------------------------------ direct-V row loads (TMA)
@@ -1390,7 +1417,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
       uint32_t sv[EWH][16], pb[EWH][16], pl[EWH][16];
       float yv[EWH][16];
       uint32_t mk[EWH][4];
+#if NEF_S_WATCH
+      asm volatile("bar.sync %0, %1;" ::"r"(6 + b), "n"((NEW + 1) * 32) : "memory");
+#else
       mbar_wait_ew(s_full + 8 * b, bph);
+#endif
       if (warp == W_EW0 && lane == 0) trace_ev(a, t, EV_EW_S);
       tc_fence_after();
 #pragma unroll
@@ -1440,7 +1471,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
       }
       tc_fence_before();
       __syncwarp();
+#if NEF_ND_BAR
+      asm volatile("bar.arrive %0, %1;" ::"r"(3 + b), "n"((NEW + 1) * 32) : "memory");
+#else
       if (lane == 0) mbar_arrive(p_full + 8 * b);      // P(t) in TMEM (or, loss only: S(t) consumed)
+#endif
       if (warp == W_EW0 && lane == 0) trace_ev(a, t, EV_EW_DONE);
       if (lane == 0) trace_ev(a, t, 16 + warp - W_EW0);     // per-warp arrival (diagnostics)
       if (a.mode != 2 && t % G == G - 1 && t != T - 1) {
