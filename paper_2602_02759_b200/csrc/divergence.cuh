@@ -397,20 +397,24 @@ struct Ew<EW_A05_B0_SQ> {
 // ---- App. B losses; y = max(yhat, 1e-30) is the model (odds for Bernoulli / binomial)
 __device__ __forceinline__ float xlogy0(float x, float ly) { return x > 0.f ? x * ly : 0.f; }   // 0 log y = 0 (R8)
 
+// One reciprocal for both weights: r = 1 / (y (c + y)), a = x (c + y) r, b = (c' ...) y r - one MUFU
+// per entry instead of two (the two-MUFU forms made these kinds MUFU-bound: 16 k MUFU per tile)
 template <>
 struct Ew<EW_NB> {  // a = x / y, b = (phi + x) / (phi + y); L = (phi + x) log(phi + y) - x log y
   static constexpr bool kLinX = true;
   static constexpr bool kSignedA = false;
   static __device__ __forceinline__ void ab(float x, float yh, const DivParams& d, float& av, float& bv) {
-    av = x * frcp(yh);
-    bv = (d.prm + x) * frcp(d.prm + yh);
+    const float py = d.prm + yh;
+    const float r = frcp(yh * py);
+    av = x * py * r;
+    bv = (d.prm + x) * yh * r;
   }
   static __device__ __forceinline__ void ab2(float2 x, float2 yh, const DivParams& d, float2& av, float2& bv) {
     ab(x.x, yh.x, d, av.x, bv.x);
     ab(x.y, yh.y, d, av.y, bv.y);
   }
   static __device__ __forceinline__ float loss(float x, float yh, const DivParams& d) {
-    return (d.prm + x) * logf(d.prm + yh) - xlogy0(x, logf(yh));
+    return (d.prm + x) * flog(d.prm + yh) - xlogy0(x, flog(yh));
   }
   static __device__ __forceinline__ void abl2(float2 x, float2 yh, const DivParams& d, float2& av, float2& bv,
                                               float2& l) {
@@ -432,15 +436,17 @@ struct Ew<EW_BERN> {  // odds: a = x / y, b = 1 / (1 + y); L = log(1 + y) - x lo
   static constexpr bool kLinX = true;
   static constexpr bool kSignedA = false;
   static __device__ __forceinline__ void ab(float x, float yh, const DivParams&, float& av, float& bv) {
-    av = x * frcp(yh);
-    bv = frcp(1.f + yh);
+    const float py = 1.f + yh;
+    const float r = frcp(yh * py);
+    av = x * py * r;
+    bv = yh * r;
   }
   static __device__ __forceinline__ void ab2(float2 x, float2 yh, const DivParams& d, float2& av, float2& bv) {
     ab(x.x, yh.x, d, av.x, bv.x);
     ab(x.y, yh.y, d, av.y, bv.y);
   }
   static __device__ __forceinline__ float loss(float x, float yh, const DivParams&) {
-    return log1pf(yh) - xlogy0(x, logf(yh));
+    return log1pf(yh) - xlogy0(x, flog(yh));
   }
   static __device__ __forceinline__ void abl2(float2 x, float2 yh, const DivParams& d, float2& av, float2& bv,
                                               float2& l) {
@@ -454,15 +460,17 @@ struct Ew<EW_BINOM> {  // odds with n trials: a = x / y, b = n / (1 + y); L = n 
   static constexpr bool kLinX = true;
   static constexpr bool kSignedA = false;
   static __device__ __forceinline__ void ab(float x, float yh, const DivParams& d, float& av, float& bv) {
-    av = x * frcp(yh);
-    bv = d.prm * frcp(1.f + yh);
+    const float py = 1.f + yh;
+    const float r = frcp(yh * py);
+    av = x * py * r;
+    bv = d.prm * yh * r;
   }
   static __device__ __forceinline__ void ab2(float2 x, float2 yh, const DivParams& d, float2& av, float2& bv) {
     ab(x.x, yh.x, d, av.x, bv.x);
     ab(x.y, yh.y, d, av.y, bv.y);
   }
   static __device__ __forceinline__ float loss(float x, float yh, const DivParams& d) {
-    return d.prm * log1pf(yh) - xlogy0(x, logf(yh));
+    return d.prm * log1pf(yh) - xlogy0(x, flog(yh));
   }
   static __device__ __forceinline__ void abl2(float2 x, float2 yh, const DivParams& d, float2& av, float2& bv,
                                               float2& l) {

@@ -991,7 +991,7 @@ struct RunCursor {
 // pipeline timeline (diagnostics): event e of tile t in CTA (0,0)
 enum TraceEv : int {
   EV_TMA_ISSUE = 0, EV_VG_START, EV_VG_DONE, EV_MMA1_ISSUE, EV_MMA23_ISSUE, EV_EW_S, EV_EW_Y, EV_EW_HALF,
-  EV_EW_DONE, EV_VG_ISSUED
+  EV_EW_DONE, EV_VG_ISSUED, EV_EW_LDW, EV_EW_MATH
 };
 // compiled in only with -DNEF_TRACE=1 (scripts/build_variants.sh): the checks cost issue slots
 #ifndef NEF_TRACE
@@ -1436,6 +1436,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
       }
 #pragma unroll
       for (int h = 0; h < EWH; ++h) tmem_ld_wait(sv[h]);
+      if (warp == W_EW0 && lane == 0) trace_ev(a, t, EV_EW_LDW);
       __syncwarp();
       if (lane == 0) mbar_arrive(y_empty + 8 * st);  // Y / mask stage read by this warp
 #pragma unroll
@@ -1449,6 +1450,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
           for (int j = 0; j < 16; ++j) pb[h][j] = sv[h][j] + __float_as_uint(yv[h][j]) + mk[h][j >> 2];
         }
       }
+      if (warp == W_EW0 && lane == 0) trace_ev(a, t, EV_EW_MATH);
       if (a.mode != 2) {
 #pragma unroll
         for (int h = 0; h < EWH; ++h) {

@@ -11,7 +11,8 @@ sys.path.insert(0, ".")
 from nef_inputs import CONFIGS, generate_torch  # noqa: E402
 from paper_2602_02759_b200 import nef  # noqa: E402
 
-EV = ["TMA", "VG_START", "VG_DONE", "MMA1", "MMA23", "EW_S", "EW_Y", "EW_PEMPTY", "EW_DONE", "VG_ISSUED"]
+EV = ["TMA", "VG_START", "VG_DONE", "MMA1", "MMA23", "EW_S", "EW_Y", "EW_PEMPTY", "EW_DONE", "VG_ISSUED", "EW_LDW",
+      "EW_MATH"]
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="c5")
 ap.add_argument("--ell", type=int, default=0)
@@ -41,7 +42,8 @@ for i in range(lo, hi):
     print("%4d " % i + " ".join("%9d" % (t[i, j] - base) for j in range(len(EV))))
 per = np.diff(t[lo:hi + 1, EV.index("EW_DONE")])
 print("cycles per tile (EW_DONE to EW_DONE): median %d" % np.median(per))
-for a_, b_ in [("MMA1", "EW_S"), ("EW_S", "EW_PEMPTY"), ("EW_PEMPTY", "EW_DONE"), ("EW_DONE", "MMA23"),
+for a_, b_ in [("MMA1", "EW_S"), ("EW_S", "EW_Y"), ("EW_Y", "EW_LDW"), ("EW_LDW", "EW_MATH"), ("EW_MATH", "EW_PEMPTY"),
+               ("EW_S", "EW_PEMPTY"), ("EW_PEMPTY", "EW_DONE"), ("EW_DONE", "MMA23"),
                ("VG_START", "VG_DONE"), ("VG_START", "VG_ISSUED"), ("VG_ISSUED", "VG_DONE"), ("VG_DONE", "MMA1"),
                ("TMA", "EW_Y")]:
     dd = t[lo:hi, EV.index(b_)] - t[lo:hi, EV.index(a_)]
