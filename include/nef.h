@@ -70,8 +70,10 @@ enum nef_status {
  *   NEF_LOSS_JS        Jensen-Shannon: a = log((x+y)/(2y)), b = 1, g = log
  * param: phi (NEGBIN) or n (BINOMIAL) for every entry, used when aux == NULL (must be > 0).
  * aux: optional device float tensor with Y's (local) shape and layout holding a per-entry phi_i or
- * n_i (NEGBIN / BINOMIAL only; else must be NULL).  It is streamed with Y (+4 B per entry) and, in
- * this build, only by the CUDA-core kernel.  Domain errors: NEF_E_DOMAIN (unknown kind, alpha = 0
+ * n_i (NEGBIN / BINOMIAL only; else must be NULL).  It is streamed with Y (+4 B per entry): by the
+ * tcgen05 kernel as a second TMA ring (16-byte aligned base; Y streamed as nef_fit's sentinel copy
+ * or unmasked), else by the CUDA-core kernel.  Valid for yhat * (phi + yhat) < 3e38 (one shared
+ * reciprocal per entry).  Domain errors: NEF_E_DOMAIN (unknown kind, alpha = 0
  * with beta != 1, param <= 0 without aux); NEF_E_ARG (aux misaligned / not applicable). */
 enum nef_loss_kind { NEF_LOSS_AB = 0, NEF_LOSS_NEGBIN = 1, NEF_LOSS_BERNOULLI = 2, NEF_LOSS_BINOMIAL = 3, NEF_LOSS_JS = 4 };
 typedef struct nef_loss_spec {

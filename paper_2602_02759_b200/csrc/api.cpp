@@ -266,9 +266,14 @@ struct StreamOut {
   bool lconst = false;            // loss partials hold only the factor-dependent part (R25)
 };
 
-bool use_tc(const nef::Lowering& L, const uint8_t* M, bool sentinel = false, const float* aux = nullptr) {
-  return g_policy == 0 && L.tc_ok && !aux &&
-         (!M || sentinel || (L.tc_mask_ok && (reinterpret_cast<uintptr_t>(M) & 15) == 0));
+// the tcgen05 kernel takes a per-entry parameter stream (NB phi_i / binomial n_i) as a second TMA
+// ring next to the sentinel copy or unmasked Y (not next to a streamed uint8 mask)
+bool use_tc(const nef::Lowering& L, const uint8_t* M, bool sentinel = false, const float* aux = nullptr,
+            int kind = 0) {
+  if (aux && (!(kind == nef::EW_NB || kind == nef::EW_BINOM) || (M && !sentinel) ||
+              (reinterpret_cast<uintptr_t>(aux) & 15)))
+    return false;
+  return g_policy == 0 && L.tc_ok && (!M || sentinel || (L.tc_mask_ok && (reinterpret_cast<uintptr_t>(M) & 15) == 0));
 }
 
 // One streaming pass over Y (+mask) for lowering L: the tcgen05 kernel where the planner
@@ -368,7 +373,7 @@ int stream_pass_multi(const Ctx* cs, int S, const nef::Lowering& L, const float*
   // losses of one pass); update-only passes stream the train-folded sentinel copy
   const bool sent = c.ysent && (M || c.sqy) && !(c.split && mode != 0);
   nef::DivParams dvk = dv;
-  if (use_tc(L, M, sent, c.aux) && (S == 1 || (g_vdirect && L.vd_tab >= 0))) {
+  if (use_tc(L, M, sent, c.aux, dv.kind) && (S == 1 || (g_vdirect && L.vd_tab >= 0))) {
     const float* Yk = Y;
     const uint8_t* Mk = M;
     if (sent) {   // stream the NaN-sentinel copy: no mask stream (4 B / entry)
@@ -407,7 +412,7 @@ int stream_pass_multi(const Ctx* cs, int S, const nef::Lowering& L, const float*
     }
     t0.nrs = S > 1 ? S : 0;
     prof_begin(c.s);
-    CK(nef::tc::launch(t0, Yk, Mk, L.tc_row_blocks, chunks, c.s));
+    CK(nef::tc::launch(t0, Yk, Mk, L.tc_row_blocks, chunks, c.s, c.aux));
     prof_end(c.s, bytes);
     ++g_launches;
     return NEF_OK;
@@ -889,7 +894,7 @@ int nef_fit_ex(nef_plan_t plan, const float* Y, const uint8_t* mask, const nef_l
   // R35: the (0.5, 0) pair needs the data only as sqrt(y) (a = y^(1/2) yhat^-1, the loss split of
   // R25): the once-per-fit copy holds sqrt(y), masked or not, and the passes save one MUFU per entry
   c.sqy = dv.kind == nef::EW_A05_B0 && any_tc && g_policy == 0 && !g_no_sentinel && !sp.aux && !g_no_sqy;
-  if ((mask || c.sqy) && g_policy == 0 && !g_no_sentinel && !sp.aux) {
+  if ((mask || c.sqy) && g_policy == 0 && !g_no_sentinel) {
     if (any_tc) {
       float* ys = reinterpret_cast<float*>(c.ws + p.ws_sent);
       CK(nef::launch_sentinel(Y, mask, ys, p.n_local, dterm, dpart, dcpart, dslot,
@@ -1012,7 +1017,7 @@ int nef_fit_restarts(nef_plan_t plan, const float* Y, const uint8_t* mask, const
   bool any_tc = false;
   for (const auto& Lw : p.low) any_tc |= Lw.tc_ok;
   const bool sqy = dv.kind == nef::EW_A05_B0 && any_tc && g_policy == 0 && !g_no_sentinel && !sp.aux && !g_no_sqy;
-  if ((mask || sqy) && any_tc && g_policy == 0 && !g_no_sentinel && !sp.aux) {
+  if ((mask || sqy) && any_tc && g_policy == 0 && !g_no_sentinel) {
     double* dslot = reinterpret_cast<double*>(ws + p.ws_dterm);
     double* dpart = reinterpret_cast<double*>(ws + p.ws_dpart);
     float* ys = reinterpret_cast<float*>(ws + per * S);
@@ -1084,7 +1089,7 @@ int nef_fit_split(nef_plan_t plan, const float* Y, const uint8_t* labels, const 
   const nef::UpdArgs u = nef::make_upd_fam(sp.fam, sp.alpha, sp.beta, eps);
   bool any_tc = false;
   for (const auto& L : p.low) any_tc |= L.tc_ok;
-  if (any_tc && g_policy == 0 && !g_no_sentinel && !sp.aux) {   // train entries folded into a sentinel copy
+  if (any_tc && g_policy == 0 && !g_no_sentinel) {   // train entries folded into a sentinel copy
     double* dslot = reinterpret_cast<double*>(c.ws + p.ws_dterm);
     double* dpart = reinterpret_cast<double*>(c.ws + p.ws_dpart);
     float* ys = reinterpret_cast<float*>(c.ws + p.ws_sent);

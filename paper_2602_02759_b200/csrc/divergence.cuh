@@ -423,11 +423,13 @@ struct Ew<EW_NB> {  // a = x / y, b = (phi + x) / (phi + y); L = (phi + x) log(p
   }
   // per-entry phi (aux): the same forms with phi_i in place of the scalar
   static __device__ __forceinline__ void ab_aux(float x, float yh, float phi, float& av, float& bv) {
-    av = x * frcp(yh);
-    bv = (phi + x) * frcp(phi + yh);
+    const float py = phi + yh;
+    const float r = frcp(yh * py);
+    av = x * py * r;
+    bv = (phi + x) * yh * r;
   }
   static __device__ __forceinline__ float loss_aux(float x, float yh, float phi) {
-    return (phi + x) * logf(phi + yh) - xlogy0(x, logf(yh));
+    return (phi + x) * flog(phi + yh) - xlogy0(x, flog(yh));
   }
 };
 
@@ -478,11 +480,13 @@ struct Ew<EW_BINOM> {  // odds with n trials: a = x / y, b = n / (1 + y); L = n 
     l = make_float2(loss(x.x, yh.x, d), loss(x.y, yh.y, d));
   }
   static __device__ __forceinline__ void ab_aux(float x, float yh, float n, float& av, float& bv) {
-    av = x * frcp(yh);
-    bv = n * frcp(1.f + yh);
+    const float py = 1.f + yh;
+    const float r = frcp(yh * py);
+    av = x * py * r;
+    bv = n * yh * r;
   }
   static __device__ __forceinline__ float loss_aux(float x, float yh, float n) {
-    return n * log1pf(yh) - xlogy0(x, logf(yh));
+    return n * log1pf(yh) - xlogy0(x, flog(yh));
   }
 };
 

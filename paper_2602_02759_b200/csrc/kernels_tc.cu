@@ -43,13 +43,14 @@ constexpr int BM = 128, BN = 64;
 #endif
 // Y (/ mask) pipeline stages: 3 with the uint8 mask stream (4 for KB = 32), else NEF_NS (NEF_NS32)
 template <int KB, int MM> struct YStages {
-  static constexpr int value = KB == 32 ? (MM == 1 ? 4 : NEF_NS32) : (MM == 1 ? 3 : NEF_NS);
+  static constexpr int value = MM == 2 ? 2 : KB == 32 ? (MM == 1 ? 4 : NEF_NS32) : (MM == 1 ? 3 : NEF_NS);
 };
 // V tile stages: 3 with a uint8 mask stream (its stages take the smem), else 4
 #ifndef NEF_NV0
 #define NEF_NV0 4
 #endif
-template <int KB, int MM> struct VStages { static constexpr int value = MM == 1 ? 3 : NEF_NV0; };
+// (MM = 2, the per-entry parameter stream: 2 Y + 2 parameter stages; 3 V stages for bond 64)
+template <int KB, int MM> struct VStages { static constexpr int value = MM == 1 ? 3 : (MM == 2 && KB == 64) ? 3 : NEF_NV0; };
 #ifndef NEF_PA_RN
 #define NEF_PA_RN 0   // 1: plain RN for P_a in the Euclidean pair too (diagnostics)
 #endif
@@ -100,6 +101,7 @@ template <int KB> struct VSt {
 struct __align__(64) Params {
   CUtensorMap tmY;
   CUtensorMap tmM;
+  CUtensorMap tmA;   // MM = 2: per-entry loss parameter stream (phi_i / n_i), Y's geometry
   CUtensorMap tmV[kMaxRestarts];   // direct-V table rows per restart (2-D {K, var_rows}, box {32, 64}, SW128)
   TcArgs a;
 };
@@ -892,6 +894,44 @@ __device__ __forceinline__ void ew_half_sent(const TcArgs& a, uint32_t (&sv)[16]
   }
 }
 
+// The sentinel-path stage with a per-entry loss parameter (MM = 2: negative binomial phi_i,
+// binomial n_i; kLinX kinds): x < 0 marks a missing entry (its parameter, possibly garbage or
+// TMA zero fill, is replaced by 1 before use), a and b as ew_half_sent.
+template <int KIND>
+__device__ __forceinline__ void ew_half_aux(const TcArgs& a, uint32_t (&sv)[16], float (&yv)[16], const float (&xa)[16],
+                                            int cv, bool row_ok, uint32_t (&pb)[16], double& lacc, long long& cnt) {
+  if constexpr (KIND == EW_NB || KIND == EW_BINOM) {
+    if (a.absy) {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) yv[j] = fabsf(yv[j]);
+    }
+    const uint32_t vbits = (!row_ok || cv <= 0) ? 0u : (cv >= 16 ? 0xffffu : ((1u << cv) - 1u));
+    if (vbits != 0xffffu) {
+#pragma unroll
+      for (int j = 0; j < 16; ++j) yv[j] = ((vbits >> j) & 1u) ? yv[j] : -1.f;
+    }
+    float l = 0.f;
+#pragma unroll
+    for (int j = 0; j < 16; j += 2) {
+      const float2 yh = yhat_floor(sv[j], sv[j + 1]);
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const float x = yv[j + e], y = e ? yh.y : yh.x;
+        const float ax = x >= 0.f ? xa[j + e] : 1.f;
+        float av, bv;
+        Ew<KIND>::ab_aux(x, y, ax, av, bv);
+        sv[j + e] = (uint32_t)__viaddmax_s32(__float_as_int(av), 0x1000, 0);
+        pb[j + e] = pb_sent<KIND>(bv, x);
+        if (a.mode != 0) {
+          l += x >= 0.f ? Ew<KIND>::loss_aux(x, y, ax) : 0.f;
+          if (a.mode == 2) cnt += x >= 0.f ? 1 : 0;
+        }
+      }
+    }
+    if (a.mode != 0) lacc += (double)l;
+  }
+}
+
 // linear column index of the first column of a tile
 __device__ __forceinline__ int64_t tile_col0(const TcArgs& a, int64_t tile) {
   if (a.layout == 0) return tile * BN;
@@ -1045,7 +1085,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
   unsigned char* gbase = smraw + (base - raw);
   const uint32_t sY = base;                                  // NS x 32 KB
   const uint32_t sM = sY + NS * Y_STAGE;                     // NS x 8 KB
-  const uint32_t sV = sM + (MM == 1 ? NS * M_STAGE : 0);     // NV x (V | V^T)
+  const uint32_t sV = sM + (MM == 1 ? NS * M_STAGE : MM == 2 ? NS * Y_STAGE : 0);   // NV x (V | V^T)
   const uint32_t sBar = sV + NV * V_STAGE;
   const uint32_t y_full = sBar, y_empty = y_full + 8 * NS;
   const uint32_t v_full = y_empty + 8 * NS, v_empty = v_full + 8 * NV;
@@ -1107,7 +1147,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
   if (warp == W_TMA) {
     // ------------------------------------------------------------ TMA producer
     if (lane == 0) {
-      const uint32_t bytes = (uint32_t)Y_STAGE + (a.has_mask ? (uint32_t)M_STAGE : 0u);
+      const uint32_t bytes = (uint32_t)Y_STAGE + (a.has_mask ? (uint32_t)M_STAGE : 0u) + (MM == 2 ? (uint32_t)Y_STAGE : 0u);
       for (int t = 0; t < T; ++t) {
         const int st = t % NS;
         mbar_wait_relaxed(y_empty + 8 * st, ((t / NS) & 1) ^ 1);
@@ -1116,23 +1156,34 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
         const uint32_t bar = y_full + 8 * st;
         mbar_expect_tx(bar, bytes);
         const uint32_t dY = sY + st * Y_STAGE, dM = sM + st * M_STAGE;
-        if (a.layout == 0) {
-          tma_load_2d(dY, &P.tmY, (int)row0, (int)(tile * BN), bar);
-          if (a.has_mask) tma_load_2d(dM, &P.tmM, (int)row0, (int)(tile * BN), bar);
-        } else {
-          const int64_t ti = tile % a.tiles_inner, to = tile / a.tiles_inner;
-          if (a.layout == 1) {
-            if (a.y3d) {
-              tma_load_3d(dY, &P.tmY, 0, (int)(ti * 2), (int)row0, bar);
-            } else {
-              tma_load_2d(dY, &P.tmY, (int)(ti * BN), (int)row0, bar);
-              tma_load_2d(dY + Y_STAGE / 2, &P.tmY, (int)(ti * BN + 32), (int)row0, bar);
-            }
-            if (a.has_mask) tma_load_2d(dM, &P.tmM, (int)(ti * BN), (int)row0, bar);
+        // the Y tile (and, MM = 2, the parameter tile of the same geometry into the second ring)
+        auto load_f32 = [&](uint32_t dst, const CUtensorMap* tm) {
+          if (a.layout == 0) {
+            tma_load_2d(dst, tm, (int)row0, (int)(tile * BN), bar);
           } else {
-            tma_load_3d(dY, &P.tmY, (int)(ti * BN), (int)row0, (int)to, bar);
-            tma_load_3d(dY + Y_STAGE / 2, &P.tmY, (int)(ti * BN + 32), (int)row0, (int)to, bar);
-            if (a.has_mask) tma_load_3d(dM, &P.tmM, (int)(ti * BN), (int)row0, (int)to, bar);
+            const int64_t ti = tile % a.tiles_inner, to = tile / a.tiles_inner;
+            if (a.layout == 1) {
+              if (a.y3d) {
+                tma_load_3d(dst, tm, 0, (int)(ti * 2), (int)row0, bar);
+              } else {
+                tma_load_2d(dst, tm, (int)(ti * BN), (int)row0, bar);
+                tma_load_2d(dst + Y_STAGE / 2, tm, (int)(ti * BN + 32), (int)row0, bar);
+              }
+            } else {
+              tma_load_3d(dst, tm, (int)(ti * BN), (int)row0, (int)to, bar);
+              tma_load_3d(dst + Y_STAGE / 2, tm, (int)(ti * BN + 32), (int)row0, (int)to, bar);
+            }
+          }
+        };
+        load_f32(dY, &P.tmY);
+        if constexpr (MM == 2) load_f32(sM + st * Y_STAGE, &P.tmA);
+        if (a.has_mask) {
+          if (a.layout == 0) {
+            tma_load_2d(dM, &P.tmM, (int)row0, (int)(tile * BN), bar);
+          } else {
+            const int64_t ti = tile % a.tiles_inner, to = tile / a.tiles_inner;
+            if (a.layout == 1) tma_load_2d(dM, &P.tmM, (int)(ti * BN), (int)row0, bar);
+            else tma_load_3d(dM, &P.tmM, (int)(ti * BN), (int)row0, (int)to, bar);
           }
         }
       }
@@ -1428,11 +1479,16 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
       for (int h = 0; h < EWH; ++h) tmem_ld16(tc + 16 * h, sv[h]);
       mbar_spin(y_full + 8 * st, sph);
       if (warp == W_EW0 && lane == 0) trace_ev(a, t, EV_EW_Y);
+      float xa[MM == 2 ? EWH : 1][16];   // MM = 2: the per-entry parameters of the entries
 #pragma unroll
       for (int h = 0; h < EWH; ++h) {
         mk[h][0] = mk[h][1] = mk[h][2] = mk[h][3] = 0u;
         ew_load_y(a, gY + st * Y_STAGE, gM + st * M_STAGE, (cg0 + h) >> 1, (cg0 + h) & 1, m, yoff[h], yswz[h], yv[h],
                   mk[h]);   // (MM == 0: a.has_mask = 0)
+        if constexpr (MM == 2) {
+          uint32_t dummy[4];
+          ew_load_y(a, gM + st * Y_STAGE, gM, (cg0 + h) >> 1, (cg0 + h) & 1, m, yoff[h], yswz[h], xa[h], dummy);
+        }
       }
 #pragma unroll
       for (int h = 0; h < EWH; ++h) tmem_ld_wait(sv[h]);
@@ -1443,7 +1499,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
       for (int h = 0; h < EWH; ++h) {
         const int cv = cols_here - 16 * (cg0 + h);
         if (!(NEF_DBG & 256)) {
-          if (MM == 1) ew_half<KIND, SPA>(a, sv[h], yv[h], mk[h], cv, row_ok, pb[h], pl[h], lsum, cnt);
+          if constexpr (MM == 1) ew_half<KIND, SPA>(a, sv[h], yv[h], mk[h], cv, row_ok, pb[h], pl[h], lsum, cnt);
+          else if constexpr (MM == 2) ew_half_aux<KIND>(a, sv[h], yv[h], xa[h], cv, row_ok, pb[h], loss_acc[0], cnt[0]);
           else ew_half_sent<KIND, SPA>(a, sv[h], yv[h], cv, row_ok, pb[h], pl[h], loss_acc[0], cnt[0]);
         } else {   // NEF_DBG 256: timing experiment without the elementwise math (P_b = S + Y)
 #pragma unroll
@@ -1571,23 +1628,28 @@ struct TcLauncher {
   }
   template <int KIND>
   cudaError_t operator()() const {
+    if (MM == 2) {   // per-entry parameter stream: the kinds that have one
+      if constexpr (KIND == EW_NB || KIND == EW_BINOM) return KB == 32 ? go<32, KIND, 2>() : go<64, KIND, 2>();
+      else return cudaErrorInvalidValue;
+    }
     if (KB == 32) return MM ? go<32, KIND, 1>() : go<32, KIND, 0>();
     return MM ? go<64, KIND, 1>() : go<64, KIND, 0>();
   }
 };
 
 size_t smem_bytes(int mm, int kb) {
-  const int nv = kb == 32 ? (mm == 1 ? VStages<32, 1>::value : VStages<32, 0>::value)
-                          : (mm == 1 ? VStages<64, 1>::value : VStages<64, 0>::value);
-  const int ns = kb == 32 ? (mm == 1 ? YStages<32, 1>::value : YStages<32, 0>::value)
-                          : (mm == 1 ? YStages<64, 1>::value : YStages<64, 0>::value);
+  const int nv = kb == 32 ? (mm == 1 ? VStages<32, 1>::value : mm == 2 ? VStages<32, 2>::value : VStages<32, 0>::value)
+                          : (mm == 1 ? VStages<64, 1>::value : mm == 2 ? VStages<64, 2>::value : VStages<64, 0>::value);
+  const int ns = kb == 32 ? (mm == 1 ? YStages<32, 1>::value : mm == 2 ? YStages<32, 2>::value : YStages<32, 0>::value)
+                          : (mm == 1 ? YStages<64, 1>::value : mm == 2 ? YStages<64, 2>::value : YStages<64, 0>::value);
   const int vst = kb == 32 ? VSt<32>::SIZE : VSt<64>::SIZE;
-  return 1024 + ns * Y_STAGE + (mm == 1 ? ns * M_STAGE : 0) + nv * vst + 512 + 64;
+  return 1024 + ns * Y_STAGE + (mm == 1 ? ns * M_STAGE : mm == 2 ? ns * Y_STAGE : 0) + nv * vst + 512 + 64;
 }
 
 cudaError_t launch(const TcArgs& args, const float* Y, const uint8_t* M, int64_t row_blocks, int64_t chunks,
-                   cudaStream_t s) {
+                   cudaStream_t s, const float* aux) {
   if (!get_encode()) return cudaErrorNotSupported;
+  if (aux && M) return cudaErrorInvalidValue;   // the parameter stream runs with the sentinel copy only
   Params P;
   std::memset(&P, 0, sizeof(P));
   P.a = args;
@@ -1598,6 +1660,7 @@ cudaError_t launch(const TcArgs& args, const float* Y, const uint8_t* M, int64_t
     uint64_t sy[1] = {(uint64_t)args.R * 4};
     uint32_t by[2] = {128, 64};
     ok = encode(&P.tmY, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, Y, d, sy, by, CU_TENSOR_MAP_SWIZZLE_NONE);
+    if (ok && aux) ok = encode(&P.tmA, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, aux, d, sy, by, CU_TENSOR_MAP_SWIZZLE_NONE);
     if (ok && M) {
       uint64_t sm[1] = {(uint64_t)args.R};
       ok = encode(&P.tmM, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, M, d, sm, by, CU_TENSOR_MAP_SWIZZLE_NONE);
@@ -1611,11 +1674,13 @@ cudaError_t launch(const TcArgs& args, const float* Y, const uint8_t* M, int64_t
       uint64_t sy[2] = {128, (uint64_t)args.CI * 4};
       uint32_t by[3] = {32, 2, 128};
       ok = encode(&P.tmY, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, Y, d, sy, by, CU_TENSOR_MAP_SWIZZLE_128B);
+      if (ok && aux) ok = encode(&P.tmA, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, aux, d, sy, by, CU_TENSOR_MAP_SWIZZLE_128B);
     } else {
       uint64_t d[2] = {(uint64_t)args.CI, (uint64_t)args.R};
       uint64_t sy[1] = {(uint64_t)args.CI * 4};
       uint32_t by[2] = {32, 128};
       ok = encode(&P.tmY, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, Y, d, sy, by, CU_TENSOR_MAP_SWIZZLE_128B);
+      if (ok && aux) ok = encode(&P.tmA, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, aux, d, sy, by, CU_TENSOR_MAP_SWIZZLE_128B);
     }
     if (ok && M) {
       uint64_t dm[2] = {(uint64_t)args.CI, (uint64_t)args.R};
@@ -1628,6 +1693,7 @@ cudaError_t launch(const TcArgs& args, const float* Y, const uint8_t* M, int64_t
     uint64_t sy[2] = {(uint64_t)args.CI * 4, (uint64_t)args.CI * (uint64_t)args.R * 4};
     uint32_t by[3] = {32, 128, 1};
     ok = encode(&P.tmY, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, Y, d, sy, by, CU_TENSOR_MAP_SWIZZLE_128B);
+    if (ok && aux) ok = encode(&P.tmA, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, aux, d, sy, by, CU_TENSOR_MAP_SWIZZLE_128B);
     if (ok && M) {
       uint64_t sm[2] = {(uint64_t)args.CI, (uint64_t)args.CI * (uint64_t)args.R};
       uint32_t bm[3] = {64, 128, 1};
@@ -1655,7 +1721,7 @@ cudaError_t launch(const TcArgs& args, const float* Y, const uint8_t* M, int64_t
   if (!ok) return cudaErrorInvalidValue;
   P.a.has_mask = M ? 1 : 0;
   dim3 grid((unsigned)row_blocks, (unsigned)chunks, (unsigned)P.a.nrs);
-  return dispatch_ew(args.dv.kind, TcLauncher{P, grid, s, args.KB, M ? 1 : 0});
+  return dispatch_ew(args.dv.kind, TcLauncher{P, grid, s, args.KB, M ? 1 : aux ? 2 : 0});
 }
 
 }  // namespace tc

@@ -67,9 +67,11 @@ struct TcArgs {
 
 };
 
-size_t smem_bytes(int mm, int kb);   // mm: 1 = uint8 mask stream, 0 = none / NaN-sentinel Y; kb: 32 | 64
+size_t smem_bytes(int mm, int kb);   // mm: 1 = uint8 mask stream, 2 = parameter stream, 0 = none; kb: 32 | 64
+// aux: per-entry loss parameter (NB phi_i / binomial n_i), Y's layout, streamed as a second TMA
+// ring (MM = 2; with the sentinel copy or unmasked Y only)
 cudaError_t launch(const TcArgs& args, const float* Y, const uint8_t* M, int64_t row_blocks, int64_t chunks,
-                   cudaStream_t s);
+                   cudaStream_t s, const float* aux = nullptr);
 
 }  // namespace tc
 }  // namespace nef

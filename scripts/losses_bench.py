@@ -67,7 +67,7 @@ for name, kw, aux in cases:
     Y = data[kind].contiguous()
     spec = nef.loss_spec(kind, aux=aux, **kw)
     F = [f.clone() for f in d["init"]]
-    run(name + (" (CUDA-core: per-entry stream)" if aux is not None else ""),
+    run(name + (" (per-entry parameter stream, +4 B/entry)" if aux is not None else ""),
         lambda k: plan.fit_ex(Y, M, spec, F, k, aux=aux))
 # split fit (N2): train / validation / heldout labels from the config's mask
 lab = torch.where(M != 0, torch.ones_like(M), torch.zeros_like(M))

@@ -97,17 +97,19 @@ def test_appb_loss_parity(nef, kind, case, pm):
 
 
 @pytest.mark.parametrize("kind", ["negbin", "binomial"])
-@pytest.mark.parametrize("case", CASES[::2], ids=lambda c: "x".join(map(str, c[1])))
-def test_per_entry_parameter_stream(nef, kind, case):
+@pytest.mark.parametrize("case", CASES, ids=lambda c: "x".join(map(str, c[1])))
+@pytest.mark.parametrize("pm", [0.0, 0.1])
+def test_per_entry_parameter_stream(nef, kind, case, pm):
     """NB with a per-entry dispersion phi_i and binomial with per-entry trials n_i:
-    the aux tensor is streamed with Y (CUDA-core kernel)."""
+    the parameter tensor is streamed with Y - a second TMA ring of the tcgen05 kernel next to the
+    sentinel copy (masked) or the raw Y (unmasked), or the CUDA-core kernel (c1 shape)."""
     ms, shape, ranks, _ = case
     Y, aux, _, init = _data(kind, ms, shape, ranks, seed=33, per_entry=True)
-    M = (np.random.default_rng(34).random(shape) >= 0.1).astype(np.uint8)
+    M = (np.random.default_rng(34).random(shape) >= pm).astype(np.uint8) if pm > 0 else None
     plan = nef.Plan(ms, shape, ranks)
     Ad = torch.from_numpy(aux).cuda()
     spec = nef.loss_spec(kind, aux=Ad)
-    Yd, Md = torch.from_numpy(Y).cuda(), torch.from_numpy(M).cuda()
+    Yd, Md = torch.from_numpy(Y).cuda(), (torch.from_numpy(M).cuda() if M is not None else None)
     F = [torch.from_numpy(f.copy()).cuda() for f in init]
     tr = plan.fit_ex(Yd, Md, spec, F, 1, aux=Ad)
     ref, rtr = O.fit(ms, Y, M, init, O.make_loss(kind), None, 1, aux=aux)
