@@ -1063,6 +1063,8 @@ __device__ __forceinline__ uint32_t buf_col(int b) { return b == 2 ? 384u : 128u
 //   S(0), S(1), then for each t: [P(t) ready] N,D += P(t) V(t); [buffer t&1 retired] S(t+2)
 // MM: 1 = uint8 mask streamed alongside Y; 0 = no mask stream (no mask, or the NaN-sentinel Y)
 template <int KB, int KIND, int MM>
+// registers: 80 per thread is the ceiling at 23 warps (the register file is split over the four
+// sub-partitions: 16 K registers for the 6 warps of the fullest one; 88 fails to launch)
 __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_constant__ Params P) {
   constexpr int NV = VStages<KB, MM>::value;
   constexpr int NS = YStages<KB, MM>::value;
@@ -1214,8 +1216,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
         const uint64_t vd = sdesc(sV + vs * V_STAGE, 16, 1024);
         const uint32_t d = tmem + buf_col(b);
         // one asm block, one elect: U_hi and U_lo steps interleaved (tUl = tUh + KB)
-        if (KB == 64) mma_s_block_64<id1>(d, tUh, vd, 0u);
-        else mma_s_block_32<id1>(d, tUh, vd, 0u);
+        if constexpr ((NEF_DBG & 512) != 0) {   // timing experiment: no U_lo MMAs
+          if (KB == 64) mma_s1_block_64<id1>(d, tUh, vd, 0u);
+          else mma_s1_block_32<id1>(d, tUh, vd, 0u);
+        } else if (KB == 64) {
+          mma_s_block_64<id1>(d, tUh, vd, 0u);
+        } else {
+          mma_s_block_32<id1>(d, tUh, vd, 0u);
+        }
         mma_commit_elect(s_full + 8 * b);
       };
       if (!NEF_SPLIT_ISSUE)
