@@ -273,3 +273,43 @@ def test_uber_parameter_count_from_library(golden):
     p = nef.Plan(g["model"], g["shape"], g["ranks"])
     total = sum(int(np.prod(s)) for s in p.factor_shapes())
     assert total == g["value"]
+
+
+def test_loss_spec_validation_before_device_work():
+    """nef_*_ex, nef_fit_split and nef_fit_restarts reject a bad loss spec / rule / restart count with
+    DOMAIN or ARG before any device work (raw C calls, fake device pointers: no GPU needed)."""
+    import ctypes as C
+    p = nef.Plan("ir,jr->ij", (3, 4), (2,))
+    ws = p.info["workspace_bytes"]
+    F = (C.c_void_p * 2)(4096, 8192)
+
+    def fit_ex(spec):
+        return nef.NEF_STATUS[nef.LIB.nef_fit_ex(p.h, C.c_void_p(4096), None, C.byref(spec), 1e-12, F, 1, None,
+                                                 C.c_void_p(1 << 20), ws, C.c_void_p(0))]
+
+    assert fit_ex(nef.nef_loss_spec(7, 1.0, 0.0, 0.0, None)) == "DOMAIN"            # unknown kind
+    assert fit_ex(nef.nef_loss_spec(0, 0.0, 0.5, 0.0, None)) == "DOMAIN"            # alpha = 0, beta != 1
+    assert fit_ex(nef.nef_loss_spec(1, 0.0, 0.0, 0.0, None)) == "DOMAIN"            # NB without phi
+    assert fit_ex(nef.nef_loss_spec(3, 0.0, 0.0, -2.0, None)) == "DOMAIN"           # binomial n <= 0
+    assert fit_ex(nef.nef_loss_spec(2, 0.0, 0.0, 0.0, C.c_void_p(4096))) == "ARG"   # aux for Bernoulli
+    assert fit_ex(nef.nef_loss_spec(1, 0.0, 0.0, 0.0, C.c_void_p(4098))) == "ARG"   # misaligned aux
+    rule = nef.nef_stop_rule(10, 1e-6, 5)
+    tr = (C.c_double * 33)()
+    cnt = (C.c_int64 * 3)()
+    sw, rs = C.c_int(), C.c_int()
+    spec = nef.nef_loss_spec(0, 1.0, 0.0, 0.0, None)
+    code = nef.LIB.nef_fit_split(p.h, C.c_void_p(4096), None, C.byref(spec), 1e-12, F, C.byref(rule), tr, cnt,
+                                 C.byref(sw), C.byref(rs), C.c_void_p(1 << 20), ws, C.c_void_p(0))
+    assert nef.NEF_STATUS[code] == "ARG"                                             # null labels
+    bad = nef.nef_stop_rule(-1, 1e-6, 5)
+    code = nef.LIB.nef_fit_split(p.h, C.c_void_p(4096), C.c_void_p(8192), C.byref(spec), 1e-12, F, C.byref(bad), tr,
+                                 cnt, C.byref(sw), C.byref(rs), C.c_void_p(1 << 20), ws, C.c_void_p(0))
+    assert nef.NEF_STATUS[code] == "ARG"                                             # negative max_iters
+    need = nef.nef_restarts_workspace_bytes(p.h, 2)
+    assert need > 2 * ws // 2
+    code = nef.LIB.nef_fit_restarts(p.h, C.c_void_p(4096), None, C.byref(spec), 1e-12, F, 0, 1, None,
+                                    C.c_void_p(1 << 20), need, C.c_void_p(0))
+    assert nef.NEF_STATUS[code] == "ARG"                                             # zero restarts
+    code = nef.LIB.nef_fit_restarts(p.h, C.c_void_p(4096), None, C.byref(spec), 1e-12, F, 1, 1, None,
+                                    C.c_void_p(1 << 20), 16, C.c_void_p(0))
+    assert nef.NEF_STATUS[code] == "ARG"                                             # workspace too small
