@@ -140,7 +140,19 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
 #ifndef NEF_SPIN_HINT
 #define NEF_SPIN_HINT 0
 #endif
+#ifndef NEF_SPIN_BOUND
+#define NEF_SPIN_BOUND 1   // 0: unbounded spin (two instructions per poll instead of five; experiment)
+#endif
 __device__ __forceinline__ void mbar_spin(uint32_t bar, uint32_t parity) {
+#if !NEF_SPIN_BOUND
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "SPIN_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra SPIN_%=;\n}" ::"r"(bar), "r"(parity)
+      : "memory");
+  return;
+#endif
   uint32_t done = 0;
   for (uint32_t it = 0;; ++it) {
 #if NEF_SPIN_HINT
