@@ -1059,6 +1059,9 @@ __device__ __forceinline__ void trace_ev(const TcArgs& a, int t, int e) {
 #endif
 }
 
+#ifndef NEF_UWARP
+#define NEF_UWARP 1
+#endif
 #ifndef NEF_NBUF3
 #define NEF_NBUF3 1   // bond <= 32: three TMEM tile buffers (0: two, as for bond 64)
 #endif
@@ -1090,7 +1093,13 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
   extern __shared__ unsigned char smraw[];
   const TcArgs& a = P.a;
   const int tid = threadIdx.x;
+#if NEF_UWARP
+  // warp index through a shuffle: provably warp-uniform, so every role branch and the code under
+  // it (loop counters, stage indices, descriptors) can live in uniform registers
+  const int warp = __shfl_sync(0xffffffffu, tid >> 5, 0);
+#else
   const int warp = tid >> 5;
+#endif
   const int lane = tid & 31;
 
   // 1024-aligned carve-up
@@ -1154,7 +1163,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+#if NEF_UWARP
+  const uint32_t tmem = __shfl_sync(0xffffffffu, *gTmem, 0);
+#else
   const uint32_t tmem = *gTmem;
+#endif
   const uint32_t tNa = tmem + 256, tNb = tmem + 256 + KB;
   const uint32_t tUh = tmem + 256 + 2 * KB, tUl = tmem + 256 + 3 * KB;
 
@@ -1648,12 +1661,17 @@ struct TcLauncher {
   }
   template <int KIND>
   cudaError_t operator()() const {
+#ifdef NEF_SASS_ONLY   // SASS experiments: compile one instantiation (KIND, bond 64, no mask stream)
+    if constexpr (KIND != NEF_SASS_ONLY) return cudaErrorInvalidValue;
+    else return go<64, KIND, 0>();
+#else
     if (MM == 2) {   // per-entry parameter stream: the kinds that have one
       if constexpr (KIND == EW_NB || KIND == EW_BINOM) return KB == 32 ? go<32, KIND, 2>() : go<64, KIND, 2>();
       else return cudaErrorInvalidValue;
     }
     if (KB == 32) return MM ? go<32, KIND, 1>() : go<32, KIND, 0>();
     return MM ? go<64, KIND, 1>() : go<64, KIND, 0>();
+#endif
   }
 };
 
