@@ -164,7 +164,7 @@ __device__ __forceinline__ float kl_loss(float x, float y) {
 // (paper convention; EW_* in kernels.h).  Ew<EW_GENERIC> defers to the runtime codes.
 // ab2 evaluates two entries at once; the specialisations use the packed fp32x2 multiplies of
 // sm_100 (FMUL2: one issue slot for two products).
-// Traits: kLinX - a = x * (positive factor), so a carries the sign of x (the sentinel's "missing");
+// Traits: kLinX - a = x * (positive factor), so a is NaN where x is the sentinel copy's NaN ("missing");
 // kSignedA - a may be negative at an observed entry (log forms: the (0,1) pair, Jensen-Shannon),
 // so the sentinel path selects on x instead of clamping a at zero.
 template <int KIND>
@@ -570,8 +570,7 @@ struct LossOff<EW_A05_B0> {
     const float2 r = make_float2(frsqrt(yh.x), frsqrt(yh.y));
     const float2 sx = make_float2(fsqrt(fabsf(x.x)), fsqrt(fabsf(x.y)));
     bv = r;
-    const float2 a = __fmul2_rn(sx, __fmul2_rn(r, r));   // sqrt(x) / y, signed like x below
-    av = make_float2(copysignf(a.x, x.x), copysignf(a.y, x.y));
+    av = __fmul2_rn(sx, __fmul2_rn(r, r));   // sqrt(x) / y (NaN at a missing entry: x is the sentinel NaN)
     const float2 sy = __fmul2_rn(yh, r);
     rem = __ffma2_rn(__fmul2_rn(sx, make_float2(-0.5f, -0.5f)), make_float2(flog(yh.x), flog(yh.y)), sy);   // scale 4
   }
@@ -583,7 +582,7 @@ struct LossOff<EW_A05_B0_SQ> {   // the (0.5, 0) split with s = sqrt(x) streamed
   static __device__ __forceinline__ void abr2(float2 s, float2 yh, float2& av, float2& bv, float2& rem) {
     const float2 r = make_float2(frsqrt(yh.x), frsqrt(yh.y));
     bv = r;
-    av = __fmul2_rn(s, __fmul2_rn(r, r));   // signed like s (the sentinel's -1 at missing entries)
+    av = __fmul2_rn(s, __fmul2_rn(r, r));   // NaN at missing entries (the sentinel copy's NaN)
     const float2 sy = __fmul2_rn(yh, r);
     const float2 sa = make_float2(fabsf(s.x), fabsf(s.y));
     rem = __ffma2_rn(__fmul2_rn(sa, make_float2(-0.5f, -0.5f)), make_float2(flog(yh.x), flog(yh.y)), sy);   // scale 4

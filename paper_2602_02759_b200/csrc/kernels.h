@@ -14,6 +14,11 @@ enum PowCode : int { POW_0 = 0, POW_1, POW_M1, POW_H, POW_MH, POW_M15, POW_15, P
 int pow_code(double p);
 
 // compile-time specialisations of the elementwise stage (divergence.cuh)
+// Missing entries of the sentinel copy of Y (R5): the canonical NaN 0x7fffffff.  Every
+// fp32 result that takes it as an input is the same canonical NaN, whose bits + a TF32 rounding
+// offset overflow to a negative int32, so the kernels' add-then-max (max(bits + d, 0)) rounds an
+// observed weight and zeroes a missing one without a separate select, and x >= 0 is false.
+constexpr unsigned kSentMissingBits = 0x7fffffffu;
 enum EwKind : int { EW_GENERIC = 0, EW_KL, EW_EUC, EW_B_M05, EW_A05_B0, EW_B05, EW_B2, EW_A05_B1,
                     // App. B losses: negative binomial (scalar phi, or per-entry phi streamed
                     // as aux), Bernoulli odds, binomial odds (scalar n, or per-entry n as aux), Jensen-Shannon

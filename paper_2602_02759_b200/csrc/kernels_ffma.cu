@@ -703,11 +703,12 @@ __global__ void sentinel_kernel(const float* __restrict__ Y, const uint8_t* __re
     if (sqy) {   // R35: sqrt(y) streamed for (0.5, 0); |y| so that an observed -0 is +0
       y.x = sqrtf(fabsf(y.x)); y.y = sqrtf(fabsf(y.y)); y.z = sqrtf(fabsf(y.z)); y.w = sqrtf(fabsf(y.w));
     }
-    // observed: + 0 turns -0 into +0 (the kernel reads the sign); missing: -1
-    y.x = (w & 0xffu) ? y.x + 0.f : -1.f;
-    y.y = (w & 0xff00u) ? y.y + 0.f : -1.f;
-    y.z = (w & 0xff0000u) ? y.z + 0.f : -1.f;
-    y.w = (w & 0xff000000u) ? y.w + 0.f : -1.f;
+    // observed: + 0 turns -0 into +0; missing: the canonical NaN (kSentMissingBits)
+    const float mis = __uint_as_float(kSentMissingBits);
+    y.x = (w & 0xffu) ? y.x + 0.f : mis;
+    y.y = (w & 0xff00u) ? y.y + 0.f : mis;
+    y.z = (w & 0xff0000u) ? y.z + 0.f : mis;
+    y.w = (w & 0xff000000u) ? y.w + 0.f : mis;
     __stcs(reinterpret_cast<float4*>(out) + i, y);
   }
   if (dpart) sent_block_sum(acc, cnt, dpart, dcpart, blockIdx.x);
@@ -720,7 +721,7 @@ __global__ void sentinel_tail_kernel(const float* __restrict__ Y, const uint8_t*
   for (long long i = from + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
     const bool o = !M || (split ? M[i] == 1 : M[i] != 0);
     if (o) { ++cnt; acc += dterm_c(dterm, Y[i]); }
-    out[i] = o ? (sqy ? sqrtf(fabsf(Y[i])) : Y[i] + 0.f) : -1.f;
+    out[i] = o ? (sqy ? sqrtf(fabsf(Y[i])) : Y[i] + 0.f) : __uint_as_float(kSentMissingBits);
   }
   if (dpart) sent_block_sum(acc, cnt, dpart, dcpart, slot + blockIdx.x);
 }

@@ -141,9 +141,32 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
 #define NEF_SPIN_HINT 0
 #endif
 #ifndef NEF_SPIN_BOUND
-#define NEF_SPIN_BOUND 1   // 0: unbounded spin (two instructions per poll instead of five; experiment)
+#define NEF_SPIN_BOUND 2   // 2: eight two-instruction polls per bound check (c3 -2 %, c4 -3 % against 1:
+                           // a bound check per poll, five instructions); 0: unbounded (experiment)
 #endif
 __device__ __forceinline__ void mbar_spin(uint32_t bar, uint32_t parity) {
+#if NEF_SPIN_BOUND == 2
+  // eight polls of two instructions (try_wait, branch) per bound check; traps after 2^24 rounds
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t.reg .u32 c;\n\t"
+      "mov.u32 c, 0;\n\t"
+      "SPIN_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t@p bra DONE_%=;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t@p bra DONE_%=;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t@p bra DONE_%=;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t@p bra DONE_%=;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t@p bra DONE_%=;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t@p bra DONE_%=;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t@p bra DONE_%=;\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t@p bra DONE_%=;\n\t"
+      "add.u32 c, c, 1;\n\t"
+      "setp.lt.u32 p, c, 16777216;\n\t"
+      "@p bra SPIN_%=;\n\t"
+      "trap;\n\t"
+      "DONE_%=:\n}" ::"r"(bar), "r"(parity)
+      : "memory");
+  return;
+#endif
 #if !NEF_SPIN_BOUND
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
@@ -794,24 +817,38 @@ __device__ __forceinline__ void ew_half(const TcArgs& a, uint32_t (&sv)[16], con
   }
 }
 
-// P_b bits of one entry in the sentinel path: b > 0 at an observed entry takes the sign of x by a
-// copysign, and the add-then-max rounds it (TF32 RN) and zeroes a missing entry; b == 1 kinds
+// P_b bits of one entry in the sentinel path: b > 0 at an observed entry; x * 0 + b is b there and
+// NaN at a missing entry (x NaN), and the add-then-max rounds it (TF32 RN) or zeroes it; b == 1 kinds
 // (KL, Jensen-Shannon: exact in TF32) are one compare-and-set
 template <int KIND>
 __device__ __forceinline__ uint32_t pb_sent(float bv, float x) {
   if constexpr (KIND == EW_KL || KIND == EW_JS) return x >= 0.f ? 0x3f800000u : 0u;
-  else return (uint32_t)__viaddmax_s32(__float_as_int(copysignf(bv, x)), 0x1000, 0);
+  else return (uint32_t)__viaddmax_s32(__float_as_int(__fmaf_rn(x, 0.f, bv)), 0x1000, 0);
+}
+// two entries: b is made NaN at a missing entry (x NaN) by one packed x * 0 + b, which is b
+// exactly at an observed one; the add-then-max then rounds (TF32 RN) or zeroes it
+template <int KIND>
+__device__ __forceinline__ void pb_sent2(float2 bv, float2 x, uint32_t& p0, uint32_t& p1) {
+  if constexpr (KIND == EW_KL || KIND == EW_JS) {
+    p0 = pb_sent<KIND>(bv.x, x.x);
+    p1 = pb_sent<KIND>(bv.y, x.y);
+  } else {
+    const float2 q = __ffma2_rn(x, make_float2(0.f, 0.f), bv);
+    p0 = (uint32_t)__viaddmax_s32(__float_as_int(q.x), 0x1000, 0);
+    p1 = (uint32_t)__viaddmax_s32(__float_as_int(q.y), 0x1000, 0);
+  }
 }
 
-// P_a bits of one entry in the sentinel path: a >= 0 kinds clamp (a carries the sign of x, so the
+// P_a bits of one entry in the sentinel path: a >= 0 kinds clamp (a is NaN where x is, so the
 // add-then-max both rounds and zeroes a missing entry); signed-a kinds (log forms) select on x.
 template <int KIND>
 __device__ __forceinline__ uint32_t pa_sent(float av, float x, int j) {
+  // (every a >= 0 kind computes a from x - directly or through |x| - so a is NaN at a missing entry)
   if constexpr (Ew<KIND>::kSignedA) return x >= 0.f ? __float_as_uint(av) + pa_round<KIND>(j) : 0u;
-  else return (uint32_t)__viaddmax_s32(__float_as_int(Ew<KIND>::kLinX ? av : copysignf(av, x)), (int)pa_round<KIND>(j), 0);
+  else return (uint32_t)__viaddmax_s32(__float_as_int(av), (int)pa_round<KIND>(j), 0);
 }
 
-// The same for the sentinel path (a >= 0 kinds; x < 0 = missing): hi = max(RN(a), 0), lo = a - hi
+// The same for the sentinel path (a >= 0 kinds; x NaN = missing): hi = max(RN(a), 0), lo = a - hi
 template <int KIND, bool SPA>
 __device__ __forceinline__ void put_pa_sent(uint32_t (&sv)[16], uint32_t (&pl)[16], int j, float av, float x) {
   if constexpr (SPA) {
@@ -823,12 +860,12 @@ __device__ __forceinline__ void put_pa_sent(uint32_t (&sv)[16], uint32_t (&pl)[1
   }
 }
 
-// The same without a mask stream: a missing entry carries -1 in Y (the sentinel copy nef_fit
-// makes once per fit, R5; observed data are >= +0).  a has the sign of x (directly, or
-// by a copysign for the sqrt forms) and b gets it by a copysign, so one add-then-max per value,
+// The same without a mask stream: a missing entry carries the canonical NaN in Y (the sentinel
+// copy nef_fit makes once per fit, R5; observed data are >= +0).  a is NaN there (every
+// a >= 0 kind computes a from x or |x|) and b is made NaN by x * 0 + b, so one add-then-max per value,
 // max(bits + 0x1000, 0), both rounds (TF32 RN of the value the tensor core truncates) and zeroes
 // the missing entries.  Entries outside the tile's valid rows / columns (TMA zero fill) are
-// turned into -1 first.
+// turned into the NaN first.
 template <int KIND, bool SPA>
 __device__ __forceinline__ void ew_half_sent(const TcArgs& a, uint32_t (&sv)[16], float (&yv)[16], int cv, bool row_ok,
                                              uint32_t (&pb)[16], uint32_t (&pl)[16], double& lacc, long long& cnt) {
@@ -839,7 +876,7 @@ __device__ __forceinline__ void ew_half_sent(const TcArgs& a, uint32_t (&sv)[16]
   const uint32_t vbits = (!row_ok || cv <= 0) ? 0u : (cv >= 16 ? 0xffffu : ((1u << cv) - 1u));
   if (vbits != 0xffffu) {
 #pragma unroll
-    for (int j = 0; j < 16; ++j) yv[j] = ((vbits >> j) & 1u) ? yv[j] : -1.f;
+    for (int j = 0; j < 16; ++j) yv[j] = ((vbits >> j) & 1u) ? yv[j] : __uint_as_float(kSentMissingBits);
   }
   if constexpr (LossOff<KIND>::value) {
     if (a.mode != 0 && a.lconst) {   // loss without its data-only part (R25; count from the sentinel pass)
@@ -853,16 +890,15 @@ __device__ __forceinline__ void ew_half_sent(const TcArgs& a, uint32_t (&sv)[16]
         l2 = __fadd2_rn(l2, make_float2(x.x >= 0.f ? rv.x : 0.f, x.y >= 0.f ? rv.y : 0.f));
         sv[j] = (uint32_t)__viaddmax_s32(__float_as_int(av.x), (int)pa_round<KIND>(j), 0);
         sv[j + 1] = (uint32_t)__viaddmax_s32(__float_as_int(av.y), (int)pa_round<KIND>(j + 1), 0);
-        pb[j] = pb_sent<KIND>(bv.x, x.x);
-        pb[j + 1] = pb_sent<KIND>(bv.y, x.y);
+        pb_sent2<KIND>(bv, x, pb[j], pb[j + 1]);
       }
       lacc += (double)(l2.x + l2.y);   // (inside the uniform loss branch: nothing in update passes)
       return;
     }
   }
   if (a.mode != 0) {   // loss of the iterate entering the sweep (uniform branch)
-    // a, b and the loss from |x| (a missing entry's -1 becomes a harmless 1), then the sign of x
-    // selects: the loss of a missing entry is dropped, a and b are zeroed by the add-then-max.
+    // a, b and the loss from |x| (NaN at a missing entry), then x >= 0 selects: the loss of a
+    // missing entry is dropped, a and b are zeroed by the add-then-max.
     // The observed count is constant over a fit: only the loss-only pass (mode 2) counts.
     float2 l2 = make_float2(0.f, 0.f);
 #pragma unroll
@@ -877,14 +913,13 @@ __device__ __forceinline__ void ew_half_sent(const TcArgs& a, uint32_t (&sv)[16]
         sv[j] = pa_sent<KIND>(av.x, x.x, j);
         sv[j + 1] = pa_sent<KIND>(av.y, x.y, j + 1);
       } else if constexpr (SPA) {
-        put_pa_sent<KIND, SPA>(sv, pl, j, copysignf(av.x, x.x), x.x);
-        put_pa_sent<KIND, SPA>(sv, pl, j + 1, copysignf(av.y, x.y), x.y);
+        put_pa_sent<KIND, SPA>(sv, pl, j, av.x, x.x);
+        put_pa_sent<KIND, SPA>(sv, pl, j + 1, av.y, x.y);
       } else {
-        sv[j] = (uint32_t)__viaddmax_s32(__float_as_int(copysignf(av.x, x.x)), (int)pa_round<KIND>(j), 0);
-        sv[j + 1] = (uint32_t)__viaddmax_s32(__float_as_int(copysignf(av.y, x.y)), (int)pa_round<KIND>(j + 1), 0);
+        sv[j] = (uint32_t)__viaddmax_s32(__float_as_int(av.x), (int)pa_round<KIND>(j), 0);
+        sv[j + 1] = (uint32_t)__viaddmax_s32(__float_as_int(av.y), (int)pa_round<KIND>(j + 1), 0);
       }
-      pb[j] = pb_sent<KIND>(bv.x, x.x);
-      pb[j + 1] = pb_sent<KIND>(bv.y, x.y);
+      pb_sent2<KIND>(bv, x, pb[j], pb[j + 1]);
     }
     lacc += (double)(l2.x + l2.y);
     return;
@@ -895,19 +930,18 @@ __device__ __forceinline__ void ew_half_sent(const TcArgs& a, uint32_t (&sv)[16]
     const float2 yh = yhat_floor(sv[j], sv[j + 1]);
     float2 av, bv;
     if (Ew<KIND>::kLinX) {
-      Ew<KIND>::ab2(x, yh, a.dv, av, bv);   // a = x * (positive): carries the sign of x
+      Ew<KIND>::ab2(x, yh, a.dv, av, bv);   // a = x * (positive): NaN where x is
     } else {
       Ew<KIND>::ab2(make_float2(fabsf(x.x), fabsf(x.y)), yh, a.dv, av, bv);
     }
     put_pa_sent<KIND, SPA>(sv, pl, j, av.x, x.x);
     put_pa_sent<KIND, SPA>(sv, pl, j + 1, av.y, x.y);
-    pb[j] = pb_sent<KIND>(bv.x, x.x);
-    pb[j + 1] = pb_sent<KIND>(bv.y, x.y);
+    pb_sent2<KIND>(bv, x, pb[j], pb[j + 1]);
   }
 }
 
 // The sentinel-path stage with a per-entry loss parameter (MM = 2: negative binomial phi_i,
-// binomial n_i; kLinX kinds): x < 0 marks a missing entry (its parameter, possibly garbage or
+// binomial n_i; kLinX kinds): x NaN marks a missing entry (its parameter, possibly garbage or
 // TMA zero fill, is replaced by 1 before use), a and b as ew_half_sent.
 template <int KIND>
 __device__ __forceinline__ void ew_half_aux(const TcArgs& a, uint32_t (&sv)[16], float (&yv)[16], const float (&xa)[16],
@@ -920,7 +954,7 @@ __device__ __forceinline__ void ew_half_aux(const TcArgs& a, uint32_t (&sv)[16],
     const uint32_t vbits = (!row_ok || cv <= 0) ? 0u : (cv >= 16 ? 0xffffu : ((1u << cv) - 1u));
     if (vbits != 0xffffu) {
 #pragma unroll
-      for (int j = 0; j < 16; ++j) yv[j] = ((vbits >> j) & 1u) ? yv[j] : -1.f;
+      for (int j = 0; j < 16; ++j) yv[j] = ((vbits >> j) & 1u) ? yv[j] : __uint_as_float(kSentMissingBits);
     }
     float l = 0.f;
 #pragma unroll
@@ -1486,6 +1520,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
     // (no 64-bit division in the loop)
     const int64_t cext = a.layout == 0 ? a.CO : a.CI;
     const int tiles_blk = (int)(a.layout == 0 ? a.tiles : a.tiles_inner);
+    // only the last tile of a column block can be ragged: its valid columns, computed once
+    const int last_tin = tiles_blk - 1;
+    const int last_cols = (int)(cext - (int64_t)last_tin * BN);
     int tin = (int)(a.layout == 0 ? t_begin : t_begin % a.tiles_inner);
     int b = 0;           // tile buffer t % NBUF
     uint32_t bph = 0;    // (t / NBUF) & 1
@@ -1494,8 +1531,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
     const uint32_t tlane = tmem + lane_off + 16 * cg0;   // this warp's columns in a tile buffer
     for (int t = 0; t < T; ++t, ++tin) {
       if (tin >= tiles_blk) tin = 0;
-      const int64_t crem = cext - (int64_t)tin * BN;
-      const int cols_here = (int)(crem < BN ? crem : BN);
+      const int cols_here = tin == last_tin ? last_cols : BN;
       const uint32_t tc = tlane + buf_col(b);   // S / P_a columns of this warp
       float lsum[3] = {0.f, 0.f, 0.f};
       uint32_t sv[EWH][16], pb[EWH][16], pl[EWH][16];

@@ -10,7 +10,8 @@ import sys
 rep, cubin, fn, entries = sys.argv[1], sys.argv[2], sys.argv[3], float(sys.argv[4])
 top = int(sys.argv[5]) if len(sys.argv) > 5 else 25
 tiles = entries / 8192.0
-src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"], capture_output=True,
+import os
+src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"] + os.environ.get("NCU_FILTER", "").split(), capture_output=True,
                      text=True).stdout
 rows = list(csv.reader(io.StringIO(src)))
 hdr = rows[1]
