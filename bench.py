@@ -50,7 +50,7 @@ def _workload(cfg):
 # ------------------------------------------------------------------------------ clocks
 class Clocks:
     FIELDS = "clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown," \
-             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,power.draw,power.limit"
     NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, index):
@@ -75,7 +75,7 @@ class Clocks:
         time.sleep(0.25)
         self.proc.terminate()
         self.proc.wait()
-        sm, mx, reasons = [], [], set()
+        sm, mx, pw, lim, reasons = [], [], [], [], set()
         for line in open(self.path):
             parts = [p.strip() for p in line.split(",")]
             if len(parts) < 6:
@@ -85,12 +85,18 @@ class Clocks:
                 mx.append(float(parts[1]))
             except ValueError:
                 continue
-            for n, v in zip(self.NAMES, parts[2:]):
+            for n, v in zip(self.NAMES, parts[2:6]):
                 if v.lower().startswith("active"):
                     reasons.add(n)
+            try:
+                pw.append(float(parts[6]))
+                lim.append(float(parts[7]))
+            except (ValueError, IndexError):
+                pass
         os.unlink(self.path)
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": sorted(reasons), "samples": len(sm)}
+                "reasons": sorted(reasons), "samples": len(sm),
+                "power_w": statistics.median(pw) if pw else None, "power_limit_w": max(lim) if lim else None}
 
 
 # ------------------------------------------------------------------------------ oracle timing

@@ -86,10 +86,31 @@ constexpr int NVG = 4;                     // V-generator warps (16 tile columns
 #ifndef NEF_S_WATCH
 #define NEF_S_WATCH 0
 #endif
+// NEF_WARP_MAP 2 (experiment): the MMA issuer's sub-partition (warp % 4 == 2) hosts no other
+// producer - V generators on warps 16, 17, 19, 23, the direct-V loads on 21, warp 18 idle
+#ifndef NEF_WARP_MAP
+#define NEF_WARP_MAP 3   // measured (ab7): c4 -1.9 %, c3 -0.5 %, c5 -0.2 % against the V generators above the elementwise warps
+#endif
+#if NEF_WARP_MAP == 3
+// V generators below the elementwise warps (the schedulers favour higher warp ids: the V
+// generators, which run a tile ahead, take the issue slots the elementwise warps leave idle)
+constexpr int W_VG0 = 0, W_EW0 = NVG, W_DV = NEW + 4, W_TMA = NEW + 5, W_MMA = NEW + 6, W_MMA2 = NEW + 7;
+constexpr int W_SW = NEW + 7 + NEF_SPLIT_ISSUE;
+__device__ __forceinline__ int vg_index(int warp) { return warp < NVG ? warp : -1; }
+constexpr int NTHREADS = (NEW + 7 + NEF_SPLIT_ISSUE + NEF_S_WATCH) * 32;
+#elif NEF_WARP_MAP == 2
+constexpr int W_EW0 = 0, W_VG0 = NEW, W_DV = NEW + 5, W_TMA = NEW + 4, W_MMA = NEW + 6, W_MMA2 = NEW + 8;
+constexpr int W_SW = NEW + 8 + NEF_SPLIT_ISSUE;
+__device__ __forceinline__ int vg_index(int warp) {
+  return warp == NEW ? 0 : warp == NEW + 1 ? 1 : warp == NEW + 3 ? 2 : warp == NEW + 7 ? 3 : -1;
+}
+constexpr int NTHREADS = (NEW + 8 + NEF_SPLIT_ISSUE + NEF_S_WATCH) * 32;
+#else
 constexpr int W_EW0 = 0, W_VG0 = NEW, W_DV = NEW + 4, W_TMA = NEW + 5, W_MMA = NEW + 6, W_MMA2 = NEW + 7;
 constexpr int W_SW = NEW + 7 + NEF_SPLIT_ISSUE;   // S watcher (NEF_S_WATCH)
 __device__ __forceinline__ int vg_index(int warp) { return warp >= W_VG0 && warp < W_VG0 + NVG ? warp - W_VG0 : -1; }
 constexpr int NTHREADS = (NEW + 7 + NEF_SPLIT_ISSUE + NEF_S_WATCH) * 32;
+#endif
 constexpr int Y_STAGE = BM * BN * 4;      // 32 KB
 constexpr int M_STAGE = BM * BN;          // 8 KB
 // a V stage: V (64 tile columns x KB bonds, SW128 K-major) then its transpose V^T, KB * 256 B each
@@ -679,7 +700,7 @@ __device__ __forceinline__ void ew_load_y(const TcArgs& a, const unsigned char* 
     }
   } else {
     // (a.y3d: rows m and m + 4 share a swizzle phase -> 2-way bank conflict, cheaper than
-    // reading the chunk pairs swapped and selecting them back)
+    // reading the chunk pairs swapped and selecting them back: measured +3 % c5, +5 % c3)
     const unsigned char* sub = ys + yoff;
 #pragma unroll
     for (int q = 0; q < 4; ++q) {

@@ -8,7 +8,8 @@ import sys
 
 rep, cubin, fn, l0, l1 = sys.argv[1], sys.argv[2], sys.argv[3], int(sys.argv[4]), int(sys.argv[5])
 top = int(sys.argv[6]) if len(sys.argv) > 6 else 40
-src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"], capture_output=True,
+import os
+src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"] + os.environ.get("NCU_FILTER", "").split(), capture_output=True,
                      text=True).stdout
 rows = list(csv.reader(io.StringIO(src)))
 hdr = rows[1]
