@@ -200,7 +200,8 @@ int run_prog(const Ctx& c, const nef::EinProgram& pr, int64_t from1 = -1, int64_
     return resolve(c, b);
   };
   for (const auto& st : pr.steps) {
-    cudaError_t e = nef::launch_einstep(st, res(st.a), st.b.kind == nef::BUF_NONE ? nullptr : res(st.b), res(st.c), c.s);
+    cudaError_t e = nef::launch_einstep(st, res(st.a), st.b.kind == nef::BUF_NONE ? nullptr : res(st.b), res(st.c), c.s,
+                                        reinterpret_cast<float*>(c.ws + c.p->ws_escr));
     ++g_launches;
     if (e != cudaSuccess) return fail(NEF_E_CUDA, std::string("einstep: ") + cudaGetErrorString(e));
   }

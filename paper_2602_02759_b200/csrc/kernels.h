@@ -71,8 +71,12 @@ struct FusedArgs {
 
 cudaError_t launch_fused_ffma(const FusedArgs& a, cudaStream_t s);
 
-// Small einsum step (C = sum A*B, optional B), fp64 accumulation
-cudaError_t launch_einstep(const EinStep& st, const float* A, const float* B, float* C, cudaStream_t s);
+// Small einsum step (C = sum A*B, optional B), fp64 accumulation.  GEMM-shaped steps run as a
+// tiled product; those with few output tiles and long sums split the sum over blocks and need
+// `scratch` (einstep_scratch_floats(st) floats; without it they take the per-output kernels).
+cudaError_t launch_einstep(const EinStep& st, const float* A, const float* B, float* C, cudaStream_t s,
+                           float* scratch = nullptr);
+int64_t einstep_scratch_floats(const EinStep& st);
 
 // out[i] = M[i] ? Y[i] + 0 : -1  (the sentinel copy of Y; M nonzero = observed; observed data >= 0).
 // With dpart (kSentBlocks + 1 partials each of dpart / dcpart): also *dslot = sum over observed

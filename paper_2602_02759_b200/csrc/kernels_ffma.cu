@@ -537,7 +537,231 @@ __global__ void einstep1_kernel(const __grid_constant__ EinStep1Dev st, const fl
   }
 }
 
-cudaError_t launch_einstep(const EinStep& st, const float* A, const float* B, float* C, cudaStream_t s) {
+// GEMM-shaped steps: every summed index in both operands, every output index in A only (M),
+// in B only (N) or in both (batch).  C[b, m, n] = sum_k A[b, m, k] B[b, n, k] as a shared-memory
+// tiled product: a block computes a (16 TM) x (16 TN) output tile with 256 threads (TM x TN
+// outputs each), K in chunks of 16 staged through shared memory; fp32 partial sums over 256
+// terms carried in fp64 (fixed order: deterministic).  The Tucker side operands and
+// epilogues (c2: 1-17 M MAC per step) took 13-23 us per step on the per-output kernels above
+// (each thread gathering its own terms, ~20 % of the SMs busy).
+struct EinGemmDev {
+  int nm, nn, nb, nk;
+  int mdim[3], am[3], cm[3];
+  int ndim[3], bn[3], cn[3];
+  int bdim[2], ab[2], bb[2], cb[2];
+  int kdim[2], ak[2], bk[2];
+  int M, N, K, NB;
+  int a_kfast, b_kfast;   // the operand's innermost summed index has stride 1: load along k
+  int ksplit, kc;         // the sum split over ksplit blocks of kc terms (multiple of 16) each
+  float* part;            // ksplit > 1: dense partials [ksplit][NB][M][N], summed by einstep_gemm_reduce
+};
+__device__ __forceinline__ int gemm_koff(const EinGemmDev& g, int k, bool isA) {
+  if (g.nk == 1) return k * (isA ? g.ak[0] : g.bk[0]);
+  const int k1 = k % g.kdim[1], k0 = k / g.kdim[1];
+  return isA ? k0 * g.ak[0] + k1 * g.ak[1] : k0 * g.bk[0] + k1 * g.bk[1];
+}
+template <int TM, int TN>
+__global__ void __launch_bounds__(256) einstep_gemm_kernel(const __grid_constant__ EinGemmDev g, const float* __restrict__ A,
+                                                           const float* __restrict__ B, float* __restrict__ C) {
+  constexpr int BM = 16 * TM, BN = 16 * TN, BK = 16;
+  __shared__ float As[BK][BM + 1], Bs[BK][BN + 1];
+  __shared__ int aoff[BM], boff[BN], coff_m[BM], coff_n[BN];
+  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
+  const int n0 = blockIdx.x * BN, m0 = blockIdx.y * BM;
+  int abo = 0, bbo = 0, cbo = 0;
+  const int sp = (int)blockIdx.z % g.ksplit, bz = (int)blockIdx.z / g.ksplit;
+  const int kbeg = sp * g.kc, kend = min(g.K, kbeg + g.kc);
+  {
+    int rem = bz;
+    for (int d = g.nb - 1; d >= 0; --d) {
+      const int i = rem % g.bdim[d];
+      rem /= g.bdim[d];
+      abo += i * g.ab[d];
+      bbo += i * g.bb[d];
+      cbo += i * g.cb[d];
+    }
+  }
+  for (int i = tid; i < BM; i += 256) {
+    int rem = m0 + i, ao = 0, co = 0;
+    const bool ok = rem < g.M;
+    for (int d = g.nm - 1; d >= 0; --d) {
+      const int q = rem % g.mdim[d];
+      rem /= g.mdim[d];
+      ao += q * g.am[d];
+      co += q * g.cm[d];
+    }
+    aoff[i] = ok ? abo + ao : -1;
+    coff_m[i] = cbo + co;
+  }
+  for (int i = tid; i < BN; i += 256) {
+    int rem = n0 + i, bo = 0, co = 0;
+    const bool ok = rem < g.N;
+    for (int d = g.nn - 1; d >= 0; --d) {
+      const int q = rem % g.ndim[d];
+      rem /= g.ndim[d];
+      bo += q * g.bn[d];
+      co += q * g.cn[d];
+    }
+    boff[i] = ok ? bbo + bo : -1;
+    coff_n[i] = co;
+  }
+  __syncthreads();
+  float acc[TM][TN];
+  double dacc[TM][TN];
+#pragma unroll
+  for (int i = 0; i < TM; ++i)
+#pragma unroll
+    for (int j = 0; j < TN; ++j) { acc[i][j] = 0.f; dacc[i][j] = 0.0; }
+  int chunk = 0;
+  for (int k0 = kbeg; k0 < kend; k0 += BK, ++chunk) {
+    for (int e = tid; e < BM * BK; e += 256) {
+      const int mm = g.a_kfast ? e / BK : e % BM, kk = g.a_kfast ? e % BK : e / BM;
+      const int k = k0 + kk, ao = aoff[mm];
+      As[kk][mm] = (k < kend && ao >= 0) ? __ldg(A + ao + gemm_koff(g, k, true)) : 0.f;
+    }
+    for (int e = tid; e < BN * BK; e += 256) {
+      const int nn = g.b_kfast ? e / BK : e % BN, kk = g.b_kfast ? e % BK : e / BN;
+      const int k = k0 + kk, bo = boff[nn];
+      Bs[kk][nn] = (k < kend && bo >= 0) ? __ldg(B + bo + gemm_koff(g, k, false)) : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < BK; ++kk) {
+      float av[TM], bv[TN];
+#pragma unroll
+      for (int i = 0; i < TM; ++i) av[i] = As[kk][ty * TM + i];
+#pragma unroll
+      for (int j = 0; j < TN; ++j) bv[j] = Bs[kk][tx * TN + j];
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+    }
+    __syncthreads();
+    if ((chunk & 15) == 15) {   // every 256 terms: fp32 partial -> fp64
+#pragma unroll
+      for (int i = 0; i < TM; ++i)
+#pragma unroll
+        for (int j = 0; j < TN; ++j) { dacc[i][j] += (double)acc[i][j]; acc[i][j] = 0.f; }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < TM; ++i) {
+    const int mm = ty * TM + i;
+    if (aoff[mm] < 0) continue;
+#pragma unroll
+    for (int j = 0; j < TN; ++j) {
+      const int nn = tx * TN + j;
+      if (boff[nn] < 0) continue;
+      const float v = (float)(dacc[i][j] + (double)acc[i][j]);
+      if (g.ksplit == 1) C[coff_m[mm] + coff_n[nn]] = v;
+      else g.part[(((int64_t)sp * g.NB + bz) * g.M + m0 + mm) * g.N + n0 + nn] = v;
+    }
+  }
+}
+// the split partials of einstep_gemm_kernel summed in split order (fp64), written through C's strides
+__global__ void einstep_gemm_reduce(const __grid_constant__ EinGemmDev g, float* __restrict__ C) {
+  const int64_t tot = (int64_t)g.NB * g.M * g.N;
+  for (int64_t o = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; o < tot; o += (int64_t)gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (int sp = 0; sp < g.ksplit; ++sp) acc += (double)g.part[sp * tot + o];
+    int n = (int)(o % g.N), m = (int)((o / g.N) % g.M), b = (int)(o / ((int64_t)g.N * g.M));
+    int co = 0;
+    for (int d = g.nn - 1; d >= 0; --d) { co += (n % g.ndim[d]) * g.cn[d]; n /= g.ndim[d]; }
+    for (int d = g.nm - 1; d >= 0; --d) { co += (m % g.mdim[d]) * g.cm[d]; m /= g.mdim[d]; }
+    for (int d = g.nb - 1; d >= 0; --d) { co += (b % g.bdim[d]) * g.cb[d]; b /= g.bdim[d]; }
+    C[co] = (float)acc;
+  }
+}
+
+// Classifies a step for the GEMM kernel (false: not GEMM-shaped, or beyond its limits) and picks
+// the tile (tm, tn) and the split of the sum: steps whose output tiles would occupy fewer than
+// ~2 blocks per SM split long sums (K > 64) over up to 64 blocks of >= 64 terms.
+static bool gemm_classify(const EinStep& st, bool hasB, EinGemmDev& g, int& tm, int& tn, dim3& grid) {
+  static const bool off = std::getenv("NEF_EINSTEP_NOGEMM") != nullptr;   // diagnostics
+  g = EinGemmDev{};
+  if (off || !hasB || st.nsum < 1 || st.nsum > 2 || st.nout > kMaxDims) return false;
+  long long cst[kMaxDims];
+  long long acc = 1;
+  for (int k = st.nout - 1; k >= 0; --k) { cst[k] = acc; acc *= st.odim[k]; }
+  long long M = 1, N = 1, NB = 1, K = 1, span_a = 0, span_b = 0;
+  for (int k = 0; k < st.nsum; ++k) {
+    if (st.as_s[k] == 0 || st.bs_s[k] == 0) return false;
+    g.kdim[g.nk] = (int)st.sdim[k]; g.ak[g.nk] = (int)st.as_s[k]; g.bk[g.nk] = (int)st.bs_s[k]; ++g.nk;
+    K *= st.sdim[k];
+    span_a += (st.sdim[k] - 1) * st.as_s[k];
+    span_b += (st.sdim[k] - 1) * st.bs_s[k];
+  }
+  for (int k = 0; k < st.nout; ++k) {
+    const bool ia = st.as_o[k] != 0, ib = st.bs_o[k] != 0;
+    if (st.odim[k] == 1) continue;
+    if (ia && ib) {
+      if (g.nb == 2) return false;
+      g.bdim[g.nb] = (int)st.odim[k]; g.ab[g.nb] = (int)st.as_o[k]; g.bb[g.nb] = (int)st.bs_o[k]; g.cb[g.nb] = (int)cst[k]; ++g.nb;
+      NB *= st.odim[k];
+    } else if (ia) {
+      if (g.nm == 3) return false;
+      g.mdim[g.nm] = (int)st.odim[k]; g.am[g.nm] = (int)st.as_o[k]; g.cm[g.nm] = (int)cst[k]; ++g.nm;
+      M *= st.odim[k];
+    } else if (ib) {
+      if (g.nn == 3) return false;
+      g.ndim[g.nn] = (int)st.odim[k]; g.bn[g.nn] = (int)st.bs_o[k]; g.cn[g.nn] = (int)cst[k]; ++g.nn;
+      N *= st.odim[k];
+    } else {
+      return false;   // an output index in neither operand (broadcast): not a product
+    }
+    span_a += (st.odim[k] - 1) * st.as_o[k];
+    span_b += (st.odim[k] - 1) * st.bs_o[k];
+  }
+  if (g.nm == 0) { g.nm = 1; g.mdim[0] = 1; }
+  if (g.nn == 0) { g.nn = 1; g.ndim[0] = 1; }
+  if (span_a >= (1ll << 30) || span_b >= (1ll << 30) || acc >= (1ll << 30) || NB > 65535) return false;
+  if (K >= (1ll << 30) || M * N * NB >= (1ll << 30)) return false;
+  g.M = (int)M; g.N = (int)N; g.K = (int)K; g.NB = (int)NB;
+  g.a_kfast = g.ak[g.nk - 1] == 1;
+  g.b_kfast = g.bk[g.nk - 1] == 1;
+  tm = M >= 48 ? 4 : M >= 24 ? 2 : 1;
+  tn = N >= 48 ? 4 : N >= 24 ? 2 : 1;
+  const long long tiles = ((N + 16 * tn - 1) / (16 * tn)) * ((M + 16 * tm - 1) / (16 * tm)) * NB;
+  long long ks = 1;
+  if (K > 64 && tiles < 296) ks = std::min<long long>(std::min<long long>((296 + tiles - 1) / tiles, (K + 63) / 64), 64);
+  g.kc = (int)(((K + ks - 1) / ks + 15) / 16 * 16);
+  g.ksplit = (int)((K + g.kc - 1) / g.kc);
+  grid = dim3((unsigned)((N + 16 * tn - 1) / (16 * tn)), (unsigned)((M + 16 * tm - 1) / (16 * tm)), (unsigned)(NB * g.ksplit));
+  return grid.y <= 65535 && grid.z <= 65535;
+}
+
+int64_t einstep_scratch_floats(const EinStep& st) {
+  EinGemmDev g;
+  int tm, tn;
+  dim3 grid;
+  if (!gemm_classify(st, st.b.kind != BUF_NONE, g, tm, tn, grid) || g.ksplit == 1) return 0;
+  return (int64_t)g.ksplit * g.NB * g.M * g.N;
+}
+
+static bool einstep_gemm(const EinStep& st, const float* A, const float* B, float* C, cudaStream_t s, float* scratch) {
+  EinGemmDev g;
+  int tm, tn;
+  dim3 grid;
+  if (!gemm_classify(st, B != nullptr, g, tm, tn, grid)) return false;
+  if (g.ksplit > 1) {
+    if (!scratch) return false;   // (no scratch: the per-output kernels)
+    g.part = scratch;
+  }
+#define NEF_GEMM_CASE(A_, B_) \
+  if (tm == A_ && tn == B_) einstep_gemm_kernel<A_, B_><<<grid, 256, 0, s>>>(g, A, B, C);
+  NEF_GEMM_CASE(4, 4) NEF_GEMM_CASE(4, 2) NEF_GEMM_CASE(4, 1) NEF_GEMM_CASE(2, 4) NEF_GEMM_CASE(2, 2)
+  NEF_GEMM_CASE(2, 1) NEF_GEMM_CASE(1, 4) NEF_GEMM_CASE(1, 2) NEF_GEMM_CASE(1, 1)
+#undef NEF_GEMM_CASE
+  if (g.ksplit > 1) {
+    const int64_t tot = (int64_t)g.NB * g.M * g.N;
+    einstep_gemm_reduce<<<(unsigned)std::min<int64_t>((tot + 255) / 256, 148 * 8), 256, 0, s>>>(g, C);
+  }
+  return true;
+}
+
+cudaError_t launch_einstep(const EinStep& st, const float* A, const float* B, float* C, cudaStream_t s, float* scratch) {
+  if (einstep_gemm(st, A, B, C, s, scratch)) return cudaGetLastError();
   static const bool no_fast = std::getenv("NEF_EINSTEP_GENERIC") != nullptr;   // diagnostics
   {
     // fast path eligibility: one summed index, <= 3 output indices, 32-bit offsets

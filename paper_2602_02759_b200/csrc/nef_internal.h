@@ -45,6 +45,9 @@ struct EinStep {
   int64_t out_size = 1, sum_size = 1;
 };
 
+// fp32 scratch floats a GEMM-shaped step needs for its split partials (0: none; kernels_ffma.cu)
+int64_t einstep_scratch_floats(const EinStep& st);
+
 struct EinProgram {
   std::vector<EinStep> steps;     // executed in order; last step writes the result
   BufRef result;                  // where the result lives (may alias an input when steps empty)
@@ -129,6 +132,7 @@ struct Plan {
   int64_t ws_dpart = 0;              // their kSentParts block partials (doubles, then counts)
   int64_t ws_fsave = 0;              // factor copies of nef_fit_split (iterate entering a sweep)
   int64_t ws_sent = 0;               // NaN-sentinel copy of Y (nef_fit with a mask)
+  int64_t ws_escr = 0;               // split partials of GEMM-shaped einsum steps (launch_einstep)
   // sharding
   int shard_mode = -1, rank = 0, world = 1;
   int64_t local_begin = 0, local_len = 0;

@@ -612,8 +612,17 @@ int lower_all(Plan& p, std::string& err) {
     for (auto d : sh) n *= d;
     fbytes += (n * 4 + 255) / 256 * 256;
   }
+  // split partials of GEMM-shaped einsum steps (side operands, epilogues): the largest need
+  int64_t escr = 0;
+  for (const auto& L : p.low) {
+    for (const auto& st : L.uprog.steps) escr = std::max<int64_t>(escr, einstep_scratch_floats(st));
+    for (const auto& t : L.tabs)
+      for (const auto& st : t.prog.steps) escr = std::max<int64_t>(escr, einstep_scratch_floats(st));
+    for (const auto& st : L.epi.steps) escr = std::max<int64_t>(escr, einstep_scratch_floats(st));
+  }
+  p.ws_escr = (p.ws_fsave + fbytes + 255) / 256 * 256;
   // NaN-sentinel copy of the local Y (nef_fit with a mask, R5): 4 B per local entry
-  p.ws_sent = (p.ws_fsave + fbytes + 255) / 256 * 256;
+  p.ws_sent = (p.ws_escr + escr * 4 + 255) / 256 * 256;
   p.ws_bytes = (size_t)(p.ws_sent + p.n_local * 4 + 256);
   return NEF_OK;
 }
