@@ -108,7 +108,7 @@ int nef_plan(const char* einsum, int n_modes, const int64_t* shape, int n_ranks,
  * need for a problem WITH a mask (a maskless problem needs no more).  Any out-pointer may
  * be NULL.
  * Memory: workspace_bytes includes a 4-byte-per-local-entry copy of Y (the mask folded in as a
- * sign sentinel, R22) that masked fits stream instead of Y + mask - e.g. +17.2 GB for
+ * NaN sentinel, R22) that masked fits stream instead of Y + mask - e.g. +17.2 GB for
  * the 2048x2048x1024 tensor, on top of Y (17.2 GB) and the mask (4.3 GB); plus small per-factor
  * scratch (side operands, split partials, < 1 % of Y). */
 int nef_plan_info(nef_plan_t plan, int* n_factors, int* shard_mode, int64_t* local_begin, int64_t* local_len,
@@ -133,7 +133,7 @@ int nef_plan_describe(nef_plan_t plan, char* buf, size_t cap, size_t* len);
  * every factor that does not contain the shard mode and the loss are all-reduced over
  * NCCL; every rank ends with identical replicated factors.
  * Once per fit (R22, R25): with a mask, the mask is folded into a copy of Y in the
- * workspace (missing -> -1) that the streaming passes read instead of Y + mask, and for the
+ * workspace (missing -> canonical NaN) that the streaming passes read instead of Y + mask, and for the
  * (alpha,beta) pairs (1,0), (1,-0.5), (0.5,0) the data-only part of the loss is summed there
  * (without a mask, by a read-only pass when iters >= 3); Y and the mask are never written. */
 int nef_fit(nef_plan_t plan, const float* Y, const uint8_t* mask, double alpha, double beta, double eps,

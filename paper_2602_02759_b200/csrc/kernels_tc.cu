@@ -51,6 +51,9 @@ template <int KB, int MM> struct YStages {
 #endif
 // (MM = 2, the per-entry parameter stream: 2 Y + 2 parameter stages; 3 V stages for bond 64)
 template <int KB, int MM> struct VStages { static constexpr int value = MM == 1 ? 3 : (MM == 2 && KB == 64) ? 3 : NEF_NV0; };
+#ifndef NEF_ND_MN
+#define NEF_ND_MN 0   // numerator / denominator MMAs read V MN-major (no V^T copy)
+#endif
 #ifndef NEF_PA_RN
 #define NEF_PA_RN 0   // 1: plain RN for P_a in the Euclidean pair too (diagnostics)
 #endif
@@ -116,7 +119,7 @@ constexpr int M_STAGE = BM * BN;          // 8 KB
 // a V stage: V (64 tile columns x KB bonds, SW128 K-major) then its transpose V^T, KB * 256 B each
 template <int KB> struct VSt {
   static constexpr int VT_OFF = BN * KB * 4;     // V^T copy after V inside a stage
-  static constexpr int SIZE = 2 * VT_OFF;        // 32 KB for KB = 64, 16 KB for KB = 32
+  static constexpr int SIZE = NEF_ND_MN ? VT_OFF : 2 * VT_OFF;   // (NEF_ND_MN: V only)
 };
 
 struct __align__(64) Params {
@@ -568,9 +571,11 @@ __device__ __forceinline__ void vblock_store(unsigned char* vrow, int vb, int cx
     w[r][3] = tf32_bits(p[r].w) & m;
     *reinterpret_cast<uint4*>(vrow + vb + r * 128 + ((cx ^ r) << 4)) = make_uint4(w[r][0], w[r][1], w[r][2], w[r][3]);
   }
+  if (!NEF_ND_MN) {
 #pragma unroll
-  for (int e = 0; e < 4; ++e)
-    *reinterpret_cast<uint4*>(vrow + vtb + e * 128 + ((xc ^ e) << 4)) = make_uint4(w[0][e], w[1][e], w[2][e], w[3][e]);
+    for (int e = 0; e < 4; ++e)
+      *reinterpret_cast<uint4*>(vrow + vtb + e * 128 + ((xc ^ e) << 4)) = make_uint4(w[0][e], w[1][e], w[2][e], w[3][e]);
+  }
 }
 
 // Direct path: bonds beyond K are TMA zero fill times a zero constant row, rows beyond the
@@ -587,9 +592,11 @@ __device__ __forceinline__ void vblock_store_direct(unsigned char* vrow, int vb,
     w[r][3] = __float_as_uint(p[r].w) + 0x1000u;
     *reinterpret_cast<uint4*>(vrow + vb + r * 128 + ((cx ^ r) << 4)) = make_uint4(w[r][0], w[r][1], w[r][2], w[r][3]);
   }
+  if (!NEF_ND_MN) {
 #pragma unroll
-  for (int e = 0; e < 4; ++e)
-    *reinterpret_cast<uint4*>(vrow + vtb + e * 128 + ((xc ^ e) << 4)) = make_uint4(w[0][e], w[1][e], w[2][e], w[3][e]);
+    for (int e = 0; e < 4; ++e)
+      *reinterpret_cast<uint4*>(vrow + vtb + e * 128 + ((xc ^ e) << 4)) = make_uint4(w[0][e], w[1][e], w[2][e], w[3][e]);
+  }
 }
 
 // Slow paths (several varying tables, or non-vectorisable tables), out of line so the fast
@@ -639,7 +646,7 @@ __device__ __noinline__ void vtile_store_slow(const TcArgs& a, int xw, int lane,
         }
         const uint32_t w = tf32_bits(p);
         *reinterpret_cast<uint32_t*>(vrow + sw128_off(x, k, BN)) = w;
-        *reinterpret_cast<uint32_t*>(vrow + VSt<KB>::VT_OFF + sw128_off(k, x, KB)) = w;
+        if (!NEF_ND_MN) *reinterpret_cast<uint32_t*>(vrow + VSt<KB>::VT_OFF + sw128_off(k, x, KB)) = w;
       }
     }
   }
@@ -1323,11 +1330,25 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
         if (lane == 0) trace_ev(a, u, EV_MMA23_ISSUE);
         __syncwarp();
         if (a.mode != 2 && !(NEF_DBG & 64)) {   // NEF_DBG 64: timing experiment without N/D MMAs
-          // B = V^T, K-major SW128: rows = bond (N), K = tile columns (2 atoms of 32)
-          const uint64_t vtd = sdesc(sV + vs * V_STAGE + VSt<KB>::VT_OFF, 16, 1024);
           const uint32_t pa = tmem + buf_col(b);   // P_a; P_b at pa + 64
           // the accumulators restart at every drain group (see the elementwise loop)
           const uint32_t acc = (u % G) != 0 ? 1u : 0u;
+#if NEF_ND_MN
+          // B = V itself read MN-major: bonds (N) contiguous in its 128-byte rows, the second
+          // 32-bond column block 64 rows * 128 B further (LBO), 8 tile columns (K) per 1024-byte atom
+          const uint64_t vtd = sdesc(sV + vs * V_STAGE, (uint32_t)BN * 128u, 1024);
+          constexpr uint32_t id2m = id2 | (1u << 16);   // B MN-major
+          if constexpr (SPA) {
+            if (b == 0) mma_nd3_mn_block_32_b0<id2m>(tNa, tNb, pa, vtd, acc);
+            else mma_nd3_mn_block_32_b1<id2m>(tNa, tNb, pa, vtd, acc);
+          } else if constexpr (KB == 64) {
+            mma_nd_mn_block_64<id2m>(tNa, tNb, pa, vtd, acc);
+          } else {
+            mma_nd_mn_block_32<id2m>(tNa, tNb, pa, vtd, acc);
+          }
+#else
+          // B = V^T, K-major SW128: rows = bond (N), K = tile columns (2 atoms of 32)
+          const uint64_t vtd = sdesc(sV + vs * V_STAGE + VSt<KB>::VT_OFF, 16, 1024);
           if constexpr (SPA) {
             if (b == 0) mma_nd3_block_32_b0<id2>(tNa, tNb, pa, vtd, acc);
             else mma_nd3_block_32_b1<id2>(tNa, tNb, pa, vtd, acc);
@@ -1336,6 +1357,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
           } else {
             mma_nd_block_32<id2>(tNa, tNb, pa, vtd, acc);
           }
+#endif
         }
         mma_commit_elect(v_empty + 8 * vs);
         mma_commit_elect(buf_free + 8 * b);
