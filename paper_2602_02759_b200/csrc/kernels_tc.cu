@@ -52,7 +52,7 @@ template <int KB, int MM> struct YStages {
 // (MM = 2, the per-entry parameter stream: 2 Y + 2 parameter stages; 3 V stages for bond 64)
 template <int KB, int MM> struct VStages { static constexpr int value = MM == 1 ? 3 : (MM == 2 && KB == 64) ? 3 : NEF_NV0; };
 #ifndef NEF_ND_MN
-#define NEF_ND_MN 0   // numerator / denominator MMAs read V MN-major (no V^T copy)
+#define NEF_ND_MN 1   // one V copy (32-byte-atom swizzle) read K-major by S and MN-major by N / D: c5 -3 %, c3 -2.3 %, c4 -5.7 %
 #endif
 #ifndef NEF_PA_RN
 #define NEF_PA_RN 0   // 1: plain RN for P_a in the Euclidean pair too (diagnostics)
@@ -361,15 +361,29 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 
-// UMMA shared-memory descriptor, SWIZZLE_128B, sm_100 (version 1)
-__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+// UMMA shared-memory descriptor, sm_100 (version 1); layout 2 = SWIZZLE_128B, 1 = SWIZZLE_128B
+// with 32-byte atoms (the V stage under NEF_ND_MN)
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo, uint32_t layout = 2) {
   uint64_t d = 0;
   d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
   d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
   d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
   d |= (uint64_t)1 << 46;
-  d |= (uint64_t)2 << 61;
+  d |= (uint64_t)layout << 61;
   return d;
+}
+// The V stage (rows = tile columns, 128-byte rows of 32 bonds, a 32-bond column block per
+// BN * 128 bytes).  NEF_ND_MN: the 128-byte swizzle with 32-byte atoms (byte bits 5-6 ^= bits 7-8;
+// descriptor layout 1, TMA SWIZZLE_128B_ATOM_32B), which the tensor core reads both K-major (the
+// reconstruction, B = V with K = bonds; LBO = BN * 128, SBO = 512) and MN-major (numerator /
+// denominator, B = V with N = bonds, K = tile columns) - one copy of V serves both MMAs
+// (ubench/mn32.cu).  Otherwise the plain 128-byte swizzle, V^T beside it.
+// 16-byte chunk j of a V row r: its physical chunk
+__device__ __forceinline__ int v_chunk(int j, int r) {
+  return NEF_ND_MN ? ((((j >> 1) ^ (r & 3)) << 1) | (j & 1)) : (j ^ (r & 7));
+}
+__device__ __forceinline__ int v_off(int row, int k, int rows) {
+  return (k >> 5) * (rows * 128) + (row >> 3) * 1024 + (row & 7) * 128 + (v_chunk((k & 31) >> 2, row) << 4) + (k & 3) * 4;
 }
 // instruction descriptor: kind::tf32, D f32, A/B tf32, A and B K-major
 __host__ __device__ constexpr uint32_t idesc_tf32(int M, int N) {
@@ -548,7 +562,7 @@ struct VOff {
     for (int i = 0; i < NB; ++i) {
       const int x0 = xw + 4 * vl_rg(lane, i);
       vb[i] = (c >> 3) * (BN * 128) + (x0 >> 3) * 1024 + (x0 & 7) * 128;
-      cx[i] = (c & 7) ^ (x0 & 7);
+      cx[i] = NEF_ND_MN ? (c & 7) : ((c & 7) ^ (x0 & 7));   // (v_chunk(cx, r): the 4 rows of the block)
       const int k0 = 4 * c;
       vtb[i] = VSt<KB>::VT_OFF + (x0 >> 5) * (KB * 128) + (k0 >> 3) * 1024 + (k0 & 7) * 128;
       xc[i] = ((x0 & 31) >> 2) ^ (k0 & 7);
@@ -569,7 +583,7 @@ __device__ __forceinline__ void vblock_store(unsigned char* vrow, int vb, int cx
     w[r][1] = tf32_bits(p[r].y) & m;
     w[r][2] = tf32_bits(p[r].z) & m;
     w[r][3] = tf32_bits(p[r].w) & m;
-    *reinterpret_cast<uint4*>(vrow + vb + r * 128 + ((cx ^ r) << 4)) = make_uint4(w[r][0], w[r][1], w[r][2], w[r][3]);
+    *reinterpret_cast<uint4*>(vrow + vb + r * 128 + (v_chunk(cx, r) << 4)) = make_uint4(w[r][0], w[r][1], w[r][2], w[r][3]);
   }
   if (!NEF_ND_MN) {
 #pragma unroll
@@ -590,7 +604,7 @@ __device__ __forceinline__ void vblock_store_direct(unsigned char* vrow, int vb,
     w[r][1] = __float_as_uint(p[r].y) + 0x1000u;
     w[r][2] = __float_as_uint(p[r].z) + 0x1000u;
     w[r][3] = __float_as_uint(p[r].w) + 0x1000u;
-    *reinterpret_cast<uint4*>(vrow + vb + r * 128 + ((cx ^ r) << 4)) = make_uint4(w[r][0], w[r][1], w[r][2], w[r][3]);
+    *reinterpret_cast<uint4*>(vrow + vb + r * 128 + (v_chunk(cx, r) << 4)) = make_uint4(w[r][0], w[r][1], w[r][2], w[r][3]);
   }
   if (!NEF_ND_MN) {
 #pragma unroll
@@ -645,7 +659,7 @@ __device__ __noinline__ void vtile_store_slow(const TcArgs& a, int xw, int lane,
           if (p != 0.f) p *= __ldg(a.tab[q] + to + a.boff[q][k]);
         }
         const uint32_t w = tf32_bits(p);
-        *reinterpret_cast<uint32_t*>(vrow + sw128_off(x, k, BN)) = w;
+        *reinterpret_cast<uint32_t*>(vrow + v_off(x, k, BN)) = w;
         if (!NEF_ND_MN) *reinterpret_cast<uint32_t*>(vrow + VSt<KB>::VT_OFF + sw128_off(k, x, KB)) = w;
       }
     }
@@ -1300,7 +1314,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
         tc_fence_after();
         if (lane == 0) trace_ev(a, t, EV_MMA1_ISSUE);
         __syncwarp();
-        const uint64_t vd = sdesc(sV + vs * V_STAGE, 16, 1024);
+        const uint64_t vd = NEF_ND_MN ? sdesc(sV + vs * V_STAGE, (uint32_t)BN * 128u, 512, 1) : sdesc(sV + vs * V_STAGE, 16, 1024);
         const uint32_t d = tmem + buf_col(b);
         // one asm block, one elect: U_hi and U_lo steps interleaved (tUl = tUh + KB)
         if constexpr ((NEF_DBG & 512) != 0) {   // timing experiment: no U_lo MMAs
@@ -1334,9 +1348,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
           // the accumulators restart at every drain group (see the elementwise loop)
           const uint32_t acc = (u % G) != 0 ? 1u : 0u;
 #if NEF_ND_MN
-          // B = V itself read MN-major: bonds (N) contiguous in its 128-byte rows, the second
-          // 32-bond column block 64 rows * 128 B further (LBO), 8 tile columns (K) per 1024-byte atom
-          const uint64_t vtd = sdesc(sV + vs * V_STAGE, (uint32_t)BN * 128u, 1024);
+          // B = V itself read MN-major (32-byte-atom swizzle, see v_chunk): bonds (N) contiguous in
+          // its 128-byte rows, the second 32-bond column block BN rows * 128 B further (LBO), 4
+          // tile columns (K) per 512 bytes (SBO), 8 per K step
+          const uint64_t vtd = sdesc(sV + vs * V_STAGE, (uint32_t)BN * 128u, 512, 1);
           constexpr uint32_t id2m = id2 | (1u << 16);   // B MN-major
           if constexpr (SPA) {
             if (b == 0) mma_nd3_mn_block_32_b0<id2m>(tNa, tNb, pa, vtd, acc);
@@ -1383,7 +1398,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
         tc_fence_after();
         if (lane == 0) trace_ev(a, t, EV_MMA1_ISSUE);
         __syncwarp();
-        const uint64_t vd = sdesc(sV + vs * V_STAGE, 16, 1024);
+        const uint64_t vd = NEF_ND_MN ? sdesc(sV + vs * V_STAGE, (uint32_t)BN * 128u, 512, 1) : sdesc(sV + vs * V_STAGE, 16, 1024);
         const uint32_t d = tmem + buf_col(b);
         if (KB == 64) mma_s_block_64<id1>(d, tUh, vd, 0u);
         else mma_s_block_32<id1>(d, tUh, vd, 0u);
@@ -1453,7 +1468,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
         float4 p[4];
 #pragma unroll
         for (int r = 0; r < 4; ++r) {
-          const float4 f = *reinterpret_cast<const float4*>(vrow + vo.vb[i] + r * 128 + ((vo.cx[i] ^ r) << 4));
+          const float4 f = *reinterpret_cast<const float4*>(vrow + vo.vb[i] + r * 128 + (v_chunk(vo.cx[i], r) << 4));
           const float2 lo = __fmul2_rn(make_float2(f.x, f.y), make_float2(cst.x, cst.y));
           const float2 hi = __fmul2_rn(make_float2(f.z, f.w), make_float2(cst.z, cst.w));
           p[r] = make_float4(lo.x, lo.y, hi.x, hi.y);
@@ -1833,7 +1848,8 @@ cudaError_t launch(const TcArgs& args, const float* Y, const uint8_t* M, int64_t
     uint64_t d[2] = {(uint64_t)args.K, (uint64_t)args.var_rows};
     uint64_t sv[1] = {(uint64_t)args.vd_pitch * 4};
     uint32_t bv[2] = {32, 64};
-    ok = encode(&P.tmV[r], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, P.a.vdr[r], d, sv, bv, CU_TENSOR_MAP_SWIZZLE_128B);
+    ok = encode(&P.tmV[r], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, P.a.vdr[r], d, sv, bv,
+                NEF_ND_MN ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B);
   }
   if (!ok) return cudaErrorInvalidValue;
   P.a.has_mask = M ? 1 : 0;
