@@ -22,6 +22,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
+#include <cuda_bf16.h>
 
 #include <cstdint>
 #include <cstdlib>
@@ -51,6 +52,12 @@ template <int KB, int MM> struct YStages {
 #endif
 // (MM = 2, the per-entry parameter stream: 2 Y + 2 parameter stages; 3 V stages for bond 64)
 template <int KB, int MM> struct VStages { static constexpr int value = MM == 1 ? 3 : (MM == 2 && KB == 64) ? 3 : NEF_NV0; };
+#ifndef NEF_ULO_BF16
+#define NEF_ULO_BF16 1   // bond 64: the U_lo correction of S as BF16 MMAs (K = 16) on a BF16 copy of V (c5 -4 %)
+#endif
+#if NEF_ULO_BF16 && NEF_SPLIT_ISSUE
+#error "NEF_ULO_BF16 has no split-issue path"
+#endif
 #ifndef NEF_ND_MN
 #define NEF_ND_MN 1   // one V copy (32-byte-atom swizzle) read K-major by S and MN-major by N / D: c5 -3 %, c3 -2.3 %, c4 -5.7 %
 #endif
@@ -119,7 +126,9 @@ constexpr int M_STAGE = BM * BN;          // 8 KB
 // a V stage: V (64 tile columns x KB bonds, SW128 K-major) then its transpose V^T, KB * 256 B each
 template <int KB> struct VSt {
   static constexpr int VT_OFF = BN * KB * 4;     // V^T copy after V inside a stage
-  static constexpr int SIZE = NEF_ND_MN ? VT_OFF : 2 * VT_OFF;   // (NEF_ND_MN: V only)
+  static constexpr bool ULB = NEF_ULO_BF16 && KB == 64;   // BF16 copy of V for the U_lo MMAs
+  static constexpr int VB_OFF = NEF_ND_MN ? VT_OFF : 2 * VT_OFF;
+  static constexpr int SIZE = VB_OFF + (ULB ? BN * KB * 2 : 0);   // (NEF_ND_MN: V only)
 };
 
 struct __align__(64) Params {
@@ -319,6 +328,39 @@ __device__ __forceinline__ void mma_ts_elect(uint32_t d, uint32_t a, uint64_t bd
       : "memory");
 }
 #include "mma_blocks.inc"
+// instruction descriptor: kind::f16 with BF16 A and B, D f32, K-major
+__host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
+  return (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+// S += U_lo V in BF16 (NEF_ULO_BF16, bond 64): four K = 16 MMAs, A = U_lo packed two per TMEM
+// column (alo + 8 s), B = the stage's BF16 copy of V (K-major 128-byte swizzle, +32 B per step)
+template <uint32_t IDESC>
+__device__ __forceinline__ void mma_slo_bf16_64(uint32_t d, uint32_t alo, uint64_t b) {
+  asm volatile(
+      "{\n\t"
+      ".reg .pred e, t;\n\t"
+      ".reg .b32 bl, bh, bk, ak;\n\t"
+      ".reg .b64 bd;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.eq.b32 t, %1, %1;\n\t"
+      "mov.b64 {bl, bh}, %2;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, t;\n\t"
+      "add.u32 ak, %1, 8;\n\t"
+      "add.u32 bk, bl, 2;\n\t"
+      "mov.b64 bd, {bk, bh};\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ak], bd, %3, t;\n\t"
+      "add.u32 ak, %1, 16;\n\t"
+      "add.u32 bk, bl, 4;\n\t"
+      "mov.b64 bd, {bk, bh};\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ak], bd, %3, t;\n\t"
+      "add.u32 ak, %1, 24;\n\t"
+      "add.u32 bk, bl, 6;\n\t"
+      "mov.b64 bd, {bk, bh};\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [ak], bd, %3, t;\n\t"
+      "}\n" ::"r"(d),
+      "r"(alo), "l"(b), "n"(IDESC)
+      : "memory");
+}
 __device__ __forceinline__ void mma_commit_elect(uint32_t bar) {
   asm volatile(
       "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
@@ -359,6 +401,11 @@ __device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16
       : "memory");
 }
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&r)[8]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(taddr), "r"(r[0]),
+               "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+               : "memory");
+}
 
 
 // UMMA shared-memory descriptor, sm_100 (version 1); layout 2 = SWIZZLE_128B, 1 = SWIZZLE_128B
@@ -556,11 +603,15 @@ template <int KB>
 struct VOff {
   static constexpr int C = KB / 4, NB = (4 * C) / 32;
   int vb[NB], vtb[NB], cx[NB], xc[NB];
+  int c16, rowoff[NB], x7[NB];   // (BF16 copy of V: bond chunk, row offset and row & 7 of each block)
   __device__ __forceinline__ void init(int xw, int lane) {
     const int c = vl_c<KB>(lane);
+    c16 = c;
 #pragma unroll
     for (int i = 0; i < NB; ++i) {
       const int x0 = xw + 4 * vl_rg(lane, i);
+      rowoff[i] = (x0 >> 3) * 1024 + (x0 & 7) * 128;
+      x7[i] = x0 & 7;
       vb[i] = (c >> 3) * (BN * 128) + (x0 >> 3) * 1024 + (x0 & 7) * 128;
       cx[i] = NEF_ND_MN ? (c & 7) : ((c & 7) ^ (x0 & 7));   // (v_chunk(cx, r): the 4 rows of the block)
       const int k0 = 4 * c;
@@ -570,6 +621,21 @@ struct VOff {
   }
 };
 
+// BF16 copy of V (VSt::ULB, K-major 128-byte swizzle: row x = 64 bonds in 128 bytes): the 4x4 block
+// at rows x0..x0+3 (rowoff, x7 = x0 & 7), bonds 4c..4c+3 as four 8-byte stores, RN
+template <int KB>
+__device__ __forceinline__ void vb16_store(unsigned char* vrow, int rowoff, int x7, int c, const float4 (&p)[4],
+                                           uint32_t okbits = 0xfu) {
+  if constexpr (VSt<KB>::ULB) {
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const uint32_t m = ((okbits >> r) & 1u) ? 0xffffffffu : 0u;
+      const __nv_bfloat162 lo = __floats2bfloat162_rn(p[r].x, p[r].y), hi = __floats2bfloat162_rn(p[r].z, p[r].w);
+      const uint2 v = make_uint2(*reinterpret_cast<const uint32_t*>(&lo) & m, *reinterpret_cast<const uint32_t*>(&hi) & m);
+      *reinterpret_cast<uint2*>(vrow + VSt<KB>::VB_OFF + rowoff + r * 128 + ((((c >> 1) ^ ((x7 + r) & 7))) << 4) + (c & 1) * 8) = v;
+    }
+  }
+}
 // Store one 4x4 block (rows x0..x0+3, bonds 4c..4c+3): four 16-byte rows of V and four
 // 16-byte columns of V^T, TF32 round-to-nearest, zeros where invalid.
 template <int KB>
@@ -641,6 +707,7 @@ __device__ __noinline__ void vtile_store_slow(const TcArgs& a, int xw, int lane,
       }
       const uint32_t ok = kok ? ((v.vmask >> (4 * rg)) & 0xfu) : 0u;
       vblock_store<KB>(vrow, vo.vb[i], vo.cx[i], vo.vtb[i], vo.xc[i], ok, p);
+      vb16_store<KB>(vrow, vo.rowoff[i], vo.x7[i], vo.c16, p, ok);
     }
     return;
   }
@@ -660,6 +727,9 @@ __device__ __noinline__ void vtile_store_slow(const TcArgs& a, int xw, int lane,
         }
         const uint32_t w = tf32_bits(p);
         *reinterpret_cast<uint32_t*>(vrow + v_off(x, k, BN)) = w;
+        if constexpr (VSt<KB>::ULB)
+          *reinterpret_cast<__nv_bfloat16*>(vrow + VSt<KB>::VB_OFF + (x >> 3) * 1024 + (x & 7) * 128 +
+                                            (((k >> 3) ^ (x & 7)) << 4) + (k & 7) * 2) = __float2bfloat16_rn(p);
         if (!NEF_ND_MN) *reinterpret_cast<uint32_t*>(vrow + VSt<KB>::VT_OFF + sw128_off(k, x, KB)) = w;
       }
     }
@@ -686,6 +756,7 @@ __device__ __forceinline__ void vtile_store(const TcArgs& a, int xw, int lane, c
       p[r] = make_float4(v.cst.x * v.ld[i][r].x, v.cst.y * v.ld[i][r].y, v.cst.z * v.ld[i][r].z, v.cst.w * v.ld[i][r].w);
     const uint32_t ok = (v.mode == 0 && kok) ? ((v.vmask >> (4 * rg)) & 0xfu) : 0u;
     vblock_store<KB>(vrow, vo.vb[i], vo.cx[i], vo.vtb[i], vo.xc[i], ok, p);
+    vb16_store<KB>(vrow, vo.rowoff[i], vo.x7[i], vo.c16, p, ok);
   }
 }
 
@@ -1320,6 +1391,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
         if constexpr ((NEF_DBG & 512) != 0) {   // timing experiment: no U_lo MMAs
           if (KB == 64) mma_s1_block_64<id1>(d, tUh, vd, 0u);
           else mma_s1_block_32<id1>(d, tUh, vd, 0u);
+        } else if constexpr (VSt<KB>::ULB) {
+          mma_s1_block_64<id1>(d, tUh, vd, 0u);
+          mma_slo_bf16_64<idesc_bf16(128, BN)>(d, tUl, sdesc(sV + vs * V_STAGE + VSt<KB>::VB_OFF, 16, 1024));
         } else if (KB == 64) {
           mma_s_block_64<id1>(d, tUh, vd, 0u);
         } else {
@@ -1473,8 +1547,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
           const float2 hi = __fmul2_rn(make_float2(f.z, f.w), make_float2(cst.z, cst.w));
           p[r] = make_float4(lo.x, lo.y, hi.x, hi.y);
         }
-        if (!(NEF_DBG & 128))   // NEF_DBG 128: timing experiment without the V / V^T stores
+        if (!(NEF_DBG & 128)) {   // NEF_DBG 128: timing experiment without the V / V^T stores
           vblock_store_direct<KB>(vrow, vo.vb[i], vo.cx[i], vo.vtb[i], vo.xc[i], p);
+          vb16_store<KB>(vrow, vo.rowoff[i], vo.x7[i], vo.c16, p);
+        }
       }
       if (warp == W_VG0 && lane == 0) trace_ev(a, t, EV_VG_ISSUED);
       fence_async_smem();
@@ -1533,9 +1609,19 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
           const int k = h * 16 + j;
           const float u = (row_ok && k < a.K) ? __ldg(a.Ur[rs] + row * a.K + k) : 0.f;
           const uint32_t hi = tf32_bits(u);
-          r[j] = lo ? tf32_bits(u - __uint_as_float(hi)) : hi;
+          r[j] = lo ? (VSt<KB>::ULB ? __float_as_uint(u - __uint_as_float(hi)) : tf32_bits(u - __uint_as_float(hi))) : hi;
         }
-        tmem_st16((lo ? tUl : tUh) + lane_off + h * 16, r);
+        if (VSt<KB>::ULB && lo) {   // U_lo as BF16 pairs (k even in the low half): 8 TMEM columns
+          uint32_t r2[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const __nv_bfloat162 v = __floats2bfloat162_rn(__uint_as_float(r[2 * j]), __uint_as_float(r[2 * j + 1]));
+            r2[j] = *reinterpret_cast<const uint32_t*>(&v);
+          }
+          tmem_st8(tUl + lane_off + h * 8, r2);
+        } else {
+          tmem_st16((lo ? tUl : tUh) + lane_off + h * 16, r);
+        }
       }
       tmem_st_wait();
       tc_fence_before();
