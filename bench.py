@@ -155,7 +155,8 @@ def host_info():
 
 
 PRECISION = ("f32 data and factors; tcgen05 kind::tf32 MMAs (reconstruction with the updated factor's side "
-             "split hi + lo, numerator / denominator operands TF32 round-to-nearest, Euclidean bond <= 32: "
+             "split hi + lo - for bonds 33-64 the small lo term as kind::f16 BF16 MMAs on BF16 copies of U_lo "
+             "and V - numerator / denominator operands TF32 round-to-nearest, Euclidean bond <= 32: "
              "numerator operand split hi + lo); fp32 tensor-core accumulation drained every 256 tiles; fp64 "
              "split-partial, loss and update arithmetic")
 
@@ -318,7 +319,7 @@ def main():
     if rank == 0:
         out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                "warmup": args.warmup, "ms_per_step": t_max / args.steps, "higher_is_better": True,
-               "scaling": "strong", "vs_baseline": None, "dtype": "f32/tf32", "precision": PRECISION,
+               "scaling": "strong", "vs_baseline": None, "dtype": "f32/tf32/bf16", "precision": PRECISION,
                "data": "synthetic", "host": host_info(),
                "config": dict(_workload(cfg), parallelism=("shard mode %d over %d ranks, NCCL all-reduce of partials"
                                                            % (sm, world)) if world > 1 else "single GPU",
