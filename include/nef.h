@@ -249,8 +249,10 @@ int nef_profile_read(double* kernel_ms, int64_t* launches, double* algorithmic_b
 
 /* Select the streaming kernel: bit 0 clear = automatic (tcgen05 where supported), set = CUDA-core
  * FFMA kernel only; bit 1 set = no sweep graphs (nef_fit then launches every kernel of every sweep
- * itself instead of replaying its cached one-sweep CUDA graph).  Process-wide; for tests and A/B
- * measurement. */
+ * itself instead of replaying its cached one-sweep CUDA graph); bit 2 set = no side-operand reuse
+ * inside a sweep (every update recomputes its U and column tables; by default an update reads
+ * the identical table an earlier update of the same sweep left in the workspace).
+ * Process-wide; for tests and A/B measurement. */
 int nef_set_kernel_policy(int policy);
 
 /* Test hook: when device_buffer != NULL the tcgen05 streaming kernel writes the P_a tile

@@ -59,6 +59,7 @@ thread_local int64_t g_launches = 0;
 int g_policy = 0;
 float* g_debug = nullptr;   // optional device dump of the tcgen05 kernel's first tile (tests)
 long long* g_trace = nullptr;   // optional pipeline timeline of the tcgen05 kernel (diagnostics)
+bool g_no_memo = std::getenv("NEF_NO_REUSE") != nullptr;        // diagnostics: recompute every side operand
 bool g_no_sentinel = std::getenv("NEF_NO_SENTINEL") != nullptr;   // diagnostics: stream the uint8 mask
 bool g_no_lconst = std::getenv("NEF_NO_LCONST") != nullptr;     // diagnostics: loss passes compute the whole divergence (R25 off)
 bool g_no_sqy = std::getenv("NEF_NO_SQY") != nullptr;           // diagnostics: (0.5, 0) streams y, not sqrt(y)
@@ -176,6 +177,8 @@ struct Ctx {
   const float* aux = nullptr;     // per-entry phi / n (App. B losses), Y's layout; CUDA-core kernel only
   bool sqy = false;               // ysent holds sqrt(y) for the (0.5, 0) pair (R35), masked or not
   int split = 0;                  // the mask holds labels 0..3 (R29); loss slots are [3] per pass
+  bool memo = false;              // inside a sweep run in update order: skip the side-operand
+                                  // programs the planner marked as reusable (sweep_reuse)
   // split fits: after the loss-carrying pass, copy the loss slots to pinned host memory and
   // record an event, so the host can take the stopping decision while the sweep continues
   void* pin = nullptr;
@@ -223,11 +226,12 @@ nef::FusedArgs fused_args(const Ctx& c, const nef::Lowering& L, const float* Y, 
   a.nc = (int)L.col_modes.size();
   for (int k = 0; k < a.nr; ++k) { a.rdim[k] = L.rdim[k]; a.rys[k] = L.rystride[k]; }
   for (int k = 0; k < a.nc; ++k) { a.cdim[k] = L.cdim[k]; a.cys[k] = L.cystride[k]; }
-  a.U = prog_result(c, L.uprog);
+  a.U = (c.memo && L.reuse_u) ? resolve(c, L.alias_u) : prog_result(c, L.uprog);
   a.ntab = (int)L.tabs.size();
   boff_host.clear();
   for (int q = 0; q < a.ntab; ++q) {
-    a.tab[q] = prog_result(c, L.tabs[q].prog);
+    a.tab[q] = (c.memo && q < (int)L.reuse_tab.size() && L.reuse_tab[q]) ? resolve(c, L.alias_tab[q])
+                                                                          : prog_result(c, L.tabs[q].prog);
     for (int k = 0; k < a.nc; ++k) a.tcs[q][k] = L.tabs[q].cstride[k];
     boff_host.insert(boff_host.end(), L.tabs[q].boff.begin(), L.tabs[q].boff.end());
   }
@@ -248,10 +252,11 @@ nef::FusedArgs fused_args(const Ctx& c, const nef::Lowering& L, const float* Y, 
 }
 
 int side_operands(const Ctx& c, const nef::Lowering& L) {
-  int st = run_prog(c, L.uprog);
+  int st = (c.memo && L.reuse_u) ? NEF_OK : run_prog(c, L.uprog);
   if (st) return st;
-  for (const auto& t : L.tabs) {
-    st = run_prog(c, t.prog);
+  for (size_t q = 0; q < L.tabs.size(); ++q) {
+    if (c.memo && q < L.reuse_tab.size() && L.reuse_tab[q]) continue;
+    st = run_prog(c, L.tabs[q].prog);
     if (st) return st;
   }
   return NEF_OK;
@@ -637,11 +642,12 @@ int validate_spec(const nef_loss_spec* l, Spec& sp) {
 // profiling events before each replay when nef_profile is on.
 std::string sweep_key(const Ctx& c, const float* Y, const uint8_t* M, const nef::DivParams& dv, const nef::UpdArgs& u) {
   std::string k;
-  char buf[64];
+  char buf[128];
   auto add = [&](const void* q) { std::snprintf(buf, sizeof buf, "%p,", q); k += buf; };
   add(Y); add(M); add(c.ws); add(c.ysent); add(c.loff); add(c.aux);
   for (size_t l = 0; l < c.p->ops.size(); ++l) add(c.F[l]);
-  std::snprintf(buf, sizeof buf, "%zu,%d,%d,%d,%.17g,", c.ws_bytes, g_policy, (int)g_vdirect, (int)c.sqy, c.lscale);
+  std::snprintf(buf, sizeof buf, "%zu,%d,%d,%d,%.17g,%d,", c.ws_bytes, g_policy, (int)g_vdirect, (int)c.sqy, c.lscale,
+                (int)g_no_memo);
   k += buf;
   k.append(reinterpret_cast<const char*>(&dv), sizeof dv);
   k.append(reinterpret_cast<const char*>(&u), sizeof u);
@@ -665,6 +671,7 @@ SweepGraph* sweep_graph(nef_plan_t plan, const Ctx& c, const float* Y, const uin
   }
   Ctx cc = c;                 // captured on the private stream; replayed on the caller's
   cc.s = plan->cap_stream;
+  cc.memo = !g_no_memo;       // the updates run in order 0, 1, ... below
   auto* sg = new SweepGraph();
   sg->key = key;
   const int kSlots = 2048;
@@ -796,9 +803,10 @@ int nef_debug_trace(int64_t* device_buffer) {
 }
 
 int nef_set_kernel_policy(int policy) {
-  if (policy < 0 || policy > 3) return fail(NEF_E_ARG, "policy must be 0..3");
+  if (policy < 0 || policy > 7) return fail(NEF_E_ARG, "policy must be 0..7");
   g_policy = policy & 1;
   g_graphs = (policy & 2) == 0 && [] { const char* e = std::getenv("NEF_NO_GRAPH"); return !e || e[0] != '1'; }();
+  g_no_memo = (policy & 4) != 0 || std::getenv("NEF_NO_REUSE") != nullptr;
   return NEF_OK;
 }
 
@@ -945,11 +953,13 @@ int nef_fit_ex(nef_plan_t plan, const float* Y, const uint8_t* mask, const nef_l
       t0 = iters;
     }
   }
+  Ctx cm = c;
+  cm.memo = !g_no_memo;   // one sweep = the updates in order 0, 1, ...
   for (int t = t0; t < iters; ++t) {
     if (t - base >= kSlots) { if ((st = flush(t))) return st; }
     for (int ell = 0; ell < (int)p.ops.size(); ++ell) {
       int mode = (ell == 0) ? 1 : 0;
-      st = update_one(c, ell, Y, mask, dv, u, mode, slots + (t - base), cslots + (t - base));
+      st = update_one(cm, ell, Y, mask, dv, u, mode, slots + (t - base), cslots + (t - base));
       if (st) return st;
     }
   }
@@ -1131,8 +1141,10 @@ int nef_fit_split(nef_plan_t plan, const float* Y, const uint8_t* labels, const 
       c.pin_counts = (t == 0);
       if (t < T) {   // sweep t + 1; its first pass carries the losses of iterate t
         for (int l = 0; l < L; ++l) CK(cudaMemcpyAsync(fsave[l], factors[l], fbytes[l], cudaMemcpyDeviceToDevice, c.s));
+        Ctx cm = c;
+        cm.memo = !g_no_memo;   // one sweep = the updates in order 0, 1, ...
         for (int ell = 0; ell < L; ++ell)
-          if (int r = update_one(c, ell, Y, labels, dv, u, ell == 0 ? 1 : 0, slots, cslots)) return r;
+          if (int r = update_one(cm, ell, Y, labels, dv, u, ell == 0 ? 1 : 0, slots, cslots)) return r;
       } else if (int r = loss_pass(c, Y, labels, dv, slots, cslots)) {
         return r;
       }

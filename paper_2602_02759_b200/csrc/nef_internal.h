@@ -113,6 +113,13 @@ struct Lowering {
   int64_t vd_Kp = 0;            // TMA row pitch (elements): K rounded up to 4
   int64_t ws_vpad = -1;         // padded copy of the table when K % 4 != 0 (else -1)
   bool tabs_merged = false;     // all column factors merged into one table (small column space)
+  std::vector<std::pair<int64_t, int64_t>> ws_allocs;   // every workspace region [offset, end) it uses
+  // inside a sweep (updates in order 0, 1, ...): U / table q are the result an earlier update
+  // of the same sweep left in the workspace (planner: sweep_reuse)
+  bool reuse_u = false;
+  std::vector<char> reuse_tab;
+  BufRef alias_u;                  // where the reused result lives
+  std::vector<BufRef> alias_tab;
 };
 
 struct Plan {

@@ -89,9 +89,11 @@ struct Operand {
 // bump allocator over the workspace (bytes, 256-aligned)
 struct Bump {
   int64_t off = 0;
+  std::vector<std::pair<int64_t, int64_t>> log;   // every region handed out: [offset, end)
   int64_t take(int64_t bytes) {
     int64_t o = (off + 255) / 256 * 256;
     off = o + std::max<int64_t>(bytes, 0);
+    log.emplace_back(o, off);
     return o;
   }
 };
@@ -554,6 +556,80 @@ double candidate_cost(const Plan& p, const Lowering& L) {
 
 }  // namespace
 
+// Side-operand reuse inside one sweep (factor updates ell = 0, 1, ... in order): a program of
+// update ell (its U or a column table) need not run when an earlier update e of the same sweep
+// computed the same contraction (same steps over the same factors, same result layout), none
+// of its input factors was updated in e .. ell - 1 (update m rewrites factor m only), and no
+// workspace region of the updates e + 1 .. ell (other than the skipped program's own) overlaps
+// the region holding e's result: update ell then reads that region.  c2: update 3's U (ijc) is
+// update 2's table; c4: update 1's table (tdl) is update 0's, updates 3 and 4 use update 2's
+// ijl.  The values are the floats the skipped launches would write (same kernels, same
+// inputs), so results are bit-identical.
+static bool prog_sem(const EinProgram& pr, std::string& sig, std::vector<int>& fac, std::vector<int64_t>& made) {
+  std::ostringstream o;
+  auto ref = [&](const BufRef& b) -> bool {
+    if (b.kind == BUF_FACTOR) { fac.push_back((int)b.id); o << 'F' << b.id; return true; }
+    if (b.kind == BUF_NONE) { o << '-'; return true; }
+    const auto it = std::find(made.begin(), made.end(), b.id);
+    if (it == made.end()) return false;   // reads a region it did not write: never reused
+    o << '#' << (it - made.begin());
+    return true;
+  };
+  for (const auto& st : pr.steps) {
+    if (!ref(st.a) || !ref(st.b)) return false;
+    o << ',' << st.a_idx << ',' << st.b_idx << ',' << st.c_idx << ';';
+    made.push_back(st.c.id);
+  }
+  o << '>' << pr.result_idx << ':' << pr.result.elems;
+  sig = o.str();
+  return !pr.steps.empty() && pr.result.kind == BUF_WS && pr.steps.back().c.id == pr.result.id;
+}
+void sweep_reuse(Plan& p) {
+  const int L = (int)p.low.size();
+  struct Done { std::string sig; std::vector<int> fac; BufRef where; };
+  std::vector<std::vector<Done>> done(L);   // per update: its programs and where their results are
+  for (int ell = 0; ell < L; ++ell) {
+    Lowering& cur = p.low[ell];
+    cur.reuse_u = false;
+    cur.reuse_tab.assign(cur.tabs.size(), 0);
+    cur.alias_tab.assign(cur.tabs.size(), BufRef{});
+    for (int q = -1; q < (int)cur.tabs.size(); ++q) {
+      const EinProgram& pr = q < 0 ? cur.uprog : cur.tabs[q].prog;
+      std::string sig;
+      std::vector<int> fac;
+      std::vector<int64_t> own;
+      if (!prog_sem(pr, sig, fac, own)) continue;
+      BufRef where = pr.result;
+      bool reused = false;
+      for (int e = ell - 1; e >= 0 && !reused; --e) {
+        for (const Done& d : done[e]) {
+          if (d.sig != sig) continue;
+          bool ok = true;
+          for (int f : fac) ok = ok && (f < e || f >= ell);
+          const int64_t r0 = d.where.id, r1 = d.where.id + d.where.elems * 4;
+          for (int m = e + 1; m <= ell && ok; ++m)
+            for (const auto& a : p.low[m].ws_allocs) {
+              if (m == ell && std::find(own.begin(), own.end(), a.first) != own.end()) continue;
+              ok = ok && (a.second <= r0 || a.first >= r1);
+            }
+          if (ok) { where = d.where; reused = true; }
+          break;   // the nearest update that computed it decides
+        }
+        if (!done[e].empty() && !reused) {
+          bool found = false;
+          for (const Done& d : done[e]) found = found || d.sig == sig;
+          if (found) break;
+        }
+      }
+      if (reused) {
+        if (q < 0) { cur.reuse_u = true; cur.alias_u = where; }
+        else { cur.reuse_tab[q] = 1; cur.alias_tab[q] = where; }
+      }
+      done[ell].push_back({sig, fac, where});
+    }
+  }
+}
+
 int lower_all(Plan& p, std::string& err) {
   const int M = (int)p.out.size();
   const int Lf = (int)p.ops.size();
@@ -597,9 +673,11 @@ int lower_all(Plan& p, std::string& err) {
     lower_candidate(p, ell, best_rm, best_pa, L, why);
     finish_lowering(p, L, bump);
     L.cost = best_cost;
+    L.ws_allocs = bump.log;
     ws = std::max<int64_t>(ws, L.ws_end);
     p.low[ell] = std::move(L);
   }
+  sweep_reuse(p);
   p.ws_trace = (ws + 255) / 256 * 256;
   // sentinel pass sums (R25): [data-only loss sum][observed count], then its block partials
   p.ws_dterm = p.ws_trace + (int64_t)8 * 4096;
@@ -748,7 +826,9 @@ std::string describe_plan(const Plan& p) {
     }
     o << "],\"Q\":\"W" << L.ws_Q << "\",\"epi_identity\":" << (L.epi_identity ? "true" : "false") << ",\"epi\":";
     json_prog(o, L.epi);
-    o << ",\"cost\":" << L.cost << "}";
+    o << ",\"reuse_u\":" << (L.reuse_u ? "true" : "false") << ",\"reuse_tab\":[";
+    for (size_t q = 0; q < L.reuse_tab.size(); ++q) o << (q ? "," : "") << (L.reuse_tab[q] ? "true" : "false");
+    o << "],\"cost\":" << L.cost << "}";
   }
   o << "]}";
   return o.str();

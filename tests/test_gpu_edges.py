@@ -311,3 +311,43 @@ def test_no_out_of_bounds_writes(nef, case):
     assert torch.equal(Yd.cpu(), torch.from_numpy(Y))
     if M is not None:
         assert torch.equal(Md.cpu(), torch.from_numpy(M))
+
+
+# models whose sweeps reuse a side operand across updates (planner sweep_reuse): c2's Tucker
+# (update 3's U is update 2's table), c4's spatiotemporal model, LR-Tucker and a 6-mode CP
+REUSE_CASES = [
+    ("ia,jb,kc,abc->ijk", (70, 45, 52), (16, 16, 16), (1.0, 1.0), 0.1),
+    ("ik,jk,tl,dl,kl->ijtd", (26, 26, 12, 36), (20, 10), (0.5, 0.0), 0.0),
+    ("ia,jb,kc,ar,br,cr->ijk", (40, 36, 44), (4, 5, 6, 3), (1.0, 0.0), 0.05),
+    ("ar,br,cr,dr,er,fr->abcdef", (6, 7, 5, 6, 4, 8), (5,), (1.0, 0.0), 0.0),
+]
+
+
+@pytest.mark.parametrize("case", REUSE_CASES, ids=lambda c: c[0].split("->")[0])
+def test_sweep_reuse_bit_identical(nef, case):
+    """Side-operand reuse inside a sweep skips launches whose results an earlier
+    update of the same sweep left in the workspace: the fit must be bit-identical to the fit
+    that recomputes every side operand (kernel policy bit 2), through the sweep graph and
+    through plain launches, and match the oracle at the parity bar."""
+    ms, shape, ranks, ab, pm = case
+    Y, init = _problem(ms, shape, ranks, 7)
+    M = (np.random.default_rng(8).random(shape) >= pm).astype(np.uint8) if pm > 0 else None
+    plan = nef.Plan(ms, shape, ranks)
+    assert any(L["reuse_u"] or any(L["reuse_tab"]) for L in plan.describe()["lowerings"])
+    runs = {}
+    try:
+        for pol in (0, 4, 2, 6):
+            nef.nef_set_kernel_policy(pol)
+            runs[pol] = _fit(nef, ms, shape, ranks, Y, M, init, ab, 3)
+    finally:
+        nef.nef_set_kernel_policy(0)
+    for pol in (4, 2, 6):
+        for a, b in zip(runs[0][1], runs[pol][1]):
+            assert np.array_equal(a, b), pol
+        assert list(runs[0][2]) == list(runs[pol][2]), pol
+    ref, rtr = O.fit(ms, Y, M, init, ab[0], ab[1], 3)
+    assert _rel(runs[0][2], rtr) <= TRACE_RTOL, _rel(runs[0][2], rtr)
+    _, F1, _ = _fit(nef, ms, shape, ranks, Y, M, init, ab, 1)
+    ref1, _ = O.fit(ms, Y, M, init, ab[0], ab[1], 1)
+    err = max(_rel(g, r) for g, r in zip(F1, ref1))
+    assert err <= FACTOR_RTOL, err

@@ -313,3 +313,44 @@ def test_loss_spec_validation_before_device_work():
     code = nef.LIB.nef_fit_restarts(p.h, C.c_void_p(4096), None, C.byref(spec), 1e-12, F, 1, 1, None,
                                     C.c_void_p(1 << 20), 16, C.c_void_p(0))
     assert nef.NEF_STATUS[code] == "ARG"                                             # workspace too small
+
+
+def _prog_sem(prog):
+    """(operands as factors or 'W', index strings) of a described side-operand program"""
+    return tuple((st["a"] if st["a"].startswith("F") else "W", st["a_idx"],
+                  st["b"] if st["b"] and st["b"].startswith("F") else "W", st["b_idx"], st["c_idx"])
+                 for st in prog["steps"]), prog["result_idx"]
+
+
+def _prog_factors(prog):
+    return {int(x[1:]) for st in prog["steps"] for x in (st["a"], st["b"]) if x and x.startswith("F")}
+
+
+@pytest.mark.parametrize("ms,shape,ranks,expect", [
+    ("ia,jb,kc,abc->ijk", (256, 256, 256), (16, 16, 16), {(3, -1)}),                   # c2
+    ("ik,jk,tl,dl,kl->ijtd", (260, 260, 24, 365), (20, 10), {(1, 0), (3, 0)}),        # c4
+    ("ir,jr,kr->ijk", (2048, 2048, 1024), (64,), set()),                             # c5: none
+    ("ia,jb,kc,ar,br,cr->ijk", (40, 36, 44), (4, 5, 6, 3), None),
+    ("ar,br,cr,dr,er,fr->abcdef", (6, 7, 5, 6, 4, 8), (5,), None),
+])
+def test_sweep_reuse_is_sound(ms, shape, ranks, expect):
+    """A side-operand program that update ell of a sweep skips (reuse_u / reuse_tab) must be a
+    contraction an earlier update e of the same sweep computed, over factors none of the
+    updates e .. ell - 1 rewrote (update m rewrites factor m, Algorithm 1 order P:152-182), so
+    the values it would produce are the ones already in the workspace."""
+    d = nef.Plan(ms, shape, ranks).describe()
+    low = d["lowerings"]
+    got = set()
+    for L in low:
+        progs = [(-1, L["U"], L["reuse_u"])] + [(q, t["prog"], L["reuse_tab"][q]) for q, t in enumerate(L["tables"])]
+        for q, prog, reused in progs:
+            if not reused:
+                continue
+            got.add((L["ell"], q))
+            sem, fac = _prog_sem(prog), _prog_factors(prog)
+            src = [e for e in range(L["ell"]) if any(
+                _prog_sem(p) == sem for p in [low[e]["U"]] + [t["prog"] for t in low[e]["tables"]])]
+            assert src, (L["ell"], q)
+            assert not (fac & set(range(max(src), L["ell"]))), (L["ell"], q, fac, max(src))
+    if expect is not None:
+        assert got == expect
