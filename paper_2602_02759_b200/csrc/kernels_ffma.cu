@@ -722,7 +722,14 @@ static bool gemm_classify(const EinStep& st, bool hasB, EinGemmDev& g, int& tm, 
   g.b_kfast = g.bk[g.nk - 1] == 1;
   tm = M >= 48 ? 4 : M >= 24 ? 2 : 1;
   tn = N >= 48 ? 4 : N >= 24 ? 2 : 1;
-  const long long tiles = ((N + 16 * tn - 1) / (16 * tn)) * ((M + 16 * tm - 1) / (16 * tm)) * NB;
+  auto ntiles = [&] { return ((N + 16 * tn - 1) / (16 * tn)) * ((M + 16 * tm - 1) / (16 * tm)) * NB; };
+  // small outputs: smaller per-thread tiles until the blocks cover the SMs (a 65 536-output
+  // step at 4 x 4 ran as 16 blocks on 16 SMs, its latency chain ~4 loads + 16 stores deep)
+  while (ntiles() < 148 && (tm > 1 || tn > 1)) {
+    if (tm >= tn) tm /= 2;
+    else tn /= 2;
+  }
+  const long long tiles = ntiles();
   long long ks = 1;
   if (K > 64 && tiles < 296) ks = std::min<long long>(std::min<long long>((296 + tiles - 1) / tiles, (K + 63) / 64), 64);
   g.kc = (int)(((K + ks - 1) / ks + 15) / 16 * 16);
