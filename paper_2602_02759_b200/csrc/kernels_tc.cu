@@ -1092,9 +1092,23 @@ __device__ __forceinline__ void ew_half_aux(const TcArgs& a, uint32_t (&sv)[16],
 }
 
 // linear column index of the first column of a tile
+// q = x / d, r = x % d for x >= 0, d > 0: the 32-bit divide when both fit (the 64-bit one is a
+// ~100-instruction dependent chain; the index arithmetic below sits in front of every launch's
+// first V load - timing-neutral on its own, profiles/r02_prologue_trace.txt)
+__device__ __forceinline__ void divmod_nn(int64_t x, int64_t d, int64_t& q, int64_t& r) {
+  if ((((uint64_t)x | (uint64_t)d) >> 32) == 0) {
+    const uint32_t xq = (uint32_t)x / (uint32_t)d;
+    q = xq;
+    r = (uint32_t)x - xq * (uint32_t)d;
+  } else {
+    q = x / d;
+    r = x - q * d;
+  }
+}
 __device__ __forceinline__ int64_t tile_col0(const TcArgs& a, int64_t tile) {
   if (a.layout == 0) return tile * BN;
-  const int64_t ti = tile % a.tiles_inner, to = tile / a.tiles_inner;
+  int64_t ti, to;
+  divmod_nn(tile, a.tiles_inner, to, ti);
   return to * a.CI + ti * BN;
 }
 
@@ -1106,8 +1120,9 @@ __device__ __forceinline__ int64_t tile_col0(const TcArgs& a, int64_t tile) {
 __device__ __noinline__ int direct_var_row(const TcArgs& a, int64_t col) {
   int off = 0;
   for (int d = a.nc - 1; d >= 0; --d) {
-    const int64_t dig = d > 0 ? col % a.cdim[d] : col;
-    col = d > 0 ? col / a.cdim[d] : 0;
+    int64_t dig = col, rest = 0;
+    if (d > 0) divmod_nn(col, a.cdim[d], rest, dig);
+    col = rest;
     off += (int)dig * (int)a.tcs[a.var_tab][d];
   }
   return off / a.K;
@@ -1118,8 +1133,9 @@ __device__ __noinline__ TabOffs direct_offs(const TcArgs& a, int64_t col) {
   TabOffs r;
   for (int q = 0; q < kMaxTabs; ++q) r.o[q] = 0;
   for (int d = a.nc - 1; d >= 0; --d) {
-    const int64_t dig = d > 0 ? col % a.cdim[d] : col;
-    col = d > 0 ? col / a.cdim[d] : 0;
+    int64_t dig = col, rest = 0;
+    if (d > 0) divmod_nn(col, a.cdim[d], rest, dig);
+    col = rest;
     for (int q = 0; q < a.ntab; ++q) r.o[q] += (int)dig * (int)a.tcs[q][d];
   }
   return r;
@@ -1161,8 +1177,11 @@ struct RunCursor {
     tin = (int)(a.layout == 0 ? a.tiles : a.tiles_inner);
     ci = a.layout == 0 ? 0 : a.CI;
     tile = t0;
-    k = (int)(t0 % tpr);
-    ti = (int)(t0 % tin);
+    int64_t qq, rr;
+    divmod_nn(t0, tpr, qq, rr);
+    k = (int)rr;
+    divmod_nn(t0, tin, qq, rr);
+    ti = (int)rr;
     off = tile_col0(a, t0) - tile_col0(a, t0 - k);
     blk_off = off - (int64_t)ti * BN;
   }
@@ -1287,6 +1306,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
   // every G tiles and restarted.
   constexpr int G = kDrainTiles;   // (power of two: t % G is a mask)
 
+  if (tid == 0) trace_ev(a, 1023, 0);   // (trace build: launch phases in row 1023 - entry)
   if (tid == 0) {
     for (int i = 0; i < NS; ++i) { mbar_init(y_full + 8 * i, 1); mbar_init(y_empty + 8 * i, NEW); }
     for (int i = 0; i < NV; ++i) { mbar_init(v_full + 8 * i, NVG); mbar_init(v_empty + 8 * i, 1); }
@@ -1310,6 +1330,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  if (tid == 0) trace_ev(a, 1023, 1);   // barriers initialised, TMEM allocated
 #if NEF_UWARP
   const uint32_t tmem = __shfl_sync(0xffffffffu, *gTmem, 0);
 #else
@@ -1376,6 +1397,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
       // the explicit wait on the N/D commit.
       const bool war_wait = (NEF_DBG & 16) != 0;
       mbar_wait_mma(u_ready, 0);
+      if (lane == 0) trace_ev(a, 1023, 8);   // (trace) U in TMEM
       tc_fence_after();
       // S(t) = U_hi V(t)^T + U_lo V(t)^T into buffer t & 1 (split reconstruction)
       auto mma_s = [&](int t, int b, uint32_t ph) {   // b = t % NBUF, ph = (t / NBUF) & 1
@@ -1461,6 +1483,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
     if (T > 0) {
       constexpr uint32_t id1 = idesc_tf32(128, BN);
       mbar_wait_mma(u_ready, 0);
+      if (lane == 0) trace_ev(a, 1023, 8);   // (trace) U in TMEM
       tc_fence_after();
       int b = 0;
       uint32_t ph = 0;
@@ -1501,6 +1524,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
         const int vs = t % NV;
         mbar_wait_relaxed(v_empty + 8 * vs, ((t / NV) & 1) ^ 1);
         const uint32_t bar = vraw_full + 8 * vs;
+        if (t == 0) trace_ev(a, 1023, 5);   // (trace) first direct-V TMA issued
         mbar_expect_tx(bar, (uint32_t)(KB * BN * 4));
 #pragma unroll
         for (int h = 0; h < KB / 32; ++h) tma_load_2d(sV + vs * V_STAGE + h * (BN * 128), &P.tmV[rs], 32 * h, rowv, bar);
@@ -1521,8 +1545,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
     bool pend = false;
     if (T > 0) {
       rn.init(a, t_begin);
+      if (warp == W_VG0 && lane == 0) trace_ev(a, 1023, 9);   // (trace) first constant rows issued
       cst_issue(a, a.tabr[rs], tile_col0(a, t_begin), c, ld);
       cst = cst_product(a, c, ld);
+      if (warp == W_VG0 && lane == 0) trace_ev(a, 1023, 6);   // (trace) first constant rows landed
     }
     for (int t = 0; t < T; ++t) {
       if (pend) {
@@ -1627,6 +1653,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(u_ready);
+      if (warp == W_EW0 && lane == 0) trace_ev(a, 1023, 7);   // (trace) this warp's U chunks stored
     }
     // N | D (2 NCH chunks of 16 columns, shared out among the column groups) -> this CTA's split
     // partial of drain group grp (zeros when zero: a chunk with fewer tiles than others)
@@ -1766,10 +1793,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
       if (T > 0) {
         mbar_spin(nd_full, 0);
         tc_fence_after();
+        if (warp == W_EW0 && lane == 0) trace_ev(a, 1023, 2);   // last N / D MMAs retired
         drain_nd((T - 1) / G, false);
         g0 = (T - 1) / G + 1;
       }
       for (int64_t grp = g0; grp < a.n_groups; ++grp) drain_nd(grp, true);
+      if (warp == W_EW0 && lane == 0) trace_ev(a, 1023, 3);     // partials written
     } else if (T > 0) {
       mbar_spin(nd_full, 0);
     }
@@ -1796,6 +1825,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
   }
   tc_fence_before();
   __syncthreads();
+  if (tid == 0) trace_ev(a, 1023, 4);   // every role done
   if (warp == W_MMA) {
     tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");

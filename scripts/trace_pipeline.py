@@ -33,9 +33,20 @@ torch.cuda.synchronize()
 nef.nef_debug_trace(None)
 full = tr.cpu().numpy().reshape(1024, 32).astype(np.int64)
 t = full[:, :len(EV)]
-valid = (t[:, EV.index("EW_DONE")] > 0).sum()
+valid = (t[:1023, EV.index("EW_DONE")] > 0).sum()   # (row 1023 holds the launch phases)
 print("tiles traced", valid)
-lo, hi = args.first, min(args.first + args.n, valid - 1)
+ph = full[1023, :10]
+if ph[0] > 0:
+    print("prologue (cycles after entry): first V TMA issued %d, constant rows issued %d landed %d, "
+          "EW warp 0 U stored %d, issuer saw U %d, first raw V landed (VG_START) %d"
+          % (ph[5] - ph[0], ph[9] - ph[0], ph[6] - ph[0], ph[7] - ph[0], ph[8] - ph[0], t[0, EV.index("VG_START")] - ph[0]))
+if ph[0] > 0:   # launch phases of CTA (0, 0), cycles after kernel entry
+    last = t[valid - 1, EV.index("EW_DONE")] if valid > 0 else ph[0]
+    print("launch phases (cycles after entry): setup done %d, first TMA %d, first MMA1 %d, first EW_DONE %d, "
+          "last EW_DONE %d, last N/D retired %d, partials written %d, all roles done %d"
+          % (ph[1] - ph[0], t[0, EV.index("TMA")] - ph[0], t[0, EV.index("MMA1")] - ph[0],
+             t[0, EV.index("EW_DONE")] - ph[0], last - ph[0], ph[2] - ph[0], ph[3] - ph[0], ph[4] - ph[0]))
+lo, hi = min(args.first, max(valid - 2, 0)), min(args.first + args.n, valid - 1)
 base = t[lo, EV.index("MMA1")]
 print("tile " + " ".join("%9s" % e for e in EV))
 for i in range(lo, hi):
