@@ -1516,8 +1516,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) fused_tc_kernel(const __grid_cons
     // ------------------------------------------------------------ direct-V row loads (TMA)
     if (lane == 0 && a.vdirect && T > 0) {
       RunCursor rc;
+      trace_ev(a, 1023, 10);   // (trace) loader lane starts
       rc.init(a, t_begin);
+      trace_ev(a, 1023, 11);   // (trace) run cursor initialised
       int run_row = direct_var_row(a, tile_col0(a, t_begin) - rc.off);
+      trace_ev(a, 1023, 12);   // (trace) first table row known
       for (int t = 0; t < T; ++t) {
         if (t > 0 && rc.next()) run_row = direct_var_row(a, tile_col0(a, rc.tile));
         const int rowv = run_row + (int)rc.off;

@@ -35,8 +35,10 @@ full = tr.cpu().numpy().reshape(1024, 32).astype(np.int64)
 t = full[:, :len(EV)]
 valid = (t[:1023, EV.index("EW_DONE")] > 0).sum()   # (row 1023 holds the launch phases)
 print("tiles traced", valid)
-ph = full[1023, :10]
+ph = full[1023, :13]
 if ph[0] > 0:
+    print("direct-V loader lane (cycles after entry): starts %d, run cursor initialised %d, first table row known %d, "
+          "first TMA issued %d" % (ph[10] - ph[0], ph[11] - ph[0], ph[12] - ph[0], ph[5] - ph[0]))
     print("prologue (cycles after entry): first V TMA issued %d, constant rows issued %d landed %d, "
           "EW warp 0 U stored %d, issuer saw U %d, first raw V landed (VG_START) %d"
           % (ph[5] - ph[0], ph[9] - ph[0], ph[6] - ph[0], ph[7] - ph[0], ph[8] - ph[0], t[0, EV.index("VG_START")] - ph[0]))
